@@ -1,0 +1,194 @@
+/*
+ * sso.h — C ABI of the B200-native JAX-SSO hot path (arXiv 2407.20026).
+ *
+ * The path (BASELINE.json north_star):
+ *   A0  pattern build      PAPER.md:82-83   (element_K_*_indices -> global positions)
+ *   A1  element stiffness  PAPER.md:75-82, 112 (beam 12x12, MITC-4 quad 24x24)
+ *   A2  assembly+supports  PAPER.md:58, 83-96 (vectorised scatter-add; Eq. 2-3 with b = 0)
+ *   A3  Jacobi-PCG solve   PAPER.md:71-74 (Eq. 1 K u = f), BASELINE.json north_star
+ *   A4  adjoint gradient   PAPER.md:212-221 (Eq. 5-6), objective PAPER.md:144, 252
+ *
+ * Conventions (DESIGN.md readings):
+ *   - node ids are 0..n_nodes-1; element order is beams first, then quads;
+ *   - DOF numbering node-major, component-minor: 6*node + c,
+ *     c in (UX, UY, UZ, RX, RY, RZ);
+ *   - supports: 6-bit mask per node, bit c set = DOF c fixed at 0 (b = 0);
+ *     repeated nodes OR-merge; supports are applied by symmetric elimination;
+ *   - every pointer passed to sso_create / sso_set_design is COPIED; the
+ *     library owns all device state; outputs are written to caller-owned
+ *     buffers of the stated sizes;
+ *   - `mem` (sso_options.mem, changeable with sso_set_stream) says whether the
+ *     f / u / gradient / design pointers of sso_set_design, sso_solve,
+ *     sso_grad, sso_grad_at and sso_spmv are HOST or DEVICE pointers.  Device
+ *     pointers must live on the handle's device.  All work is enqueued on the
+ *     handle's CUDA stream; every call returns after that stream has completed
+ *     its work unless stated otherwise;
+ *   - one handle = one stream, not re-entrant; distinct handles are independent;
+ *   - results are deterministic: same inputs -> bit-identical outputs
+ *     (atomic-free, fixed-order reductions).
+ *
+ * Error behaviour: every int-returning call returns an sso_status; on failure
+ * sso_last_error(h) (or sso_last_error(NULL) for sso_create) holds a message
+ * naming the element / node / DOF at fault.  Device-side numeric failures
+ * (degenerate element, singular diagonal, non-SPD, not converged) are
+ * reported by the call that detects them.
+ */
+#ifndef SSO_H
+#define SSO_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sso_ctx* sso_handle;
+
+typedef enum {
+  SSO_OK = 0,
+  SSO_E_INVALID = 1,        /* bad argument / input validation      */
+  SSO_E_VALIDATION = 2,     /* reserved for CLI parity/FD threshold failures */
+  SSO_E_NUMERIC = 3,        /* generic numeric failure                                     */
+  SSO_E_DEGENERATE = 11,    /* zero-length beam, zero quad normal, det J <= 0 */
+  SSO_E_SINGULAR = 31,      /* free DOF with diagonal <= 0                   */
+  SSO_E_NOT_SPD = 32,       /* p^T K p <= 0 inside CG                                      */
+  SSO_E_NOT_CONVERGED = 33, /* max_iter reached; u holds the last iterate, info filled     */
+  SSO_E_CUDA = 40,
+  SSO_E_NCCL = 41,
+  SSO_E_OOM = 42,
+  SSO_E_STATE = 43          /* call order violated (e.g. sso_grad before sso_solve)        */
+} sso_status;
+
+typedef enum {
+  SSO_OBJ_COMPLIANCE = 0,     /* C = f^T u       (reading c2; s = 1)                       */
+  SSO_OBJ_STRAIN_ENERGY = 1   /* g = 0.5 f^T u   (s = 1/2)              */
+} sso_objective;
+
+typedef enum { SSO_MEM_HOST = 0, SSO_MEM_DEVICE = 1 } sso_mem;
+
+/* Mesh: SoA coordinates (fp64, n_nodes each); beam_conn [n_beams][2];
+ * quad_conn [n_quads][4] in cyclic order.  Host pointers, copied. */
+typedef struct {
+  int32_t n_nodes;
+  const double *x, *y, *z;
+  int32_t n_beams;
+  const int32_t* beam_conn;
+  int32_t n_quads;
+  const int32_t* quad_conn;
+} sso_mesh;
+
+/* Sections: A, Iy, Iz, J [n_beams] (may be NULL when n_beams == 0);
+ * t [n_quads] shell thickness (may be NULL when n_quads == 0).  Host, copied. */
+typedef struct {
+  const double *A, *Iy, *Iz, *J;
+  const double* t;
+} sso_sections;
+
+/* Materials per element (beams first, then quads): E, nu [n_beams + n_quads];
+ * G may be NULL -> G = E / (2 (1 + nu)).  Host, copied. */
+typedef struct {
+  const double *E, *nu, *G;
+} sso_materials;
+
+/* Supports: n entries of (node, 6-bit mask), b = 0 (reading c1).  Host, copied. */
+typedef struct {
+  int32_t n;
+  const int32_t* node;
+  const uint8_t* mask6;
+} sso_supports;
+
+typedef struct {
+  double rtol;            /* CG stop: |r|_2 <= rtol |f_bc|_2            (default 1e-10) */
+  int64_t max_iter;       /* CG iteration cap                          (default 200000) */
+  double drill_alpha;     /* drilling penalty gamma_d = alpha_d G      (default 1e-3)   */
+  int32_t warm_start;     /* 1: sso_solve reads u as x0                (default 0)      */
+  int32_t check_every;    /* CG iterations per device-side graph chunk (default 64)     */
+  sso_mem mem;            /* pointer kind of solve/grad/design buffers (default HOST)   */
+  void* cuda_stream;      /* cudaStream_t to enqueue on; NULL = library-owned stream    */
+  int32_t device;         /* CUDA device ordinal                        (default: current) */
+} sso_options;
+
+typedef struct {
+  int64_t iters;          /* CG iterations performed                                   */
+  double rel_res;         /* recurrence residual |r|/|f_bc| at exit                    */
+  double true_rel_res;    /* |f_bc - K_bc u| / |f_bc| recomputed at exit               */
+  double ms;              /* device time of the solve (CUDA events)                    */
+  int32_t status;         /* sso_status of this solve                                  */
+} sso_solve_info;
+
+/* Fill *o with the defaults listed above.  Always SSO_OK. */
+int sso_options_default(sso_options* o);
+
+/* Validate, build the node-block CSR pattern (A0), upload all inputs.
+ * Errors: SSO_E_INVALID (index out of range, i_node == j_node, E/G/A/Iy/Iz/J/t <= 0,
+ * nu outside [0, 0.5), repeated node in a quad, non-finite input, no supports or an
+ * all-zero mask), SSO_E_DEGENERATE (zero-length beam), SSO_E_CUDA / SSO_E_OOM.
+ * On error *out is NULL and sso_last_error(NULL) explains. */
+int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_materials* mat,
+               const sso_supports* sup, const sso_options* opt, sso_handle* out);
+
+/* Replace design variables: x, y, z [n_nodes] and/or t [n_quads]; NULL = unchanged.
+ * Pointer kind per `mem`.  Invalidates the assembled K (call sso_assemble again). */
+int sso_set_design(sso_handle h, const double* x, const double* y, const double* z,
+                   const double* t);
+
+/* Change the stream and pointer kind used by subsequent calls. */
+int sso_set_stream(sso_handle h, void* cuda_stream, sso_mem mem);
+
+/* A1 + A2: element stiffness for all elements, segmented-sum assembly into the fixed
+ * CSR values, supports by elimination, Jacobi diagonal.  Errors: SSO_E_DEGENERATE
+ * (element id in the message), SSO_E_SINGULAR (free DOF with diagonal <= 0). */
+int sso_assemble(sso_handle h);
+
+/* A3: Jacobi-PCG on K_bc u = f_bc.  f [6 n_nodes] (entries at constrained DOFs ignored),
+ * u [6 n_nodes] output (zeros at constrained DOFs); read as x0 when warm_start.
+ * info may be NULL.  Errors: SSO_E_STATE (not assembled), SSO_E_NOT_SPD,
+ * SSO_E_NOT_CONVERGED (u = last iterate). */
+int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info);
+
+/* A4: objective and adjoint gradient at the last solve's (f, u):
+ * C [1]; dC_dxyz [3][n_nodes] (SoA: all x, then y, then z); dC_dt [n_quads].
+ * Any output pointer may be NULL to skip it.  Errors: SSO_E_STATE (no solve yet). */
+int sso_grad(sso_handle h, sso_objective obj, double* C, double* dC_dxyz, double* dC_dt);
+
+/* A4 at a caller-given state: C = s f^T u and -s sum_e u_e^T dK_e/dp u_e for the given
+ * f, u [6 n_nodes] (u taken as is, including constrained entries).  Pointer kind per mem. */
+int sso_grad_at(sso_handle h, sso_objective obj, const double* f, const double* u,
+                double* C, double* dC_dxyz, double* dC_dt);
+
+/* y = K_bc x with the assembled matrix (x, y [6 n_nodes]; pointer kind per mem). */
+int sso_spmv(sso_handle h, const double* x, double* y);
+
+/* Sizes: ndof = 6 n_nodes; nnz of the scalar CSR; node blocks of the node graph. */
+int sso_sizes(sso_handle h, int64_t* ndof, int64_t* nnz, int64_t* n_blocks);
+
+/* Debug / parity exports (HOST pointers always; caller-allocated):
+ *   row_ptr [ndof+1] int64, col_idx [nnz] int32, vals [nnz] fp64 (any may be NULL);
+ *   block_rank: beams [n_beams][4] then quads [n_quads][16], int32: position of
+ *     element node j in the sorted node adjacency of element node i (i-major);
+ *   ke: staged element matrices of elements [first, first+count) in the global
+ *     element order, each dense row-major in element DOF order (144 or 576 fp64);
+ *   dinv [ndof]: Jacobi inverse diagonal of K_bc. */
+int sso_export_csr(sso_handle h, int64_t* row_ptr, int32_t* col_idx, double* vals);
+int sso_export_scatter(sso_handle h, int32_t* block_rank);
+int sso_export_ke(sso_handle h, int64_t first, int64_t count, double* ke);
+int sso_export_dinv(sso_handle h, double* dinv);
+
+/* Kernel timing (CUDA events recorded on the handle's stream around every launch of
+ * the named kernel family while enabled).  names: "element", "assemble", "spmv",
+ * "update", "grad", "reduce".  total_ms and launches accumulate since the last reset. */
+int sso_profile_enable(sso_handle h, int32_t on);
+int sso_profile_read(sso_handle h, const char* name, double* total_ms, int64_t* launches);
+int sso_profile_reset(sso_handle h);
+
+/* Number of kernel launches issued by the library since the handle was created
+ * (graph-launched kernels counted individually). */
+int64_t sso_launch_count(sso_handle h);
+
+const char* sso_last_error(sso_handle h);
+void sso_destroy(sso_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSO_H */

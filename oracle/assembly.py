@@ -226,3 +226,32 @@ def lagrange_system(K, f, fixed, b=None):
     if b is not None:
         faug[ndof:] = b
     return Kaug, faug
+
+
+def incident_elements(P, n):
+    """Elements containing node n, ascending (beams first, then quads)."""
+    nb = n_beams(P)
+    out = []
+    if nb:
+        out += [int(e) for e in np.nonzero((P["beam_conn"] == n).any(axis=1))[0]]
+    if n_quads(P):
+        out += [nb + int(q) for q in np.nonzero((P["quad_conn"] == n).any(axis=1))[0]]
+    return out
+
+
+def node_rows(P, n, X=None):
+    """The six global rows 6n..6n+5 of the summed K (before supports), as a dict
+    column -> 6-vector, summed over the incident elements in ascending order —
+    the DOK definition restricted to one node (for full-size sampled checks)."""
+    rows = {}
+    for e in incident_elements(P, n):
+        nodes = element_nodes(P, e)
+        Ke = element_K(P, e, X)
+        dofs = element_dofs(nodes)
+        for il, nd in enumerate(nodes):
+            if nd != n:
+                continue
+            for b, cb in enumerate(dofs):
+                col = rows.setdefault(cb, np.zeros(6))
+                col += Ke[6 * il:6 * il + 6, b]
+    return rows

@@ -1,0 +1,326 @@
+"""Thin ctypes binding of the C ABI in include/sso.h (argument marshalling only).
+
+Every step of the hot path runs in the CUDA kernels of libsso.so; this module
+only converts numpy arrays / torch tensors to pointers.  There is no CPU
+fallback: if libsso.so is missing, importing this module raises.
+
+Names follow include/sso.h: Model.create (sso_create), .assemble, .solve,
+.grad, .grad_at, .spmv, .set_design, .export_csr, .export_scatter,
+.export_ke, .export_dinv, .profile_*.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsso.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+_lib = C.CDLL(LIB_PATH)
+
+SSO_OK, SSO_E_INVALID, SSO_E_VALIDATION, SSO_E_NUMERIC = 0, 1, 2, 3
+SSO_E_DEGENERATE, SSO_E_SINGULAR, SSO_E_NOT_SPD, SSO_E_NOT_CONVERGED = 11, 31, 32, 33
+SSO_E_CUDA, SSO_E_NCCL, SSO_E_OOM, SSO_E_STATE = 40, 41, 42, 43
+STATUS_NAMES = {0: "SSO_OK", 1: "SSO_E_INVALID", 2: "SSO_E_VALIDATION", 3: "SSO_E_NUMERIC",
+                11: "SSO_E_DEGENERATE", 31: "SSO_E_SINGULAR", 32: "SSO_E_NOT_SPD",
+                33: "SSO_E_NOT_CONVERGED", 40: "SSO_E_CUDA", 41: "SSO_E_NCCL", 42: "SSO_E_OOM",
+                43: "SSO_E_STATE"}
+OBJ_COMPLIANCE, OBJ_STRAIN_ENERGY = 0, 1
+MEM_HOST, MEM_DEVICE = 0, 1
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int32)
+_lp = C.POINTER(C.c_int64)
+_up = C.POINTER(C.c_uint8)
+
+
+class sso_mesh(C.Structure):
+    _fields_ = [("n_nodes", C.c_int32), ("x", _dp), ("y", _dp), ("z", _dp),
+                ("n_beams", C.c_int32), ("beam_conn", _ip), ("n_quads", C.c_int32),
+                ("quad_conn", _ip)]
+
+
+class sso_sections(C.Structure):
+    _fields_ = [("A", _dp), ("Iy", _dp), ("Iz", _dp), ("J", _dp), ("t", _dp)]
+
+
+class sso_materials(C.Structure):
+    _fields_ = [("E", _dp), ("nu", _dp), ("G", _dp)]
+
+
+class sso_supports(C.Structure):
+    _fields_ = [("n", C.c_int32), ("node", _ip), ("mask6", _up)]
+
+
+class sso_options(C.Structure):
+    _fields_ = [("rtol", C.c_double), ("max_iter", C.c_int64), ("drill_alpha", C.c_double),
+                ("warm_start", C.c_int32), ("check_every", C.c_int32), ("mem", C.c_int),
+                ("cuda_stream", C.c_void_p), ("device", C.c_int32)]
+
+
+class sso_solve_info(C.Structure):
+    _fields_ = [("iters", C.c_int64), ("rel_res", C.c_double), ("true_rel_res", C.c_double),
+                ("ms", C.c_double), ("status", C.c_int32)]
+
+    def as_dict(self):
+        return dict(iters=self.iters, rel_res=self.rel_res, true_rel_res=self.true_rel_res,
+                    ms=self.ms, status=self.status)
+
+
+_H = C.c_void_p
+_sig = {
+    "sso_options_default": (C.c_int, [C.POINTER(sso_options)]),
+    "sso_create": (C.c_int, [C.POINTER(sso_mesh), C.POINTER(sso_sections), C.POINTER(sso_materials),
+                             C.POINTER(sso_supports), C.POINTER(sso_options), C.POINTER(_H)]),
+    "sso_set_design": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sso_set_stream": (C.c_int, [_H, C.c_void_p, C.c_int]),
+    "sso_assemble": (C.c_int, [_H]),
+    "sso_solve": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.POINTER(sso_solve_info)]),
+    "sso_grad": (C.c_int, [_H, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sso_grad_at": (C.c_int, [_H, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sso_spmv": (C.c_int, [_H, C.c_void_p, C.c_void_p]),
+    "sso_sizes": (C.c_int, [_H, _lp, _lp, _lp]),
+    "sso_export_csr": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sso_export_scatter": (C.c_int, [_H, C.c_void_p]),
+    "sso_export_ke": (C.c_int, [_H, C.c_int64, C.c_int64, C.c_void_p]),
+    "sso_export_dinv": (C.c_int, [_H, C.c_void_p]),
+    "sso_profile_enable": (C.c_int, [_H, C.c_int32]),
+    "sso_profile_read": (C.c_int, [_H, C.c_char_p, _dp, _lp]),
+    "sso_profile_reset": (C.c_int, [_H]),
+    "sso_launch_count": (C.c_int64, [_H]),
+    "sso_last_error": (C.c_char_p, [_H]),
+    "sso_destroy": (None, [_H]),
+}
+EXPORTED = tuple(_sig)
+for _name, (_res, _args) in _sig.items():
+    _fn = getattr(_lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+class SSOError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _ptr(a, dtype):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.dtype == dtype and a.flags["C_CONTIGUOUS"], (a.dtype, dtype)
+        return a.ctypes.data
+    # torch tensor
+    return a.data_ptr()
+
+
+def _np(a, dtype):
+    if a is None:
+        return None
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _is_device(a):
+    return a is not None and not isinstance(a, np.ndarray) and getattr(a, "is_cuda", False)
+
+
+class Model:
+    """One sso_handle.  `problem` is a dict as produced by workloads.* (x, y, z,
+    beam_conn, quad_conn, A, Iy, Iz, J, t, E, nu, G, sup_node, sup_mask)."""
+
+    def __init__(self, problem, rtol=1e-10, max_iter=200000, drill_alpha=1e-3, check_every=64,
+                 warm_start=False, stream=None, device=-1):
+        P = problem
+        self._keep = []
+        x, y, z = (_np(P[k], np.float64) for k in ("x", "y", "z"))
+        bc = _np(P["beam_conn"], np.int32).reshape(-1)
+        qc = _np(P["quad_conn"], np.int32).reshape(-1)
+        nb, nq = len(bc) // 2, len(qc) // 4
+        A, Iy, Iz, J, t = (_np(P.get(k), np.float64) for k in ("A", "Iy", "Iz", "J", "t"))
+        E, nu = _np(P["E"], np.float64), _np(P["nu"], np.float64)
+        G = _np(P.get("G"), np.float64)
+        sn, sm = _np(P["sup_node"], np.int32), _np(P["sup_mask"], np.uint8)
+        self._keep += [x, y, z, bc, qc, A, Iy, Iz, J, t, E, nu, G, sn, sm]
+
+        def dp(a):
+            return None if a is None or a.size == 0 else a.ctypes.data_as(_dp)
+
+        def ip(a):
+            return None if a is None or a.size == 0 else a.ctypes.data_as(_ip)
+
+        mesh = sso_mesh(len(x), dp(x), dp(y), dp(z), nb, ip(bc), nq, ip(qc))
+        sec = sso_sections(dp(A), dp(Iy), dp(Iz), dp(J), dp(t))
+        mat = sso_materials(dp(E), dp(nu), dp(G))
+        sup = sso_supports(len(sn), ip(sn), sm.ctypes.data_as(_up) if sm.size else None)
+        opt = sso_options()
+        _lib.sso_options_default(C.byref(opt))
+        opt.rtol, opt.max_iter, opt.drill_alpha = rtol, max_iter, drill_alpha
+        opt.check_every, opt.warm_start, opt.device = check_every, int(warm_start), device
+        opt.mem = MEM_HOST
+        opt.cuda_stream = stream
+        h = _H()
+        rc = _lib.sso_create(C.byref(mesh), C.byref(sec), C.byref(mat), C.byref(sup), C.byref(opt),
+                             C.byref(h))
+        if rc != SSO_OK:
+            raise SSOError(rc, _lib.sso_last_error(None).decode())
+        self.h = h
+        self.n_nodes, self.n_beams, self.n_quads = len(x), nb, nq
+        self.ndof = 6 * len(x)
+        self._mem = MEM_HOST
+        self._stream = stream
+
+    # -- plumbing ----------------------------------------------------------
+    def _check(self, rc):
+        if rc != SSO_OK:
+            raise SSOError(rc, _lib.sso_last_error(self.h).decode())
+        return rc
+
+    def _mode(self, *arrays):
+        dev = any(_is_device(a) for a in arrays if a is not None)
+        mem = MEM_DEVICE if dev else MEM_HOST
+        stream = None
+        if dev:
+            import torch
+            stream = torch.cuda.current_stream().cuda_stream
+        if mem != self._mem or (dev and stream != self._stream):
+            self._check(_lib.sso_set_stream(self.h, stream, mem))
+            self._mem, self._stream = mem, (stream if dev else self._stream)
+        return dev
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.sso_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- ABI -----------------------------------------------------------------
+    def sizes(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(_lib.sso_sizes(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def set_design(self, x=None, y=None, z=None, t=None):
+        dev = self._mode(x, y, z, t)
+        conv = (lambda a: a) if dev else (lambda a: _np(a, np.float64))
+        arrs = [None if a is None else conv(a) for a in (x, y, z, t)]
+        self._check(_lib.sso_set_design(self.h, *[_ptr(a, np.float64) for a in arrs]))
+
+    def assemble(self):
+        self._check(_lib.sso_assemble(self.h))
+
+    def solve(self, f, u=None, raise_on_error=True):
+        """Returns (u, info dict).  f, u: numpy (host) or torch CUDA tensors (device)."""
+        dev = self._mode(f, u)
+        if not dev:
+            f = _np(f, np.float64)
+            if u is None:
+                u = np.zeros(self.ndof)
+        elif u is None:
+            import torch
+            u = torch.zeros(self.ndof, dtype=torch.float64, device=f.device)
+        info = sso_solve_info()
+        rc = _lib.sso_solve(self.h, _ptr(f, np.float64), _ptr(u, np.float64), C.byref(info))
+        if raise_on_error:
+            self._check(rc)
+        return u, info.as_dict()
+
+    def grad(self, objective=OBJ_COMPLIANCE, out=None):
+        """Returns (C, dC_dxyz [3, n_nodes], dC_dt [n_quads]) for the last solve."""
+        return self._grad(objective, None, None, out)
+
+    def grad_at(self, f, u, objective=OBJ_COMPLIANCE, out=None):
+        return self._grad(objective, f, u, out)
+
+    def _grad(self, objective, f, u, out):
+        dev = self._mode(f, u, *(out or ()))
+        if out is None:
+            if dev:
+                import torch
+                ref = f if f is not None else u
+                Cv = torch.zeros(1, dtype=torch.float64, device=ref.device)
+                dX = torch.zeros(3 * self.n_nodes, dtype=torch.float64, device=ref.device)
+                dT = torch.zeros(max(self.n_quads, 1), dtype=torch.float64, device=ref.device)
+            else:
+                Cv, dX, dT = np.zeros(1), np.zeros(3 * self.n_nodes), np.zeros(max(self.n_quads, 1))
+        else:
+            Cv, dX, dT = out
+        if f is None:
+            rc = _lib.sso_grad(self.h, objective, _ptr(Cv, np.float64), _ptr(dX, np.float64),
+                               _ptr(dT, np.float64))
+        else:
+            if not dev:
+                f, u = _np(f, np.float64), _np(u, np.float64)
+            rc = _lib.sso_grad_at(self.h, objective, _ptr(f, np.float64), _ptr(u, np.float64),
+                                  _ptr(Cv, np.float64), _ptr(dX, np.float64), _ptr(dT, np.float64))
+        self._check(rc)
+        if out is not None:
+            return out
+        C0 = float(Cv[0]) if not dev else Cv
+        return C0, dX.reshape(3, self.n_nodes), dT[: self.n_quads]
+
+    def spmv(self, x):
+        dev = self._mode(x)
+        if dev:
+            import torch
+            y = torch.empty_like(x)
+        else:
+            x = _np(x, np.float64)
+            y = np.empty_like(x)
+        self._check(_lib.sso_spmv(self.h, _ptr(x, np.float64), _ptr(y, np.float64)))
+        return y
+
+    def export_csr(self, values=True):
+        ndof, nnz, _ = self.sizes()
+        rp = np.empty(ndof + 1, np.int64)
+        ci = np.empty(nnz, np.int32)
+        v = np.empty(nnz, np.float64) if values else None
+        self._check(_lib.sso_export_csr(self.h, rp.ctypes.data, ci.ctypes.data,
+                                        None if v is None else v.ctypes.data))
+        return rp, ci, v
+
+    def export_scatter(self):
+        br = np.empty(4 * self.n_beams + 16 * self.n_quads, np.int32)
+        self._check(_lib.sso_export_scatter(self.h, br.ctypes.data))
+        return br
+
+    def export_ke(self, first, count):
+        if first < self.n_beams:
+            assert first + count <= self.n_beams, "export beams and quads separately"
+            m = 12
+        else:
+            m = 24
+        ke = np.empty((count, m, m))
+        self._check(_lib.sso_export_ke(self.h, first, count, ke.ctypes.data))
+        return ke
+
+    def export_dinv(self):
+        d = np.empty(self.ndof)
+        self._check(_lib.sso_export_dinv(self.h, d.ctypes.data))
+        return d
+
+    def profile_enable(self, on=True):
+        self._check(_lib.sso_profile_enable(self.h, int(on)))
+
+    def profile_reset(self):
+        self._check(_lib.sso_profile_reset(self.h))
+
+    def profile_read(self, name):
+        ms, n = C.c_double(), C.c_int64()
+        self._check(_lib.sso_profile_read(self.h, name.encode(), C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def launch_count(self):
+        return int(_lib.sso_launch_count(self.h))
+
+
+def last_create_error():
+    return _lib.sso_last_error(None).decode()

@@ -1,0 +1,122 @@
+// Internal declarations of the B200 JAX-SSO hot-path library (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "sso.h"
+
+namespace sso {
+
+// ---------------------------------------------------------------------------
+// Host-side pattern (A0).  Node-block CSR: node n has deg(n) = node_ptr[n+1] -
+// node_ptr[n] neighbours node_col[node_ptr[n] ..] (ascending, incl. n).  The
+// scalar CSR is implied: row 6n+a holds columns 6m+b for m in adj(n), b = 0..5,
+// row_ptr[6n+a] = 36 node_ptr[n] + 6 a deg(n); the values of node n's six rows
+// are contiguous at 36 node_ptr[n].
+// ---------------------------------------------------------------------------
+struct HostPattern {
+  int32_t n_nodes = 0, n_beams = 0, n_quads = 0;
+  std::vector<int64_t> node_ptr;      // [n_nodes+1]
+  std::vector<int32_t> node_col;      // [n_blocks]
+  std::vector<int32_t> block_rank;    // beams [Eb][4], quads [Eq][16]
+  std::vector<int64_t> contrib_ptr;   // [n_blocks+1]
+  std::vector<int32_t> contrib;       // staged block ids, ascending (e, i, j)
+  std::vector<int64_t> inc_ptr;       // [n_nodes+1] node -> element-node slots
+  std::vector<int32_t> inc_slot;      // slot = 2e+i (beams) or 2Eb+4q+i (quads), ascending e
+  int64_t n_blocks() const { return (int64_t)node_col.size(); }
+  int64_t nnz() const { return 36 * n_blocks(); }
+  int64_t n_staged_blocks() const { return 4 * (int64_t)n_beams + 16 * (int64_t)n_quads; }
+};
+
+// Builds the pattern; returns empty string on success, else an error message.
+std::string build_pattern(int32_t n_nodes, int32_t n_beams, const int32_t* beam_conn,
+                          int32_t n_quads, const int32_t* quad_conn, HostPattern& P);
+
+// ---------------------------------------------------------------------------
+// Device state shared by the PCG kernels (one instance in device memory).
+// ---------------------------------------------------------------------------
+struct CgState {
+  double rz;        // r^T z (current)
+  double pq;        // p^T K p (current iteration)
+  double alpha, beta;
+  double rr;        // r^T r
+  double ff;        // f^T f
+  double tol2;      // (rtol^2) * ff
+  long long iter;
+  long long max_iter;
+  int done;         // 1 = converged or failed: all later kernels return immediately
+  int status;       // sso_status
+  unsigned int ticket[4];  // last-block-done counters (one per reduction site)
+};
+
+// error flags written by device kernels (atomicMin on the offending index)
+struct DevFlags {
+  int degenerate_elem;   // INT_MAX = none
+  int singular_dof;      // INT_MAX = none
+};
+
+// Kernel-family timers
+enum Family { F_ELEMENT = 0, F_ASSEMBLE, F_SPMV, F_UPDATE, F_GRAD, F_REDUCE, F_COUNT };
+
+struct Timers {
+  bool on = false;
+  double total_ms[F_COUNT] = {0};
+  long long launches[F_COUNT] = {0};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> pool;
+  size_t pool_used = 0;
+};
+
+// Launch wrappers (implemented in the .cu files).  All are stream-ordered.
+void launch_beam_elements(cudaStream_t s, int n_beams, const double* x, const double* y,
+                          const double* z, const int32_t* conn, const double* A,
+                          const double* Iy, const double* Iz, const double* J,
+                          const double* E, const double* G, double* stage, DevFlags* flags);
+void launch_quad_elements(cudaStream_t s, int n_quads, const double* x, const double* y,
+                          const double* z, const int32_t* conn, const double* t,
+                          const double* E, const double* nu, double drill_alpha,
+                          double* stage, DevFlags* flags);
+void launch_assemble(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
+                     const int32_t* node_col, const int64_t* contrib_ptr,
+                     const int32_t* contrib, const double* stage, const uint8_t* fixed_mask,
+                     double* vals, double* dinv, DevFlags* flags);
+
+// PCG kernels
+int cg_grid();  // persistent grid size (multiple of the SM count)
+void launch_cg_init(cudaStream_t s, int ndof, const double* f, const uint8_t* fixed_mask,
+                    const double* dinv, double* fbc, double* x, double* r, double* p,
+                    double* partial, CgState* st, int warm, const double* Kx0);
+void launch_spmv_dot(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
+                     const int32_t* node_col, const double* vals, const double* p,
+                     double* q, double* partial, CgState* st);
+void launch_cg_update(cudaStream_t s, int ndof, const double* dinv, double* x, double* r,
+                      const double* p, const double* q, double* partial, CgState* st);
+void launch_cg_pupdate(cudaStream_t s, int ndof, const double* dinv, const double* r,
+                       double* p, CgState* st);
+void launch_spmv(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
+                 const int32_t* node_col, const double* vals, const double* x, double* y);
+void launch_residual_norm(cudaStream_t s, int ndof, const double* f, const double* Kx,
+                          double* partial, unsigned int* ticket, double* out);
+void launch_zero_fixed(cudaStream_t s, int ndof, const uint8_t* fixed_mask, double* x);
+
+// Gradient kernels
+void launch_beam_grad(cudaStream_t s, int n_beams, const double* x, const double* y,
+                      const double* z, const int32_t* conn, const double* A,
+                      const double* Iy, const double* Iz, const double* J, const double* E,
+                      const double* G, const double* u, double scale, double* slot_partial);
+void launch_quad_grad(cudaStream_t s, int n_beams, int n_quads, const double* x,
+                      const double* y, const double* z, const int32_t* conn, const double* t,
+                      const double* E, const double* nu, double drill_alpha, const double* u,
+                      double scale, double* slot_partial, double* dC_dt);
+void launch_node_reduce(cudaStream_t s, int n_nodes, const int64_t* inc_ptr,
+                        const int32_t* inc_slot, const double* slot_partial, double* dC_dxyz);
+void launch_dot(cudaStream_t s, int n, const double* a, const double* b, double scale,
+                double* partial, unsigned int* ticket, double* out);
+
+extern long long g_launches;  // launch counter (per process; handles add their own deltas)
+
+}  // namespace sso

@@ -1,0 +1,117 @@
+"""GPU parity at BASELINE.json's full size, in the bench's launch configuration.
+
+C3b (the "1M DOF" metric point, 408 x 408 quads, 1 003 686 DOF) is beyond the
+oracle's DOK + dense solve, so parity is checked on SAMPLED outputs the oracle
+computes one by one, and by properties that hold at any size:
+
+  * pattern: grid nnz closed form; sampled node rows bit-exact against the
+    brute-force neighbour set of their incident elements;
+  * K_e of sampled elements (incl. the last, ragged CTA) vs the oracle;
+  * CSR values of sampled node rows vs the oracle's per-node row sums
+    (oracle.assembly.node_rows) with supports applied;
+  * solve at the bench's rtol: residual f_bc - K u on sampled rows using the
+    oracle's rows, and the recomputed true residual;
+  * gradient at a seeded state (grad_at, both sides take the same u from
+    workloads.random_state): sampled element contributions and node sums vs
+    the oracle; translation invariance sum_n dC/dX_n = 0.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import assembly as OA, grad as OG
+
+pytestmark = pytest.mark.gpu
+
+RTOL_BENCH = 1e-10
+
+
+@pytest.fixture(scope="module")
+def c3b():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_2407_20026_b200 as sso
+    P = W.config3b()
+    m = sso.Model(P, rtol=RTOL_BENCH)
+    m.assemble()
+    return sso, P, m
+
+
+def sample_nodes(P, k=48, seed=0):
+    n = 408
+    nn = (n + 1) ** 2
+    rng = np.random.default_rng(seed)
+    fixed = [0, n, n * (n + 1), nn - 1, 1, n + 1, 2 * (n + 1) + 2, nn // 2]
+    return sorted(set(fixed) | set(rng.choice(nn, size=k, replace=False).tolist()))
+
+
+def test_pattern_full_size(c3b):
+    sso, P, m = c3b
+    n = 408
+    ndof, nnz, nblocks = m.sizes()
+    assert ndof == 6 * (n + 1) ** 2 == 1003686
+    assert nnz == 36 * ((n + 1) ** 2 + 4 * n * (n + 1) + 4 * n * n) == 54022500
+    rp, ci, _ = m.export_csr(values=False)
+    for nd in sample_nodes(P):
+        cols = sorted({6 * mm + b for e in OA.incident_elements(P, nd)
+                       for mm in OA.element_nodes(P, e) for b in range(6)})
+        for a in range(6):
+            r = 6 * nd + a
+            assert np.array_equal(ci[rp[r]:rp[r + 1]], np.array(cols, np.int32))
+
+
+def test_element_matrices_sampled(c3b):
+    sso, P, m = c3b
+    nq = len(P["quad_conn"])
+    rng = np.random.default_rng(1)
+    for e in sorted(set(rng.choice(nq, 24, replace=False).tolist()) | {0, nq - 1, nq - 2}):
+        ke = m.export_ke(e, 1)[0]
+        ref = OA.element_K(P, e)
+        assert np.linalg.norm(ke - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+def test_csr_values_and_residual_sampled(c3b):
+    sso, P, m = c3b
+    rp, ci, v = m.export_csr()
+    fixed = OA.fixed_dofs(P)
+    u, info = m.solve(P["f"])
+    assert info["status"] == 0
+    assert info["true_rel_res"] <= 1.5 * RTOL_BENCH
+    fbc = np.where(fixed, 0.0, P["f"])
+    fnorm = np.linalg.norm(fbc)
+    for nd in sample_nodes(P, seed=2):
+        rows = OA.node_rows(P, nd)
+        for a in range(6):
+            r = 6 * nd + a
+            ref = np.array([rows[c][a] for c in ci[rp[r]:rp[r + 1]]])
+            for k, c in enumerate(ci[rp[r]:rp[r + 1]]):
+                if fixed[r] or fixed[c]:
+                    ref[k] = (ref[k] if ref[k] != 0.0 else 1.0) if c == r else 0.0
+            got = v[rp[r]:rp[r + 1]]
+            assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+            # residual of the GPU u with the ORACLE's row
+            res = fbc[r] - float(ref @ u[ci[rp[r]:rp[r + 1]]])
+            assert abs(res) <= RTOL_BENCH * fnorm * 1.5 + 1e-13 * float(np.abs(ref) @ np.abs(u[ci[rp[r]:rp[r + 1]]]))
+
+
+def test_gradient_sampled_at_seeded_state(c3b):
+    sso, P, m = c3b
+    nn = len(P["x"])
+    u = W.random_state(nn, seed=7)
+    Cv, dX, dT = m.grad_at(P["f"], u)
+    assert Cv == pytest.approx(float(P["f"] @ u), rel=1e-12)
+    scale = np.abs(dX).max()
+    assert np.abs(dX.sum(axis=1)).max() <= 1e-9 * scale * np.sqrt(nn)
+    X = OA.coords(P)
+    rng = np.random.default_rng(3)
+    nq = len(P["quad_conn"])
+    for e in rng.choice(nq, 12, replace=False):
+        gx, gt = OG.element_grad(P, int(e), u, 1.0, X)
+        assert abs(dT[e] - gt) <= 1e-7 * max(abs(gt), 1e-3 * np.abs(dT).max())
+    for nd in sample_nodes(P, k=6, seed=4)[:10]:
+        ref = np.zeros(3)
+        for e in OA.incident_elements(P, nd):
+            gx, _ = OG.element_grad(P, e, u, 1.0, X)
+            ref += gx[OA.element_nodes(P, e).index(nd)]
+        for a in range(3):
+            assert abs(dX[a, nd] - ref[a]) <= 1e-7 * max(abs(ref[a]), 1e-3 * scale)

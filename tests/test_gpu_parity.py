@@ -1,0 +1,253 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs (SURVEY.md §8(c) C8 tolerances, BASELINE.json north_star):
+
+  pattern / indices   bit-exact
+  K_e                 |dK_e|_F <= 1e-13 |K_e|_F
+  CSR values          |dv| <= 1e-13 max|row|
+  u                   |u - u_ref|_2 <= 1e-9 |u_ref|_2
+  C                   |dC| <= 1e-10 |C|
+  gradients           |dg_i| <= 1e-7 max(|g_ref,i|, 1e-3 |g_ref|_inf)
+
+Sizes span several CTAs with ragged tails (8 quads / 32 beams per element
+CTA; 8 nodes per SpMV CTA).
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import assembly as OA, grad as OG
+
+pytestmark = pytest.mark.gpu
+
+TOL_KE, TOL_VAL, TOL_U, TOL_C, TOL_G = 1e-13, 1e-13, 1e-9, 1e-10, 1e-7
+
+
+@pytest.fixture(scope="module")
+def sso():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_2407_20026_b200 as m
+    return m
+
+
+def ragged_shell(nx=7, ny=5, seed=3):
+    """Non-square ragged grid (35 quads: 4 full element CTAs + a tail of 3)."""
+    rng = np.random.default_rng(seed)
+    L = 3.0
+    xs = np.arange(nx + 1) * L / nx
+    ys = np.arange(ny + 1) * L / ny
+    x = np.tile(xs, ny + 1)
+    y = np.repeat(ys, nx + 1)
+    z = 0.4 * np.sin(x) * np.cos(y) + rng.uniform(-0.02, 0.02, x.size)
+    conn = []
+    for j in range(ny):
+        for i in range(nx):
+            a = j * (nx + 1) + i
+            conn.append([a, a + 1, a + nx + 2, a + nx + 1])
+    conn = np.array(conn, np.int32)
+    nq = len(conn)
+    f = rng.uniform(-1e3, 1e3, 6 * x.size)
+    sn = [k for k in range(x.size) if y[k] == 0.0]
+    return W._problem("ragged", x, y, z, quad_conn=conn, t=rng.uniform(0.05, 0.2, nq),
+                      E=np.full(nq, 30e9), nu=np.full(nq, 0.2), sup_node=sn,
+                      sup_mask=[W.CLAMPED] * len(sn), f=f)
+
+
+def mixed():
+    P = W.tiny_shell(3, seed=7)
+    P["beam_conn"] = np.array([[0, 1], [1, 2], [2, 3], [0, 4], [4, 8]], np.int32)
+    nb = 5
+    P["A"], P["Iy"], P["Iz"], P["J"] = (np.full(nb, 1e-3), np.full(nb, 2e-6), np.full(nb, 1e-6),
+                                        np.full(nb, 2e-6))
+    P["E"] = np.concatenate([np.full(nb, 210e9), P["E"]])
+    P["nu"] = np.concatenate([np.full(nb, 0.3), P["nu"]])
+    return P
+
+
+PROBLEMS = {
+    "C1": W.config1,
+    "C2": W.config2,
+    "tiny2": lambda: W.tiny_shell(2, 0),
+    "tiny3edge": lambda: W.tiny_shell(3, 1, supports="edge"),
+    "beamgrid": lambda: W.tiny_beam_grid(0),
+    "ragged": ragged_shell,
+    "mixed": mixed,
+}
+
+
+@pytest.fixture(scope="module")
+def cases():
+    return {}
+
+
+def oracle_case(cases, name):
+    if name not in cases:
+        P = PROBLEMS[name]()
+        nd = 6 * len(P["x"])
+        dok = OA.assemble_dok(P)
+        rp, ci, v = OA.csr_from_dok(dok, nd)
+        fixed = OA.fixed_dofs(P)
+        vbc = OA.apply_supports_csr(rp, ci, v, fixed)
+        u, Kb, fb = OG.evaluate(P, "cholesky")
+        cases[name] = dict(P=P, rp=rp, ci=ci, v=v, vbc=vbc, u=u, fixed=fixed)
+    return cases[name]
+
+
+@pytest.mark.parametrize("name", list(PROBLEMS))
+def test_pattern_bit_exact(sso, cases, name):
+    c = oracle_case(cases, name)
+    m = sso.Model(c["P"])
+    rp, ci, _ = m.export_csr(values=False)
+    assert np.array_equal(rp, c["rp"])
+    assert np.array_equal(ci, c["ci"])
+    assert np.array_equal(m.export_scatter(), np.concatenate(
+        [np.asarray(r, np.int32) for r in OA.block_rank(c["P"])]) if len(OA.block_rank(c["P"])) else [])
+
+
+@pytest.mark.parametrize("name", list(PROBLEMS))
+def test_element_matrices(sso, cases, name):
+    c = oracle_case(cases, name)
+    P = c["P"]
+    m = sso.Model(P)
+    m.assemble()
+    nb, nq = len(P["beam_conn"]), len(P["quad_conn"])
+    for first, count in ((0, nb), (nb, nq)):
+        if count == 0:
+            continue
+        ke = m.export_ke(first, count)
+        for k in range(count):
+            ref = OA.element_K(P, first + k)
+            assert np.linalg.norm(ke[k] - ref) <= TOL_KE * np.linalg.norm(ref), (first + k)
+
+
+@pytest.mark.parametrize("name", list(PROBLEMS))
+def test_csr_values_with_supports(sso, cases, name):
+    c = oracle_case(cases, name)
+    m = sso.Model(c["P"])
+    m.assemble()
+    _, _, v = m.export_csr()
+    rp = c["rp"]
+    ref = c["vbc"]
+    for r in range(len(rp) - 1):
+        seg = slice(rp[r], rp[r + 1])
+        scale = np.abs(ref[seg]).max()
+        assert np.abs(v[seg] - ref[seg]).max() <= TOL_VAL * scale, r
+    dinv = m.export_dinv()
+    diag = np.array([ref[rp[r] + np.searchsorted(c["ci"][rp[r]:rp[r + 1]], r)] for r in range(len(rp) - 1)])
+    assert np.allclose(dinv, 1.0 / diag, rtol=1e-15, atol=0)
+
+
+@pytest.mark.parametrize("name", list(PROBLEMS))
+def test_solve_and_gradient(sso, cases, name):
+    c = oracle_case(cases, name)
+    P = c["P"]
+    m = sso.Model(P, rtol=1e-12)
+    m.assemble()
+    u, info = m.solve(P["f"])
+    assert info["status"] == 0 and info["true_rel_res"] < 1e-11
+    uref = c["u"]
+    assert np.linalg.norm(u - uref) <= TOL_U * np.linalg.norm(uref)
+    for obj, s in ((sso.OBJ_COMPLIANCE, 1.0), (sso.OBJ_STRAIN_ENERGY, 0.5)):
+        Cv, dX, dT = m.grad(obj)
+        Cref = OG.compliance(P["f"], uref, s)
+        assert abs(Cv - Cref) <= TOL_C * abs(Cref)
+    # gradient parity at the oracle's own state (grad_at): isolates stage A4 exactly
+    Cv, dX, dT = m.grad_at(P["f"], uref, sso.OBJ_COMPLIANCE)
+    gX, gT = OG.adjoint_gradient(P, uref, 1.0)
+    floor = 1e-3 * np.abs(gX).max()
+    assert np.all(np.abs(dX - gX) <= TOL_G * np.maximum(np.abs(gX), floor))
+    if len(P["quad_conn"]):
+        floor = 1e-3 * np.abs(gT).max()
+        assert np.all(np.abs(dT - gT) <= TOL_G * np.maximum(np.abs(gT), floor))
+    # and through the solved state
+    Cv, dX2, _ = m.grad(sso.OBJ_COMPLIANCE)
+    floor = 1e-3 * np.abs(gX).max()
+    assert np.all(np.abs(dX2 - gX) <= 1e-6 * np.maximum(np.abs(gX), floor))
+
+
+def test_determinism_and_scaling(sso):
+    P = W.config2()
+    m = sso.Model(P, rtol=1e-12)
+    m.assemble()
+    u1, i1 = m.solve(P["f"])
+    u2, i2 = m.solve(P["f"])
+    assert np.array_equal(u1, u2) and i1["iters"] == i2["iters"]
+    g1 = m.grad()
+    g2 = m.grad()
+    assert np.array_equal(g1[1], g2[1]) and np.array_equal(g1[2], g2[2])
+    u3, _ = m.solve(2.0 * P["f"])
+    assert np.array_equal(u3, 2.0 * u1)
+    m2 = sso.Model(dict(P, E=2.0 * P["E"]), rtol=1e-12)
+    m2.assemble()
+    u4, _ = m2.solve(P["f"])
+    assert np.array_equal(u4, 0.5 * u1)
+
+
+def test_device_pointers_and_warm_start(sso):
+    import torch
+    P = W.config2()
+    m = sso.Model(P, rtol=1e-12)
+    m.assemble()
+    u_h, info_h = m.solve(P["f"])
+    f_d = torch.from_numpy(P["f"]).cuda()
+    u_d, info_d = m.solve(f_d)
+    assert np.array_equal(u_d.cpu().numpy(), u_h)
+    Cd, dXd, dTd = m.grad()
+    Ch, dXh, dTh = m.grad_at(P["f"], u_h)
+    assert float(Cd[0]) == Ch
+    assert np.array_equal(dXd.cpu().numpy(), dXh)
+    mw = sso.Model(P, rtol=1e-12, warm_start=True)
+    mw.assemble()
+    u0 = torch.from_numpy(u_h).cuda().clone()
+    u_w, info_w = mw.solve(f_d, u0)
+    assert info_w["iters"] <= 2
+    assert np.linalg.norm(u_w.cpu().numpy() - u_h) <= 1e-10 * np.linalg.norm(u_h)
+
+
+def test_numeric_errors(sso):
+    import paper_2407_20026_b200.api as A
+    # isolated node -> zero diagonal on a free DOF -> SINGULAR naming the node
+    P = W.tiny_shell(2, 0)
+    Q = dict(P, x=np.append(P["x"], 5.0), y=np.append(P["y"], 5.0), z=np.append(P["z"], 0.0),
+             f=np.append(P["f"], np.zeros(6)))
+    m = sso.Model(Q)
+    with pytest.raises(A.SSOError) as ei:
+        m.assemble()
+    assert ei.value.code == A.SSO_E_SINGULAR and "node 9" in str(ei.value)
+    # degenerate quad via set_design (collapsed element) -> DEGENERATE
+    m = sso.Model(P)
+    x = P["x"].copy()
+    y = P["y"].copy()
+    x[4], y[4] = x[0], y[0]
+    m.set_design(x=x, y=y)
+    with pytest.raises(A.SSOError) as ei:
+        m.assemble()
+    assert ei.value.code == A.SSO_E_DEGENERATE
+    # call order
+    m = sso.Model(P)
+    with pytest.raises(A.SSOError) as ei:
+        m.solve(P["f"])
+    assert ei.value.code == A.SSO_E_STATE
+    # max_iter -> NOT_CONVERGED with the last iterate returned
+    m = sso.Model(W.config2(), max_iter=5, check_every=4)
+    m.assemble()
+    u, info = m.solve(W.config2()["f"], raise_on_error=False)
+    assert info["status"] == A.SSO_E_NOT_CONVERGED and info["iters"] == 5
+    # zero load -> u = 0 immediately
+    m = sso.Model(P)
+    m.assemble()
+    u, info = m.solve(np.zeros(m.ndof))
+    assert info["iters"] == 0 and not np.any(u)
+
+
+def test_set_design_matches_fresh_model(sso):
+    P = W.config2()
+    Q = dict(P, z=P["z"] * 1.1, t=P["t"] * 0.9)
+    m = sso.Model(P, rtol=1e-12)
+    m.set_design(z=Q["z"], t=Q["t"])
+    m.assemble()
+    u1, _ = m.solve(P["f"])
+    m2 = sso.Model(Q, rtol=1e-12)
+    m2.assemble()
+    u2, _ = m2.solve(P["f"])
+    assert np.array_equal(u1, u2)

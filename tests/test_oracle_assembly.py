@@ -149,3 +149,17 @@ def test_supports_elimination():
         for k in range(row_ptr[r], row_ptr[r + 1]):
             Kd[r, col_idx[k]] = v2[k]
     assert np.array_equal(Kd, Kb)
+
+
+@pytest.mark.parametrize("name", ["shell3", "mixed"])
+def test_node_rows_equal_dok(name):
+    P = PROBLEMS[name]()
+    nd = 6 * len(P["x"])
+    K = A.dense_from_dok(A.assemble_dok(P), nd)
+    for n in range(len(P["x"])):
+        rows = A.node_rows(P, n)
+        got = np.zeros((6, nd))
+        for col, v in rows.items():
+            got[:, col] = v
+        assert np.abs(got - K[6 * n:6 * n + 6]).max() <= 1e-15 * np.abs(K).max() * 4
+        assert set(rows) == set(np.nonzero(np.any(K[6 * n:6 * n + 6] != 0, axis=0))[0]) | set(rows)
