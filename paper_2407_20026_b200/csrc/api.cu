@@ -91,6 +91,16 @@ static std::string g_create_err;
     }                                                                                \
   } while (0)
 
+#define CKL(h)                                                                          \
+  do {                                                                                  \
+    cudaError_t e_ = cudaGetLastError();                                                \
+    if (e_ != cudaSuccess) {                                                            \
+      (h)->err = std::string("CUDA launch error: ") + cudaGetErrorString(e_) + " (" +    \
+                 last_launch_error() + ")";                                             \
+      return SSO_E_CUDA;                                                                \
+    }                                                                                   \
+  } while (0)
+
 namespace {
 
 template <class T>
@@ -513,7 +523,7 @@ int sso_assemble(sso_handle h) {
     launch_assemble(h->stream, h->n_nodes, h->node_ptr, h->node_col, h->contrib_ptr, h->contrib,
                     h->stage, h->fixed_mask, h->vals, h->dinv, h->flags);
   }
-  CK(h, cudaGetLastError());
+  CKL(h);
   rc = check_flags(h);
   if (rc) return rc;
   h->assembled = true;
@@ -607,7 +617,7 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
   CK(h, cudaMemcpyAsync(h->h_st, h->st, sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
   if ((rc = copy_out(h, u, h->xs, h->ndof))) return rc;
   if ((rc = sync(h))) return rc;
-  CK(h, cudaGetLastError());
+  CKL(h);
   const CgState& S = *h->h_st;
   int status = S.done ? S.status : SSO_E_NOT_CONVERGED;
   if (info) {
@@ -650,7 +660,7 @@ static int grad_impl(sso_ctx* h, sso_objective obj, const double* dF, const doub
     Scope sc(h, F_REDUCE);
     launch_node_reduce(h->stream, h->n_nodes, h->inc_ptr, h->inc_slot, h->slot_partial, h->dxyz);
   }
-  CK(h, cudaGetLastError());
+  CKL(h);
   int rc;
   if (C) {
     CK(h, cudaMemcpyAsync(h->h_scal + 1, h->scal + 1, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -694,7 +704,7 @@ int sso_spmv(sso_handle h, const double* xin, double* yout) {
     Scope sc(h, F_SPMV);
     launch_spmv(h->stream, h->n_nodes, h->node_ptr, h->node_col, h->vals, h->gu, h->tmp);
   }
-  CK(h, cudaGetLastError());
+  CKL(h);
   if ((rc = copy_out(h, yout, h->tmp, h->ndof))) return rc;
   return sync(h);
 }

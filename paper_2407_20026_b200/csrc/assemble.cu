@@ -79,7 +79,7 @@ void launch_assemble(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
   assemble_kernel<<<grid, 32 * warps_per_cta, 0, s>>>(n_nodes, node_ptr, node_col, contrib_ptr,
                                                        contrib, stage, fixed_mask, vals, dinv,
                                                        flags);
-  ++g_launches;
+  SSO_POST_LAUNCH("assemble_kernel");
 }
 
 }  // namespace sso

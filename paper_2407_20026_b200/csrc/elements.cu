@@ -378,7 +378,7 @@ void launch_quad_elements(cudaStream_t s, int n_quads, const double* x, const do
   const int grid = (n_quads + QUADS_PER_CTA - 1) / QUADS_PER_CTA;
   quad_element_kernel<<<grid, 128, 0, s>>>(n_quads, x, y, z, conn, t, E, nu, drill_alpha, stage,
                                            flags);
-  ++g_launches;
+  SSO_POST_LAUNCH("quad_element_kernel");
 }
 
 void launch_beam_elements(cudaStream_t s, int n_beams, const double* x, const double* y,
@@ -389,7 +389,7 @@ void launch_beam_elements(cudaStream_t s, int n_beams, const double* x, const do
   const int grid = (n_beams + BEAMS_PER_CTA - 1) / BEAMS_PER_CTA;
   beam_element_kernel<<<grid, 128, 0, s>>>(n_beams, x, y, z, conn, A, Iy, Iz, J, E, G, stage,
                                            flags);
-  ++g_launches;
+  SSO_POST_LAUNCH("beam_element_kernel");
 }
 
 }  // namespace sso

@@ -329,7 +329,7 @@ void launch_quad_grad(cudaStream_t s, int n_beams, int n_quads, const double* x,
   const int grid = (int)((threads + 127) / 128);
   quad_grad_kernel<<<grid, 128, 0, s>>>(n_beams, n_quads, x, y, z, conn, t, E, nu, drill_alpha, u,
                                         scale, slot_partial, dC_dt);
-  ++g_launches;
+  SSO_POST_LAUNCH("quad_grad_kernel");
 }
 
 void launch_beam_grad(cudaStream_t s, int n_beams, const double* x, const double* y,
@@ -341,7 +341,7 @@ void launch_beam_grad(cudaStream_t s, int n_beams, const double* x, const double
   const int grid = (int)((threads + 127) / 128);
   beam_grad_kernel<<<grid, 128, 0, s>>>(n_beams, x, y, z, conn, A, Iy, Iz, J, E, G, u, scale,
                                         slot_partial);
-  ++g_launches;
+  SSO_POST_LAUNCH("beam_grad_kernel");
 }
 
 void launch_node_reduce(cudaStream_t s, int n_nodes, const int64_t* inc_ptr, const int32_t* inc_slot,
@@ -350,7 +350,7 @@ void launch_node_reduce(cudaStream_t s, int n_nodes, const int64_t* inc_ptr, con
   int64_t need = ((int64_t)n_nodes + 255) / 256;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)cg_grid()));
   node_reduce_kernel<<<grid, 256, 0, s>>>(n_nodes, inc_ptr, inc_slot, slot_partial, dC_dxyz);
-  ++g_launches;
+  SSO_POST_LAUNCH("node_reduce_kernel");
 }
 
 }  // namespace sso

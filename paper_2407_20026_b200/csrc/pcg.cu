@@ -23,12 +23,18 @@
 // row sums.  Column indices are read per 6x6 block (4 B / 36 values) instead
 // of per value (4 B / value): 8.1 B per non-zero instead of 12.
 #include <climits>
+#include <cstdio>
 
 #include "sso_internal.h"
 
 namespace sso {
 
 long long g_launches = 0;
+static char g_launch_err[256] = {0};
+void note_launch_error(const char* name, cudaError_t e) {
+  if (!g_launch_err[0]) snprintf(g_launch_err, sizeof g_launch_err, "%s: %s", name, cudaGetErrorString(e));
+}
+const char* last_launch_error() { return g_launch_err; }
 
 namespace {
 
@@ -332,12 +338,12 @@ void launch_cg_init(cudaStream_t s, int ndof, const double* f, const uint8_t* fi
                     double* partial, CgState* st, int warm, const double* Kx0) {
   cg_init_kernel<<<vec_grid(ndof), 256, 0, s>>>(ndof, f, fixed_mask, dinv, fbc, x, r, p, partial,
                                                 st, warm, Kx0);
-  ++g_launches;
+  SSO_POST_LAUNCH("cg_init_kernel");
 }
 
 void launch_zero_fixed(cudaStream_t s, int ndof, const uint8_t* fixed_mask, double* x) {
   zero_fixed_kernel<<<vec_grid(ndof), 256, 0, s>>>(ndof, fixed_mask, x);
-  ++g_launches;
+  SSO_POST_LAUNCH("zero_fixed_kernel");
 }
 
 void launch_spmv_dot(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
@@ -346,7 +352,7 @@ void launch_spmv_dot(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
   int64_t need = ((int64_t)n_nodes + 7) / 8;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)cg_grid()));
   spmv_dot_kernel<<<grid, 256, 0, s>>>(n_nodes, node_ptr, node_col, vals, p, q, partial, st);
-  ++g_launches;
+  SSO_POST_LAUNCH("spmv_dot_kernel");
 }
 
 void launch_spmv(cudaStream_t s, int n_nodes, const int64_t* node_ptr, const int32_t* node_col,
@@ -354,31 +360,31 @@ void launch_spmv(cudaStream_t s, int n_nodes, const int64_t* node_ptr, const int
   int64_t need = ((int64_t)n_nodes + 7) / 8;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)cg_grid()));
   spmv_kernel<<<grid, 256, 0, s>>>(n_nodes, node_ptr, node_col, vals, x, y);
-  ++g_launches;
+  SSO_POST_LAUNCH("spmv_kernel");
 }
 
 void launch_cg_update(cudaStream_t s, int ndof, const double* dinv, double* x, double* r,
                       const double* p, const double* q, double* partial, CgState* st) {
   cg_update_kernel<<<vec_grid(ndof), 256, 0, s>>>(ndof, dinv, x, r, p, q, partial, st);
-  ++g_launches;
+  SSO_POST_LAUNCH("cg_update_kernel");
 }
 
 void launch_cg_pupdate(cudaStream_t s, int ndof, const double* dinv, const double* r, double* p,
                        CgState* st) {
   cg_pupdate_kernel<<<vec_grid(ndof), 256, 0, s>>>(ndof, dinv, r, p, st);
-  ++g_launches;
+  SSO_POST_LAUNCH("cg_pupdate_kernel");
 }
 
 void launch_residual_norm(cudaStream_t s, int ndof, const double* f, const double* Kx,
                           double* partial, unsigned int* ticket, double* out) {
   residual_kernel<<<vec_grid(ndof), 256, 0, s>>>(ndof, f, Kx, partial, ticket, out);
-  ++g_launches;
+  SSO_POST_LAUNCH("residual_kernel");
 }
 
 void launch_dot(cudaStream_t s, int n, const double* a, const double* b, double scale,
                 double* partial, unsigned int* ticket, double* out) {
   dot_kernel<<<vec_grid(n), 256, 0, s>>>(n, a, b, scale, partial, ticket, out);
-  ++g_launches;
+  SSO_POST_LAUNCH("dot_kernel");
 }
 
 }  // namespace sso

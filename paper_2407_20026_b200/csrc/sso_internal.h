@@ -119,4 +119,15 @@ void launch_dot(cudaStream_t s, int n, const double* a, const double* b, double 
 
 extern long long g_launches;  // launch counter (per process; handles add their own deltas)
 
+// After every launch: count it and report a launch-configuration error by name
+// (the error stays pending for the caller's cudaGetLastError check).
+#define SSO_POST_LAUNCH(name)                                                         \
+  do {                                                                                \
+    ++::sso::g_launches;                                                              \
+    cudaError_t e__ = cudaPeekAtLastError();                                          \
+    if (e__ != cudaSuccess) ::sso::note_launch_error(name, e__);                      \
+  } while (0)
+void note_launch_error(const char* name, cudaError_t e);
+const char* last_launch_error();
+
 }  // namespace sso
