@@ -64,7 +64,6 @@ struct sso_ctx {
 
   bool assembled = false, solved = false;
   cudaGraphExec_t chunk_exec = nullptr;
-  bool chunk_profiled = false;
   long long kernels_per_chunk = 0;
   std::vector<cudaEvent_t> chunk_ev;  // profiling: 2 per iteration
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_done[2] = {nullptr, nullptr};
@@ -185,6 +184,8 @@ void flush_timers(sso_ctx* h) {
     if (cudaEventElapsedTime(&ms, pe.second.first, pe.second.second) == cudaSuccess) {
       T.total_ms[pe.first] += ms;
       T.launches[pe.first] += 1;
+    } else {
+      (void)cudaGetLastError();  // never leave a timing failure pending for a later check
     }
   }
   T.pending.clear();
@@ -234,21 +235,11 @@ int build_chunk_graph(sso_ctx* h) {
     h->chunk_exec = nullptr;
   }
   const int K = h->check_every;
-  const bool prof = h->tm.on;
-  if (prof && (int)h->chunk_ev.size() < 2 * K) {
-    for (int i = (int)h->chunk_ev.size(); i < 2 * K; ++i) {
-      cudaEvent_t e;
-      CK(h, cudaEventCreate(&e));
-      h->chunk_ev.push_back(e);
-    }
-  }
   long long g0 = g_launches;
   CK(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
   for (int i = 0; i < K; ++i) {
-    if (prof) cudaEventRecord(h->chunk_ev[2 * i], h->cap_stream);
     launch_spmv_dot(h->cap_stream, h->n_nodes, h->node_ptr, h->node_col, h->vals, h->p, h->q,
                     h->partial, h->st);
-    if (prof) cudaEventRecord(h->chunk_ev[2 * i + 1], h->cap_stream);
     launch_cg_update(h->cap_stream, (int)h->ndof, h->dinv, h->xs, h->r, h->p, h->q, h->partial, h->st);
     launch_cg_pupdate(h->cap_stream, (int)h->ndof, h->dinv, h->r, h->p, h->st);
   }
@@ -266,7 +257,6 @@ int build_chunk_graph(sso_ctx* h) {
     h->err = std::string("graph instantiate failed: ") + cudaGetErrorString(e);
     return SSO_E_CUDA;
   }
-  h->chunk_profiled = prof;
   return SSO_OK;
 }
 
@@ -559,18 +549,39 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
     launch_cg_init(h->stream, (int)h->ndof, h->f, h->fixed_mask, h->dinv, h->fbc, h->xs, h->r, h->p,
                    h->partial, h->st, warm, h->tmp);
   }
-  if (!h->chunk_exec || h->chunk_profiled != h->tm.on) {
+  const bool prof = h->tm.on;
+  if (!prof && !h->chunk_exec) {
     if ((rc = build_chunk_graph(h))) return rc;
+  }
+  if (prof && (int)h->chunk_ev.size() < 2 * h->check_every) {
+    for (int i = (int)h->chunk_ev.size(); i < 2 * h->check_every; ++i) {
+      cudaEvent_t e;
+      CK(h, cudaEventCreate(&e));
+      h->chunk_ev.push_back(e);
+    }
   }
   // Chunked device-side loop: every chunk replays check_every iterations; kernels
   // after convergence return immediately.  Without profiling one chunk is kept in
-  // flight ahead of the flag being polled.
-  const bool prof = h->tm.on;
+  // flight ahead of the flag being polled.  With profiling on, the same kernels are
+  // launched directly (no graph) with CUDA events around every SpMV.
   const int64_t max_chunks = (h->max_iter + h->check_every - 1) / h->check_every + 1;
   int64_t launched = 0;
   auto launch_chunk = [&](int slot) -> int {
-    CK(h, cudaGraphLaunch(h->chunk_exec, h->stream));
-    h->launches += h->kernels_per_chunk;
+    if (!prof) {
+      CK(h, cudaGraphLaunch(h->chunk_exec, h->stream));
+      h->launches += h->kernels_per_chunk;
+    } else {
+      long long g0 = g_launches;
+      for (int i = 0; i < h->check_every; ++i) {
+        CK(h, cudaEventRecord(h->chunk_ev[2 * i], h->stream));
+        launch_spmv_dot(h->stream, h->n_nodes, h->node_ptr, h->node_col, h->vals, h->p, h->q,
+                        h->partial, h->st);
+        CK(h, cudaEventRecord(h->chunk_ev[2 * i + 1], h->stream));
+        launch_cg_update(h->stream, (int)h->ndof, h->dinv, h->xs, h->r, h->p, h->q, h->partial, h->st);
+        launch_cg_pupdate(h->stream, (int)h->ndof, h->dinv, h->r, h->p, h->st);
+      }
+      h->launches += g_launches - g0;
+    }
     CK(h, cudaMemcpyAsync(&h->h_done[slot], &h->st->done, sizeof(int), cudaMemcpyDeviceToHost,
                           h->stream));
     CK(h, cudaEventRecord(h->ev_done[slot], h->stream));
@@ -597,10 +608,9 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
       iters_before = h->h_st->iter;
       for (long long i = 0; i < std::min<long long>(ran, h->check_every); ++i) {
         float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, h->chunk_ev[2 * i], h->chunk_ev[2 * i + 1]) == cudaSuccess) {
-          h->tm.total_ms[F_SPMV] += ms;
-          h->tm.launches[F_SPMV] += 1;
-        }
+        CK(h, cudaEventElapsedTime(&ms, h->chunk_ev[2 * i], h->chunk_ev[2 * i + 1]));
+        h->tm.total_ms[F_SPMV] += ms;
+        h->tm.launches[F_SPMV] += 1;
       }
       if (h->h_done[0] || launched >= max_chunks) break;
     }
@@ -625,7 +635,7 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
     info->rel_res = S.ff > 0 ? std::sqrt(S.rr / S.ff) : 0.0;
     info->true_rel_res = S.ff > 0 ? std::sqrt(h->h_scal[0] / S.ff) : 0.0;
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, h->ev_a, h->ev_b);
+    if (cudaEventElapsedTime(&ms, h->ev_a, h->ev_b) != cudaSuccess) (void)cudaGetLastError();
     info->ms = ms;
     info->status = status;
   }

@@ -134,7 +134,7 @@ def test_csr_values_with_supports(sso, cases, name):
         assert np.abs(v[seg] - ref[seg]).max() <= TOL_VAL * scale, r
     dinv = m.export_dinv()
     diag = np.array([ref[rp[r] + np.searchsorted(c["ci"][rp[r]:rp[r + 1]], r)] for r in range(len(rp) - 1)])
-    assert np.allclose(dinv, 1.0 / diag, rtol=1e-15, atol=0)
+    assert np.allclose(dinv, 1.0 / diag, rtol=1e-13, atol=0)
 
 
 @pytest.mark.parametrize("name", list(PROBLEMS))
@@ -194,8 +194,8 @@ def test_device_pointers_and_warm_start(sso):
     assert np.array_equal(u_d.cpu().numpy(), u_h)
     Cd, dXd, dTd = m.grad()
     Ch, dXh, dTh = m.grad_at(P["f"], u_h)
-    assert float(Cd[0]) == Ch
-    assert np.array_equal(dXd.cpu().numpy(), dXh)
+    assert Cd == Ch
+    assert np.array_equal(dXd, dXh)
     mw = sso.Model(P, rtol=1e-12, warm_start=True)
     mw.assemble()
     u0 = torch.from_numpy(u_h).cuda().clone()
@@ -218,8 +218,9 @@ def test_numeric_errors(sso):
     m = sso.Model(P)
     x = P["x"].copy()
     y = P["y"].copy()
-    x[4], y[4] = x[0], y[0]
-    m.set_design(x=x, y=y)
+    z = P["z"].copy()
+    x[4], y[4], z[4] = x[0], y[0], z[0]
+    m.set_design(x=x, y=y, z=z)
     with pytest.raises(A.SSOError) as ei:
         m.assemble()
     assert ei.value.code == A.SSO_E_DEGENERATE
