@@ -174,9 +174,12 @@ int sso_export_scatter(sso_handle h, int32_t* block_rank);
 int sso_export_ke(sso_handle h, int64_t first, int64_t count, double* ke);
 int sso_export_dinv(sso_handle h, double* dinv);
 
-/* Kernel timing (CUDA events recorded on the handle's stream around every launch of
- * the named kernel family while enabled).  names: "element", "assemble", "spmv",
- * "update", "grad", "reduce".  total_ms and launches accumulate since the last reset. */
+/* Kernel timing with CUDA events recorded on the handle's stream while enabled.
+ * names: "element", "assemble", "spmv", "update", "grad", "reduce".  Outside the
+ * CG loop every launch of the family is bracketed; inside sso_solve's CG loop
+ * (graph replays) every 16th SpMV launch is bracketed by event nodes (a live
+ * sample; the cost stays below 0.5 % of the solve).  total_ms and launches cover
+ * the timed launches and accumulate since the last reset. */
 int sso_profile_enable(sso_handle h, int32_t on);
 int sso_profile_read(sso_handle h, const char* name, double* total_ms, int64_t* launches);
 int sso_profile_reset(sso_handle h);

@@ -59,13 +59,14 @@ struct sso_ctx {
   // pinned host mirrors
   CgState* h_st = nullptr;
   double* h_scal = nullptr;
-  int* h_done = nullptr;  // [2] polled flags
+  CgState* h_chunk = nullptr;  // [2] pinned per-chunk state snapshots (polled)
   DevFlags* h_flags = nullptr;
 
   bool assembled = false, solved = false;
-  cudaGraphExec_t chunk_exec = nullptr;
+  cudaGraphExec_t chunk_exec = nullptr;   // K CG iterations
+  cudaGraphExec_t prof_exec[2] = {nullptr, nullptr};  // same, with SpMV event nodes (slot 0/1)
   long long kernels_per_chunk = 0;
-  std::vector<cudaEvent_t> chunk_ev;  // profiling: 2 per iteration
+  std::vector<cudaEvent_t> chunk_ev[2];   // profiling: 2 per iteration per slot
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_done[2] = {nullptr, nullptr};
 
   Timers tm;
@@ -229,17 +230,34 @@ int reset_flags(sso_ctx* h) {
   return SSO_OK;
 }
 
-int build_chunk_graph(sso_ctx* h) {
-  if (h->chunk_exec) {
-    cudaGraphExecDestroy(h->chunk_exec);
-    h->chunk_exec = nullptr;
+// Capture K = check_every CG iterations into a graph.  prof_slot >= 0 adds
+// external event-record nodes around every PROF_EVERY-th SpMV (events of that
+// slot): a live sample of the SpMV launch duration that costs < 0.5 % of the step.
+constexpr int PROF_EVERY = 16;
+int build_chunk_graph(sso_ctx* h, int prof_slot, cudaGraphExec_t* out) {
+  if (*out) {
+    cudaGraphExecDestroy(*out);
+    *out = nullptr;
   }
   const int K = h->check_every;
+  if (prof_slot >= 0) {
+    auto& ev = h->chunk_ev[prof_slot];
+    while ((int)ev.size() < 2 * K) {
+      cudaEvent_t e;
+      CK(h, cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+  }
   long long g0 = g_launches;
   CK(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
   for (int i = 0; i < K; ++i) {
+    const bool rec = prof_slot >= 0 && (i % PROF_EVERY) == 0;
+    if (rec)
+      cudaEventRecordWithFlags(h->chunk_ev[prof_slot][2 * i], h->cap_stream, cudaEventRecordExternal);
     launch_spmv_dot(h->cap_stream, h->n_nodes, h->node_ptr, h->node_col, h->vals, h->p, h->q,
                     h->partial, h->st);
+    if (rec)
+      cudaEventRecordWithFlags(h->chunk_ev[prof_slot][2 * i + 1], h->cap_stream, cudaEventRecordExternal);
     launch_cg_update(h->cap_stream, (int)h->ndof, h->dinv, h->xs, h->r, h->p, h->q, h->partial, h->st);
     launch_cg_pupdate(h->cap_stream, (int)h->ndof, h->dinv, h->r, h->p, h->st);
   }
@@ -251,7 +269,7 @@ int build_chunk_graph(sso_ctx* h) {
     h->err = std::string("graph capture failed: ") + cudaGetErrorString(e);
     return SSO_E_CUDA;
   }
-  e = cudaGraphInstantiate(&h->chunk_exec, g, 0);
+  e = cudaGraphInstantiate(out, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) {
     h->err = std::string("graph instantiate failed: ") + cudaGetErrorString(e);
@@ -270,10 +288,13 @@ int free_all(sso_ctx* h) {
     if (p) cudaFree(p);
   if (h->h_st) cudaFreeHost(h->h_st);
   if (h->h_scal) cudaFreeHost(h->h_scal);
-  if (h->h_done) cudaFreeHost(h->h_done);
+  if (h->h_chunk) cudaFreeHost(h->h_chunk);
   if (h->h_flags) cudaFreeHost(h->h_flags);
   if (h->chunk_exec) cudaGraphExecDestroy(h->chunk_exec);
-  for (auto e : h->chunk_ev) cudaEventDestroy(e);
+  for (int k = 0; k < 2; ++k) {
+    if (h->prof_exec[k]) cudaGraphExecDestroy(h->prof_exec[k]);
+    for (auto e : h->chunk_ev[k]) cudaEventDestroy(e);
+  }
   for (auto e : h->tm.pool) cudaEventDestroy(e);
   if (h->ev_a) cudaEventDestroy(h->ev_a);
   if (h->ev_b) cudaEventDestroy(h->ev_b);
@@ -458,7 +479,7 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
       cudaMemset(h->xs, 0, h->ndof * sizeof(double)) != cudaSuccess) { h->err = "memset failed"; return bail(SSO_E_CUDA); }
   if (cudaMallocHost(&h->h_st, sizeof(CgState)) != cudaSuccess ||
       cudaMallocHost(&h->h_scal, 8 * sizeof(double)) != cudaSuccess ||
-      cudaMallocHost(&h->h_done, 2 * sizeof(int)) != cudaSuccess ||
+      cudaMallocHost(&h->h_chunk, 2 * sizeof(CgState)) != cudaSuccess ||
       cudaMallocHost(&h->h_flags, sizeof(DevFlags)) != cudaSuccess) { h->err = "cudaMallocHost failed"; return bail(SSO_E_OOM); }
   cudaEventCreate(&h->ev_a);
   cudaEventCreate(&h->ev_b);
@@ -551,69 +572,47 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
   }
   const bool prof = h->tm.on;
   if (!prof && !h->chunk_exec) {
-    if ((rc = build_chunk_graph(h))) return rc;
+    if ((rc = build_chunk_graph(h, -1, &h->chunk_exec))) return rc;
   }
-  if (prof && (int)h->chunk_ev.size() < 2 * h->check_every) {
-    for (int i = (int)h->chunk_ev.size(); i < 2 * h->check_every; ++i) {
-      cudaEvent_t e;
-      CK(h, cudaEventCreate(&e));
-      h->chunk_ev.push_back(e);
-    }
+  if (prof && !h->prof_exec[0]) {
+    if ((rc = build_chunk_graph(h, 0, &h->prof_exec[0]))) return rc;
+    if ((rc = build_chunk_graph(h, 1, &h->prof_exec[1]))) return rc;
   }
-  // Chunked device-side loop: every chunk replays check_every iterations; kernels
-  // after convergence return immediately.  Without profiling one chunk is kept in
-  // flight ahead of the flag being polled.  With profiling on, the same kernels are
-  // launched directly (no graph) with CUDA events around every SpMV.
+  // Device-side loop in chunks of check_every iterations (graph replays); kernels
+  // after convergence return immediately.  One chunk is always queued ahead of the
+  // state snapshot being polled, so the GPU never idles on the host.  With
+  // profiling on, slot-alternating graphs carry event nodes around every SpMV and
+  // the elapsed times of the iterations that actually ran are accumulated.
   const int64_t max_chunks = (h->max_iter + h->check_every - 1) / h->check_every + 1;
   int64_t launched = 0;
   auto launch_chunk = [&](int slot) -> int {
-    if (!prof) {
-      CK(h, cudaGraphLaunch(h->chunk_exec, h->stream));
-      h->launches += h->kernels_per_chunk;
-    } else {
-      long long g0 = g_launches;
-      for (int i = 0; i < h->check_every; ++i) {
-        CK(h, cudaEventRecord(h->chunk_ev[2 * i], h->stream));
-        launch_spmv_dot(h->stream, h->n_nodes, h->node_ptr, h->node_col, h->vals, h->p, h->q,
-                        h->partial, h->st);
-        CK(h, cudaEventRecord(h->chunk_ev[2 * i + 1], h->stream));
-        launch_cg_update(h->stream, (int)h->ndof, h->dinv, h->xs, h->r, h->p, h->q, h->partial, h->st);
-        launch_cg_pupdate(h->stream, (int)h->ndof, h->dinv, h->r, h->p, h->st);
-      }
-      h->launches += g_launches - g0;
-    }
-    CK(h, cudaMemcpyAsync(&h->h_done[slot], &h->st->done, sizeof(int), cudaMemcpyDeviceToHost,
+    CK(h, cudaGraphLaunch(prof ? h->prof_exec[slot] : h->chunk_exec, h->stream));
+    h->launches += h->kernels_per_chunk;
+    CK(h, cudaMemcpyAsync(&h->h_chunk[slot], h->st, sizeof(CgState), cudaMemcpyDeviceToHost,
                           h->stream));
     CK(h, cudaEventRecord(h->ev_done[slot], h->stream));
     ++launched;
     return SSO_OK;
   };
   long long iters_before = 0;
-  if (!prof) {
-    // pipelined: chunk k+1 is queued before the flag of chunk k is polled
-    if ((rc = launch_chunk(0))) return rc;
-    for (int64_t k = 0;; ++k) {
-      const int slot = (int)(k & 1);
-      if (launched < max_chunks && (rc = launch_chunk(1 - slot))) return rc;
-      CK(h, cudaEventSynchronize(h->ev_done[slot]));
-      if (h->h_done[slot] || launched == k + 1) break;
-    }
-  } else {
-    for (;;) {
-      if ((rc = launch_chunk(0))) return rc;
-      CK(h, cudaEventSynchronize(h->ev_done[0]));
-      CK(h, cudaMemcpy(h->h_st, h->st, sizeof(CgState), cudaMemcpyDeviceToHost));
-      long long ran = h->h_st->iter - iters_before;
-      if (h->h_st->done && h->h_st->status == SSO_E_NOT_SPD) ran += 1;
-      iters_before = h->h_st->iter;
-      for (long long i = 0; i < std::min<long long>(ran, h->check_every); ++i) {
+  if ((rc = launch_chunk(0))) return rc;
+  for (int64_t k = 0;; ++k) {
+    const int slot = (int)(k & 1);
+    if (launched < max_chunks && (rc = launch_chunk(1 - slot))) return rc;
+    CK(h, cudaEventSynchronize(h->ev_done[slot]));
+    const CgState& S = h->h_chunk[slot];
+    if (prof) {
+      long long ran = S.iter - iters_before;
+      if (S.done && S.status == SSO_E_NOT_SPD && ran < h->check_every) ran += 1;
+      iters_before = S.iter;
+      for (long long i = 0; i < std::min<long long>(ran, h->check_every); i += PROF_EVERY) {
         float ms = 0.f;
-        CK(h, cudaEventElapsedTime(&ms, h->chunk_ev[2 * i], h->chunk_ev[2 * i + 1]));
+        CK(h, cudaEventElapsedTime(&ms, h->chunk_ev[slot][2 * i], h->chunk_ev[slot][2 * i + 1]));
         h->tm.total_ms[F_SPMV] += ms;
         h->tm.launches[F_SPMV] += 1;
       }
-      if (h->h_done[0] || launched >= max_chunks) break;
     }
+    if (S.done || launched == k + 1) break;
   }
   CK(h, cudaEventRecord(h->ev_b, h->stream));
   // true residual |f_bc - K x| / |f_bc|

@@ -24,6 +24,7 @@
 // of per value (4 B / value): 8.1 B per non-zero instead of 12.
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 #include "sso_internal.h"
 
@@ -123,76 +124,191 @@ __device__ __forceinline__ double reduce6(double (&acc)[8], int lane) {
   return acc[0];
 }
 
-// y = K x for node n (warp-cooperative); returns y[6n + vi(lane)] in every lane.
-__device__ __forceinline__ double node_row_products(int64_t n, const int64_t* __restrict__ node_ptr,
-                                                    const int32_t* __restrict__ node_col,
-                                                    const double* __restrict__ vals,
-                                                    const double* __restrict__ x, int lane) {
-  const int64_t b0 = node_ptr[n];
-  const int deg = (int)(node_ptr[n + 1] - b0);
+// ---------------------------------------------------------------------------
+// TMA-pipelined node-block SpMV, warp-independent.
+//
+// Every warp owns a contiguous range of nodes.  The six rows of a node are ONE
+// contiguous run of 36 deg values, so lane 0 of the warp streams the runs of
+// its next nodes into a private ring of SPMV_STAGES shared-memory slots with
+// cp.async.bulk (TMA bulk copy, completion on a per-slot mbarrier, L2
+// evict-first so the CG vectors stay L2-resident) while the warp computes the
+// current node.  Warps never wait for each other.  Per node the warp gathers
+// p[6m+b] once per row position (m from a register copy of the node's column
+// list, via shuffle; prefetched one node ahead) and applies it to the six
+// rows; a 9-shuffle transposed butterfly reduces the six row sums.  A node
+// whose run exceeds a slot (degree > SLOT_DEG) is read from global memory.
+// ---------------------------------------------------------------------------
+constexpr int SPMV_WARPS = 8;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// Six row sums of a node whose 36 deg values start at `base` (shared or global);
+// ncol = node_col[b0 + lane] for lane < deg (deg <= 32), else read from node_col.
+// Returns y[6n + vi(lane)] in every lane.
+__device__ __forceinline__ double node_rows(const double* base, int64_t b0, int deg, int ncol,
+                                            const int32_t* __restrict__ node_col,
+                                            const double* __restrict__ x, int lane) {
   const int rowlen = 6 * deg;
-  const double* base = vals + 36 * b0;
   double acc[8];
 #pragma unroll
   for (int a = 0; a < 8; ++a) acc[a] = 0.0;
-#pragma unroll 2
-  for (int rem = lane; rem < rowlen; rem += 32) {
-    const int k = rem / 6;
-    const int b = rem - 6 * k;
-    const int m = __ldg(node_col + b0 + k);
-    const double xv = x[6 * (int64_t)m + b];
+  if (deg <= 32) {
+    for (int r0 = 0; r0 < rowlen; r0 += 64) {
+      // two row positions per lane in flight: gathers first, then the 12 products
+      const int ra = r0 + lane, rb = r0 + 32 + lane;
+      const bool aa = ra < rowlen, ab = rb < rowlen;
+      const int ka = aa ? ra / 6 : 0, kb = ab ? rb / 6 : 0;
+      const int ma = __shfl_sync(0xffffffffu, ncol, ka);
+      const int mb = __shfl_sync(0xffffffffu, ncol, kb);
+      const double xa = aa ? x[6 * (int64_t)ma + (ra - 6 * ka)] : 0.0;
+      const double xb = ab ? x[6 * (int64_t)mb + (rb - 6 * kb)] : 0.0;
+      if (aa) {
 #pragma unroll
-    for (int a = 0; a < 6; ++a) acc[a] += __ldcs(base + a * rowlen + rem) * xv;
+        for (int a = 0; a < 6; ++a) acc[a] += base[a * rowlen + ra] * xa;
+      }
+      if (ab) {
+#pragma unroll
+        for (int a = 0; a < 6; ++a) acc[a] += base[a * rowlen + rb] * xb;
+      }
+    }
+  } else {
+    for (int rem = lane; rem < rowlen; rem += 32) {
+      const int k = rem / 6;
+      const int m = __ldg(node_col + b0 + k);
+      const double xv = x[6 * (int64_t)m + (rem - 6 * k)];
+#pragma unroll
+      for (int a = 0; a < 6; ++a) acc[a] += base[a * rowlen + rem] * xv;
+    }
   }
   return reduce6(acc, lane);
 }
 
-__global__ void __launch_bounds__(256) spmv_dot_kernel(
-    int n_nodes, const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ node_col,
-    const double* __restrict__ vals, const double* __restrict__ p, double* __restrict__ q,
-    double* __restrict__ partial, CgState* st) {
+// q = K p; with DOT also p^T q -> alpha (CG) and an early exit once `done`.
+// STAGES ring slots of SLOT_DEG 6x6 blocks per warp; MINB CTAs per SM.
+template <bool DOT, int SPMV_STAGES, int SLOT_DEG, int MINB>
+__global__ void __launch_bounds__(SPMV_WARPS * 32, MINB) spmv_tma_kernel(
+    int n_nodes, int nodes_per_warp, const int64_t* __restrict__ node_ptr,
+    const int32_t* __restrict__ node_col, const double* __restrict__ vals,
+    const double* __restrict__ p, double* __restrict__ q, double* __restrict__ partial,
+    CgState* st) {
+  constexpr int SLOT_DOUBLES = 36 * SLOT_DEG;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar[SPMV_WARPS][SPMV_STAGES];
   __shared__ double sm[32];
-  if (st->done) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (DOT && st->done) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * SPMV_WARPS + warp;
+  const int64_t nb = gw * nodes_per_warp;
+  const int64_t left = (int64_t)n_nodes - nb;
+  const int cnt = left <= 0 ? 0 : (int)(left < nodes_per_warp ? left : nodes_per_warp);
+  double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * SPMV_STAGES * SLOT_DOUBLES;
+  uint64_t* wbar = bar[warp];
+  uint64_t pol = 0;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < SPMV_STAGES; ++s) mbar_init(&wbar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    pol = evict_first_policy();
+  }
+  __syncwarp();
+  auto issue = [&](int k) {  // lane 0 only
+    const int64_t n = nb + k;
+    const int s = k % SPMV_STAGES;
+    const int64_t b0 = node_ptr[n], b1 = node_ptr[n + 1];
+    if (b1 - b0 <= SLOT_DEG) {
+      const unsigned bytes = (unsigned)(288 * (b1 - b0));
+      mbar_arrive_expect_tx(&wbar[s], bytes);
+      bulk_g2s(ring + (size_t)s * SLOT_DOUBLES, vals + 36 * b0, bytes, &wbar[s], pol);
+    } else {
+      mbar_arrive(&wbar[s]);  // oversized node: read from global, keep the phase sequence
+    }
+  };
+  if (lane == 0)
+    for (int k = 0; k < min(SPMV_STAGES - 1, cnt); ++k) issue(k);
   const int vi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
   const bool writer = ((lane & 3) == 0) && vi < 6;
   double pq[1] = {0.0};
-  for (int64_t n = warp; n < n_nodes; n += nwarps) {
-    const double y = node_row_products(n, node_ptr, node_col, vals, p, lane);
+  // metadata of the current node, prefetched one node ahead
+  int64_t b0n = 0;
+  int degn = 0, ncoln = 0;
+  if (cnt > 0) {
+    b0n = node_ptr[nb];
+    degn = (int)(node_ptr[nb + 1] - b0n);
+    ncoln = (lane < degn) ? __ldg(node_col + b0n + lane) : 0;
+  }
+  for (int k = 0; k < cnt; ++k) {
+    const int s = k % SPMV_STAGES;
+    if (lane == 0 && k + SPMV_STAGES - 1 < cnt) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(k + SPMV_STAGES - 1);
+    }
+    const int64_t n = nb + k;
+    const int64_t b0 = b0n;
+    const int deg = degn, ncol = ncoln;
+    if (k + 1 < cnt) {
+      b0n = node_ptr[n + 1];
+      degn = (int)(node_ptr[n + 2] - b0n);
+      ncoln = (lane < degn) ? __ldg(node_col + b0n + lane) : 0;
+    }
+    mbar_wait(&wbar[s], (unsigned)((k / SPMV_STAGES) & 1));
+    const double* base = (deg <= SLOT_DEG) ? ring + (size_t)s * SLOT_DOUBLES : vals + 36 * b0;
+    const double y = node_rows(base, b0, deg, ncol, node_col, p, lane);
     if (writer) {
       q[6 * n + vi] = y;
-      pq[0] += p[6 * n + vi] * y;
+      if (DOT) pq[0] += p[6 * n + vi] * y;
     }
+    __syncwarp();
   }
-  if (grid_sum<1>(pq, partial, &st->ticket[0], sm) && threadIdx.x == 0) {
-    st->pq = pq[0];
-    if (!(pq[0] > 0.0)) {
-      st->status = SSO_E_NOT_SPD;
-      st->done = 1;
-    } else {
-      st->alpha = st->rz / pq[0];
+  if (DOT) {
+    if (grid_sum<1>(pq, partial, &st->ticket[0], sm) && threadIdx.x == 0) {
+      st->pq = pq[0];
+      if (!(pq[0] > 0.0)) {
+        st->status = SSO_E_NOT_SPD;
+        st->done = 1;
+      } else {
+        st->alpha = st->rz / pq[0];
+      }
     }
   }
 }
 
-__global__ void __launch_bounds__(256) spmv_kernel(int n_nodes, const int64_t* __restrict__ node_ptr,
-                                                   const int32_t* __restrict__ node_col,
-                                                   const double* __restrict__ vals,
-                                                   const double* __restrict__ x,
-                                                   double* __restrict__ y) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int vi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-  const bool writer = ((lane & 3) == 0) && vi < 6;
-  for (int64_t n = warp; n < n_nodes; n += nwarps) {
-    const double v = node_row_products(n, node_ptr, node_col, vals, x, lane);
-    if (writer) y[6 * n + vi] = v;
-  }
-}
-
+// x += alpha p, r -= alpha q, z = dinv r; partial r^T z, r^T r.  double2 streams
+// (ndof = 6 n is even; cudaMalloc buffers are 256 B aligned).
 __global__ void __launch_bounds__(256) cg_update_kernel(int ndof, const double* __restrict__ dinv,
                                                         double* __restrict__ x,
                                                         double* __restrict__ r,
@@ -204,15 +320,24 @@ __global__ void __launch_bounds__(256) cg_update_kernel(int ndof, const double* 
   if (st->done) return;
   const double alpha = st->alpha;
   double v[2] = {0.0, 0.0};  // r^T z, r^T r
+  const int64_t n2 = ndof / 2;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndof; i += stride) {
-    const double xi = x[i] + alpha * p[i];
-    const double ri = r[i] - alpha * q[i];
-    x[i] = xi;
-    r[i] = ri;
-    const double zi = dinv[i] * ri;
-    v[0] += ri * zi;
-    v[1] += ri * ri;
+  const double2* __restrict__ p2 = reinterpret_cast<const double2*>(p);
+  const double2* __restrict__ q2 = reinterpret_cast<const double2*>(q);
+  const double2* __restrict__ d2 = reinterpret_cast<const double2*>(dinv);
+  double2* __restrict__ x2 = reinterpret_cast<double2*>(x);
+  double2* __restrict__ r2 = reinterpret_cast<double2*>(r);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
+    const double2 pi = p2[i], qi = q2[i], di = d2[i];
+    double2 xi = x2[i], ri = r2[i];
+    xi.x += alpha * pi.x;
+    xi.y += alpha * pi.y;
+    ri.x -= alpha * qi.x;
+    ri.y -= alpha * qi.y;
+    x2[i] = xi;
+    r2[i] = ri;
+    v[0] += ri.x * (di.x * ri.x) + ri.y * (di.y * ri.y);
+    v[1] += ri.x * ri.x + ri.y * ri.y;
   }
   if (grid_sum<2>(v, partial, &st->ticket[1], sm) && threadIdx.x == 0) {
     const double rz_new = v[0];
@@ -236,9 +361,18 @@ __global__ void __launch_bounds__(256) cg_pupdate_kernel(int ndof, const double*
                                                          const CgState* st) {
   if (st->done) return;
   const double beta = st->beta;
+  const int64_t n2 = ndof / 2;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndof; i += stride)
-    p[i] = dinv[i] * r[i] + beta * p[i];
+  const double2* __restrict__ r2 = reinterpret_cast<const double2*>(r);
+  const double2* __restrict__ d2 = reinterpret_cast<const double2*>(dinv);
+  double2* __restrict__ p2 = reinterpret_cast<double2*>(p);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
+    const double2 ri = r2[i], di = d2[i];
+    double2 pi = p2[i];
+    pi.x = di.x * ri.x + beta * pi.x;
+    pi.y = di.y * ri.y + beta * pi.y;
+    p2[i] = pi;
+  }
 }
 
 // f_bc = f with fixed DOFs zeroed; x = x0 (fixed zeroed) or 0; r = f_bc - K x0; p = z = dinv r.
@@ -346,22 +480,64 @@ void launch_zero_fixed(cudaStream_t s, int ndof, const uint8_t* fixed_mask, doub
   SSO_POST_LAUNCH("zero_fixed_kernel");
 }
 
-void launch_spmv_dot(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
-                     const int32_t* node_col, const double* vals, const double* p, double* q,
-                     double* partial, CgState* st) {
-  int64_t need = ((int64_t)n_nodes + 7) / 8;
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)cg_grid()));
-  spmv_dot_kernel<<<grid, 256, 0, s>>>(n_nodes, node_ptr, node_col, vals, p, q, partial, st);
+struct SpmvVariant {
+  int stages, slot_deg, minb;
+  void (*dot)(int, int, const int64_t*, const int32_t*, const double*, const double*, double*,
+              double*, CgState*);
+  void (*plain)(int, int, const int64_t*, const int32_t*, const double*, const double*, double*,
+                double*, CgState*);
+};
+#define SPMV_VARIANT(S, D, M) \
+  { S, D, M, spmv_tma_kernel<true, S, D, M>, spmv_tma_kernel<false, S, D, M> }
+static const SpmvVariant kSpmvVariants[] = {
+    SPMV_VARIANT(4, 10, 2), SPMV_VARIANT(3, 10, 3), SPMV_VARIANT(2, 9, 4), SPMV_VARIANT(3, 9, 3),
+    SPMV_VARIANT(2, 10, 4)};
+
+static const SpmvVariant& spmv_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SSO_SPMV_VARIANT");
+    v = e ? atoi(e) : 2;  // default: 2-slot ring, 4 CTAs per SM (measured best at C3b)
+    const int nv = (int)(sizeof(kSpmvVariants) / sizeof(kSpmvVariants[0]));
+    if (v < 0 || v >= nv) v = 0;
+    const SpmvVariant& V = kSpmvVariants[v];
+    const int smem = SPMV_WARPS * V.stages * 36 * V.slot_deg * 8;
+    cudaFuncSetAttribute(V.dot, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(V.plain, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  }
+  return kSpmvVariants[v];
+}
+
+static void spmv_config(int n_nodes, int* grid, int* npw, int* smem) {
+  const SpmvVariant& V = spmv_variant();
+  const int ctas = V.minb * (cg_grid() / 4);  // persistent: minb CTAs per SM
+  const int64_t warps = (int64_t)ctas * SPMV_WARPS;
+  int per = (int)((n_nodes + warps - 1) / warps);
+  if (per < 1) per = 1;
+  *npw = per;
+  *grid = (int)std::max<int64_t>(1, (((int64_t)n_nodes + per - 1) / per + SPMV_WARPS - 1) / SPMV_WARPS);
+  *smem = SPMV_WARPS * V.stages * 36 * V.slot_deg * 8;
+}
+
+void launch_spmv_dot(cudaStream_t s, int n_nodes, const int64_t* node_ptr, const int32_t* node_col,
+                     const double* vals, const double* p, double* q, double* partial, CgState* st) {
+  int grid, npw, smem;
+  spmv_config(n_nodes, &grid, &npw, &smem);
+  spmv_variant().dot<<<grid, SPMV_WARPS * 32, smem, s>>>(n_nodes, npw, node_ptr, node_col, vals, p, q,
+                                                         partial, st);
   SSO_POST_LAUNCH("spmv_dot_kernel");
 }
 
 void launch_spmv(cudaStream_t s, int n_nodes, const int64_t* node_ptr, const int32_t* node_col,
                  const double* vals, const double* x, double* y) {
-  int64_t need = ((int64_t)n_nodes + 7) / 8;
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)cg_grid()));
-  spmv_kernel<<<grid, 256, 0, s>>>(n_nodes, node_ptr, node_col, vals, x, y);
+  int grid, npw, smem;
+  spmv_config(n_nodes, &grid, &npw, &smem);
+  spmv_variant().plain<<<grid, SPMV_WARPS * 32, smem, s>>>(n_nodes, npw, node_ptr, node_col, vals, x, y,
+                                                           nullptr, nullptr);
   SSO_POST_LAUNCH("spmv_kernel");
 }
+
+
 
 void launch_cg_update(cudaStream_t s, int ndof, const double* dinv, double* x, double* r,
                       const double* p, const double* q, double* partial, CgState* st) {

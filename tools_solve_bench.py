@@ -1,0 +1,28 @@
+"""Solve-only timing at C3b: iterations, ms per solve, sampled SpMV launch time."""
+import json, os, sys
+sys.path.insert(0, '.')
+import numpy as np
+import torch
+import workloads as W
+import paper_2407_20026_b200 as sso
+n = int(os.environ.get("N", "408"))
+P = W.shell_config3(n, cfg=3)
+m = sso.Model(P, rtol=1e-10)
+m.assemble()
+f = torch.from_numpy(P["f"]).cuda()
+u = torch.zeros_like(f)
+m.solve(f, u)
+m.profile_enable(True)
+m.profile_reset()
+ts = []
+for _ in range(3):
+    _, info = m.solve(f, u)
+    ts.append(info["ms"])
+ms, cnt = m.profile_read("spmv")
+ndof, nnz, nb = m.sizes()
+byts = 8 * nnz + 4 * nb + 8 * (m.n_nodes + 1) + 16 * ndof
+avg = ms / max(cnt, 1)
+print(json.dumps({"variant": os.environ.get("SSO_SPMV_VARIANT", "0"), "n": n, "iters": info["iters"],
+                  "solve_ms": min(ts), "us_per_iter": 1000 * min(ts) / info["iters"],
+                  "spmv_us": 1000 * avg, "spmv_GBs": byts / (avg / 1000) / 1e9,
+                  "true_rel_res": info["true_rel_res"]}))
