@@ -109,7 +109,7 @@ def dist_env():
 # CPU oracle baseline (bounded sample, extrapolated to the C3b workload)
 # ----------------------------------------------------------------------------
 
-def oracle_sample(P, n_elem=60, n_grad=6, pcg_grid=40, pcg_iters=40):
+def oracle_sample(P, n_elem=2000, n_grad=1000, pcg_grid=60, pcg_iters=200):
     """Times the oracle as it stands on a bounded sample of workload P:
     element stiffness + DOK insertion per element, adjoint-gradient work per
     element (complex step), and one Jacobi-PCG iteration per stored non-zero on
@@ -166,8 +166,8 @@ def cpu_baseline_obj(P, cg_iters):
     wall = time.perf_counter() - t0
     rate, t_eval = oracle_rate(C3B_NQ, C3B_NNZ, cg_iters, te, tg, ti)
     return {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": (f"oracle timed on 60 C3b elements (K_e + DOK), 6 element gradients "
-                       f"(complex step) and 40 PCG iterations on a 40x40 same-recipe grid "
+            "sample": (f"oracle timed on 2000 C3b elements (K_e + DOK), 1000 element gradients "
+                       f"(complex step) and 200 PCG iterations on a 60x60 same-recipe grid "
                        f"({wall:.1f} s of CPU); extrapolated to C3b: {C3B_NQ} elements, "
                        f"{C3B_NNZ} nnz, {cg_iters} CG iterations -> {t_eval:.1f} s per eval"),
             "per_unit_s": {"element": te, "grad_element": tg, "cg_iter_per_nnz": ti}}
@@ -184,7 +184,7 @@ def run_reference(args):
     vals = []
     for k in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        te, tg, ti = oracle_sample(P, n_elem=20, n_grad=2, pcg_grid=24, pcg_iters=20)
+        te, tg, ti = oracle_sample(P, n_elem=200, n_grad=100, pcg_grid=32, pcg_iters=60)
         dt = time.perf_counter() - t0
         if k >= args.warmup:
             times.append(dt)
@@ -197,8 +197,8 @@ def run_reference(args):
             "config": {"workload": "C3b: 408x408 MITC-4 shell quads, 1 003 686 DOF (reading c15)",
                        "rtol": RTOL, "cg_iters": cg_iters},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": ("per step: oracle on 20 C3b elements (K_e + DOK), 2 element "
-                                        "gradients, 20 PCG iterations on a 24x24 same-recipe grid; "
+                             "sample": ("per step: oracle on 200 C3b elements (K_e + DOK), 100 element "
+                                        "gradients, 60 PCG iterations on a 32x32 same-recipe grid; "
                                         f"extrapolated to C3b with {cg_iters} CG iterations; "
                                         f"median sample wall {np.median(times):.2f} s")},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
