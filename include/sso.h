@@ -106,6 +106,19 @@ typedef struct {
   sso_mem mem;            /* pointer kind of solve/grad/design buffers (default HOST)   */
   void* cuda_stream;      /* cudaStream_t to enqueue on; NULL = library-owned stream    */
   int32_t device;         /* CUDA device ordinal                        (default: current) */
+  /* Partitioning.  The node range is split into contiguous strips
+   * part_ranges[0] = 0 < ... < part_ranges[P] = n_nodes (NULL = equal node counts).
+   * nranks == 1, n_parts == P > 1: all P strips live in this handle on one GPU
+   *   (in-process transport); buffers stay global.
+   * nranks == P > 1: this handle is strip `rank` on its own GPU; halos and the CG
+   *   scalars travel through NCCL (communicator from nccl_unique_id, 128 bytes, made
+   *   by sso_nccl_unique_id on one rank and broadcast by the caller).  f, u and
+   *   dC_dxyz then cover the rank's owned nodes only, dC_dt its owned quads (first
+   *   node owned), in ascending global order; C is global.  (defaults: 1, NULL, 1, 0, NULL) */
+  int32_t n_parts;
+  const int32_t* part_ranges;
+  int32_t nranks, rank;
+  const void* nccl_unique_id;
 } sso_options;
 
 typedef struct {
@@ -173,6 +186,27 @@ int sso_export_csr(sso_handle h, int64_t* row_ptr, int32_t* col_idx, double* val
 int sso_export_scatter(sso_handle h, int32_t* block_rank);
 int sso_export_ke(sso_handle h, int64_t first, int64_t count, double* ke);
 int sso_export_dinv(sso_handle h, double* dinv);
+
+/* Partition of this handle: number of strips held, first owned global node, owned
+ * node count and owned quad count (the extents of the caller's f / u / gradients). */
+int sso_part_info(sso_handle h, int32_t* n_parts_here, int32_t* own_node_begin, int32_t* own_nodes,
+                  int32_t* own_quads);
+
+/* ncclGetUniqueId through the library's run-time NCCL binding (out: 128 bytes). */
+int sso_nccl_unique_id(void* out);
+
+/* Host-only partition queries (no GPU needed; the multi-process CPU tests use them).
+ * Rank-local CSR pattern of strip `part` (rows of its owned nodes, global column ids):
+ * call with row_ptr = col_idx = NULL to get *nnz, then with [6 n_own + 1] / [nnz] buffers.
+ * The strips' patterns concatenate to the global pattern. */
+int sso_local_pattern(const sso_mesh* mesh, const int32_t* ranges, int32_t n_parts, int32_t part,
+                      int64_t* nnz, int64_t* row_ptr, int32_t* col_idx);
+/* Halo plan of strip `part`: halo node ids (global, ordered by owner then id), the
+ * neighbour strips and, per neighbour, the owned nodes sent to it (in its halo order).
+ * Call with NULL arrays to get *n_halo and *n_nbrs; send_gid holds sum(send_count). */
+int sso_halo_plan(const sso_mesh* mesh, const int32_t* ranges, int32_t n_parts, int32_t part,
+                  int32_t* n_halo, int32_t* halo_gid, int32_t* n_nbrs, int32_t* nbr_part,
+                  int32_t* send_count, int32_t* send_gid);
 
 /* Kernel timing with CUDA events recorded on the handle's stream while enabled.
  * names: "element", "assemble", "spmv", "update", "grad", "reduce".  Outside the

@@ -7,4 +7,5 @@ This package holds the CUDA sources (csrc/), the nvcc build (build.py) and the
 ctypes binding (api.py).  It never imports `oracle/` and has no CPU fallback.
 """
 from .api import (Model, SSOError, OBJ_COMPLIANCE, OBJ_STRAIN_ENERGY, MEM_HOST, MEM_DEVICE,  # noqa: F401
-                  LIB_PATH, EXPORTED, last_create_error)
+                  LIB_PATH, EXPORTED, last_create_error, nccl_unique_id, local_pattern,
+                  halo_plan)

@@ -59,7 +59,9 @@ class sso_supports(C.Structure):
 class sso_options(C.Structure):
     _fields_ = [("rtol", C.c_double), ("max_iter", C.c_int64), ("drill_alpha", C.c_double),
                 ("warm_start", C.c_int32), ("check_every", C.c_int32), ("mem", C.c_int),
-                ("cuda_stream", C.c_void_p), ("device", C.c_int32)]
+                ("cuda_stream", C.c_void_p), ("device", C.c_int32),
+                ("n_parts", C.c_int32), ("part_ranges", _ip), ("nranks", C.c_int32),
+                ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p)]
 
 
 class sso_solve_info(C.Structure):
@@ -92,6 +94,11 @@ _sig = {
     "sso_profile_read": (C.c_int, [_H, C.c_char_p, _dp, _lp]),
     "sso_profile_reset": (C.c_int, [_H]),
     "sso_launch_count": (C.c_int64, [_H]),
+    "sso_part_info": (C.c_int, [_H, _ip, _ip, _ip, _ip]),
+    "sso_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "sso_local_pattern": (C.c_int, [C.POINTER(sso_mesh), _ip, C.c_int32, C.c_int32, _lp, C.c_void_p, C.c_void_p]),
+    "sso_halo_plan": (C.c_int, [C.POINTER(sso_mesh), _ip, C.c_int32, C.c_int32, _ip, C.c_void_p, _ip,
+                                C.c_void_p, C.c_void_p, C.c_void_p]),
     "sso_last_error": (C.c_char_p, [_H]),
     "sso_destroy": (None, [_H]),
 }
@@ -133,7 +140,8 @@ class Model:
     beam_conn, quad_conn, A, Iy, Iz, J, t, E, nu, G, sup_node, sup_mask)."""
 
     def __init__(self, problem, rtol=1e-10, max_iter=200000, drill_alpha=1e-3, check_every=64,
-                 warm_start=False, stream=None, device=-1):
+                 warm_start=False, stream=None, device=-1, n_parts=1, part_ranges=None,
+                 nranks=1, rank=0, nccl_id=None):
         P = problem
         self._keep = []
         x, y, z = (_np(P[k], np.float64) for k in ("x", "y", "z"))
@@ -162,14 +170,28 @@ class Model:
         opt.check_every, opt.warm_start, opt.device = check_every, int(warm_start), device
         opt.mem = MEM_HOST
         opt.cuda_stream = stream
+        opt.n_parts, opt.nranks, opt.rank = n_parts, nranks, rank
+        if part_ranges is not None:
+            pr = np.ascontiguousarray(part_ranges, np.int32)
+            self._keep.append(pr)
+            opt.part_ranges = pr.ctypes.data_as(_ip)
+        if nccl_id is not None:
+            idb = C.create_string_buffer(bytes(nccl_id), 128)
+            self._keep.append(idb)
+            opt.nccl_unique_id = C.cast(idb, C.c_void_p)
         h = _H()
         rc = _lib.sso_create(C.byref(mesh), C.byref(sec), C.byref(mat), C.byref(sup), C.byref(opt),
                              C.byref(h))
         if rc != SSO_OK:
             raise SSOError(rc, _lib.sso_last_error(None).decode())
         self.h = h
-        self.n_nodes, self.n_beams, self.n_quads = len(x), nb, nq
-        self.ndof = 6 * len(x)
+        self.g_nodes, self.g_quads = len(x), nq
+        a, b, c, d = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        _lib.sso_part_info(h, C.byref(a), C.byref(b), C.byref(c), C.byref(d))
+        self.n_parts_here, self.own_node_begin = a.value, b.value
+        # extents of this handle's f / u / gradient buffers (global unless multi-rank)
+        self.n_nodes, self.n_beams, self.n_quads = c.value, nb, d.value
+        self.ndof = 6 * c.value
         self._mem = MEM_HOST
         self._stream = stream
 
@@ -324,3 +346,67 @@ class Model:
 
 def last_create_error():
     return _lib.sso_last_error(None).decode()
+
+
+def nccl_unique_id():
+    buf = C.create_string_buffer(128)
+    rc = _lib.sso_nccl_unique_id(buf)
+    if rc != SSO_OK:
+        raise SSOError(rc, last_create_error())
+    return buf.raw
+
+
+def _mesh_struct(P):
+    x, y, z = (np.ascontiguousarray(P[k], np.float64) for k in ("x", "y", "z"))
+    bc = np.ascontiguousarray(P["beam_conn"], np.int32).reshape(-1)
+    qc = np.ascontiguousarray(P["quad_conn"], np.int32).reshape(-1)
+    keep = [x, y, z, bc, qc]
+    m = sso_mesh(len(x), x.ctypes.data_as(_dp), y.ctypes.data_as(_dp), z.ctypes.data_as(_dp),
+                 len(bc) // 2, bc.ctypes.data_as(_ip) if bc.size else None,
+                 len(qc) // 4, qc.ctypes.data_as(_ip) if qc.size else None)
+    return m, keep
+
+
+def local_pattern(P, ranges, part):
+    """Host-only: CSR pattern (row_ptr, col_idx in global ids) of strip `part`'s owned rows."""
+    m, keep = _mesh_struct(P)
+    rg = np.ascontiguousarray(ranges, np.int32)
+    n_parts = len(rg) - 1
+    nnz = C.c_int64()
+    rc = _lib.sso_local_pattern(C.byref(m), rg.ctypes.data_as(_ip), n_parts, part, C.byref(nnz), None, None)
+    if rc != SSO_OK:
+        raise SSOError(rc, last_create_error())
+    n_own = int(rg[part + 1] - rg[part])
+    rp = np.empty(6 * n_own + 1, np.int64)
+    ci = np.empty(nnz.value, np.int32)
+    rc = _lib.sso_local_pattern(C.byref(m), rg.ctypes.data_as(_ip), n_parts, part, C.byref(nnz),
+                                rp.ctypes.data, ci.ctypes.data)
+    if rc != SSO_OK:
+        raise SSOError(rc, last_create_error())
+    return rp, ci
+
+
+def halo_plan(P, ranges, part):
+    """Host-only: (halo_gid, {neighbour: send_gid array}) of strip `part`."""
+    m, keep = _mesh_struct(P)
+    rg = np.ascontiguousarray(ranges, np.int32)
+    n_parts = len(rg) - 1
+    nh, nn = C.c_int32(), C.c_int32()
+    rc = _lib.sso_halo_plan(C.byref(m), rg.ctypes.data_as(_ip), n_parts, part, C.byref(nh), None,
+                            C.byref(nn), None, None, None)
+    if rc != SSO_OK:
+        raise SSOError(rc, last_create_error())
+    halo = np.empty(nh.value, np.int32)
+    nbr = np.empty(nn.value, np.int32)
+    cnt = np.empty(nn.value, np.int32)
+    rc = _lib.sso_halo_plan(C.byref(m), rg.ctypes.data_as(_ip), n_parts, part, C.byref(nh),
+                            halo.ctypes.data, C.byref(nn), nbr.ctypes.data, cnt.ctypes.data, None)
+    send = np.empty(int(cnt.sum()), np.int32)
+    rc = _lib.sso_halo_plan(C.byref(m), rg.ctypes.data_as(_ip), n_parts, part, C.byref(nh),
+                            halo.ctypes.data, C.byref(nn), nbr.ctypes.data, cnt.ctypes.data,
+                            send.ctypes.data)
+    out, off = {}, 0
+    for k in range(nn.value):
+        out[int(nbr[k])] = send[off:off + cnt[k]].copy()
+        off += cnt[k]
+    return halo, out

@@ -9,6 +9,20 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsso.so")
 SOURCES = ["api.cu", "elements.cu", "assemble.cu", "pcg.cu", "grad.cu", "pattern.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nccl_include():
+    """nccl.h for the NCCL types (the library binds the functions at run time)."""
+    import glob
+    import site
+    cands = []
+    for d in site.getsitepackages() + [site.getusersitepackages()]:
+        cands += glob.glob(os.path.join(d, "nvidia", "nccl", "include"))
+    cands += ["/usr/include", "/usr/local/cuda/include"]
+    for c in cands:
+        if os.path.exists(os.path.join(c, "nccl.h")):
+            return c
+    raise RuntimeError("nccl.h not found")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
@@ -33,7 +47,8 @@ def build(verbose=False, force=False):
     log = []
     for s in srcs:
         o = os.path.join(objdir, os.path.basename(s) + ".o")
-        cmd = [nvcc(), *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c", s, "-o", o]
+        cmd = [nvcc(), *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+               "-I", nccl_include(), "-c", s, "-o", o]
         if s.endswith(".cpp"):
             cmd[1:1] = ["-x", "cu"]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -1,38 +1,93 @@
 // C-ABI entry points (include/sso.h).  Host orchestration only: validation,
-// pattern build (A0, pattern.cpp), device buffers, launch sequencing, the PCG
-// chunk graphs and the exports.  Every step of the hot path runs in the
-// kernels of elements.cu, assemble.cu, pcg.cu and grad.cu.
+// pattern / partition build (pattern.cpp), device buffers, launch sequencing,
+// the PCG chunk graphs, halo exchange + allreduce transports and the exports.
+// Every step of the hot path runs in the kernels of elements.cu, assemble.cu,
+// pcg.cu and grad.cu.
+//
+// A handle holds one or more PARTS: contiguous node strips
+// with one element layer of redundant work at each strip edge, a halo of
+// neighbour nodes, and per-part CG state.
+//   * 1 part, 1 rank   : single-GPU path; CG chunks captured in CUDA graphs.
+//   * P parts, 1 rank  : in-process partitions on one GPU (local transport:
+//                        D2D halo copies, fixed-order device allreduce).  The
+//                        user sees global buffers.
+//   * 1 part, N ranks  : one strip per process/GPU (NCCL transport: ncclSend /
+//                        ncclRecv halos, ncclAllReduce of the CG scalars).  The
+//                        user passes the rank's owned slices.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
+#include <numeric>
 #include <string>
 #include <vector>
 
+#include "nccl.h"
 #include "sso_internal.h"
 
 using namespace sso;
 
-struct sso_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  cudaStream_t cap_stream = nullptr;
-  sso_mem mem = SSO_MEM_HOST;
-  double rtol = 1e-10;
-  int64_t max_iter = 200000;
-  double drill_alpha = 1e-3;
-  int warm_start = 0;
-  int check_every = 64;
+namespace {
 
-  int32_t n_nodes = 0, n_beams = 0, n_quads = 0;
-  int64_t ndof = 0, nnz = 0, n_blocks = 0, n_staged = 0, n_slots = 0;
+// ---------------------------------------------------------------------------
+// NCCL, resolved at run time (no link-time dependency; shares the process's
+// libnccl.so.2 with torch when it is already loaded).
+// ---------------------------------------------------------------------------
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) {
+    api.err = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+    return api;
+  }
+#define SYM(f)                                             \
+  api.f = (decltype(api.f))dlsym(lib, "nccl" #f);          \
+  if (!api.f) {                                            \
+    api.err = "missing nccl" #f;                           \
+    return api;                                            \
+  }
+  SYM(GetUniqueId) SYM(CommInitRank) SYM(CommDestroy) SYM(Send) SYM(Recv) SYM(AllReduce)
+  SYM(GroupStart) SYM(GroupEnd) SYM(GetErrorString)
+#undef SYM
+  api.ok = true;
+  return api;
+}
+
+std::string g_create_err;
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// One partition's device state.
+// ---------------------------------------------------------------------------
+struct Part {
+  LocalMesh lm;
+  int32_t n_nodes = 0, n_own = 0, n_beams = 0, n_quads = 0, n_own_quads = 0;
+  int64_t ndof = 0, ndof_own = 0, nnz = 0, n_blocks = 0, n_staged = 0, n_slots = 0;
   HostPattern pat;
-
-  // device inputs
+  // inputs
   double *x = nullptr, *y = nullptr, *z = nullptr;
   int32_t *beam_conn = nullptr, *quad_conn = nullptr;
   double *A = nullptr, *Iy = nullptr, *Iz = nullptr, *J = nullptr, *t = nullptr;
@@ -47,58 +102,98 @@ struct sso_ctx {
   int32_t* inc_slot = nullptr;
   // matrix
   double *stage = nullptr, *vals = nullptr, *dinv = nullptr;
-  // solver vectors
+  // solver
   double *f = nullptr, *fbc = nullptr, *xs = nullptr, *r = nullptr, *p = nullptr, *q = nullptr,
          *tmp = nullptr, *gu = nullptr, *gf = nullptr;
   double* partial = nullptr;
   CgState* st = nullptr;
   DevFlags* flags = nullptr;
   unsigned int* tickets = nullptr;
-  double* scal = nullptr;  // device scalars [8]
-  double *slot_partial = nullptr, *dxyz = nullptr, *dt = nullptr;
-  // pinned host mirrors
+  double* scal = nullptr;
+  double *slot_partial = nullptr, *dxyz = nullptr, *dt = nullptr, *dt_own = nullptr;
+  // partition maps
+  int32_t* own_quad_local = nullptr;  // [n_own_quads]
+  int32_t* own_quad_gid = nullptr;    // [n_own_quads] global quad ids (virtual parts)
+  int32_t* send_idx = nullptr;        // concatenated send lists (local owned node ids)
+  double* sendbuf = nullptr;
+  std::vector<int64_t> send_off;      // per neighbour, in nodes
+  int64_t n_send = 0;
+};
+
+struct sso_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaStream_t cap_stream = nullptr;
+  sso_mem mem = SSO_MEM_HOST;
+  double rtol = 1e-10;
+  int64_t max_iter = 200000;
+  double drill_alpha = 1e-3;
+  int warm_start = 0;
+  int check_every = 64;
+
+  // global problem sizes and what this handle's user buffers cover
+  int32_t g_nodes = 0, g_beams = 0, g_quads = 0;
+  int32_t user_node_begin = 0, user_nodes = 0, user_quads = 0;
+  int nranks = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  std::vector<std::unique_ptr<Part>> parts;
+  CgState** d_sts = nullptr;   // device array of the parts' CgState pointers
+  double* d_dt_all = nullptr;  // virtual parts: global dC/dt assembly buffer
+  double* h_C = nullptr;       // pinned scalar
+
   CgState* h_st = nullptr;
-  double* h_scal = nullptr;
-  CgState* h_chunk = nullptr;  // [2] pinned per-chunk state snapshots (polled)
+  CgState* h_chunk = nullptr;  // [2]
   DevFlags* h_flags = nullptr;
+  double* h_scal = nullptr;
 
   bool assembled = false, solved = false;
-  cudaGraphExec_t chunk_exec = nullptr;   // K CG iterations
-  cudaGraphExec_t prof_exec[2] = {nullptr, nullptr};  // same, with SpMV event nodes (slot 0/1)
+  cudaGraphExec_t chunk_exec = nullptr;
+  cudaGraphExec_t prof_exec[2] = {nullptr, nullptr};
   long long kernels_per_chunk = 0;
-  std::vector<cudaEvent_t> chunk_ev[2];   // profiling: 2 per iteration per slot
+  std::vector<cudaEvent_t> chunk_ev[2];
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_done[2] = {nullptr, nullptr};
 
   Timers tm;
   long long launches = 0;
   std::string err;
+
+  bool distributed() const { return parts.size() > 1 || nranks > 1; }
+  Part& P0() { return *parts[0]; }
 };
 
-static std::string g_create_err;
-
-#define FAIL(h, code, msg)       \
-  do {                           \
-    (h)->err = (msg);            \
-    return (code);               \
+#define FAIL(h, code, msg) \
+  do {                     \
+    (h)->err = (msg);      \
+    return (code);         \
   } while (0)
 
-#define CK(h, call)                                                                  \
-  do {                                                                               \
-    cudaError_t e_ = (call);                                                         \
-    if (e_ != cudaSuccess) {                                                         \
+#define CK(h, call)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
       (h)->err = std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call; \
-      return e_ == cudaErrorMemoryAllocation ? SSO_E_OOM : SSO_E_CUDA;               \
+      return e_ == cudaErrorMemoryAllocation ? SSO_E_OOM : SSO_E_CUDA;                \
+    }                                                                                 \
+  } while (0)
+
+#define CKL(h)                                                                       \
+  do {                                                                               \
+    cudaError_t e_ = cudaGetLastError();                                             \
+    if (e_ != cudaSuccess) {                                                         \
+      (h)->err = std::string("CUDA launch error: ") + cudaGetErrorString(e_) + " (" + \
+                 last_launch_error() + ")";                                          \
+      return SSO_E_CUDA;                                                             \
     }                                                                                \
   } while (0)
 
-#define CKL(h)                                                                          \
-  do {                                                                                  \
-    cudaError_t e_ = cudaGetLastError();                                                \
-    if (e_ != cudaSuccess) {                                                            \
-      (h)->err = std::string("CUDA launch error: ") + cudaGetErrorString(e_) + " (" +    \
-                 last_launch_error() + ")";                                             \
-      return SSO_E_CUDA;                                                                \
-    }                                                                                   \
+#define CKN(h, call)                                                                     \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess) {                                                             \
+      (h)->err = std::string("NCCL error: ") + nccl().GetErrorString(r_) + " at " #call; \
+      return SSO_E_NCCL;                                                                 \
+    }                                                                                    \
   } while (0)
 
 namespace {
@@ -123,21 +218,11 @@ int upload(sso_ctx* h, T** p, const T* src, int64_t n) {
   return SSO_OK;
 }
 
-// copy a caller buffer (kind per h->mem) into a device buffer on h->stream
-int copy_in(sso_ctx* h, double* dst, const double* src, int64_t n) {
-  if (n <= 0) return SSO_OK;
-  CK(h, cudaMemcpyAsync(dst, src, (size_t)n * sizeof(double),
-                        h->mem == SSO_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
-                        h->stream));
-  return SSO_OK;
+cudaMemcpyKind kind_in(const sso_ctx* h) {
+  return h->mem == SSO_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
 }
-
-int copy_out(sso_ctx* h, double* dst, const double* src, int64_t n) {
-  if (n <= 0 || !dst) return SSO_OK;
-  CK(h, cudaMemcpyAsync(dst, src, (size_t)n * sizeof(double),
-                        h->mem == SSO_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
-                        h->stream));
-  return SSO_OK;
+cudaMemcpyKind kind_out(const sso_ctx* h) {
+  return h->mem == SSO_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
 }
 
 bool finite_all(const double* v, int64_t n) {
@@ -199,26 +284,102 @@ int sync(sso_ctx* h) {
   return SSO_OK;
 }
 
-int check_flags(sso_ctx* h) {
-  CK(h, cudaMemcpyAsync(h->h_flags, h->flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, h->stream));
-  int rc = sync(h);
-  if (rc) return rc;
-  if (h->h_flags->degenerate_elem != INT_MAX) {
-    int e = h->h_flags->degenerate_elem;
-    char buf[256];
-    if (e < 0) e = -e - 1;
-    snprintf(buf, sizeof buf, "degenerate element %d (%s): zero length / zero normal / det J <= 0",
-             e, e < h->n_beams ? "beam" : "quad");
-    h->err = buf;
-    return SSO_E_DEGENERATE;
+// ---------------------------------------------------------------------------
+// Transports: halo exchange of a per-part vector and allreduce of CgState::red.
+// ---------------------------------------------------------------------------
+enum VecId { V_P = 0, V_X = 1, V_GU = 2, V_TMP = 3 };
+
+double* vec_of(Part& P, int v) {
+  switch (v) {
+    case V_P: return P.p;
+    case V_X: return P.xs;
+    case V_GU: return P.gu;
+    default: return P.tmp;
   }
-  if (h->h_flags->singular_dof != INT_MAX) {
-    int d = h->h_flags->singular_dof;
-    char buf[256];
-    snprintf(buf, sizeof buf, "singular: free DOF %d (node %d, component %d) has diagonal <= 0", d,
-             d / 6, d % 6);
-    h->err = buf;
-    return SSO_E_SINGULAR;
+}
+
+int exchange(sso_ctx* h, int v) {
+  if (!h->distributed()) return SSO_OK;
+  long long g0 = g_launches;
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    launch_pack(h->stream, (int)P.n_send, P.send_idx, vec_of(P, v), P.sendbuf);
+  }
+  if (h->nranks == 1) {
+    // local transport: copy every neighbour's packed values into my halo
+    for (auto& pp : h->parts) {
+      Part& P = *pp;
+      double* dst = vec_of(P, v);
+      for (const NeighborPlan& nb : P.lm.nbrs) {
+        if (nb.recv_count == 0) continue;
+        Part& Q = *h->parts[nb.part];
+        size_t k = 0;
+        while (k < Q.lm.nbrs.size() && Q.lm.nbrs[k].part != P.lm.part) ++k;
+        if (k == Q.lm.nbrs.size() || (int64_t)Q.lm.nbrs[k].send_local.size() != nb.recv_count) {
+          h->err = "halo plan mismatch between parts";
+          return SSO_E_STATE;
+        }
+        CK(h, cudaMemcpyAsync(dst + 6 * ((int64_t)P.n_own + nb.recv_offset), Q.sendbuf + 6 * Q.send_off[k],
+                              (size_t)6 * nb.recv_count * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+      }
+    }
+  } else {
+    Part& P = h->P0();
+    double* dst = vec_of(P, v);
+    CKN(h, nccl().GroupStart());
+    for (size_t k = 0; k < P.lm.nbrs.size(); ++k) {
+      const NeighborPlan& nb = P.lm.nbrs[k];
+      if (!nb.send_local.empty())
+        CKN(h, nccl().Send(P.sendbuf + 6 * P.send_off[k], 6 * nb.send_local.size(), ncclDouble, nb.part,
+                           h->comm, h->stream));
+      if (nb.recv_count)
+        CKN(h, nccl().Recv(dst + 6 * ((int64_t)P.n_own + nb.recv_offset), (size_t)6 * nb.recv_count,
+                           ncclDouble, nb.part, h->comm, h->stream));
+    }
+    CKN(h, nccl().GroupEnd());
+  }
+  h->launches += g_launches - g0;
+  return SSO_OK;
+}
+
+int allreduce(sso_ctx* h, int nvals) {
+  if (!h->distributed()) return SSO_OK;
+  long long g0 = g_launches;
+  if (h->nranks == 1) {
+    launch_allreduce_parts(h->stream, h->d_sts, (int)h->parts.size(), nvals);
+  } else {
+    double* red = h->P0().st->red;
+    CKN(h, nccl().AllReduce(red, red, nvals, ncclDouble, ncclSum, h->comm, h->stream));
+  }
+  h->launches += g_launches - g0;
+  return SSO_OK;
+}
+
+int check_flags(sso_ctx* h) {
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    CK(h, cudaMemcpyAsync(h->h_flags, P.flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, h->stream));
+    int rc = sync(h);
+    if (rc) return rc;
+    if (h->h_flags->degenerate_elem != INT_MAX) {
+      const int e = h->h_flags->degenerate_elem;
+      const bool beam = e < P.n_beams;
+      const int g = beam ? P.lm.beam_gid[e] : P.lm.quad_gid[e - P.n_beams];
+      char buf[256];
+      snprintf(buf, sizeof buf, "degenerate element %d (%s %d): zero length / zero normal / det J <= 0",
+               beam ? g : h->g_beams + g, beam ? "beam" : "quad", g);
+      h->err = buf;
+      return SSO_E_DEGENERATE;
+    }
+    if (h->h_flags->singular_dof != INT_MAX) {
+      const int d = h->h_flags->singular_dof;
+      const int gnode = P.lm.node_gid[d / 6];
+      char buf[256];
+      snprintf(buf, sizeof buf, "singular: free DOF %d (node %d, component %d) has diagonal <= 0",
+               6 * gnode + d % 6, gnode, d % 6);
+      h->err = buf;
+      return SSO_E_SINGULAR;
+    }
   }
   return SSO_OK;
 }
@@ -226,15 +387,18 @@ int check_flags(sso_ctx* h) {
 int reset_flags(sso_ctx* h) {
   h->h_flags->degenerate_elem = INT_MAX;
   h->h_flags->singular_dof = INT_MAX;
-  CK(h, cudaMemcpyAsync(h->flags, h->h_flags, sizeof(DevFlags), cudaMemcpyHostToDevice, h->stream));
-  return SSO_OK;
+  for (auto& pp : h->parts)
+    CK(h, cudaMemcpyAsync(pp->flags, h->h_flags, sizeof(DevFlags), cudaMemcpyHostToDevice, h->stream));
+  return sync(h);
 }
 
-// Capture K = check_every CG iterations into a graph.  prof_slot >= 0 adds
-// external event-record nodes around every PROF_EVERY-th SpMV (events of that
-// slot): a live sample of the SpMV launch duration that costs < 0.5 % of the step.
+// Capture K = check_every CG iterations of the single-part solver into a graph.
+// prof_slot >= 0 adds external event-record nodes around every PROF_EVERY-th
+// SpMV (events of that slot): a live sample of the SpMV launch duration.
 constexpr int PROF_EVERY = 16;
+
 int build_chunk_graph(sso_ctx* h, int prof_slot, cudaGraphExec_t* out) {
+  Part& P = h->P0();
   if (*out) {
     cudaGraphExecDestroy(*out);
     *out = nullptr;
@@ -252,14 +416,11 @@ int build_chunk_graph(sso_ctx* h, int prof_slot, cudaGraphExec_t* out) {
   CK(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
   for (int i = 0; i < K; ++i) {
     const bool rec = prof_slot >= 0 && (i % PROF_EVERY) == 0;
-    if (rec)
-      cudaEventRecordWithFlags(h->chunk_ev[prof_slot][2 * i], h->cap_stream, cudaEventRecordExternal);
-    launch_spmv_dot(h->cap_stream, h->n_nodes, h->node_ptr, h->node_col, h->vals, h->p, h->q,
-                    h->partial, h->st);
-    if (rec)
-      cudaEventRecordWithFlags(h->chunk_ev[prof_slot][2 * i + 1], h->cap_stream, cudaEventRecordExternal);
-    launch_cg_update(h->cap_stream, (int)h->ndof, h->dinv, h->xs, h->r, h->p, h->q, h->partial, h->st);
-    launch_cg_pupdate(h->cap_stream, (int)h->ndof, h->dinv, h->r, h->p, h->st);
+    if (rec) cudaEventRecordWithFlags(h->chunk_ev[prof_slot][2 * i], h->cap_stream, cudaEventRecordExternal);
+    launch_spmv_dot(h->cap_stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.p, P.q, P.partial, P.st);
+    if (rec) cudaEventRecordWithFlags(h->chunk_ev[prof_slot][2 * i + 1], h->cap_stream, cudaEventRecordExternal);
+    launch_cg_update(h->cap_stream, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st);
+    launch_cg_pupdate(h->cap_stream, (int)P.ndof_own, P.dinv, P.r, P.p, P.st);
   }
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
@@ -278,17 +439,25 @@ int build_chunk_graph(sso_ctx* h, int prof_slot, cudaGraphExec_t* out) {
   return SSO_OK;
 }
 
-int free_all(sso_ctx* h) {
-  void* ptrs[] = {h->x, h->y, h->z, h->beam_conn, h->quad_conn, h->A, h->Iy, h->Iz, h->J, h->t,
-                  h->E, h->nu, h->G, h->fixed_mask, h->node_ptr, h->node_col, h->contrib_ptr,
-                  h->contrib, h->inc_ptr, h->inc_slot, h->stage, h->vals, h->dinv, h->f, h->fbc,
-                  h->xs, h->r, h->p, h->q, h->tmp, h->gu, h->gf, h->partial, h->st, h->flags,
-                  h->tickets, h->scal, h->slot_partial, h->dxyz, h->dt};
+void free_part(Part& P) {
+  void* ptrs[] = {P.x, P.y, P.z, P.beam_conn, P.quad_conn, P.A, P.Iy, P.Iz, P.J, P.t, P.E, P.nu, P.G,
+                  P.fixed_mask, P.node_ptr, P.node_col, P.contrib_ptr, P.contrib, P.inc_ptr,
+                  P.inc_slot, P.stage, P.vals, P.dinv, P.f, P.fbc, P.xs, P.r, P.p, P.q, P.tmp, P.gu,
+                  P.gf, P.partial, P.st, P.flags, P.tickets, P.scal, P.slot_partial, P.dxyz, P.dt,
+                  P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+}
+
+void free_all(sso_ctx* h) {
+  for (auto& pp : h->parts) free_part(*pp);
+  h->parts.clear();
+  if (h->d_sts) cudaFree(h->d_sts);
+  if (h->d_dt_all) cudaFree(h->d_dt_all);
+  if (h->h_C) cudaFreeHost(h->h_C);
   if (h->h_st) cudaFreeHost(h->h_st);
-  if (h->h_scal) cudaFreeHost(h->h_scal);
   if (h->h_chunk) cudaFreeHost(h->h_chunk);
+  if (h->h_scal) cudaFreeHost(h->h_scal);
   if (h->h_flags) cudaFreeHost(h->h_flags);
   if (h->chunk_exec) cudaGraphExecDestroy(h->chunk_exec);
   for (int k = 0; k < 2; ++k) {
@@ -300,9 +469,9 @@ int free_all(sso_ctx* h) {
   if (h->ev_b) cudaEventDestroy(h->ev_b);
   for (auto e : h->ev_done)
     if (e) cudaEventDestroy(e);
+  if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
-  return SSO_OK;
 }
 
 int validate(const sso_mesh* m, const sso_sections* s, const sso_materials* mt,
@@ -350,12 +519,187 @@ int validate(const sso_mesh* m, const sso_sections* s, const sso_materials* mt,
   return SSO_OK;
 }
 
+std::vector<int32_t> make_ranges(int32_t n_nodes, int32_t n_parts, const int32_t* given) {
+  std::vector<int32_t> r((size_t)n_parts + 1);
+  if (given) {
+    for (int32_t p = 0; p <= n_parts; ++p) r[p] = given[p];
+  } else {
+    for (int32_t p = 0; p <= n_parts; ++p) r[p] = (int32_t)(((int64_t)n_nodes * p) / n_parts);
+  }
+  return r;
+}
+
+// Build one part's device state from the (validated) global inputs.
+int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* sec,
+               const sso_materials* mat, const std::vector<uint8_t>& gmask,
+               const std::vector<double>& gG) {
+  const LocalMesh& L = P.lm;
+  P.n_nodes = (int32_t)L.node_gid.size();
+  P.n_own = L.n_own;
+  P.n_beams = (int32_t)L.beam_gid.size();
+  P.n_quads = (int32_t)L.quad_gid.size();
+  P.n_own_quads = (int32_t)L.own_quad_local.size();
+  P.ndof = 6 * (int64_t)P.n_nodes;
+  P.ndof_own = 6 * (int64_t)P.n_own;
+  std::string perr = build_pattern(P.n_nodes, P.n_beams, L.beam_conn.data(), P.n_quads,
+                                   L.quad_conn.data(), P.pat);
+  if (!perr.empty()) { h->err = perr; return SSO_E_INVALID; }
+  P.n_blocks = P.pat.n_blocks();
+  P.n_staged = P.pat.n_staged_blocks();
+  P.n_slots = 2 * (int64_t)P.n_beams + 4 * (int64_t)P.n_quads;
+  P.nnz = 36 * (P.pat.node_ptr[P.n_own]);  // owned rows only
+  const int64_t ne = (int64_t)P.n_beams + P.n_quads;
+  std::vector<double> x(P.n_nodes), y(P.n_nodes), z(P.n_nodes);
+  std::vector<uint8_t> mask(P.n_nodes);
+  for (int32_t i = 0; i < P.n_nodes; ++i) {
+    const int32_t g = L.node_gid[i];
+    x[i] = mesh->x[g];
+    y[i] = mesh->y[g];
+    z[i] = mesh->z[g];
+    mask[i] = gmask[g];
+  }
+  std::vector<double> A(P.n_beams), Iy(P.n_beams), Iz(P.n_beams), Jt(P.n_beams), t(P.n_quads);
+  std::vector<double> E(ne), nu(ne), G(ne);
+  for (int32_t k = 0; k < P.n_beams; ++k) {
+    const int32_t g = L.beam_gid[k];
+    A[k] = sec->A[g];
+    Iy[k] = sec->Iy[g];
+    Iz[k] = sec->Iz[g];
+    Jt[k] = sec->J[g];
+    E[k] = mat->E[g];
+    nu[k] = mat->nu[g];
+    G[k] = gG[g];
+  }
+  for (int32_t k = 0; k < P.n_quads; ++k) {
+    const int32_t g = L.quad_gid[k];
+    t[k] = sec->t[g];
+    E[P.n_beams + k] = mat->E[mesh->n_beams + g];
+    nu[P.n_beams + k] = mat->nu[mesh->n_beams + g];
+    G[P.n_beams + k] = gG[mesh->n_beams + g];
+  }
+  std::vector<int32_t> own_gid(P.n_own_quads);
+  for (int32_t k = 0; k < P.n_own_quads; ++k) own_gid[k] = L.quad_gid[L.own_quad_local[k]];
+  std::vector<int32_t> send;
+  P.send_off.clear();
+  for (const NeighborPlan& nb : L.nbrs) {
+    P.send_off.push_back((int64_t)send.size());
+    send.insert(send.end(), nb.send_local.begin(), nb.send_local.end());
+  }
+  P.n_send = (int64_t)send.size();
+
+  int r;
+#define UP(dst, src, n) if ((r = upload(h, &P.dst, src, n))) return r
+#define AL(dst, n) if ((r = dalloc(h, &P.dst, n))) return r
+  UP(x, x.data(), P.n_nodes);
+  UP(y, y.data(), P.n_nodes);
+  UP(z, z.data(), P.n_nodes);
+  UP(beam_conn, L.beam_conn.data(), 2 * (int64_t)P.n_beams);
+  UP(quad_conn, L.quad_conn.data(), 4 * (int64_t)P.n_quads);
+  UP(A, A.data(), P.n_beams);
+  UP(Iy, Iy.data(), P.n_beams);
+  UP(Iz, Iz.data(), P.n_beams);
+  UP(J, Jt.data(), P.n_beams);
+  UP(t, t.data(), P.n_quads);
+  UP(E, E.data(), ne);
+  UP(nu, nu.data(), ne);
+  UP(G, G.data(), ne);
+  UP(fixed_mask, mask.data(), P.n_nodes);
+  UP(node_ptr, P.pat.node_ptr.data(), P.n_nodes + 1);
+  UP(node_col, P.pat.node_col.data(), P.n_blocks);
+  UP(contrib_ptr, P.pat.contrib_ptr.data(), P.n_blocks + 1);
+  UP(contrib, P.pat.contrib.data(), P.n_staged);
+  UP(inc_ptr, P.pat.inc_ptr.data(), P.n_nodes + 1);
+  UP(inc_slot, P.pat.inc_slot.data(), P.n_slots);
+  UP(own_quad_local, L.own_quad_local.data(), P.n_own_quads);
+  UP(own_quad_gid, own_gid.data(), P.n_own_quads);
+  UP(send_idx, send.data(), P.n_send);
+  AL(sendbuf, 6 * std::max<int64_t>(P.n_send, 1));
+  AL(stage, 36 * P.n_staged);
+  AL(vals, 36 * P.n_blocks);
+  AL(dinv, P.ndof);
+  AL(f, P.ndof);
+  AL(fbc, P.ndof);
+  AL(xs, P.ndof);
+  AL(r, P.ndof);
+  AL(p, P.ndof);
+  AL(q, P.ndof);
+  AL(tmp, P.ndof);
+  AL(gu, P.ndof);
+  AL(gf, P.ndof);
+  AL(partial, 16 * (int64_t)cg_grid());
+  AL(st, 1);
+  AL(flags, 1);
+  AL(tickets, 16);
+  AL(scal, 8);
+  AL(slot_partial, 3 * std::max<int64_t>(P.n_slots, 1));
+  AL(dxyz, 3 * (int64_t)P.n_nodes);
+  AL(dt, std::max<int32_t>(P.n_quads, 1));
+  AL(dt_own, std::max<int32_t>(P.n_own_quads, 1));
+#undef UP
+#undef AL
+  CK(h, cudaMemset(P.tickets, 0, 16 * sizeof(unsigned)));
+  CK(h, cudaMemset(P.st, 0, sizeof(CgState)));
+  CK(h, cudaMemset(P.xs, 0, P.ndof * sizeof(double)));
+  CK(h, cudaMemset(P.p, 0, P.ndof * sizeof(double)));
+  CK(h, cudaMemset(P.gu, 0, P.ndof * sizeof(double)));
+  CK(h, cudaMemset(P.gf, 0, P.ndof * sizeof(double)));
+  CK(h, cudaMemset(P.f, 0, P.ndof * sizeof(double)));
+  P.pat.contrib.clear();  // only needed on the device
+  P.pat.contrib.shrink_to_fit();
+  P.pat.inc_slot.clear();
+  P.pat.inc_slot.shrink_to_fit();
+  return SSO_OK;
+}
+
+// --- user buffers <-> parts ------------------------------------------------
+// 6-DOF vectors: the user buffer covers nodes [user_node_begin, +user_nodes);
+// every part owns a contiguous global node range inside it.
+int vec_in(sso_ctx* h, const double* src, double* Part::*dst) {
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    const int64_t off = 6 * (int64_t)(P.lm.own_begin - h->user_node_begin);
+    CK(h, cudaMemcpyAsync(P.*dst, src + off, (size_t)P.ndof_own * sizeof(double), kind_in(h), h->stream));
+  }
+  return SSO_OK;
+}
+
+int vec_out(sso_ctx* h, double* dst, double* Part::*src) {
+  if (!dst) return SSO_OK;
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    const int64_t off = 6 * (int64_t)(P.lm.own_begin - h->user_node_begin);
+    CK(h, cudaMemcpyAsync(dst + off, P.*src, (size_t)P.ndof_own * sizeof(double), kind_out(h), h->stream));
+  }
+  return SSO_OK;
+}
+
+// Per-node / per-quad design arrays (global): parts take their local entries by global id.
+int design_in(sso_ctx* h, const double* src, int64_t n_global, double* Part::*dst, bool quads) {
+  if (h->nranks > 1) FAIL(h, SSO_E_INVALID, "sso_set_design is not supported on multi-rank handles");
+  if (h->parts.size() == 1) {
+    CK(h, cudaMemcpyAsync(h->P0().*dst, src, (size_t)n_global * sizeof(double), kind_in(h), h->stream));
+    return SSO_OK;
+  }
+  std::vector<double> all((size_t)n_global);
+  CK(h, cudaMemcpy(all.data(), src, all.size() * sizeof(double),
+                   h->mem == SSO_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost));
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    const std::vector<int32_t>& gid = quads ? P.lm.quad_gid : P.lm.node_gid;
+    std::vector<double> loc(gid.size());
+    for (size_t i = 0; i < gid.size(); ++i) loc[i] = all[gid[i]];
+    CK(h, cudaMemcpy(P.*dst, loc.data(), loc.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  return SSO_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
 int sso_options_default(sso_options* o) {
   if (!o) return SSO_E_INVALID;
+  std::memset(o, 0, sizeof(*o));
   o->rtol = 1e-10;
   o->max_iter = 200000;
   o->drill_alpha = 1e-3;
@@ -364,10 +708,30 @@ int sso_options_default(sso_options* o) {
   o->mem = SSO_MEM_HOST;
   o->cuda_stream = nullptr;
   o->device = -1;
+  o->n_parts = 1;
+  o->part_ranges = nullptr;
+  o->nranks = 1;
+  o->rank = 0;
+  o->nccl_unique_id = nullptr;
   return SSO_OK;
 }
 
 const char* sso_last_error(sso_handle h) { return h ? h->err.c_str() : g_create_err.c_str(); }
+
+int sso_nccl_unique_id(void* out) {
+  if (!out) return SSO_E_INVALID;
+  if (!nccl().ok) {
+    g_create_err = nccl().err;
+    return SSO_E_NCCL;
+  }
+  ncclUniqueId id;
+  if (nccl().GetUniqueId(&id) != ncclSuccess) {
+    g_create_err = "ncclGetUniqueId failed";
+    return SSO_E_NCCL;
+  }
+  std::memcpy(out, &id, sizeof(id));
+  return SSO_OK;
+}
 
 int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_materials* mat,
                const sso_supports* sup, const sso_options* opt, sso_handle* out) {
@@ -383,6 +747,24 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
     g_create_err = "options: rtol, max_iter, check_every and drill_alpha must be > 0";
     return SSO_E_INVALID;
   }
+  if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks || o.n_parts < 1 ||
+      (o.nranks > 1 && o.n_parts != o.nranks && o.n_parts != 1) || o.n_parts > mesh->n_nodes ||
+      o.nranks > mesh->n_nodes) {
+    g_create_err = "options: need 1 <= n_parts <= n_nodes, 0 <= rank < nranks, and n_parts == nranks (or 1) when nranks > 1";
+    return SSO_E_INVALID;
+  }
+  const int32_t n_parts_total = std::max(o.n_parts, o.nranks);
+  std::vector<int32_t> ranges = make_ranges(mesh->n_nodes, n_parts_total, o.part_ranges);
+  for (int32_t p = 0; p < n_parts_total; ++p)
+    if (ranges[p + 1] <= ranges[p] || ranges[0] != 0 || ranges[n_parts_total] != mesh->n_nodes) {
+      g_create_err = "options: part_ranges must be strictly increasing from 0 to n_nodes";
+      return SSO_E_INVALID;
+    }
+  if (o.nranks > 1 && !o.nccl_unique_id) {
+    g_create_err = "options: nranks > 1 needs nccl_unique_id";
+    return SSO_E_INVALID;
+  }
+
   sso_ctx* h = new sso_ctx();
   auto bail = [&](int code) {
     g_create_err = h->err;
@@ -390,18 +772,21 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
     delete h;
     return code;
   };
-  if (o.device >= 0) {
-    if (cudaSetDevice(o.device) != cudaSuccess) { h->err = "cudaSetDevice failed"; return bail(SSO_E_CUDA); }
-  }
-  if (cudaGetDevice(&h->device) != cudaSuccess) { h->err = "no CUDA device"; return bail(SSO_E_CUDA); }
+  if (o.device >= 0 && cudaSetDevice(o.device) != cudaSuccess) { h->err = "cudaSetDevice failed"; return bail(SSO_E_CUDA); }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) { h->err = "no CUDA device"; return bail(SSO_E_CUDA); }
+  if (cudaGetDevice(&h->device) != cudaSuccess) { h->err = "no CUDA device"; return bail(SSO_E_CUDA); }
   h->rtol = o.rtol;
   h->max_iter = o.max_iter;
   h->drill_alpha = o.drill_alpha;
   h->warm_start = o.warm_start;
   h->check_every = o.check_every;
   h->mem = o.mem;
+  h->nranks = o.nranks;
+  h->rank = o.rank;
+  h->g_nodes = mesh->n_nodes;
+  h->g_beams = mesh->n_beams;
+  h->g_quads = mesh->n_quads;
   if (o.cuda_stream) {
     h->stream = (cudaStream_t)o.cuda_stream;
   } else {
@@ -410,86 +795,58 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
   }
   if (cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking) != cudaSuccess) { h->err = "stream create failed"; return bail(SSO_E_CUDA); }
 
-  h->n_nodes = mesh->n_nodes;
-  h->n_beams = mesh->n_beams;
-  h->n_quads = mesh->n_quads;
-  h->ndof = 6 * (int64_t)mesh->n_nodes;
-  std::string perr = build_pattern(mesh->n_nodes, mesh->n_beams, mesh->beam_conn, mesh->n_quads,
-                                   mesh->quad_conn, h->pat);
-  if (!perr.empty()) { h->err = perr; return bail(SSO_E_INVALID); }
-  h->n_blocks = h->pat.n_blocks();
-  h->nnz = h->pat.nnz();
-  h->n_staged = h->pat.n_staged_blocks();
-  h->n_slots = 2 * (int64_t)h->n_beams + 4 * (int64_t)h->n_quads;
-  const int64_t ne = (int64_t)h->n_beams + h->n_quads;
+  const int64_t ne = (int64_t)mesh->n_beams + mesh->n_quads;
+  std::vector<double> gG((size_t)ne);
+  for (int64_t e = 0; e < ne; ++e) gG[e] = mat->G ? mat->G[e] : mat->E[e] / (2.0 * (1.0 + mat->nu[e]));
+  std::vector<uint8_t> gmask((size_t)mesh->n_nodes, 0);
+  for (int32_t k = 0; k < sup->n; ++k) gmask[sup->node[k]] |= (uint8_t)(sup->mask6[k] & 63);
 
-  // host-side derived inputs: G (beams), OR-merged support masks
-  std::vector<double> G((size_t)ne);
-  for (int64_t e = 0; e < ne; ++e) G[e] = mat->G ? mat->G[e] : mat->E[e] / (2.0 * (1.0 + mat->nu[e]));
-  std::vector<uint8_t> mask((size_t)h->n_nodes, 0);
-  for (int32_t k = 0; k < sup->n; ++k) mask[sup->node[k]] |= (uint8_t)(sup->mask6[k] & 63);
-
-  int r;
-#define UP(dst, src, n) if ((r = upload(h, &h->dst, src, n))) return bail(r)
-#define AL(dst, n) if ((r = dalloc(h, &h->dst, n))) return bail(r)
-  UP(x, mesh->x, h->n_nodes);
-  UP(y, mesh->y, h->n_nodes);
-  UP(z, mesh->z, h->n_nodes);
-  UP(beam_conn, mesh->beam_conn, 2 * (int64_t)h->n_beams);
-  UP(quad_conn, mesh->quad_conn, 4 * (int64_t)h->n_quads);
-  UP(A, sec->A, h->n_beams);
-  UP(Iy, sec->Iy, h->n_beams);
-  UP(Iz, sec->Iz, h->n_beams);
-  UP(J, sec->J, h->n_beams);
-  UP(t, sec->t, h->n_quads);
-  UP(E, mat->E, ne);
-  UP(nu, mat->nu, ne);
-  UP(G, G.data(), ne);
-  UP(fixed_mask, mask.data(), h->n_nodes);
-  UP(node_ptr, h->pat.node_ptr.data(), h->n_nodes + 1);
-  UP(node_col, h->pat.node_col.data(), h->n_blocks);
-  UP(contrib_ptr, h->pat.contrib_ptr.data(), h->n_blocks + 1);
-  UP(contrib, h->pat.contrib.data(), h->n_staged);
-  UP(inc_ptr, h->pat.inc_ptr.data(), h->n_nodes + 1);
-  UP(inc_slot, h->pat.inc_slot.data(), h->n_slots);
-  AL(stage, 36 * h->n_staged);
-  AL(vals, h->nnz);
-  AL(dinv, h->ndof);
-  AL(f, h->ndof);
-  AL(fbc, h->ndof);
-  AL(xs, h->ndof);
-  AL(r, h->ndof);
-  AL(p, h->ndof);
-  AL(q, h->ndof);
-  AL(tmp, h->ndof);
-  AL(gu, h->ndof);
-  AL(gf, h->ndof);
-  AL(partial, 4 * (int64_t)cg_grid() * 4);
-  AL(st, 1);
-  AL(flags, 1);
-  AL(tickets, 16);
-  AL(scal, 8);
-  AL(slot_partial, 3 * std::max<int64_t>(h->n_slots, 1));
-  AL(dxyz, 3 * (int64_t)h->n_nodes);
-  AL(dt, std::max<int32_t>(h->n_quads, 1));
-#undef UP
-#undef AL
-  if (cudaMemset(h->tickets, 0, 16 * sizeof(unsigned)) != cudaSuccess ||
-      cudaMemset(h->st, 0, sizeof(CgState)) != cudaSuccess ||
-      cudaMemset(h->xs, 0, h->ndof * sizeof(double)) != cudaSuccess) { h->err = "memset failed"; return bail(SSO_E_CUDA); }
+  std::vector<int32_t> mine;
+  if (o.nranks > 1) {
+    mine.push_back(o.rank);
+  } else {
+    for (int32_t p = 0; p < n_parts_total; ++p) mine.push_back(p);
+  }
+  for (int32_t p : mine) {
+    auto P = std::make_unique<Part>();
+    std::string perr = build_local_mesh(mesh->n_nodes, mesh->n_beams, mesh->beam_conn, mesh->n_quads,
+                                        mesh->quad_conn, ranges.data(), n_parts_total, p, P->lm);
+    if (!perr.empty()) { h->err = perr; return bail(SSO_E_INVALID); }
+    h->parts.push_back(std::move(P));
+    const int r = setup_part(h, *h->parts.back(), mesh, sec, mat, gmask, gG);
+    if (r) return bail(r);
+  }
+  if (o.nranks > 1) {
+    h->user_node_begin = ranges[o.rank];
+    h->user_nodes = ranges[o.rank + 1] - ranges[o.rank];
+    h->user_quads = h->P0().n_own_quads;
+  } else {
+    h->user_node_begin = 0;
+    h->user_nodes = mesh->n_nodes;
+    h->user_quads = mesh->n_quads;
+  }
+  {
+    std::vector<CgState*> sts;
+    for (auto& pp : h->parts) sts.push_back(pp->st);
+    int r = upload(h, &h->d_sts, sts.data(), (int64_t)sts.size());
+    if (r) return bail(r);
+    if (h->parts.size() > 1 && (r = dalloc(h, &h->d_dt_all, std::max<int32_t>(mesh->n_quads, 1)))) return bail(r);
+  }
+  if (o.nranks > 1) {
+    if (!nccl().ok) { h->err = nccl().err; return bail(SSO_E_NCCL); }
+    ncclUniqueId id;
+    std::memcpy(&id, o.nccl_unique_id, sizeof(id));
+    if (nccl().CommInitRank(&h->comm, o.nranks, id, o.rank) != ncclSuccess) { h->err = "ncclCommInitRank failed"; return bail(SSO_E_NCCL); }
+  }
   if (cudaMallocHost(&h->h_st, sizeof(CgState)) != cudaSuccess ||
-      cudaMallocHost(&h->h_scal, 8 * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&h->h_chunk, 2 * sizeof(CgState)) != cudaSuccess ||
+      cudaMallocHost(&h->h_scal, 8 * sizeof(double)) != cudaSuccess ||
+      cudaMallocHost(&h->h_C, sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&h->h_flags, sizeof(DevFlags)) != cudaSuccess) { h->err = "cudaMallocHost failed"; return bail(SSO_E_OOM); }
   cudaEventCreate(&h->ev_a);
   cudaEventCreate(&h->ev_b);
   cudaEventCreateWithFlags(&h->ev_done[0], cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->ev_done[1], cudaEventDisableTiming);
-  // the pattern's large contributor / incidence arrays are only needed on the device
-  h->pat.contrib.clear();
-  h->pat.contrib.shrink_to_fit();
-  h->pat.inc_slot.clear();
-  h->pat.inc_slot.shrink_to_fit();
   *out = h;
   return SSO_OK;
 }
@@ -508,10 +865,10 @@ int sso_set_stream(sso_handle h, void* cuda_stream, sso_mem mem) {
 int sso_set_design(sso_handle h, const double* x, const double* y, const double* z, const double* t) {
   if (!h) return SSO_E_INVALID;
   int rc;
-  if (x && (rc = copy_in(h, h->x, x, h->n_nodes))) return rc;
-  if (y && (rc = copy_in(h, h->y, y, h->n_nodes))) return rc;
-  if (z && (rc = copy_in(h, h->z, z, h->n_nodes))) return rc;
-  if (t && (rc = copy_in(h, h->t, t, h->n_quads))) return rc;
+  if (x && (rc = design_in(h, x, h->g_nodes, &Part::x, false))) return rc;
+  if (y && (rc = design_in(h, y, h->g_nodes, &Part::y, false))) return rc;
+  if (z && (rc = design_in(h, z, h->g_nodes, &Part::z, false))) return rc;
+  if (t && (rc = design_in(h, t, h->g_quads, &Part::t, true))) return rc;
   h->assembled = false;
   h->solved = false;
   return sync(h);
@@ -521,18 +878,21 @@ int sso_assemble(sso_handle h) {
   if (!h) return SSO_E_INVALID;
   int rc = reset_flags(h);
   if (rc) return rc;
-  {
-    Scope sc(h, F_ELEMENT);
-    launch_beam_elements(h->stream, h->n_beams, h->x, h->y, h->z, h->beam_conn, h->A, h->Iy, h->Iz,
-                         h->J, h->E, h->G, h->stage, h->flags);
-    launch_quad_elements(h->stream, h->n_quads, h->x, h->y, h->z, h->quad_conn, h->t,
-                         h->E + h->n_beams, h->nu + h->n_beams, h->drill_alpha,
-                         h->stage + 36 * 4 * (int64_t)h->n_beams, h->flags);
-  }
-  {
-    Scope sc(h, F_ASSEMBLE);
-    launch_assemble(h->stream, h->n_nodes, h->node_ptr, h->node_col, h->contrib_ptr, h->contrib,
-                    h->stage, h->fixed_mask, h->vals, h->dinv, h->flags);
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    {
+      Scope sc(h, F_ELEMENT);
+      launch_beam_elements(h->stream, P.n_beams, P.x, P.y, P.z, P.beam_conn, P.A, P.Iy, P.Iz, P.J, P.E,
+                           P.G, P.stage, P.flags);
+      launch_quad_elements(h->stream, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.E + P.n_beams,
+                           P.nu + P.n_beams, h->drill_alpha, P.stage + 36 * 4 * (int64_t)P.n_beams,
+                           P.flags);
+    }
+    {
+      Scope sc(h, F_ASSEMBLE);
+      launch_assemble(h->stream, P.n_own, P.node_ptr, P.node_col, P.contrib_ptr, P.contrib, P.stage,
+                      P.fixed_mask, P.vals, P.dinv, P.flags);
+    }
   }
   CKL(h);
   rc = check_flags(h);
@@ -542,34 +902,10 @@ int sso_assemble(sso_handle h) {
   return SSO_OK;
 }
 
-int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
-  if (!h || !f || !u) {
-    if (h) h->err = "null argument";
-    return SSO_E_INVALID;
-  }
-  if (!h->assembled) FAIL(h, SSO_E_STATE, "sso_solve before sso_assemble");
+// Single-part solve: graph chunks with alpha / beta formed inside the kernels.
+static int solve_single(sso_ctx* h) {
+  Part& P = h->P0();
   int rc;
-  if ((rc = copy_in(h, h->f, f, h->ndof))) return rc;
-  const int warm = h->warm_start ? 1 : 0;
-  if (warm) {
-    if ((rc = copy_in(h, h->xs, u, h->ndof))) return rc;
-    {
-      Scope sc(h, F_UPDATE);
-      launch_zero_fixed(h->stream, (int)h->ndof, h->fixed_mask, h->xs);
-    }
-    Scope sc(h, F_SPMV);
-    launch_spmv(h->stream, h->n_nodes, h->node_ptr, h->node_col, h->vals, h->xs, h->tmp);
-  }
-  std::memset(h->h_st, 0, sizeof(CgState));
-  h->h_st->tol2 = h->rtol * h->rtol;
-  h->h_st->max_iter = h->max_iter;
-  CK(h, cudaMemcpyAsync(h->st, h->h_st, sizeof(CgState), cudaMemcpyHostToDevice, h->stream));
-  CK(h, cudaEventRecord(h->ev_a, h->stream));
-  {
-    Scope sc(h, F_UPDATE);
-    launch_cg_init(h->stream, (int)h->ndof, h->f, h->fixed_mask, h->dinv, h->fbc, h->xs, h->r, h->p,
-                   h->partial, h->st, warm, h->tmp);
-  }
   const bool prof = h->tm.on;
   if (!prof && !h->chunk_exec) {
     if ((rc = build_chunk_graph(h, -1, &h->chunk_exec))) return rc;
@@ -581,15 +917,14 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
   // Device-side loop in chunks of check_every iterations (graph replays); kernels
   // after convergence return immediately.  One chunk is always queued ahead of the
   // state snapshot being polled, so the GPU never idles on the host.  With
-  // profiling on, slot-alternating graphs carry event nodes around every SpMV and
-  // the elapsed times of the iterations that actually ran are accumulated.
+  // profiling on, slot-alternating graphs carry event nodes around every 16th
+  // SpMV and the elapsed times of the sampled iterations that ran are accumulated.
   const int64_t max_chunks = (h->max_iter + h->check_every - 1) / h->check_every + 1;
   int64_t launched = 0;
   auto launch_chunk = [&](int slot) -> int {
     CK(h, cudaGraphLaunch(prof ? h->prof_exec[slot] : h->chunk_exec, h->stream));
     h->launches += h->kernels_per_chunk;
-    CK(h, cudaMemcpyAsync(&h->h_chunk[slot], h->st, sizeof(CgState), cudaMemcpyDeviceToHost,
-                          h->stream));
+    CK(h, cudaMemcpyAsync(&h->h_chunk[slot], P.st, sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaEventRecord(h->ev_done[slot], h->stream));
     ++launched;
     return SSO_OK;
@@ -614,25 +949,110 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
     }
     if (S.done || launched == k + 1) break;
   }
+  return SSO_OK;
+}
+
+// Partitioned solve: per iteration exchange(p), SpMV + local p^T q, allreduce,
+// alpha; updates + local r^T z, r^T r, allreduce, beta / convergence; p update.
+static int solve_dist(sso_ctx* h) {
+  int rc;
+  for (int64_t it = 0;; ++it) {
+    if ((rc = exchange(h, V_P))) return rc;
+    for (auto& pp : h->parts) {
+      Part& P = *pp;
+      Scope sc(h, F_SPMV);
+      launch_spmv_dot(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.p, P.q, P.partial, P.st);
+    }
+    if ((rc = allreduce(h, 1))) return rc;
+    for (auto& pp : h->parts) {
+      Part& P = *pp;
+      Scope sc(h, F_UPDATE);
+      launch_cg_scalar(h->stream, P.st, PH_ALPHA);
+      launch_cg_update(h->stream, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st);
+    }
+    if ((rc = allreduce(h, 2))) return rc;
+    for (auto& pp : h->parts) {
+      Part& P = *pp;
+      Scope sc(h, F_UPDATE);
+      launch_cg_scalar(h->stream, P.st, PH_BETA);
+      launch_cg_pupdate(h->stream, (int)P.ndof_own, P.dinv, P.r, P.p, P.st);
+    }
+    if ((it + 1) % h->check_every == 0 || it >= h->max_iter) {
+      CK(h, cudaMemcpyAsync(h->h_chunk, h->P0().st, sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
+      if ((rc = sync(h))) return rc;
+      if (h->h_chunk[0].done || it >= h->max_iter) break;
+    }
+  }
+  return SSO_OK;
+}
+
+int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
+  if (!h || !f || !u) {
+    if (h) h->err = "null argument";
+    return SSO_E_INVALID;
+  }
+  if (!h->assembled) FAIL(h, SSO_E_STATE, "sso_solve before sso_assemble");
+  int rc;
+  const bool dist = h->distributed();
+  if ((rc = vec_in(h, f, &Part::f))) return rc;
+  const int warm = h->warm_start ? 1 : 0;
+  if (warm) {
+    if ((rc = vec_in(h, u, &Part::xs))) return rc;
+    for (auto& pp : h->parts) {
+      Scope sc(h, F_UPDATE);
+      launch_zero_fixed(h->stream, (int)pp->ndof_own, pp->fixed_mask, pp->xs);
+    }
+    if ((rc = exchange(h, V_X))) return rc;
+    for (auto& pp : h->parts) {
+      Part& P = *pp;
+      Scope sc(h, F_SPMV);
+      launch_spmv(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.xs, P.tmp);
+    }
+  }
+  std::memset(h->h_st, 0, sizeof(CgState));
+  h->h_st->tol2 = h->rtol * h->rtol;
+  h->h_st->max_iter = h->max_iter;
+  h->h_st->dist = dist ? 1 : 0;
+  for (auto& pp : h->parts)
+    CK(h, cudaMemcpyAsync(pp->st, h->h_st, sizeof(CgState), cudaMemcpyHostToDevice, h->stream));
+  // the pinned staging struct is reused below: make the uploads complete first
+  if ((rc = sync(h))) return rc;
+  CK(h, cudaEventRecord(h->ev_a, h->stream));
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    Scope sc(h, F_UPDATE);
+    launch_cg_init(h->stream, (int)P.ndof_own, P.f, P.fixed_mask, P.dinv, P.fbc, P.xs, P.r, P.p,
+                   P.partial, P.st, warm, P.tmp);
+  }
+  if (dist) {
+    if ((rc = allreduce(h, 3))) return rc;
+    long long g0 = g_launches;
+    for (auto& pp : h->parts) launch_cg_scalar(h->stream, pp->st, PH_INIT);
+    h->launches += g_launches - g0;
+  }
+  rc = dist ? solve_dist(h) : solve_single(h);
+  if (rc) return rc;
   CK(h, cudaEventRecord(h->ev_b, h->stream));
-  // true residual |f_bc - K x| / |f_bc|
-  {
+  // true residual |f_bc - K x| / |f_bc|: local sums of squares into red[0], allreduced
+  if ((rc = exchange(h, V_X))) return rc;
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
     long long g1 = g_launches;
-    launch_spmv(h->stream, h->n_nodes, h->node_ptr, h->node_col, h->vals, h->xs, h->tmp);
-    launch_residual_norm(h->stream, (int)h->ndof, h->fbc, h->tmp, h->partial, h->tickets + 2, h->scal);
+    launch_spmv(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.xs, P.tmp);
+    launch_residual_norm(h->stream, (int)P.ndof_own, P.fbc, P.tmp, P.partial, P.tickets + 2, &P.st->red[0]);
     h->launches += g_launches - g1;
   }
-  CK(h, cudaMemcpyAsync(h->h_scal, h->scal, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  CK(h, cudaMemcpyAsync(h->h_st, h->st, sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
-  if ((rc = copy_out(h, u, h->xs, h->ndof))) return rc;
+  if ((rc = allreduce(h, 1))) return rc;
+  CK(h, cudaMemcpyAsync(h->h_st, h->P0().st, sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
+  if ((rc = vec_out(h, u, &Part::xs))) return rc;
   if ((rc = sync(h))) return rc;
   CKL(h);
   const CgState& S = *h->h_st;
-  int status = S.done ? S.status : SSO_E_NOT_CONVERGED;
+  const int status = S.done ? S.status : SSO_E_NOT_CONVERGED;
   if (info) {
     info->iters = S.iter;
     info->rel_res = S.ff > 0 ? std::sqrt(S.rr / S.ff) : 0.0;
-    info->true_rel_res = S.ff > 0 ? std::sqrt(h->h_scal[0] / S.ff) : 0.0;
+    info->true_rel_res = S.ff > 0 ? std::sqrt(S.red[0] / S.ff) : 0.0;
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, h->ev_a, h->ev_b) != cudaSuccess) (void)cudaGetLastError();
     info->ms = ms;
@@ -651,37 +1071,67 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
   return SSO_OK;
 }
 
-static int grad_impl(sso_ctx* h, sso_objective obj, const double* dF, const double* dU, double* C,
+// Objective + gradient at the parts' (fv, uvec) state (owned entries set; halos exchanged here).
+static int grad_impl(sso_ctx* h, sso_objective obj, double* Part::*fv, int uvec, double* C,
                      double* dC_dxyz, double* dC_dt) {
   const double s = (obj == SSO_OBJ_STRAIN_ENERGY) ? 0.5 : 1.0;
-  {
-    Scope sc(h, F_REDUCE);
-    launch_dot(h->stream, (int)h->ndof, dF, dU, s, h->partial, h->tickets + 3, h->scal + 1);
-  }
-  {
-    Scope sc(h, F_GRAD);
-    launch_beam_grad(h->stream, h->n_beams, h->x, h->y, h->z, h->beam_conn, h->A, h->Iy, h->Iz, h->J,
-                     h->E, h->G, dU, s, h->slot_partial);
-    launch_quad_grad(h->stream, h->n_beams, h->n_quads, h->x, h->y, h->z, h->quad_conn, h->t, h->E,
-                     h->nu, h->drill_alpha, dU, s, h->slot_partial, h->dt);
-  }
-  {
-    Scope sc(h, F_REDUCE);
-    launch_node_reduce(h->stream, h->n_nodes, h->inc_ptr, h->inc_slot, h->slot_partial, h->dxyz);
-  }
-  CKL(h);
   int rc;
-  if (C) {
-    CK(h, cudaMemcpyAsync(h->h_scal + 1, h->scal + 1, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if ((rc = exchange(h, uvec))) return rc;
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    double* U = vec_of(P, uvec);
+    {
+      Scope sc(h, F_REDUCE);
+      launch_dot_local(h->stream, (int)P.ndof_own, P.*fv, U, P.partial, P.tickets + 3, &P.st->red[0]);
+    }
+    {
+      Scope sc(h, F_GRAD);
+      launch_beam_grad(h->stream, P.n_beams, P.x, P.y, P.z, P.beam_conn, P.A, P.Iy, P.Iz, P.J, P.E, P.G,
+                       U, s, P.slot_partial);
+      launch_quad_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.E, P.nu,
+                       h->drill_alpha, U, s, P.slot_partial, P.dt);
+    }
+    {
+      Scope sc(h, F_REDUCE);
+      launch_node_reduce(h->stream, P.n_own, P.inc_ptr, P.inc_slot, P.slot_partial, P.dxyz);
+      if (h->distributed()) launch_gather(h->stream, P.n_own_quads, P.own_quad_local, P.dt, P.dt_own);
+    }
   }
-  if (dC_dxyz && (rc = copy_out(h, dC_dxyz, h->dxyz, 3 * (int64_t)h->n_nodes))) return rc;
-  if (dC_dt && (rc = copy_out(h, dC_dt, h->dt, h->n_quads))) return rc;
-  if ((rc = sync(h))) return rc;
-  if (C) {
-    if (h->mem == SSO_MEM_HOST) {
-      *C = h->h_scal[1];
+  if ((rc = allreduce(h, 1))) return rc;
+  CKL(h);
+  if (dC_dxyz) {
+    for (auto& pp : h->parts) {
+      Part& P = *pp;
+      for (int a = 0; a < 3; ++a)
+        CK(h, cudaMemcpyAsync(dC_dxyz + (int64_t)a * h->user_nodes + (P.lm.own_begin - h->user_node_begin),
+                              P.dxyz + (int64_t)a * P.n_own, (size_t)P.n_own * sizeof(double), kind_out(h),
+                              h->stream));
+    }
+  }
+  if (dC_dt && h->user_quads > 0) {
+    if (!h->distributed()) {
+      CK(h, cudaMemcpyAsync(dC_dt, h->P0().dt, (size_t)h->user_quads * sizeof(double), kind_out(h), h->stream));
+    } else if (h->nranks > 1) {
+      CK(h, cudaMemcpyAsync(dC_dt, h->P0().dt_own, (size_t)h->user_quads * sizeof(double), kind_out(h), h->stream));
     } else {
-      CK(h, cudaMemcpy(C, h->scal + 1, sizeof(double), cudaMemcpyDeviceToDevice));
+      long long g0 = g_launches;
+      for (auto& pp : h->parts) {
+        Part& P = *pp;
+        launch_scatter(h->stream, P.n_own_quads, P.own_quad_gid, P.dt_own, h->d_dt_all);
+      }
+      h->launches += g_launches - g0;
+      CK(h, cudaMemcpyAsync(dC_dt, h->d_dt_all, (size_t)h->user_quads * sizeof(double), kind_out(h), h->stream));
+    }
+  }
+  CK(h, cudaMemcpyAsync(h->h_C, &h->P0().st->red[0], sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if ((rc = sync(h))) return rc;
+  CKL(h);
+  if (C) {
+    const double v = s * h->h_C[0];
+    if (h->mem == SSO_MEM_HOST) {
+      *C = v;
+    } else {
+      CK(h, cudaMemcpy(C, &v, sizeof(double), cudaMemcpyHostToDevice));
     }
   }
   return SSO_OK;
@@ -691,7 +1141,7 @@ int sso_grad(sso_handle h, sso_objective obj, double* C, double* dC_dxyz, double
   if (!h) return SSO_E_INVALID;
   if (obj != SSO_OBJ_COMPLIANCE && obj != SSO_OBJ_STRAIN_ENERGY) FAIL(h, SSO_E_INVALID, "unknown objective");
   if (!h->solved) FAIL(h, SSO_E_STATE, "sso_grad before a successful sso_solve");
-  return grad_impl(h, obj, h->f, h->xs, C, dC_dxyz, dC_dt);
+  return grad_impl(h, obj, &Part::f, V_X, C, dC_dxyz, dC_dt);
 }
 
 int sso_grad_at(sso_handle h, sso_objective obj, const double* f, const double* u, double* C,
@@ -699,76 +1149,113 @@ int sso_grad_at(sso_handle h, sso_objective obj, const double* f, const double* 
   if (!h || !f || !u) return SSO_E_INVALID;
   if (obj != SSO_OBJ_COMPLIANCE && obj != SSO_OBJ_STRAIN_ENERGY) FAIL(h, SSO_E_INVALID, "unknown objective");
   int rc;
-  if ((rc = copy_in(h, h->gf, f, h->ndof))) return rc;
-  if ((rc = copy_in(h, h->gu, u, h->ndof))) return rc;
-  return grad_impl(h, obj, h->gf, h->gu, C, dC_dxyz, dC_dt);
+  if ((rc = vec_in(h, f, &Part::gf))) return rc;
+  if ((rc = vec_in(h, u, &Part::gu))) return rc;
+  return grad_impl(h, obj, &Part::gf, V_GU, C, dC_dxyz, dC_dt);
 }
 
 int sso_spmv(sso_handle h, const double* xin, double* yout) {
   if (!h || !xin || !yout) return SSO_E_INVALID;
   if (!h->assembled) FAIL(h, SSO_E_STATE, "sso_spmv before sso_assemble");
   int rc;
-  if ((rc = copy_in(h, h->gu, xin, h->ndof))) return rc;
-  {
+  if ((rc = vec_in(h, xin, &Part::gu))) return rc;
+  if ((rc = exchange(h, V_GU))) return rc;
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
     Scope sc(h, F_SPMV);
-    launch_spmv(h->stream, h->n_nodes, h->node_ptr, h->node_col, h->vals, h->gu, h->tmp);
+    launch_spmv(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.gu, P.tmp);
   }
   CKL(h);
-  if ((rc = copy_out(h, yout, h->tmp, h->ndof))) return rc;
+  if ((rc = vec_out(h, yout, &Part::tmp))) return rc;
   return sync(h);
 }
 
 int sso_sizes(sso_handle h, int64_t* ndof, int64_t* nnz, int64_t* n_blocks) {
   if (!h) return SSO_E_INVALID;
-  if (ndof) *ndof = h->ndof;
-  if (nnz) *nnz = h->nnz;
-  if (n_blocks) *n_blocks = h->n_blocks;
+  int64_t d = 0, z = 0, b = 0;
+  for (auto& pp : h->parts) {
+    d += pp->ndof_own;
+    z += pp->nnz;
+    b += pp->pat.node_ptr[pp->n_own];
+  }
+  if (ndof) *ndof = d;
+  if (nnz) *nnz = z;
+  if (n_blocks) *n_blocks = b;
+  return SSO_OK;
+}
+
+int sso_part_info(sso_handle h, int32_t* n_parts_here, int32_t* own_node_begin, int32_t* own_nodes,
+                  int32_t* own_quads) {
+  if (!h) return SSO_E_INVALID;
+  if (n_parts_here) *n_parts_here = (int32_t)h->parts.size();
+  if (own_node_begin) *own_node_begin = h->user_node_begin;
+  if (own_nodes) *own_nodes = h->user_nodes;
+  if (own_quads) *own_quads = h->user_quads;
   return SSO_OK;
 }
 
 int sso_export_csr(sso_handle h, int64_t* row_ptr, int32_t* col_idx, double* vals) {
   if (!h) return SSO_E_INVALID;
-  const HostPattern& P = h->pat;
-  if (row_ptr || col_idx) {
-    for (int32_t n = 0; n < h->n_nodes; ++n) {
-      const int64_t b0 = P.node_ptr[n];
-      const int64_t deg = P.node_ptr[n + 1] - b0;
-      for (int a = 0; a < 6; ++a) {
-        const int64_t start = 36 * b0 + 6 * a * deg;
-        if (row_ptr) row_ptr[6 * (int64_t)n + a] = start;
-        if (col_idx)
-          for (int64_t k = 0; k < deg; ++k)
-            for (int b = 0; b < 6; ++b) col_idx[start + 6 * k + b] = 6 * P.node_col[b0 + k] + b;
-      }
+  if (vals && !h->assembled) FAIL(h, SSO_E_STATE, "export of values before sso_assemble");
+  // rows of the owned nodes of every part, in global node order, columns in
+  // ascending GLOBAL order (the local halo numbering permuted back)
+  int64_t base = 0, row = 0;
+  std::vector<double> pv;
+  std::vector<std::pair<int32_t, int32_t>> cols;
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    const HostPattern& T = P.pat;
+    if (vals) {
+      pv.resize((size_t)P.nnz);
+      CK(h, cudaMemcpy(pv.data(), P.vals, (size_t)P.nnz * sizeof(double), cudaMemcpyDeviceToHost));
     }
-    if (row_ptr) row_ptr[h->ndof] = h->nnz;
+    for (int32_t n = 0; n < P.n_own; ++n) {
+      const int64_t b0 = T.node_ptr[n];
+      const int64_t deg = T.node_ptr[n + 1] - b0;
+      cols.clear();
+      for (int64_t k = 0; k < deg; ++k) cols.push_back({P.lm.node_gid[T.node_col[b0 + k]], (int32_t)k});
+      std::sort(cols.begin(), cols.end());
+      for (int a = 0; a < 6; ++a) {
+        const int64_t start = base + 36 * b0 + 6 * a * deg;
+        if (row_ptr) row_ptr[row + a] = start;
+        for (int64_t kk = 0; kk < deg; ++kk) {
+          const int32_t gcol = cols[kk].first, k = cols[kk].second;
+          for (int b = 0; b < 6; ++b) {
+            if (col_idx) col_idx[start + 6 * kk + b] = 6 * gcol + b;
+            if (vals) vals[start + 6 * kk + b] = pv[36 * b0 + 6 * a * deg + 6 * k + b];
+          }
+        }
+      }
+      row += 6;
+    }
+    base += P.nnz;
   }
-  if (vals) {
-    if (!h->assembled) FAIL(h, SSO_E_STATE, "export of values before sso_assemble");
-    CK(h, cudaMemcpy(vals, h->vals, h->nnz * sizeof(double), cudaMemcpyDeviceToHost));
-  }
+  if (row_ptr) row_ptr[row] = base;
   return SSO_OK;
 }
 
 int sso_export_scatter(sso_handle h, int32_t* block_rank) {
   if (!h || !block_rank) return SSO_E_INVALID;
-  std::memcpy(block_rank, h->pat.block_rank.data(), h->pat.block_rank.size() * sizeof(int32_t));
+  if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_export_scatter is defined for single-part handles");
+  std::memcpy(block_rank, h->P0().pat.block_rank.data(), h->P0().pat.block_rank.size() * sizeof(int32_t));
   return SSO_OK;
 }
 
 int sso_export_ke(sso_handle h, int64_t first, int64_t count, double* ke) {
   if (!h || !ke) return SSO_E_INVALID;
-  const int64_t ne = (int64_t)h->n_beams + h->n_quads;
+  if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_export_ke is defined for single-part handles");
+  Part& P = h->P0();
+  const int64_t ne = (int64_t)P.n_beams + P.n_quads;
   if (first < 0 || count < 0 || first + count > ne) FAIL(h, SSO_E_INVALID, "element range out of bounds");
   if (!h->assembled) FAIL(h, SSO_E_STATE, "export of K_e before sso_assemble");
   double* out = ke;
   std::vector<double> blk;
   for (int64_t e = first; e < first + count; ++e) {
-    const bool beam = e < h->n_beams;
+    const bool beam = e < P.n_beams;
     const int k = beam ? 2 : 4;
-    const int64_t sb = beam ? 4 * e : 4 * (int64_t)h->n_beams + 16 * (e - h->n_beams);
+    const int64_t sb = beam ? 4 * e : 4 * (int64_t)P.n_beams + 16 * (e - P.n_beams);
     blk.resize((size_t)k * k * 36);
-    CK(h, cudaMemcpy(blk.data(), h->stage + 36 * sb, blk.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(blk.data(), P.stage + 36 * sb, blk.size() * sizeof(double), cudaMemcpyDeviceToHost));
     const int m = 6 * k;
     for (int i = 0; i < k; ++i)
       for (int j = 0; j < k; ++j)
@@ -782,7 +1269,11 @@ int sso_export_ke(sso_handle h, int64_t first, int64_t count, double* ke) {
 int sso_export_dinv(sso_handle h, double* dinv) {
   if (!h || !dinv) return SSO_E_INVALID;
   if (!h->assembled) FAIL(h, SSO_E_STATE, "export of dinv before sso_assemble");
-  CK(h, cudaMemcpy(dinv, h->dinv, h->ndof * sizeof(double), cudaMemcpyDeviceToHost));
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    CK(h, cudaMemcpy(dinv + 6 * (int64_t)(P.lm.own_begin - h->user_node_begin), P.dinv,
+                     (size_t)P.ndof_own * sizeof(double), cudaMemcpyDeviceToHost));
+  }
   return SSO_OK;
 }
 
@@ -820,6 +1311,67 @@ void sso_destroy(sso_handle h) {
   cudaStreamSynchronize(h->stream);
   free_all(h);
   delete h;
+}
+
+// ---------------------------------------------------------------------------
+// Host-only partition queries (no GPU needed): used by the multi-process CPU
+// tests of the partition logic.
+// ---------------------------------------------------------------------------
+int sso_local_pattern(const sso_mesh* mesh, const int32_t* ranges, int32_t n_parts, int32_t part,
+                      int64_t* nnz, int64_t* row_ptr, int32_t* col_idx) {
+  if (!mesh || !nnz || n_parts < 1 || part < 0 || part >= n_parts) return SSO_E_INVALID;
+  std::vector<int32_t> rg = make_ranges(mesh->n_nodes, n_parts, ranges);
+  LocalMesh L;
+  std::string e = build_local_mesh(mesh->n_nodes, mesh->n_beams, mesh->beam_conn, mesh->n_quads,
+                                   mesh->quad_conn, rg.data(), n_parts, part, L);
+  if (!e.empty()) { g_create_err = e; return SSO_E_INVALID; }
+  HostPattern T;
+  e = build_pattern((int32_t)L.node_gid.size(), (int32_t)L.beam_gid.size(), L.beam_conn.data(),
+                    (int32_t)L.quad_gid.size(), L.quad_conn.data(), T);
+  if (!e.empty()) { g_create_err = e; return SSO_E_INVALID; }
+  *nnz = 36 * T.node_ptr[L.n_own];
+  if (!row_ptr && !col_idx) return SSO_OK;
+  std::vector<int32_t> cols;
+  int64_t row = 0;
+  for (int32_t n = 0; n < L.n_own; ++n) {
+    const int64_t b0 = T.node_ptr[n], deg = T.node_ptr[n + 1] - b0;
+    cols.clear();
+    for (int64_t k = 0; k < deg; ++k) cols.push_back(L.node_gid[T.node_col[b0 + k]]);
+    std::sort(cols.begin(), cols.end());
+    for (int a = 0; a < 6; ++a) {
+      const int64_t start = 36 * b0 + 6 * a * deg;
+      if (row_ptr) row_ptr[row + a] = start;
+      if (col_idx)
+        for (int64_t k = 0; k < deg; ++k)
+          for (int b = 0; b < 6; ++b) col_idx[start + 6 * k + b] = 6 * cols[k] + b;
+    }
+    row += 6;
+  }
+  if (row_ptr) row_ptr[row] = *nnz;
+  return SSO_OK;
+}
+
+int sso_halo_plan(const sso_mesh* mesh, const int32_t* ranges, int32_t n_parts, int32_t part,
+                  int32_t* n_halo, int32_t* halo_gid, int32_t* n_nbrs, int32_t* nbr_part,
+                  int32_t* send_count, int32_t* send_gid) {
+  if (!mesh || !n_halo || !n_nbrs || n_parts < 1 || part < 0 || part >= n_parts) return SSO_E_INVALID;
+  std::vector<int32_t> rg = make_ranges(mesh->n_nodes, n_parts, ranges);
+  LocalMesh L;
+  std::string e = build_local_mesh(mesh->n_nodes, mesh->n_beams, mesh->beam_conn, mesh->n_quads,
+                                   mesh->quad_conn, rg.data(), n_parts, part, L);
+  if (!e.empty()) { g_create_err = e; return SSO_E_INVALID; }
+  *n_halo = (int32_t)L.node_gid.size() - L.n_own;
+  *n_nbrs = (int32_t)L.nbrs.size();
+  if (halo_gid)
+    for (int32_t i = 0; i < *n_halo; ++i) halo_gid[i] = L.node_gid[L.n_own + i];
+  int64_t off = 0;
+  for (size_t k = 0; k < L.nbrs.size(); ++k) {
+    if (nbr_part) nbr_part[k] = L.nbrs[k].part;
+    if (send_count) send_count[k] = (int32_t)L.nbrs[k].send_local.size();
+    if (send_gid)
+      for (int32_t v : L.nbrs[k].send_local) send_gid[off++] = L.own_begin + v;
+  }
+  return SSO_OK;
 }
 
 }  // extern "C"

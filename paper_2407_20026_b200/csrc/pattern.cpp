@@ -138,3 +138,134 @@ std::string build_pattern(int32_t n_nodes, int32_t n_beams, const int32_t* beam_
 }
 
 }  // namespace sso
+
+namespace sso {
+
+namespace {
+
+int32_t owner_of(const int32_t* ranges, int32_t n_parts, int32_t node) {
+  // ranges ascending; binary search for the part containing node
+  int32_t lo = 0, hi = n_parts - 1;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) / 2;
+    if (ranges[mid] <= node) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Halo node set of part p (sorted by (owner, gid)) and its local element lists.
+void part_elements(int32_t n_nodes, int32_t n_beams, const int32_t* beam_conn, int32_t n_quads,
+                   const int32_t* quad_conn, int32_t b, int32_t e, std::vector<int32_t>& beams,
+                   std::vector<int32_t>& quads) {
+  (void)n_nodes;
+  beams.clear();
+  quads.clear();
+  for (int32_t k = 0; k < n_beams; ++k) {
+    const int32_t a = beam_conn[2 * k], c = beam_conn[2 * k + 1];
+    if ((a >= b && a < e) || (c >= b && c < e)) beams.push_back(k);
+  }
+  for (int32_t k = 0; k < n_quads; ++k) {
+    const int32_t* q = quad_conn + 4 * (int64_t)k;
+    bool own = false;
+    for (int i = 0; i < 4; ++i) own |= (q[i] >= b && q[i] < e);
+    if (own) quads.push_back(k);
+  }
+}
+
+std::vector<int32_t> halo_nodes(const int32_t* ranges, int32_t n_parts, int32_t p,
+                                const int32_t* beam_conn, const int32_t* quad_conn,
+                                const std::vector<int32_t>& beams, const std::vector<int32_t>& quads) {
+  const int32_t b = ranges[p], e = ranges[p + 1];
+  std::vector<int32_t> h;
+  for (int32_t k : beams)
+    for (int i = 0; i < 2; ++i) {
+      const int32_t n = beam_conn[2 * k + i];
+      if (n < b || n >= e) h.push_back(n);
+    }
+  for (int32_t k : quads)
+    for (int i = 0; i < 4; ++i) {
+      const int32_t n = quad_conn[4 * (int64_t)k + i];
+      if (n < b || n >= e) h.push_back(n);
+    }
+  std::sort(h.begin(), h.end());
+  h.erase(std::unique(h.begin(), h.end()), h.end());
+  // order by (owner part, gid): gids are sorted and parts are contiguous ranges, so
+  // sorting by gid already groups by owner in ascending part order
+  (void)n_parts;
+  return h;
+}
+
+}  // namespace
+
+std::string build_local_mesh(int32_t n_nodes, int32_t n_beams, const int32_t* beam_conn,
+                             int32_t n_quads, const int32_t* quad_conn, const int32_t* ranges,
+                             int32_t n_parts, int32_t part, LocalMesh& L) {
+  if (n_parts < 1 || part < 0 || part >= n_parts) return "bad part index";
+  if (ranges[0] != 0 || ranges[n_parts] != n_nodes) return "part ranges must cover [0, n_nodes)";
+  for (int32_t p = 0; p < n_parts; ++p)
+    if (ranges[p + 1] <= ranges[p]) return "part ranges must be strictly increasing";
+  L = LocalMesh();
+  L.part = part;
+  L.n_parts = n_parts;
+  L.own_begin = ranges[part];
+  L.own_end = ranges[part + 1];
+  L.n_own = L.own_end - L.own_begin;
+  std::vector<int32_t> beams, quads;
+  part_elements(n_nodes, n_beams, beam_conn, n_quads, quad_conn, L.own_begin, L.own_end, beams, quads);
+  std::vector<int32_t> halo = halo_nodes(ranges, n_parts, part, beam_conn, quad_conn, beams, quads);
+  L.node_gid.resize((size_t)L.n_own + halo.size());
+  for (int32_t i = 0; i < L.n_own; ++i) L.node_gid[i] = L.own_begin + i;
+  for (size_t i = 0; i < halo.size(); ++i) L.node_gid[L.n_own + i] = halo[i];
+  auto local_id = [&](int32_t g) -> int32_t {
+    if (g >= L.own_begin && g < L.own_end) return g - L.own_begin;
+    auto it = std::lower_bound(halo.begin(), halo.end(), g);
+    return L.n_own + (int32_t)(it - halo.begin());
+  };
+  L.beam_gid = beams;
+  L.quad_gid = quads;
+  L.beam_conn.resize(2 * beams.size());
+  for (size_t k = 0; k < beams.size(); ++k)
+    for (int i = 0; i < 2; ++i) L.beam_conn[2 * k + i] = local_id(beam_conn[2 * beams[k] + i]);
+  L.quad_conn.resize(4 * quads.size());
+  for (size_t k = 0; k < quads.size(); ++k) {
+    for (int i = 0; i < 4; ++i) L.quad_conn[4 * k + i] = local_id(quad_conn[4 * (int64_t)quads[k] + i]);
+    const int32_t first = quad_conn[4 * (int64_t)quads[k]];
+    if (first >= L.own_begin && first < L.own_end) L.own_quad_local.push_back((int32_t)k);
+  }
+  // receive plan: my halo grouped by owner (already sorted by gid -> by owner)
+  size_t i = 0;
+  while (i < halo.size()) {
+    const int32_t own = owner_of(ranges, n_parts, halo[i]);
+    size_t j = i;
+    while (j < halo.size() && owner_of(ranges, n_parts, halo[j]) == own) ++j;
+    NeighborPlan nb;
+    nb.part = own;
+    nb.recv_offset = (int32_t)i;
+    nb.recv_count = (int32_t)(j - i);
+    L.nbrs.push_back(nb);
+    i = j;
+  }
+  // send plan: for every other part q, the nodes of my range in q's halo (q's halo order)
+  for (int32_t q = 0; q < n_parts; ++q) {
+    if (q == part) continue;
+    std::vector<int32_t> qb, qq;
+    part_elements(n_nodes, n_beams, beam_conn, n_quads, quad_conn, ranges[q], ranges[q + 1], qb, qq);
+    std::vector<int32_t> qh = halo_nodes(ranges, n_parts, q, beam_conn, quad_conn, qb, qq);
+    std::vector<int32_t> send;
+    for (int32_t g : qh)
+      if (g >= L.own_begin && g < L.own_end) send.push_back(g - L.own_begin);
+    if (send.empty()) continue;
+    auto it = std::find_if(L.nbrs.begin(), L.nbrs.end(), [&](const NeighborPlan& n) { return n.part == q; });
+    if (it == L.nbrs.end()) {
+      NeighborPlan nb;
+      nb.part = q;
+      L.nbrs.push_back(nb);
+      it = L.nbrs.end() - 1;
+    }
+    it->send_local = send;
+  }
+  std::sort(L.nbrs.begin(), L.nbrs.end(), [](const NeighborPlan& a, const NeighborPlan& b) { return a.part < b.part; });
+  return std::string();
+}
+
+}  // namespace sso

@@ -296,6 +296,10 @@ __global__ void __launch_bounds__(SPMV_WARPS * 32, MINB) spmv_tma_kernel(
   }
   if (DOT) {
     if (grid_sum<1>(pq, partial, &st->ticket[0], sm) && threadIdx.x == 0) {
+      if (st->dist) {
+        st->red[0] = pq[0];
+        return;
+      }
       st->pq = pq[0];
       if (!(pq[0] > 0.0)) {
         st->status = SSO_E_NOT_SPD;
@@ -340,6 +344,11 @@ __global__ void __launch_bounds__(256) cg_update_kernel(int ndof, const double* 
     v[1] += ri.x * ri.x + ri.y * ri.y;
   }
   if (grid_sum<2>(v, partial, &st->ticket[1], sm) && threadIdx.x == 0) {
+    if (st->dist) {
+      st->red[0] = v[0];
+      st->red[1] = v[1];
+      return;
+    }
     const double rz_new = v[0];
     st->beta = rz_new / st->rz;
     st->rz = rz_new;
@@ -406,6 +415,12 @@ __global__ void __launch_bounds__(256) cg_init_kernel(int ndof, const double* __
     v[2] += ri * ri;
   }
   if (grid_sum<3>(v, partial, &st->ticket[2], sm) && threadIdx.x == 0) {
+    if (st->dist) {
+      st->red[0] = v[0];
+      st->red[1] = v[1];
+      st->red[2] = v[2];
+      return;
+    }
     st->ff = v[0];
     st->rz = v[1];
     st->rr = v[2];
@@ -450,12 +465,128 @@ __global__ void __launch_bounds__(256) dot_kernel(int n, const double* __restric
   if (grid_sum<1>(v, partial, ticket, sm) && threadIdx.x == 0) *out = scale * v[0];
 }
 
+// Scalar step of the partitioned CG after the cross-part allreduce of red[].
+__global__ void cg_scalar_kernel(CgState* st, int phase) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (phase == PH_INIT) {
+    const double ff = st->red[0], rz = st->red[1], rr = st->red[2];
+    st->ff = ff;
+    st->rz = rz;
+    st->rr = rr;
+    st->iter = 0;
+    st->status = SSO_OK;
+    st->done = (rr <= st->tol2 * ff || ff == 0.0) ? 1 : 0;
+    st->tol2 = st->tol2 * ff;
+    st->alpha = st->beta = 0.0;
+    return;
+  }
+  if (st->done) return;
+  if (phase == PH_ALPHA) {
+    const double pq = st->red[0];
+    st->pq = pq;
+    if (!(pq > 0.0)) {
+      st->status = SSO_E_NOT_SPD;
+      st->done = 1;
+    } else {
+      st->alpha = st->rz / pq;
+    }
+  } else {
+    const double rz_new = st->red[0];
+    st->beta = rz_new / st->rz;
+    st->rz = rz_new;
+    st->rr = st->red[1];
+    st->iter += 1;
+    if (st->rr <= st->tol2) {
+      st->done = 1;
+      st->status = SSO_OK;
+    } else if (st->iter >= st->max_iter) {
+      st->done = 1;
+      st->status = SSO_E_NOT_CONVERGED;
+    }
+  }
+}
+
+// buf[6k + c] = vec[6 idx[k] + c]  (halo send packing)
+__global__ void pack_kernel(int count, const int32_t* __restrict__ idx, const double* __restrict__ vec,
+                            double* __restrict__ buf) {
+  const int64_t n = 6 * (int64_t)count;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = vec[6 * (int64_t)idx[i / 6] + (i % 6)];
+}
+
+// In-process allreduce over parts: red[v] = sum over parts in part order, written to all.
+__global__ void allreduce_parts_kernel(CgState* const* sts, int n_parts, int nvals) {
+  const int v = threadIdx.x;
+  if (v >= nvals) return;
+  double s = 0.0;
+  for (int p = 0; p < n_parts; ++p) s += sts[p]->red[v];
+  __syncwarp();
+  for (int p = 0; p < n_parts; ++p) sts[p]->red[v] = s;
+}
+
+__global__ void gather_kernel(int n, const int32_t* __restrict__ idx, const double* __restrict__ src,
+                              double* __restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
+__global__ void scatter_kernel(int n, const int32_t* __restrict__ idx, const double* __restrict__ src,
+                               double* __restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[idx[i]] = src[i];
+}
+
+__global__ void __launch_bounds__(256) dot_local_kernel(int n, const double* __restrict__ a,
+                                                        const double* __restrict__ b,
+                                                        double* __restrict__ partial,
+                                                        unsigned int* ticket, double* out) {
+  __shared__ double sm[32];
+  double v[1] = {0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) v[0] += a[i] * b[i];
+  if (grid_sum<1>(v, partial, ticket, sm) && threadIdx.x == 0) *out = v[0];
+}
+
 int vec_grid(int64_t n) {
   int64_t need = (n + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)cg_grid()));
 }
 
 }  // namespace
+
+void launch_cg_scalar(cudaStream_t s, CgState* st, int phase) {
+  cg_scalar_kernel<<<1, 32, 0, s>>>(st, phase);
+  SSO_POST_LAUNCH("cg_scalar_kernel");
+}
+
+void launch_pack(cudaStream_t s, int count, const int32_t* idx, const double* vec, double* buf) {
+  if (count <= 0) return;
+  pack_kernel<<<vec_grid(6 * (int64_t)count), 256, 0, s>>>(count, idx, vec, buf);
+  SSO_POST_LAUNCH("pack_kernel");
+}
+
+void launch_allreduce_parts(cudaStream_t s, CgState* const* sts, int n_parts, int nvals) {
+  allreduce_parts_kernel<<<1, 32, 0, s>>>(sts, n_parts, nvals);
+  SSO_POST_LAUNCH("allreduce_parts_kernel");
+}
+
+void launch_gather(cudaStream_t s, int n, const int32_t* idx, const double* src, double* dst) {
+  if (n <= 0) return;
+  gather_kernel<<<vec_grid(n), 256, 0, s>>>(n, idx, src, dst);
+  SSO_POST_LAUNCH("gather_kernel");
+}
+
+void launch_scatter(cudaStream_t s, int n, const int32_t* idx, const double* src, double* dst) {
+  if (n <= 0) return;
+  scatter_kernel<<<vec_grid(n), 256, 0, s>>>(n, idx, src, dst);
+  SSO_POST_LAUNCH("scatter_kernel");
+}
+
+void launch_dot_local(cudaStream_t s, int n, const double* a, const double* b, double* partial,
+                      unsigned int* ticket, double* out) {
+  dot_local_kernel<<<vec_grid(n), 256, 0, s>>>(n, a, b, partial, ticket, out);
+  SSO_POST_LAUNCH("dot_local_kernel");
+}
 
 int cg_grid() {
   if (g_sms == 0) {

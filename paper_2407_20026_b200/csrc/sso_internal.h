@@ -51,6 +51,10 @@ struct CgState {
   int done;         // 1 = converged or failed: all later kernels return immediately
   int status;       // sso_status
   unsigned int ticket[4];  // last-block-done counters (one per reduction site)
+  int dist;         // 1 = partitioned: kernels write local sums to red[], a scalar
+                    //     kernel forms alpha / beta after the cross-part allreduce
+  int pad_;
+  double red[4];    // local (then global) reduction values
 };
 
 // error flags written by device kernels (atomicMin on the offending index)
@@ -103,6 +107,16 @@ void launch_residual_norm(cudaStream_t s, int ndof, const double* f, const doubl
                           double* partial, unsigned int* ticket, double* out);
 void launch_zero_fixed(cudaStream_t s, int ndof, const uint8_t* fixed_mask, double* x);
 
+// Partitioned-solve helpers
+enum ScalarPhase { PH_INIT = 0, PH_ALPHA = 1, PH_BETA = 2 };
+void launch_cg_scalar(cudaStream_t s, CgState* st, int phase);
+void launch_pack(cudaStream_t s, int count, const int32_t* idx, const double* vec, double* buf);
+void launch_allreduce_parts(cudaStream_t s, CgState* const* sts, int n_parts, int nvals);
+void launch_gather(cudaStream_t s, int n, const int32_t* idx, const double* src, double* dst);
+void launch_scatter(cudaStream_t s, int n, const int32_t* idx, const double* src, double* dst);
+void launch_dot_local(cudaStream_t s, int n, const double* a, const double* b, double* partial,
+                      unsigned int* ticket, double* out);
+
 // Gradient kernels
 void launch_beam_grad(cudaStream_t s, int n_beams, const double* x, const double* y,
                       const double* z, const int32_t* conn, const double* A,
@@ -129,5 +143,39 @@ extern long long g_launches;  // launch counter (per process; handles add their 
   } while (0)
 void note_launch_error(const char* name, cudaError_t e);
 const char* last_launch_error();
+
+}  // namespace sso
+
+namespace sso {
+
+// ---------------------------------------------------------------------------
+// Partitioning: contiguous node ranges per part.  A part's
+// local mesh = its owned nodes [begin, end) (local ids 0..n_own-1, global order)
+// followed by its halo nodes (non-owned nodes of local elements) ordered by
+// (owner part, global id).  Local elements = every element with at least one
+// owned node, in ascending global order (so owned rows sum contributions in the
+// same order as the global assembly: rank-local values are bit-identical).
+// ---------------------------------------------------------------------------
+struct NeighborPlan {
+  int32_t part;                       // neighbour part / rank
+  std::vector<int32_t> send_local;    // my owned local node ids it needs, in its halo order
+  int32_t recv_offset = 0;            // first halo slot (relative to n_own) it fills
+  int32_t recv_count = 0;
+};
+
+struct LocalMesh {
+  int32_t part = 0, n_parts = 1;
+  int32_t own_begin = 0, own_end = 0, n_own = 0;
+  std::vector<int32_t> node_gid;      // local -> global node id
+  std::vector<int32_t> beam_gid, quad_gid;   // local -> global element id (within type)
+  std::vector<int32_t> beam_conn, quad_conn; // local numbering
+  std::vector<int32_t> own_quad_local;       // local quads whose first node is owned
+  std::vector<NeighborPlan> nbrs;
+};
+
+// ranges: [n_parts + 1] node boundaries (0 = ranges[0] < ... < ranges[n_parts] = n_nodes).
+std::string build_local_mesh(int32_t n_nodes, int32_t n_beams, const int32_t* beam_conn,
+                             int32_t n_quads, const int32_t* quad_conn, const int32_t* ranges,
+                             int32_t n_parts, int32_t part, LocalMesh& L);
 
 }  // namespace sso
