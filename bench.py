@@ -6,9 +6,11 @@ compliance + adjoint gradient (sso_grad).  A0 (pattern) runs once at create.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-N > 1 runs under torchrun (one rank per GPU).  Round 1 has no partitioned
-(domain-decomposed) path yet, so every rank evaluates its own replica of the
-workload (weak scaling, no data-path collective).
+N > 1 runs under torchrun (one rank per GPU): the same C3b evaluation split
+into N contiguous node strips, one per GPU, with the halo of p and the CG
+scalars exchanged through NCCL every iteration (strong scaling; DESIGN.md
+"Multi-GPU").  --virtual-parts P runs that partitioned algorithm with P strips
+on one GPU (in-process transport).
 `--impl reference` times the CPU oracle (oracle/) on a bounded sample of the
 same workload on the host cores, extrapolated to the same metric.
 """
@@ -192,7 +194,7 @@ def run_reference(args):
     value = float(np.median(vals))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C3b: 408x408 MITC-4 shell quads, 1 003 686 DOF (reading c15)",
                        "rtol": RTOL, "cg_iters": cg_iters},
@@ -225,11 +227,27 @@ def run_gpu(args):
     P = W.config3b()
     t0 = time.perf_counter()
     stream = torch.cuda.current_stream()
-    m = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index)
+    if world > 1:
+        # strong scaling: C3b split into `world` node strips, one per GPU; halos of p
+        # and the CG scalars travel through NCCL
+        import torch.distributed as dist
+        obj = [sso.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        m = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index, nranks=world,
+                      rank=rank, nccl_id=obj[0])
+        parallelism = f"{world} node strips (NCCL halo + allreduce), strong scaling"
+    elif args.virtual_parts > 1:
+        m = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index,
+                      n_parts=args.virtual_parts)
+        parallelism = f"{args.virtual_parts} node strips on 1 GPU (in-process transport)"
+    else:
+        m = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index)
+        parallelism = "single GPU"
     t_create = time.perf_counter() - t0
     ndof, nnz, nblocks = m.sizes()
     n_nodes, nq = m.n_nodes, m.n_quads
-    f_dev = torch.from_numpy(P["f"]).to(dev)
+    f_own = P["f"][6 * m.own_node_begin: 6 * (m.own_node_begin + n_nodes)]
+    f_dev = torch.from_numpy(np.ascontiguousarray(f_own)).to(dev)
     u_dev = torch.zeros(ndof, dtype=torch.float64, device=dev)
     Cb = torch.zeros(1, dtype=torch.float64, device=dev)
     dXb = torch.zeros(3 * n_nodes, dtype=torch.float64, device=dev)
@@ -277,11 +295,11 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = world * args.steps / (ms_total / 1000.0)
+    value = args.steps / (ms_total / 1000.0)  # one (partitioned) C3b evaluation per step
     cg_iters = int(np.median(iters))
 
     # ---- e2e: host buffers through the C ABI, copies inside the timed region --
-    f_host = torch.from_numpy(P["f"]).pin_memory()
+    f_host = torch.from_numpy(np.ascontiguousarray(f_own)).pin_memory()
     u_host = torch.zeros(ndof, dtype=torch.float64).pin_memory()
     C_h = torch.zeros(1, dtype=torch.float64).pin_memory()
     dX_h = torch.zeros(3 * n_nodes, dtype=torch.float64).pin_memory()
@@ -305,11 +323,11 @@ def run_gpu(args):
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = world * e2e_steps / e2e_s
+    e2e_value = e2e_steps / e2e_s
 
     # ---- roofline of the dominant kernel (SpMV inside PCG) --------------------
     peak, peak_src = measured_peaks()
-    spmv_bytes = 8 * nnz + 4 * nblocks + 8 * (n_nodes + 1) + 16 * ndof
+    spmv_bytes = 8 * nnz + 4 * nblocks + 8 * (n_nodes + 1) + 16 * ndof  # this rank's rows
     spmv_avg_ms = spmv_ms / max(spmv_n, 1)
     achieved = spmv_bytes / (spmv_avg_ms / 1000.0) / 1e9 if spmv_n else None
     roofline = {"bound": "hbm", "kernel": "spmv_dot (CG q = K p, p^T q)",
@@ -327,12 +345,12 @@ def run_gpu(args):
         cpu = cpu_baseline_obj(P, cg_iters) if (world == 1 and not args.no_cpu) else None
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (workloads.config3b, seeded)",
                "config": {"workload": "C3b: 408x408 MITC-4 shell quads, 1 003 686 DOF (reading c15)",
                           "n_nodes": n_nodes, "n_quads": nq, "ndof": ndof, "nnz": nnz,
                           "rtol": RTOL, "cg_iters": cg_iters,
-                          "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                          "parallelism": parallelism,
                           "l2": "working set > L2 (CSR values alone 432 MB vs 126 MB L2); no flush",
                           "pattern_build_s": t_create},
                "roofline": roofline,
@@ -365,6 +383,8 @@ def main():
     ap.add_argument("--cg-iters", type=int, default=None,
                     help="CG iteration count used to extrapolate the oracle (reference arm)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--virtual-parts", type=int, default=1,
+                    help="run the partitioned (strip) algorithm with P strips on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         if args.cg_iters is None:

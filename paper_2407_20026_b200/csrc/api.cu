@@ -298,12 +298,13 @@ double* vec_of(Part& P, int v) {
   }
 }
 
-int exchange(sso_ctx* h, int v) {
+int exchange(sso_ctx* h, int v, cudaStream_t s = nullptr) {
   if (!h->distributed()) return SSO_OK;
+  if (!s) s = h->stream;
   long long g0 = g_launches;
   for (auto& pp : h->parts) {
     Part& P = *pp;
-    launch_pack(h->stream, (int)P.n_send, P.send_idx, vec_of(P, v), P.sendbuf);
+    launch_pack(s, (int)P.n_send, P.send_idx, vec_of(P, v), P.sendbuf);
   }
   if (h->nranks == 1) {
     // local transport: copy every neighbour's packed values into my halo
@@ -320,7 +321,7 @@ int exchange(sso_ctx* h, int v) {
           return SSO_E_STATE;
         }
         CK(h, cudaMemcpyAsync(dst + 6 * ((int64_t)P.n_own + nb.recv_offset), Q.sendbuf + 6 * Q.send_off[k],
-                              (size_t)6 * nb.recv_count * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+                              (size_t)6 * nb.recv_count * sizeof(double), cudaMemcpyDeviceToDevice, s));
       }
     }
   } else {
@@ -331,10 +332,10 @@ int exchange(sso_ctx* h, int v) {
       const NeighborPlan& nb = P.lm.nbrs[k];
       if (!nb.send_local.empty())
         CKN(h, nccl().Send(P.sendbuf + 6 * P.send_off[k], 6 * nb.send_local.size(), ncclDouble, nb.part,
-                           h->comm, h->stream));
+                           h->comm, s));
       if (nb.recv_count)
         CKN(h, nccl().Recv(dst + 6 * ((int64_t)P.n_own + nb.recv_offset), (size_t)6 * nb.recv_count,
-                           ncclDouble, nb.part, h->comm, h->stream));
+                           ncclDouble, nb.part, h->comm, s));
     }
     CKN(h, nccl().GroupEnd());
   }
@@ -342,14 +343,15 @@ int exchange(sso_ctx* h, int v) {
   return SSO_OK;
 }
 
-int allreduce(sso_ctx* h, int nvals) {
+int allreduce(sso_ctx* h, int nvals, cudaStream_t s = nullptr) {
   if (!h->distributed()) return SSO_OK;
+  if (!s) s = h->stream;
   long long g0 = g_launches;
   if (h->nranks == 1) {
-    launch_allreduce_parts(h->stream, h->d_sts, (int)h->parts.size(), nvals);
+    launch_allreduce_parts(s, h->d_sts, (int)h->parts.size(), nvals);
   } else {
     double* red = h->P0().st->red;
-    CKN(h, nccl().AllReduce(red, red, nvals, ncclDouble, ncclSum, h->comm, h->stream));
+    CKN(h, nccl().AllReduce(red, red, nvals, ncclDouble, ncclSum, h->comm, s));
   }
   h->launches += g_launches - g0;
   return SSO_OK;
@@ -397,8 +399,47 @@ int reset_flags(sso_ctx* h) {
 // SpMV (events of that slot): a live sample of the SpMV launch duration.
 constexpr int PROF_EVERY = 16;
 
+// One CG iteration on stream s (captured into the chunk graphs).  Single part:
+// alpha / beta are formed by the kernels' last CTAs.  Partitioned: halo of p,
+// SpMV + local p^T q, allreduce, alpha; update + local r^T z / r^T r, allreduce,
+// beta and the convergence test; p update.  `rec` brackets part 0's SpMV with
+// the event pair ev[0], ev[1].
+int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev) {
+  int rc;
+  if (!h->distributed()) {
+    Part& P = h->P0();
+    if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
+    launch_spmv_dot(s, P.n_own, P.node_ptr, P.node_col, P.vals, P.p, P.q, P.partial, P.st);
+    if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
+    launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st);
+    launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st);
+    return SSO_OK;
+  }
+  if ((rc = exchange(h, V_P, s))) return rc;
+  bool first = true;
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    if (ev && first) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
+    launch_spmv_dot(s, P.n_own, P.node_ptr, P.node_col, P.vals, P.p, P.q, P.partial, P.st);
+    if (ev && first) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
+    first = false;
+  }
+  if ((rc = allreduce(h, 1, s))) return rc;
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    launch_cg_scalar(s, P.st, PH_ALPHA);
+    launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st);
+  }
+  if ((rc = allreduce(h, 2, s))) return rc;
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    launch_cg_scalar(s, P.st, PH_BETA);
+    launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st);
+  }
+  return SSO_OK;
+}
+
 int build_chunk_graph(sso_ctx* h, int prof_slot, cudaGraphExec_t* out) {
-  Part& P = h->P0();
   if (*out) {
     cudaGraphExecDestroy(*out);
     *out = nullptr;
@@ -412,20 +453,24 @@ int build_chunk_graph(sso_ctx* h, int prof_slot, cudaGraphExec_t* out) {
       ev.push_back(e);
     }
   }
-  long long g0 = g_launches;
+  long long g0 = g_launches, l0 = h->launches;
   CK(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
-  for (int i = 0; i < K; ++i) {
+  int rc = SSO_OK;
+  for (int i = 0; i < K && rc == SSO_OK; ++i) {
     const bool rec = prof_slot >= 0 && (i % PROF_EVERY) == 0;
-    if (rec) cudaEventRecordWithFlags(h->chunk_ev[prof_slot][2 * i], h->cap_stream, cudaEventRecordExternal);
-    launch_spmv_dot(h->cap_stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.p, P.q, P.partial, P.st);
-    if (rec) cudaEventRecordWithFlags(h->chunk_ev[prof_slot][2 * i + 1], h->cap_stream, cudaEventRecordExternal);
-    launch_cg_update(h->cap_stream, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st);
-    launch_cg_pupdate(h->cap_stream, (int)P.ndof_own, P.dinv, P.r, P.p, P.st);
+    rc = cg_iteration(h, h->cap_stream, rec ? &h->chunk_ev[prof_slot][2 * i] : nullptr);
   }
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
+  // every kernel bumps g_launches once (exchange / allreduce also add to h->launches):
+  // undo both and count the chunk's kernels per replay instead
   h->kernels_per_chunk = g_launches - g0;
-  g_launches = g0;  // captured launches are counted per replay
+  h->launches = l0;
+  g_launches = g0;
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
   if (e != cudaSuccess) {
     h->err = std::string("graph capture failed: ") + cudaGetErrorString(e);
     return SSO_E_CUDA;
@@ -902,8 +947,9 @@ int sso_assemble(sso_handle h) {
   return SSO_OK;
 }
 
-// Single-part solve: graph chunks with alpha / beta formed inside the kernels.
-static int solve_single(sso_ctx* h) {
+// CG loop as replays of captured chunks of check_every iterations (single part
+// and partitioned alike).
+static int solve_chunks(sso_ctx* h) {
   Part& P = h->P0();
   int rc;
   const bool prof = h->tm.on;
@@ -952,40 +998,6 @@ static int solve_single(sso_ctx* h) {
   return SSO_OK;
 }
 
-// Partitioned solve: per iteration exchange(p), SpMV + local p^T q, allreduce,
-// alpha; updates + local r^T z, r^T r, allreduce, beta / convergence; p update.
-static int solve_dist(sso_ctx* h) {
-  int rc;
-  for (int64_t it = 0;; ++it) {
-    if ((rc = exchange(h, V_P))) return rc;
-    for (auto& pp : h->parts) {
-      Part& P = *pp;
-      Scope sc(h, F_SPMV);
-      launch_spmv_dot(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.p, P.q, P.partial, P.st);
-    }
-    if ((rc = allreduce(h, 1))) return rc;
-    for (auto& pp : h->parts) {
-      Part& P = *pp;
-      Scope sc(h, F_UPDATE);
-      launch_cg_scalar(h->stream, P.st, PH_ALPHA);
-      launch_cg_update(h->stream, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st);
-    }
-    if ((rc = allreduce(h, 2))) return rc;
-    for (auto& pp : h->parts) {
-      Part& P = *pp;
-      Scope sc(h, F_UPDATE);
-      launch_cg_scalar(h->stream, P.st, PH_BETA);
-      launch_cg_pupdate(h->stream, (int)P.ndof_own, P.dinv, P.r, P.p, P.st);
-    }
-    if ((it + 1) % h->check_every == 0 || it >= h->max_iter) {
-      CK(h, cudaMemcpyAsync(h->h_chunk, h->P0().st, sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
-      if ((rc = sync(h))) return rc;
-      if (h->h_chunk[0].done || it >= h->max_iter) break;
-    }
-  }
-  return SSO_OK;
-}
-
 int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
   if (!h || !f || !u) {
     if (h) h->err = "null argument";
@@ -1030,7 +1042,7 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
     for (auto& pp : h->parts) launch_cg_scalar(h->stream, pp->st, PH_INIT);
     h->launches += g_launches - g0;
   }
-  rc = dist ? solve_dist(h) : solve_single(h);
+  rc = solve_chunks(h);
   if (rc) return rc;
   CK(h, cudaEventRecord(h->ev_b, h->stream));
   // true residual |f_bc - K x| / |f_bc|: local sums of squares into red[0], allreduced
