@@ -119,6 +119,14 @@ typedef struct {
   const int32_t* part_ranges;
   int32_t nranks, rank;
   const void* nccl_unique_id;
+  /* Batched designs: B >= 1 designs share connectivity,
+   * supports and materials; each has its own coordinates, thicknesses, loads and CG
+   * (own alpha / beta / convergence, run in lockstep in the same kernel launches).
+   * With B > 1 (single strip, single rank only) every per-design buffer is
+   * design-major: sso_set_design x, y, z [B][n_nodes], t [B][n_quads]; sso_solve f, u
+   * [B][6 n_nodes], info [B]; sso_grad C [B], dC_dxyz [B][3][n_nodes], dC_dt
+   * [B][n_quads]; sso_grad_at / sso_spmv [B][6 n_nodes].  Exports show design 0. */
+  int32_t batch;
 } sso_options;
 
 typedef struct {
@@ -155,8 +163,8 @@ int sso_assemble(sso_handle h);
 
 /* A3: Jacobi-PCG on K_bc u = f_bc.  f [6 n_nodes] (entries at constrained DOFs ignored),
  * u [6 n_nodes] output (zeros at constrained DOFs); read as x0 when warm_start.
- * info may be NULL.  Errors: SSO_E_STATE (not assembled), SSO_E_NOT_SPD,
- * SSO_E_NOT_CONVERGED (u = last iterate). */
+ * info may be NULL ([batch] entries otherwise).  Errors: SSO_E_STATE (not assembled),
+ * SSO_E_NOT_SPD, SSO_E_NOT_CONVERGED (u = last iterate). */
 int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info);
 
 /* A4: objective and adjoint gradient at the last solve's (f, u):

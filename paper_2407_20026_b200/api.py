@@ -61,7 +61,7 @@ class sso_options(C.Structure):
                 ("warm_start", C.c_int32), ("check_every", C.c_int32), ("mem", C.c_int),
                 ("cuda_stream", C.c_void_p), ("device", C.c_int32),
                 ("n_parts", C.c_int32), ("part_ranges", _ip), ("nranks", C.c_int32),
-                ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p)]
+                ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p), ("batch", C.c_int32)]
 
 
 class sso_solve_info(C.Structure):
@@ -141,7 +141,7 @@ class Model:
 
     def __init__(self, problem, rtol=1e-10, max_iter=200000, drill_alpha=1e-3, check_every=64,
                  warm_start=False, stream=None, device=-1, n_parts=1, part_ranges=None,
-                 nranks=1, rank=0, nccl_id=None):
+                 nranks=1, rank=0, nccl_id=None, batch=1):
         P = problem
         self._keep = []
         x, y, z = (_np(P[k], np.float64) for k in ("x", "y", "z"))
@@ -170,7 +170,7 @@ class Model:
         opt.check_every, opt.warm_start, opt.device = check_every, int(warm_start), device
         opt.mem = MEM_HOST
         opt.cuda_stream = stream
-        opt.n_parts, opt.nranks, opt.rank = n_parts, nranks, rank
+        opt.n_parts, opt.nranks, opt.rank, opt.batch = n_parts, nranks, rank, batch
         if part_ranges is not None:
             pr = np.ascontiguousarray(part_ranges, np.int32)
             self._keep.append(pr)
@@ -192,6 +192,7 @@ class Model:
         # extents of this handle's f / u / gradient buffers (global unless multi-rank)
         self.n_nodes, self.n_beams, self.n_quads = c.value, nb, d.value
         self.ndof = 6 * c.value
+        self.batch = batch
         self._mem = MEM_HOST
         self._stream = stream
 
@@ -240,20 +241,24 @@ class Model:
         self._check(_lib.sso_assemble(self.h))
 
     def solve(self, f, u=None, raise_on_error=True):
-        """Returns (u, info dict).  f, u: numpy (host) or torch CUDA tensors (device)."""
+        """Returns (u, info dict) — with batch > 1, u is [B, ndof] and info a list of B dicts.
+        f, u: numpy (host) or torch CUDA tensors (device)."""
         dev = self._mode(f, u)
+        shape = (self.batch, self.ndof) if self.batch > 1 else (self.ndof,)
         if not dev:
             f = _np(f, np.float64)
             if u is None:
-                u = np.zeros(self.ndof)
+                u = np.zeros(shape)
         elif u is None:
             import torch
-            u = torch.zeros(self.ndof, dtype=torch.float64, device=f.device)
-        info = sso_solve_info()
-        rc = _lib.sso_solve(self.h, _ptr(f, np.float64), _ptr(u, np.float64), C.byref(info))
+            u = torch.zeros(shape, dtype=torch.float64, device=f.device)
+        infos = (sso_solve_info * self.batch)()
+        rc = _lib.sso_solve(self.h, _ptr(f, np.float64), _ptr(u, np.float64), infos)
         if raise_on_error:
             self._check(rc)
-        return u, info.as_dict()
+        if self.batch > 1:
+            return u, [i.as_dict() for i in infos]
+        return u, infos[0].as_dict()
 
     def grad(self, objective=OBJ_COMPLIANCE, out=None):
         """Returns (C, dC_dxyz [3, n_nodes], dC_dt [n_quads]) for the last solve."""
@@ -264,15 +269,16 @@ class Model:
 
     def _grad(self, objective, f, u, out):
         dev = self._mode(f, u, *(out or ()))
+        B = self.batch
         if out is None:
             if dev:
                 import torch
                 ref = f if f is not None else u
-                Cv = torch.zeros(1, dtype=torch.float64, device=ref.device)
-                dX = torch.zeros(3 * self.n_nodes, dtype=torch.float64, device=ref.device)
-                dT = torch.zeros(max(self.n_quads, 1), dtype=torch.float64, device=ref.device)
+                Cv = torch.zeros(B, dtype=torch.float64, device=ref.device)
+                dX = torch.zeros(B * 3 * self.n_nodes, dtype=torch.float64, device=ref.device)
+                dT = torch.zeros(B * max(self.n_quads, 1), dtype=torch.float64, device=ref.device)
             else:
-                Cv, dX, dT = np.zeros(1), np.zeros(3 * self.n_nodes), np.zeros(max(self.n_quads, 1))
+                Cv, dX, dT = np.zeros(B), np.zeros(B * 3 * self.n_nodes), np.zeros(B * max(self.n_quads, 1))
         else:
             Cv, dX, dT = out
         if f is None:
@@ -286,6 +292,8 @@ class Model:
         self._check(rc)
         if out is not None:
             return out
+        if B > 1:
+            return Cv, dX.reshape(B, 3, self.n_nodes), dT.reshape(B, -1)[:, : self.n_quads]
         C0 = float(Cv[0]) if not dev else Cv
         return C0, dX.reshape(3, self.n_nodes), dT[: self.n_quads]
 

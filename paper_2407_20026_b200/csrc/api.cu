@@ -84,6 +84,8 @@ std::string g_create_err;
 // ---------------------------------------------------------------------------
 struct Part {
   LocalMesh lm;
+  int B = 1;            // designs in a batch (single-strip handles only)
+  BatchStrides bs;
   int32_t n_nodes = 0, n_own = 0, n_beams = 0, n_quads = 0, n_own_quads = 0;
   int64_t ndof = 0, ndof_own = 0, nnz = 0, n_blocks = 0, n_staged = 0, n_slots = 0;
   HostPattern pat;
@@ -131,6 +133,7 @@ struct sso_ctx {
   double drill_alpha = 1e-3;
   int warm_start = 0;
   int check_every = 64;
+  int batch = 1;  // designs per handle
 
   // global problem sizes and what this handle's user buffers cover
   int32_t g_nodes = 0, g_beams = 0, g_quads = 0;
@@ -358,11 +361,13 @@ int allreduce(sso_ctx* h, int nvals, cudaStream_t s = nullptr) {
 }
 
 int check_flags(sso_ctx* h) {
-  for (auto& pp : h->parts) {
+  for (auto& pp : h->parts)
+   for (int bd = 0; bd < pp->B; ++bd) {
     Part& P = *pp;
-    CK(h, cudaMemcpyAsync(h->h_flags, P.flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaMemcpyAsync(h->h_flags, P.flags + bd, sizeof(DevFlags), cudaMemcpyDeviceToHost, h->stream));
     int rc = sync(h);
     if (rc) return rc;
+    const std::string dsg = P.B > 1 ? " in design " + std::to_string(bd) : std::string();
     if (h->h_flags->degenerate_elem != INT_MAX) {
       const int e = h->h_flags->degenerate_elem;
       const bool beam = e < P.n_beams;
@@ -370,7 +375,7 @@ int check_flags(sso_ctx* h) {
       char buf[256];
       snprintf(buf, sizeof buf, "degenerate element %d (%s %d): zero length / zero normal / det J <= 0",
                beam ? g : h->g_beams + g, beam ? "beam" : "quad", g);
-      h->err = buf;
+      h->err = buf + dsg;
       return SSO_E_DEGENERATE;
     }
     if (h->h_flags->singular_dof != INT_MAX) {
@@ -379,7 +384,7 @@ int check_flags(sso_ctx* h) {
       char buf[256];
       snprintf(buf, sizeof buf, "singular: free DOF %d (node %d, component %d) has diagonal <= 0",
                6 * gnode + d % 6, gnode, d % 6);
-      h->err = buf;
+      h->err = buf + dsg;
       return SSO_E_SINGULAR;
     }
   }
@@ -389,8 +394,11 @@ int check_flags(sso_ctx* h) {
 int reset_flags(sso_ctx* h) {
   h->h_flags->degenerate_elem = INT_MAX;
   h->h_flags->singular_dof = INT_MAX;
-  for (auto& pp : h->parts)
-    CK(h, cudaMemcpyAsync(pp->flags, h->h_flags, sizeof(DevFlags), cudaMemcpyHostToDevice, h->stream));
+  for (auto& pp : h->parts) {
+    for (int bd = 0; bd < pp->B; ++bd)
+      CK(h, cudaMemcpyAsync(pp->flags + bd, h->h_flags, sizeof(DevFlags), cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));  // h_flags is reused for every design
+  }
   return sync(h);
 }
 
@@ -409,10 +417,10 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev) {
   if (!h->distributed()) {
     Part& P = h->P0();
     if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
-    launch_spmv_dot(s, P.n_own, P.node_ptr, P.node_col, P.vals, P.p, P.q, P.partial, P.st);
+    launch_spmv_dot(s, P.n_own, P.node_ptr, P.node_col, P.vals, P.p, P.q, P.partial, P.st, P.bs);
     if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
-    launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st);
-    launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st);
+    launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st, P.bs);
+    launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st, P.bs);
     return SSO_OK;
   }
   if ((rc = exchange(h, V_P, s))) return rc;
@@ -420,7 +428,7 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     if (ev && first) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
-    launch_spmv_dot(s, P.n_own, P.node_ptr, P.node_col, P.vals, P.p, P.q, P.partial, P.st);
+    launch_spmv_dot(s, P.n_own, P.node_ptr, P.node_col, P.vals, P.p, P.q, P.partial, P.st, P.bs);
     if (ev && first) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
     first = false;
   }
@@ -428,13 +436,13 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     launch_cg_scalar(s, P.st, PH_ALPHA);
-    launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st);
+    launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st, P.bs);
   }
   if ((rc = allreduce(h, 2, s))) return rc;
   for (auto& pp : h->parts) {
     Part& P = *pp;
     launch_cg_scalar(s, P.st, PH_BETA);
-    launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st);
+    launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st, P.bs);
   }
   return SSO_OK;
 }
@@ -594,16 +602,28 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   P.n_slots = 2 * (int64_t)P.n_beams + 4 * (int64_t)P.n_quads;
   P.nnz = 36 * (P.pat.node_ptr[P.n_own]);  // owned rows only
   const int64_t ne = (int64_t)P.n_beams + P.n_quads;
-  std::vector<double> x(P.n_nodes), y(P.n_nodes), z(P.n_nodes);
+  const int B = P.B = h->batch;
+  P.bs.B = B;
+  P.bs.node = P.n_nodes;
+  P.bs.quad = P.n_quads;
+  P.bs.stage = 36 * P.n_staged;
+  P.bs.nnz = 36 * P.n_blocks;
+  P.bs.dof = P.ndof;
+  P.bs.partial = 16 * (int64_t)cg_grid();
+  P.bs.slot = 3 * std::max<int64_t>(P.n_slots, 1);
+  // per-design arrays start as B copies of the given design (sso_set_design replaces them)
+  std::vector<double> x((size_t)B * P.n_nodes), y((size_t)B * P.n_nodes), z((size_t)B * P.n_nodes);
   std::vector<uint8_t> mask(P.n_nodes);
   for (int32_t i = 0; i < P.n_nodes; ++i) {
     const int32_t g = L.node_gid[i];
-    x[i] = mesh->x[g];
-    y[i] = mesh->y[g];
-    z[i] = mesh->z[g];
+    for (int b = 0; b < B; ++b) {
+      x[(size_t)b * P.n_nodes + i] = mesh->x[g];
+      y[(size_t)b * P.n_nodes + i] = mesh->y[g];
+      z[(size_t)b * P.n_nodes + i] = mesh->z[g];
+    }
     mask[i] = gmask[g];
   }
-  std::vector<double> A(P.n_beams), Iy(P.n_beams), Iz(P.n_beams), Jt(P.n_beams), t(P.n_quads);
+  std::vector<double> A(P.n_beams), Iy(P.n_beams), Iz(P.n_beams), Jt(P.n_beams), t((size_t)B * P.n_quads);
   std::vector<double> E(ne), nu(ne), G(ne);
   for (int32_t k = 0; k < P.n_beams; ++k) {
     const int32_t g = L.beam_gid[k];
@@ -617,7 +637,7 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   }
   for (int32_t k = 0; k < P.n_quads; ++k) {
     const int32_t g = L.quad_gid[k];
-    t[k] = sec->t[g];
+    for (int b = 0; b < B; ++b) t[(size_t)b * P.n_quads + k] = sec->t[g];
     E[P.n_beams + k] = mat->E[mesh->n_beams + g];
     nu[P.n_beams + k] = mat->nu[mesh->n_beams + g];
     G[P.n_beams + k] = gG[mesh->n_beams + g];
@@ -635,16 +655,16 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   int r;
 #define UP(dst, src, n) if ((r = upload(h, &P.dst, src, n))) return r
 #define AL(dst, n) if ((r = dalloc(h, &P.dst, n))) return r
-  UP(x, x.data(), P.n_nodes);
-  UP(y, y.data(), P.n_nodes);
-  UP(z, z.data(), P.n_nodes);
+  UP(x, x.data(), (int64_t)B * P.n_nodes);
+  UP(y, y.data(), (int64_t)B * P.n_nodes);
+  UP(z, z.data(), (int64_t)B * P.n_nodes);
   UP(beam_conn, L.beam_conn.data(), 2 * (int64_t)P.n_beams);
   UP(quad_conn, L.quad_conn.data(), 4 * (int64_t)P.n_quads);
   UP(A, A.data(), P.n_beams);
   UP(Iy, Iy.data(), P.n_beams);
   UP(Iz, Iz.data(), P.n_beams);
   UP(J, Jt.data(), P.n_beams);
-  UP(t, t.data(), P.n_quads);
+  UP(t, t.data(), (int64_t)B * P.n_quads);
   UP(E, E.data(), ne);
   UP(nu, nu.data(), ne);
   UP(G, G.data(), ne);
@@ -659,36 +679,36 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   UP(own_quad_gid, own_gid.data(), P.n_own_quads);
   UP(send_idx, send.data(), P.n_send);
   AL(sendbuf, 6 * std::max<int64_t>(P.n_send, 1));
-  AL(stage, 36 * P.n_staged);
-  AL(vals, 36 * P.n_blocks);
-  AL(dinv, P.ndof);
-  AL(f, P.ndof);
-  AL(fbc, P.ndof);
-  AL(xs, P.ndof);
-  AL(r, P.ndof);
-  AL(p, P.ndof);
-  AL(q, P.ndof);
-  AL(tmp, P.ndof);
-  AL(gu, P.ndof);
-  AL(gf, P.ndof);
-  AL(partial, 16 * (int64_t)cg_grid());
-  AL(st, 1);
-  AL(flags, 1);
+  AL(stage, B * P.bs.stage);
+  AL(vals, B * P.bs.nnz);
+  AL(dinv, B * P.ndof);
+  AL(f, B * P.ndof);
+  AL(fbc, B * P.ndof);
+  AL(xs, B * P.ndof);
+  AL(r, B * P.ndof);
+  AL(p, B * P.ndof);
+  AL(q, B * P.ndof);
+  AL(tmp, B * P.ndof);
+  AL(gu, B * P.ndof);
+  AL(gf, B * P.ndof);
+  AL(partial, B * P.bs.partial);
+  AL(st, B);
+  AL(flags, B);
   AL(tickets, 16);
   AL(scal, 8);
-  AL(slot_partial, 3 * std::max<int64_t>(P.n_slots, 1));
-  AL(dxyz, 3 * (int64_t)P.n_nodes);
-  AL(dt, std::max<int32_t>(P.n_quads, 1));
+  AL(slot_partial, B * P.bs.slot);
+  AL(dxyz, 3 * (int64_t)B * P.n_nodes);
+  AL(dt, (int64_t)B * std::max<int32_t>(P.n_quads, 1));
   AL(dt_own, std::max<int32_t>(P.n_own_quads, 1));
 #undef UP
 #undef AL
   CK(h, cudaMemset(P.tickets, 0, 16 * sizeof(unsigned)));
-  CK(h, cudaMemset(P.st, 0, sizeof(CgState)));
-  CK(h, cudaMemset(P.xs, 0, P.ndof * sizeof(double)));
-  CK(h, cudaMemset(P.p, 0, P.ndof * sizeof(double)));
-  CK(h, cudaMemset(P.gu, 0, P.ndof * sizeof(double)));
-  CK(h, cudaMemset(P.gf, 0, P.ndof * sizeof(double)));
-  CK(h, cudaMemset(P.f, 0, P.ndof * sizeof(double)));
+  CK(h, cudaMemset(P.st, 0, B * sizeof(CgState)));
+  CK(h, cudaMemset(P.xs, 0, B * P.ndof * sizeof(double)));
+  CK(h, cudaMemset(P.p, 0, B * P.ndof * sizeof(double)));
+  CK(h, cudaMemset(P.gu, 0, B * P.ndof * sizeof(double)));
+  CK(h, cudaMemset(P.gf, 0, B * P.ndof * sizeof(double)));
+  CK(h, cudaMemset(P.f, 0, B * P.ndof * sizeof(double)));
   P.pat.contrib.clear();  // only needed on the device
   P.pat.contrib.shrink_to_fit();
   P.pat.inc_slot.clear();
@@ -703,7 +723,7 @@ int vec_in(sso_ctx* h, const double* src, double* Part::*dst) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     const int64_t off = 6 * (int64_t)(P.lm.own_begin - h->user_node_begin);
-    CK(h, cudaMemcpyAsync(P.*dst, src + off, (size_t)P.ndof_own * sizeof(double), kind_in(h), h->stream));
+    CK(h, cudaMemcpyAsync(P.*dst, src + off, (size_t)P.B * P.ndof_own * sizeof(double), kind_in(h), h->stream));
   }
   return SSO_OK;
 }
@@ -713,7 +733,7 @@ int vec_out(sso_ctx* h, double* dst, double* Part::*src) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     const int64_t off = 6 * (int64_t)(P.lm.own_begin - h->user_node_begin);
-    CK(h, cudaMemcpyAsync(dst + off, P.*src, (size_t)P.ndof_own * sizeof(double), kind_out(h), h->stream));
+    CK(h, cudaMemcpyAsync(dst + off, P.*src, (size_t)P.B * P.ndof_own * sizeof(double), kind_out(h), h->stream));
   }
   return SSO_OK;
 }
@@ -721,8 +741,9 @@ int vec_out(sso_ctx* h, double* dst, double* Part::*src) {
 // Per-node / per-quad design arrays (global): parts take their local entries by global id.
 int design_in(sso_ctx* h, const double* src, int64_t n_global, double* Part::*dst, bool quads) {
   if (h->nranks > 1) FAIL(h, SSO_E_INVALID, "sso_set_design is not supported on multi-rank handles");
-  if (h->parts.size() == 1) {
-    CK(h, cudaMemcpyAsync(h->P0().*dst, src, (size_t)n_global * sizeof(double), kind_in(h), h->stream));
+  if (h->parts.size() == 1) {  // [batch][n_global]
+    CK(h, cudaMemcpyAsync(h->P0().*dst, src, (size_t)h->batch * n_global * sizeof(double), kind_in(h),
+                          h->stream));
     return SSO_OK;
   }
   std::vector<double> all((size_t)n_global);
@@ -758,6 +779,7 @@ int sso_options_default(sso_options* o) {
   o->nranks = 1;
   o->rank = 0;
   o->nccl_unique_id = nullptr;
+  o->batch = 1;
   return SSO_OK;
 }
 
@@ -805,6 +827,10 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
       g_create_err = "options: part_ranges must be strictly increasing from 0 to n_nodes";
       return SSO_E_INVALID;
     }
+  if (o.batch < 1 || (o.batch > 1 && (o.n_parts > 1 || o.nranks > 1))) {
+    g_create_err = "options: batch >= 1, and batch > 1 needs n_parts == nranks == 1";
+    return SSO_E_INVALID;
+  }
   if (o.nranks > 1 && !o.nccl_unique_id) {
     g_create_err = "options: nranks > 1 needs nccl_unique_id";
     return SSO_E_INVALID;
@@ -829,6 +855,7 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
   h->mem = o.mem;
   h->nranks = o.nranks;
   h->rank = o.rank;
+  h->batch = o.batch;
   h->g_nodes = mesh->n_nodes;
   h->g_beams = mesh->n_beams;
   h->g_quads = mesh->n_quads;
@@ -883,8 +910,8 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
     std::memcpy(&id, o.nccl_unique_id, sizeof(id));
     if (nccl().CommInitRank(&h->comm, o.nranks, id, o.rank) != ncclSuccess) { h->err = "ncclCommInitRank failed"; return bail(SSO_E_NCCL); }
   }
-  if (cudaMallocHost(&h->h_st, sizeof(CgState)) != cudaSuccess ||
-      cudaMallocHost(&h->h_chunk, 2 * sizeof(CgState)) != cudaSuccess ||
+  if (cudaMallocHost(&h->h_st, h->batch * sizeof(CgState)) != cudaSuccess ||
+      cudaMallocHost(&h->h_chunk, 2 * h->batch * sizeof(CgState)) != cudaSuccess ||
       cudaMallocHost(&h->h_scal, 8 * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&h->h_C, sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&h->h_flags, sizeof(DevFlags)) != cudaSuccess) { h->err = "cudaMallocHost failed"; return bail(SSO_E_OOM); }
@@ -928,15 +955,15 @@ int sso_assemble(sso_handle h) {
     {
       Scope sc(h, F_ELEMENT);
       launch_beam_elements(h->stream, P.n_beams, P.x, P.y, P.z, P.beam_conn, P.A, P.Iy, P.Iz, P.J, P.E,
-                           P.G, P.stage, P.flags);
+                           P.G, P.stage, P.flags, P.bs);
       launch_quad_elements(h->stream, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.E + P.n_beams,
                            P.nu + P.n_beams, h->drill_alpha, P.stage + 36 * 4 * (int64_t)P.n_beams,
-                           P.flags);
+                           P.flags, P.bs);
     }
     {
       Scope sc(h, F_ASSEMBLE);
       launch_assemble(h->stream, P.n_own, P.node_ptr, P.node_col, P.contrib_ptr, P.contrib, P.stage,
-                      P.fixed_mask, P.vals, P.dinv, P.flags);
+                      P.fixed_mask, P.vals, P.dinv, P.flags, P.bs);
     }
   }
   CKL(h);
@@ -970,7 +997,8 @@ static int solve_chunks(sso_ctx* h) {
   auto launch_chunk = [&](int slot) -> int {
     CK(h, cudaGraphLaunch(prof ? h->prof_exec[slot] : h->chunk_exec, h->stream));
     h->launches += h->kernels_per_chunk;
-    CK(h, cudaMemcpyAsync(&h->h_chunk[slot], P.st, sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaMemcpyAsync(&h->h_chunk[slot * P.B], P.st, P.B * sizeof(CgState), cudaMemcpyDeviceToHost,
+                          h->stream));
     CK(h, cudaEventRecord(h->ev_done[slot], h->stream));
     ++launched;
     return SSO_OK;
@@ -981,11 +1009,20 @@ static int solve_chunks(sso_ctx* h) {
     const int slot = (int)(k & 1);
     if (launched < max_chunks && (rc = launch_chunk(1 - slot))) return rc;
     CK(h, cudaEventSynchronize(h->ev_done[slot]));
-    const CgState& S = h->h_chunk[slot];
+    // batch: the chunk's kernels ran while any design was active
+    bool all_done = true;
+    long long it_max = 0;
+    bool not_spd = false;
+    for (int bd = 0; bd < P.B; ++bd) {
+      const CgState& Sb = h->h_chunk[slot * P.B + bd];
+      all_done &= Sb.done != 0;
+      it_max = std::max<long long>(it_max, Sb.iter);
+      not_spd |= Sb.done && Sb.status == SSO_E_NOT_SPD;
+    }
     if (prof) {
-      long long ran = S.iter - iters_before;
-      if (S.done && S.status == SSO_E_NOT_SPD && ran < h->check_every) ran += 1;
-      iters_before = S.iter;
+      long long ran = it_max - iters_before;
+      if (not_spd && ran < h->check_every) ran += 1;
+      iters_before = it_max;
       for (long long i = 0; i < std::min<long long>(ran, h->check_every); i += PROF_EVERY) {
         float ms = 0.f;
         CK(h, cudaEventElapsedTime(&ms, h->chunk_ev[slot][2 * i], h->chunk_ev[slot][2 * i + 1]));
@@ -993,7 +1030,7 @@ static int solve_chunks(sso_ctx* h) {
         h->tm.launches[F_SPMV] += 1;
       }
     }
-    if (S.done || launched == k + 1) break;
+    if (all_done || launched == k + 1) break;
   }
   return SSO_OK;
 }
@@ -1012,21 +1049,23 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
     if ((rc = vec_in(h, u, &Part::xs))) return rc;
     for (auto& pp : h->parts) {
       Scope sc(h, F_UPDATE);
-      launch_zero_fixed(h->stream, (int)pp->ndof_own, pp->fixed_mask, pp->xs);
+      launch_zero_fixed(h->stream, (int)pp->ndof_own, pp->fixed_mask, pp->xs, pp->bs);
     }
     if ((rc = exchange(h, V_X))) return rc;
     for (auto& pp : h->parts) {
       Part& P = *pp;
       Scope sc(h, F_SPMV);
-      launch_spmv(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.xs, P.tmp);
+      launch_spmv(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.xs, P.tmp, P.bs);
     }
   }
-  std::memset(h->h_st, 0, sizeof(CgState));
-  h->h_st->tol2 = h->rtol * h->rtol;
-  h->h_st->max_iter = h->max_iter;
-  h->h_st->dist = dist ? 1 : 0;
+  std::memset(h->h_st, 0, h->batch * sizeof(CgState));
+  for (int bd = 0; bd < h->batch; ++bd) {
+    h->h_st[bd].tol2 = h->rtol * h->rtol;
+    h->h_st[bd].max_iter = h->max_iter;
+    h->h_st[bd].dist = dist ? 1 : 0;
+  }
   for (auto& pp : h->parts)
-    CK(h, cudaMemcpyAsync(pp->st, h->h_st, sizeof(CgState), cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(pp->st, h->h_st, pp->B * sizeof(CgState), cudaMemcpyHostToDevice, h->stream));
   // the pinned staging struct is reused below: make the uploads complete first
   if ((rc = sync(h))) return rc;
   CK(h, cudaEventRecord(h->ev_a, h->stream));
@@ -1034,7 +1073,7 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
     Part& P = *pp;
     Scope sc(h, F_UPDATE);
     launch_cg_init(h->stream, (int)P.ndof_own, P.f, P.fixed_mask, P.dinv, P.fbc, P.xs, P.r, P.p,
-                   P.partial, P.st, warm, P.tmp);
+                   P.partial, P.st, warm, P.tmp, P.bs);
   }
   if (dist) {
     if ((rc = allreduce(h, 3))) return rc;
@@ -1050,26 +1089,35 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     long long g1 = g_launches;
-    launch_spmv(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.xs, P.tmp);
-    launch_residual_norm(h->stream, (int)P.ndof_own, P.fbc, P.tmp, P.partial, P.tickets + 2, &P.st->red[0]);
+    launch_spmv(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.xs, P.tmp, P.bs);
+    launch_residual_norm(h->stream, (int)P.ndof_own, P.fbc, P.tmp, P.partial, P.st, P.bs);
     h->launches += g_launches - g1;
   }
   if ((rc = allreduce(h, 1))) return rc;
-  CK(h, cudaMemcpyAsync(h->h_st, h->P0().st, sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaMemcpyAsync(h->h_st, h->P0().st, h->batch * sizeof(CgState), cudaMemcpyDeviceToHost,
+                        h->stream));
   if ((rc = vec_out(h, u, &Part::xs))) return rc;
   if ((rc = sync(h))) return rc;
   CKL(h);
-  const CgState& S = *h->h_st;
-  const int status = S.done ? S.status : SSO_E_NOT_CONVERGED;
-  if (info) {
-    info->iters = S.iter;
-    info->rel_res = S.ff > 0 ? std::sqrt(S.rr / S.ff) : 0.0;
-    info->true_rel_res = S.ff > 0 ? std::sqrt(S.red[0] / S.ff) : 0.0;
-    float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, h->ev_a, h->ev_b) != cudaSuccess) (void)cudaGetLastError();
-    info->ms = ms;
-    info->status = status;
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, h->ev_a, h->ev_b) != cudaSuccess) (void)cudaGetLastError();
+  int status = SSO_OK, worst = 0;
+  for (int bd = 0; bd < h->batch; ++bd) {
+    const CgState& Sb = h->h_st[bd];
+    const int st_b = Sb.done ? Sb.status : SSO_E_NOT_CONVERGED;
+    if (info) {
+      info[bd].iters = Sb.iter;
+      info[bd].rel_res = Sb.ff > 0 ? std::sqrt(Sb.rr / Sb.ff) : 0.0;
+      info[bd].true_rel_res = Sb.ff > 0 ? std::sqrt(Sb.red[0] / Sb.ff) : 0.0;
+      info[bd].ms = ms;
+      info[bd].status = st_b;
+    }
+    if (st_b == SSO_E_NOT_SPD || (st_b != SSO_OK && status == SSO_OK)) {
+      status = st_b;
+      worst = bd;
+    }
   }
+  const CgState& S = h->h_st[worst];
   h->solved = (status == SSO_OK);
   if (status == SSO_E_NOT_SPD) FAIL(h, SSO_E_NOT_SPD, "CG breakdown: p^T K p <= 0 (matrix not SPD)");
   if (status == SSO_E_NOT_CONVERGED) {
@@ -1094,24 +1142,27 @@ static int grad_impl(sso_ctx* h, sso_objective obj, double* Part::*fv, int uvec,
     double* U = vec_of(P, uvec);
     {
       Scope sc(h, F_REDUCE);
-      launch_dot_local(h->stream, (int)P.ndof_own, P.*fv, U, P.partial, P.tickets + 3, &P.st->red[0]);
+      launch_dot_local(h->stream, (int)P.ndof_own, P.*fv, U, P.partial, P.st, P.bs);
     }
     {
       Scope sc(h, F_GRAD);
       launch_beam_grad(h->stream, P.n_beams, P.x, P.y, P.z, P.beam_conn, P.A, P.Iy, P.Iz, P.J, P.E, P.G,
-                       U, s, P.slot_partial);
+                       U, s, P.slot_partial, P.bs);
       launch_quad_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.E, P.nu,
-                       h->drill_alpha, U, s, P.slot_partial, P.dt);
+                       h->drill_alpha, U, s, P.slot_partial, P.dt, P.bs);
     }
     {
       Scope sc(h, F_REDUCE);
-      launch_node_reduce(h->stream, P.n_own, P.inc_ptr, P.inc_slot, P.slot_partial, P.dxyz);
+      launch_node_reduce(h->stream, P.n_own, P.inc_ptr, P.inc_slot, P.slot_partial, P.dxyz, P.bs);
       if (h->distributed()) launch_gather(h->stream, P.n_own_quads, P.own_quad_local, P.dt, P.dt_own);
     }
   }
   if ((rc = allreduce(h, 1))) return rc;
   CKL(h);
-  if (dC_dxyz) {
+  if (dC_dxyz && h->batch > 1) {
+    CK(h, cudaMemcpyAsync(dC_dxyz, h->P0().dxyz, (size_t)h->batch * 3 * h->user_nodes * sizeof(double),
+                          kind_out(h), h->stream));
+  } else if (dC_dxyz) {
     for (auto& pp : h->parts) {
       Part& P = *pp;
       for (int a = 0; a < 3; ++a)
@@ -1122,7 +1173,8 @@ static int grad_impl(sso_ctx* h, sso_objective obj, double* Part::*fv, int uvec,
   }
   if (dC_dt && h->user_quads > 0) {
     if (!h->distributed()) {
-      CK(h, cudaMemcpyAsync(dC_dt, h->P0().dt, (size_t)h->user_quads * sizeof(double), kind_out(h), h->stream));
+      CK(h, cudaMemcpyAsync(dC_dt, h->P0().dt, (size_t)h->batch * h->user_quads * sizeof(double), kind_out(h),
+                            h->stream));
     } else if (h->nranks > 1) {
       CK(h, cudaMemcpyAsync(dC_dt, h->P0().dt_own, (size_t)h->user_quads * sizeof(double), kind_out(h), h->stream));
     } else {
@@ -1135,15 +1187,17 @@ static int grad_impl(sso_ctx* h, sso_objective obj, double* Part::*fv, int uvec,
       CK(h, cudaMemcpyAsync(dC_dt, h->d_dt_all, (size_t)h->user_quads * sizeof(double), kind_out(h), h->stream));
     }
   }
-  CK(h, cudaMemcpyAsync(h->h_C, &h->P0().st->red[0], sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaMemcpyAsync(h->h_st, h->P0().st, h->batch * sizeof(CgState), cudaMemcpyDeviceToHost,
+                        h->stream));
   if ((rc = sync(h))) return rc;
   CKL(h);
   if (C) {
-    const double v = s * h->h_C[0];
+    std::vector<double> v(h->batch);
+    for (int bd = 0; bd < h->batch; ++bd) v[bd] = s * h->h_st[bd].red[0];
     if (h->mem == SSO_MEM_HOST) {
-      *C = v;
+      std::memcpy(C, v.data(), v.size() * sizeof(double));
     } else {
-      CK(h, cudaMemcpy(C, &v, sizeof(double), cudaMemcpyHostToDevice));
+      CK(h, cudaMemcpy(C, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
     }
   }
   return SSO_OK;
@@ -1175,7 +1229,7 @@ int sso_spmv(sso_handle h, const double* xin, double* yout) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     Scope sc(h, F_SPMV);
-    launch_spmv(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.gu, P.tmp);
+    launch_spmv(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.gu, P.tmp, P.bs);
   }
   CKL(h);
   if ((rc = vec_out(h, yout, &Part::tmp))) return rc;

@@ -25,7 +25,14 @@ __global__ void __launch_bounds__(256) assemble_kernel(
     int n_nodes, const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ node_col,
     const int64_t* __restrict__ contrib_ptr, const int32_t* __restrict__ contrib,
     const double* __restrict__ stage, const uint8_t* __restrict__ fixed_mask,
-    double* __restrict__ vals, double* __restrict__ dinv, DevFlags* flags) {
+    double* __restrict__ vals, double* __restrict__ dinv, DevFlags* flags, BatchStrides bs) {
+  {  // design of a batch (blockIdx.y)
+    const int bd = blockIdx.y;
+    stage += bd * bs.stage;
+    vals += bd * bs.nnz;
+    dinv += bd * bs.dof;
+    flags += bd;
+  }
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -71,14 +78,14 @@ __global__ void __launch_bounds__(256) assemble_kernel(
 void launch_assemble(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
                      const int32_t* node_col, const int64_t* contrib_ptr,
                      const int32_t* contrib, const double* stage, const uint8_t* fixed_mask,
-                     double* vals, double* dinv, DevFlags* flags) {
+                     double* vals, double* dinv, DevFlags* flags, const BatchStrides& bs) {
   if (n_nodes <= 0) return;
   const int warps_per_cta = 8;
   int64_t need = ((int64_t)n_nodes + warps_per_cta - 1) / warps_per_cta;
-  int grid = (int)std::min<int64_t>(need, (int64_t)cg_grid() * 4);
+  const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)cg_grid() * 4 / bs.B)), bs.B);
   assemble_kernel<<<grid, 32 * warps_per_cta, 0, s>>>(n_nodes, node_ptr, node_col, contrib_ptr,
                                                        contrib, stage, fixed_mask, vals, dinv,
-                                                       flags);
+                                                       flags, bs);
   SSO_POST_LAUNCH("assemble_kernel");
 }
 

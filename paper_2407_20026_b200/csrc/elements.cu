@@ -75,8 +75,17 @@ __global__ void __launch_bounds__(128) quad_element_kernel(
     const double* __restrict__ gz, const int32_t* __restrict__ conn,
     const double* __restrict__ gt, const double* __restrict__ gE,
     const double* __restrict__ gnu, double drill_alpha, double* __restrict__ stage,
-    DevFlags* flags) {
+    DevFlags* flags, BatchStrides bs) {
   __shared__ double sm[QUADS_PER_CTA * 16 * STAGE_PITCH];
+  {  // design of a batch (blockIdx.y)
+    const int bd = blockIdx.y;
+    gx += bd * bs.node;
+    gy += bd * bs.node;
+    gz += bd * bs.node;
+    gt += bd * bs.quad;
+    stage += bd * bs.stage;
+    flags += bd;
+  }
   const int tid = threadIdx.x;
   const int le = tid >> 4, blk = tid & 15;
   const int bi = blk >> 2, bj = blk & 3;
@@ -310,8 +319,16 @@ __global__ void __launch_bounds__(128) beam_element_kernel(
     const double* __restrict__ gA, const double* __restrict__ gIy,
     const double* __restrict__ gIz, const double* __restrict__ gJ,
     const double* __restrict__ gE, const double* __restrict__ gG, double* __restrict__ stage,
-    DevFlags* flags) {
+    DevFlags* flags, BatchStrides bs) {
   __shared__ double sm[BEAMS_PER_CTA * 4 * STAGE_PITCH];
+  {  // design of a batch (blockIdx.y)
+    const int bd = blockIdx.y;
+    gx += bd * bs.node;
+    gy += bd * bs.node;
+    gz += bd * bs.node;
+    stage += bd * bs.stage;
+    flags += bd;
+  }
   const int tid = threadIdx.x;
   const int le = tid >> 2, blk = tid & 3;
   const int bi = blk >> 1, bj = blk & 1;
@@ -373,22 +390,23 @@ __global__ void __launch_bounds__(128) beam_element_kernel(
 void launch_quad_elements(cudaStream_t s, int n_quads, const double* x, const double* y,
                           const double* z, const int32_t* conn, const double* t,
                           const double* E, const double* nu, double drill_alpha,
-                          double* stage, DevFlags* flags) {
+                          double* stage, DevFlags* flags, const BatchStrides& bs) {
   if (n_quads <= 0) return;
-  const int grid = (n_quads + QUADS_PER_CTA - 1) / QUADS_PER_CTA;
+  const dim3 grid((n_quads + QUADS_PER_CTA - 1) / QUADS_PER_CTA, bs.B);
   quad_element_kernel<<<grid, 128, 0, s>>>(n_quads, x, y, z, conn, t, E, nu, drill_alpha, stage,
-                                           flags);
+                                           flags, bs);
   SSO_POST_LAUNCH("quad_element_kernel");
 }
 
 void launch_beam_elements(cudaStream_t s, int n_beams, const double* x, const double* y,
                           const double* z, const int32_t* conn, const double* A,
                           const double* Iy, const double* Iz, const double* J,
-                          const double* E, const double* G, double* stage, DevFlags* flags) {
+                          const double* E, const double* G, double* stage, DevFlags* flags,
+                          const BatchStrides& bs) {
   if (n_beams <= 0) return;
-  const int grid = (n_beams + BEAMS_PER_CTA - 1) / BEAMS_PER_CTA;
+  const dim3 grid((n_beams + BEAMS_PER_CTA - 1) / BEAMS_PER_CTA, bs.B);
   beam_element_kernel<<<grid, 128, 0, s>>>(n_beams, x, y, z, conn, A, Iy, Iz, J, E, G, stage,
-                                           flags);
+                                           flags, bs);
   SSO_POST_LAUNCH("beam_element_kernel");
 }
 

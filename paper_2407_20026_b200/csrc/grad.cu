@@ -197,7 +197,17 @@ __global__ void __launch_bounds__(128) quad_grad_kernel(
     const double* __restrict__ gz, const int32_t* __restrict__ conn,
     const double* __restrict__ gt, const double* __restrict__ gE,
     const double* __restrict__ gnu, double drill_alpha, const double* __restrict__ u,
-    double scale, double* __restrict__ slot_partial, double* __restrict__ dC_dt) {
+    double scale, double* __restrict__ slot_partial, double* __restrict__ dC_dt, BatchStrides bs) {
+  {  // design of a batch (blockIdx.y)
+    const int bd = blockIdx.y;
+    gx += bd * bs.node;
+    gy += bd * bs.node;
+    gz += bd * bs.node;
+    gt += bd * bs.quad;
+    u += bd * bs.dof;
+    slot_partial += bd * bs.slot;
+    dC_dt += bd * bs.quad;
+  }
   const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4;
   const int p = threadIdx.x & 15;
   if (q >= n_quads || p > 12) return;
@@ -237,7 +247,15 @@ __global__ void __launch_bounds__(128) beam_grad_kernel(
     const double* __restrict__ gA, const double* __restrict__ gIy,
     const double* __restrict__ gIz, const double* __restrict__ gJ,
     const double* __restrict__ gE, const double* __restrict__ gG, const double* __restrict__ u,
-    double scale, double* __restrict__ slot_partial) {
+    double scale, double* __restrict__ slot_partial, BatchStrides bs) {
+  {  // design of a batch (blockIdx.y)
+    const int bd = blockIdx.y;
+    gx += bd * bs.node;
+    gy += bd * bs.node;
+    gz += bd * bs.node;
+    u += bd * bs.dof;
+    slot_partial += bd * bs.slot;
+  }
   const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
   const int p = threadIdx.x & 7;
   if (e >= n_beams || p > 5) return;
@@ -302,7 +320,9 @@ __global__ void __launch_bounds__(128) beam_grad_kernel(
 __global__ void __launch_bounds__(256) node_reduce_kernel(int n_nodes, const int64_t* __restrict__ inc_ptr,
                                                           const int32_t* __restrict__ inc_slot,
                                                           const double* __restrict__ slot_partial,
-                                                          double* __restrict__ out) {
+                                                          double* __restrict__ out, BatchStrides bs) {
+  slot_partial += blockIdx.y * bs.slot;
+  out += blockIdx.y * 3 * bs.node;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < n_nodes; n += stride) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -323,33 +343,33 @@ __global__ void __launch_bounds__(256) node_reduce_kernel(int n_nodes, const int
 void launch_quad_grad(cudaStream_t s, int n_beams, int n_quads, const double* x, const double* y,
                       const double* z, const int32_t* conn, const double* t, const double* E,
                       const double* nu, double drill_alpha, const double* u, double scale,
-                      double* slot_partial, double* dC_dt) {
+                      double* slot_partial, double* dC_dt, const BatchStrides& bs) {
   if (n_quads <= 0) return;
   const int64_t threads = 16 * (int64_t)n_quads;
-  const int grid = (int)((threads + 127) / 128);
+  const dim3 grid((unsigned)((threads + 127) / 128), bs.B);
   quad_grad_kernel<<<grid, 128, 0, s>>>(n_beams, n_quads, x, y, z, conn, t, E, nu, drill_alpha, u,
-                                        scale, slot_partial, dC_dt);
+                                        scale, slot_partial, dC_dt, bs);
   SSO_POST_LAUNCH("quad_grad_kernel");
 }
 
 void launch_beam_grad(cudaStream_t s, int n_beams, const double* x, const double* y,
                       const double* z, const int32_t* conn, const double* A, const double* Iy,
                       const double* Iz, const double* J, const double* E, const double* G,
-                      const double* u, double scale, double* slot_partial) {
+                      const double* u, double scale, double* slot_partial, const BatchStrides& bs) {
   if (n_beams <= 0) return;
   const int64_t threads = 8 * (int64_t)n_beams;
-  const int grid = (int)((threads + 127) / 128);
+  const dim3 grid((unsigned)((threads + 127) / 128), bs.B);
   beam_grad_kernel<<<grid, 128, 0, s>>>(n_beams, x, y, z, conn, A, Iy, Iz, J, E, G, u, scale,
-                                        slot_partial);
+                                        slot_partial, bs);
   SSO_POST_LAUNCH("beam_grad_kernel");
 }
 
 void launch_node_reduce(cudaStream_t s, int n_nodes, const int64_t* inc_ptr, const int32_t* inc_slot,
-                        const double* slot_partial, double* dC_dxyz) {
+                        const double* slot_partial, double* dC_dxyz, const BatchStrides& bs) {
   if (n_nodes <= 0) return;
   int64_t need = ((int64_t)n_nodes + 255) / 256;
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)cg_grid()));
-  node_reduce_kernel<<<grid, 256, 0, s>>>(n_nodes, inc_ptr, inc_slot, slot_partial, dC_dxyz);
+  const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)cg_grid() / bs.B)), bs.B);
+  node_reduce_kernel<<<grid, 256, 0, s>>>(n_nodes, inc_ptr, inc_slot, slot_partial, dC_dxyz, bs);
   SSO_POST_LAUNCH("node_reduce_kernel");
 }
 

@@ -225,11 +225,21 @@ __global__ void __launch_bounds__(SPMV_WARPS * 32, MINB) spmv_tma_kernel(
     int n_nodes, int nodes_per_warp, const int64_t* __restrict__ node_ptr,
     const int32_t* __restrict__ node_col, const double* __restrict__ vals,
     const double* __restrict__ p, double* __restrict__ q, double* __restrict__ partial,
-    CgState* st) {
+    CgState* st, BatchStrides bs) {
   constexpr int SLOT_DOUBLES = 36 * SLOT_DEG;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bar[SPMV_WARPS][SPMV_STAGES];
   __shared__ double sm[32];
+  {  // design of a batch (blockIdx.y)
+    const int bd = blockIdx.y;
+    vals += bd * bs.nnz;
+    p += bd * bs.dof;
+    q += bd * bs.dof;
+    if (DOT) {
+      partial += bd * bs.partial;
+      st += bd;
+    }
+  }
   if (DOT && st->done) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t gw = (int64_t)blockIdx.x * SPMV_WARPS + warp;
@@ -319,8 +329,18 @@ __global__ void __launch_bounds__(256) cg_update_kernel(int ndof, const double* 
                                                         const double* __restrict__ p,
                                                         const double* __restrict__ q,
                                                         double* __restrict__ partial,
-                                                        CgState* st) {
+                                                        CgState* st, BatchStrides bs) {
   __shared__ double sm[64];
+  {  // design of a batch (blockIdx.y)
+    const int bd = blockIdx.y;
+    dinv += bd * bs.dof;
+    x += bd * bs.dof;
+    r += bd * bs.dof;
+    p += bd * bs.dof;
+    q += bd * bs.dof;
+    partial += bd * bs.partial;
+    st += bd;
+  }
   if (st->done) return;
   const double alpha = st->alpha;
   double v[2] = {0.0, 0.0};  // r^T z, r^T r
@@ -367,7 +387,14 @@ __global__ void __launch_bounds__(256) cg_update_kernel(int ndof, const double* 
 __global__ void __launch_bounds__(256) cg_pupdate_kernel(int ndof, const double* __restrict__ dinv,
                                                          const double* __restrict__ r,
                                                          double* __restrict__ p,
-                                                         const CgState* st) {
+                                                         const CgState* st, BatchStrides bs) {
+  {  // design of a batch (blockIdx.y)
+    const int bd = blockIdx.y;
+    dinv += bd * bs.dof;
+    r += bd * bs.dof;
+    p += bd * bs.dof;
+    st += bd;
+  }
   if (st->done) return;
   const double beta = st->beta;
   const int64_t n2 = ndof / 2;
@@ -393,8 +420,21 @@ __global__ void __launch_bounds__(256) cg_init_kernel(int ndof, const double* __
                                                       double* __restrict__ r,
                                                       double* __restrict__ p,
                                                       double* __restrict__ partial, CgState* st,
-                                                      int warm, const double* __restrict__ Kx0) {
+                                                      int warm, const double* __restrict__ Kx0,
+                                                      BatchStrides bs) {
   __shared__ double sm[96];
+  {  // design of a batch (blockIdx.y)
+    const int bd = blockIdx.y;
+    f += bd * bs.dof;
+    dinv += bd * bs.dof;
+    fbc += bd * bs.dof;
+    x += bd * bs.dof;
+    r += bd * bs.dof;
+    p += bd * bs.dof;
+    Kx0 += bd * bs.dof;
+    partial += bd * bs.partial;
+    st += bd;
+  }
   double v[3] = {0.0, 0.0, 0.0};  // f^T f, r^T z, r^T r
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndof; i += stride) {
@@ -433,7 +473,9 @@ __global__ void __launch_bounds__(256) cg_init_kernel(int ndof, const double* __
 }
 
 // zero fixed entries of x (warm start)
-__global__ void zero_fixed_kernel(int ndof, const uint8_t* __restrict__ fixed_mask, double* x) {
+__global__ void zero_fixed_kernel(int ndof, const uint8_t* __restrict__ fixed_mask, double* x,
+                                  BatchStrides bs) {
+  x += blockIdx.y * bs.dof;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndof; i += stride)
     if ((fixed_mask[i / 6] >> (i % 6)) & 1) x[i] = 0.0;
@@ -442,27 +484,22 @@ __global__ void zero_fixed_kernel(int ndof, const uint8_t* __restrict__ fixed_ma
 __global__ void __launch_bounds__(256) residual_kernel(int ndof, const double* __restrict__ f,
                                                        const double* __restrict__ Kx,
                                                        double* __restrict__ partial,
-                                                       unsigned int* ticket, double* out) {
+                                                       CgState* st, BatchStrides bs) {
   __shared__ double sm[32];
+  {  // design of a batch (blockIdx.y)
+    const int bd = blockIdx.y;
+    f += bd * bs.dof;
+    Kx += bd * bs.dof;
+    partial += bd * bs.partial;
+    st += bd;
+  }
   double v[1] = {0.0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndof; i += stride) {
     const double d = f[i] - Kx[i];
     v[0] += d * d;
   }
-  if (grid_sum<1>(v, partial, ticket, sm) && threadIdx.x == 0) *out = v[0];
-}
-
-__global__ void __launch_bounds__(256) dot_kernel(int n, const double* __restrict__ a,
-                                                  const double* __restrict__ b, double scale,
-                                                  double* __restrict__ partial, unsigned int* ticket,
-                                                  double* out) {
-  __shared__ double sm[32];
-  double v[1] = {0.0};
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    v[0] += a[i] * b[i];
-  if (grid_sum<1>(v, partial, ticket, sm) && threadIdx.x == 0) *out = scale * v[0];
+  if (grid_sum<1>(v, partial, &st->ticket[3], sm) && threadIdx.x == 0) st->red[0] = v[0];
 }
 
 // Scalar step of the partitioned CG after the cross-part allreduce of red[].
@@ -539,17 +576,24 @@ __global__ void scatter_kernel(int n, const int32_t* __restrict__ idx, const dou
 __global__ void __launch_bounds__(256) dot_local_kernel(int n, const double* __restrict__ a,
                                                         const double* __restrict__ b,
                                                         double* __restrict__ partial,
-                                                        unsigned int* ticket, double* out) {
+                                                        CgState* st, BatchStrides bs) {
   __shared__ double sm[32];
+  {  // design of a batch (blockIdx.y)
+    const int bd = blockIdx.y;
+    a += bd * bs.dof;
+    b += bd * bs.dof;
+    partial += bd * bs.partial;
+    st += bd;
+  }
   double v[1] = {0.0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) v[0] += a[i] * b[i];
-  if (grid_sum<1>(v, partial, ticket, sm) && threadIdx.x == 0) *out = v[0];
+  if (grid_sum<1>(v, partial, &st->ticket[3], sm) && threadIdx.x == 0) st->red[0] = v[0];
 }
 
-int vec_grid(int64_t n) {
+int vec_grid(int64_t n, int B = 1) {
   int64_t need = (n + 255) / 256;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)cg_grid()));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)cg_grid() / B));
 }
 
 }  // namespace
@@ -583,8 +627,8 @@ void launch_scatter(cudaStream_t s, int n, const int32_t* idx, const double* src
 }
 
 void launch_dot_local(cudaStream_t s, int n, const double* a, const double* b, double* partial,
-                      unsigned int* ticket, double* out) {
-  dot_local_kernel<<<vec_grid(n), 256, 0, s>>>(n, a, b, partial, ticket, out);
+                      CgState* st, const BatchStrides& bs) {
+  dot_local_kernel<<<dim3(vec_grid(n, bs.B), bs.B), 256, 0, s>>>(n, a, b, partial, st, bs);
   SSO_POST_LAUNCH("dot_local_kernel");
 }
 
@@ -600,23 +644,25 @@ int cg_grid() {
 
 void launch_cg_init(cudaStream_t s, int ndof, const double* f, const uint8_t* fixed_mask,
                     const double* dinv, double* fbc, double* x, double* r, double* p,
-                    double* partial, CgState* st, int warm, const double* Kx0) {
-  cg_init_kernel<<<vec_grid(ndof), 256, 0, s>>>(ndof, f, fixed_mask, dinv, fbc, x, r, p, partial,
-                                                st, warm, Kx0);
+                    double* partial, CgState* st, int warm, const double* Kx0,
+                    const BatchStrides& bs) {
+  cg_init_kernel<<<dim3(vec_grid(ndof, bs.B), bs.B), 256, 0, s>>>(ndof, f, fixed_mask, dinv, fbc, x, r, p,
+                                                                partial, st, warm, Kx0, bs);
   SSO_POST_LAUNCH("cg_init_kernel");
 }
 
-void launch_zero_fixed(cudaStream_t s, int ndof, const uint8_t* fixed_mask, double* x) {
-  zero_fixed_kernel<<<vec_grid(ndof), 256, 0, s>>>(ndof, fixed_mask, x);
+void launch_zero_fixed(cudaStream_t s, int ndof, const uint8_t* fixed_mask, double* x,
+                       const BatchStrides& bs) {
+  zero_fixed_kernel<<<dim3(vec_grid(ndof, bs.B), bs.B), 256, 0, s>>>(ndof, fixed_mask, x, bs);
   SSO_POST_LAUNCH("zero_fixed_kernel");
 }
 
 struct SpmvVariant {
   int stages, slot_deg, minb;
   void (*dot)(int, int, const int64_t*, const int32_t*, const double*, const double*, double*,
-              double*, CgState*);
+              double*, CgState*, BatchStrides);
   void (*plain)(int, int, const int64_t*, const int32_t*, const double*, const double*, double*,
-                double*, CgState*);
+                double*, CgState*, BatchStrides);
 };
 #define SPMV_VARIANT(S, D, M) \
   { S, D, M, spmv_tma_kernel<true, S, D, M>, spmv_tma_kernel<false, S, D, M> }
@@ -639,9 +685,9 @@ static const SpmvVariant& spmv_variant() {
   return kSpmvVariants[v];
 }
 
-static void spmv_config(int n_nodes, int* grid, int* npw, int* smem) {
+static void spmv_config(int n_nodes, int B, int* grid, int* npw, int* smem) {
   const SpmvVariant& V = spmv_variant();
-  const int ctas = V.minb * (cg_grid() / 4);  // persistent: minb CTAs per SM
+  const int ctas = std::max(1, V.minb * (cg_grid() / 4) / B);  // persistent: minb CTAs per SM in total
   const int64_t warps = (int64_t)ctas * SPMV_WARPS;
   int per = (int)((n_nodes + warps - 1) / warps);
   if (per < 1) per = 1;
@@ -651,47 +697,43 @@ static void spmv_config(int n_nodes, int* grid, int* npw, int* smem) {
 }
 
 void launch_spmv_dot(cudaStream_t s, int n_nodes, const int64_t* node_ptr, const int32_t* node_col,
-                     const double* vals, const double* p, double* q, double* partial, CgState* st) {
+                     const double* vals, const double* p, double* q, double* partial, CgState* st,
+                     const BatchStrides& bs) {
   int grid, npw, smem;
-  spmv_config(n_nodes, &grid, &npw, &smem);
-  spmv_variant().dot<<<grid, SPMV_WARPS * 32, smem, s>>>(n_nodes, npw, node_ptr, node_col, vals, p, q,
-                                                         partial, st);
+  spmv_config(n_nodes, bs.B, &grid, &npw, &smem);
+  spmv_variant().dot<<<dim3(grid, bs.B), SPMV_WARPS * 32, smem, s>>>(n_nodes, npw, node_ptr, node_col, vals,
+                                                                     p, q, partial, st, bs);
   SSO_POST_LAUNCH("spmv_dot_kernel");
 }
 
 void launch_spmv(cudaStream_t s, int n_nodes, const int64_t* node_ptr, const int32_t* node_col,
-                 const double* vals, const double* x, double* y) {
+                 const double* vals, const double* x, double* y, const BatchStrides& bs) {
   int grid, npw, smem;
-  spmv_config(n_nodes, &grid, &npw, &smem);
-  spmv_variant().plain<<<grid, SPMV_WARPS * 32, smem, s>>>(n_nodes, npw, node_ptr, node_col, vals, x, y,
-                                                           nullptr, nullptr);
+  spmv_config(n_nodes, bs.B, &grid, &npw, &smem);
+  spmv_variant().plain<<<dim3(grid, bs.B), SPMV_WARPS * 32, smem, s>>>(n_nodes, npw, node_ptr, node_col,
+                                                                       vals, x, y, nullptr, nullptr, bs);
   SSO_POST_LAUNCH("spmv_kernel");
 }
 
 
 
 void launch_cg_update(cudaStream_t s, int ndof, const double* dinv, double* x, double* r,
-                      const double* p, const double* q, double* partial, CgState* st) {
-  cg_update_kernel<<<vec_grid(ndof), 256, 0, s>>>(ndof, dinv, x, r, p, q, partial, st);
+                      const double* p, const double* q, double* partial, CgState* st,
+                      const BatchStrides& bs) {
+  cg_update_kernel<<<dim3(vec_grid(ndof, bs.B), bs.B), 256, 0, s>>>(ndof, dinv, x, r, p, q, partial, st, bs);
   SSO_POST_LAUNCH("cg_update_kernel");
 }
 
 void launch_cg_pupdate(cudaStream_t s, int ndof, const double* dinv, const double* r, double* p,
-                       CgState* st) {
-  cg_pupdate_kernel<<<vec_grid(ndof), 256, 0, s>>>(ndof, dinv, r, p, st);
+                       CgState* st, const BatchStrides& bs) {
+  cg_pupdate_kernel<<<dim3(vec_grid(ndof, bs.B), bs.B), 256, 0, s>>>(ndof, dinv, r, p, st, bs);
   SSO_POST_LAUNCH("cg_pupdate_kernel");
 }
 
 void launch_residual_norm(cudaStream_t s, int ndof, const double* f, const double* Kx,
-                          double* partial, unsigned int* ticket, double* out) {
-  residual_kernel<<<vec_grid(ndof), 256, 0, s>>>(ndof, f, Kx, partial, ticket, out);
+                          double* partial, CgState* st, const BatchStrides& bs) {
+  residual_kernel<<<dim3(vec_grid(ndof, bs.B), bs.B), 256, 0, s>>>(ndof, f, Kx, partial, st, bs);
   SSO_POST_LAUNCH("residual_kernel");
-}
-
-void launch_dot(cudaStream_t s, int n, const double* a, const double* b, double scale,
-                double* partial, unsigned int* ticket, double* out) {
-  dot_kernel<<<vec_grid(n), 256, 0, s>>>(n, a, b, scale, partial, ticket, out);
-  SSO_POST_LAUNCH("dot_kernel");
 }
 
 }  // namespace sso

@@ -75,37 +75,61 @@ struct Timers {
   size_t pool_used = 0;
 };
 
+// Batched designs: B designs share connectivity, supports and
+// materials; per-design arrays are design-major with these strides (elements of
+// the array type).  Kernels take the design from blockIdx.y.  B = 1: strides unused.
+struct BatchStrides {
+  int B = 1;
+  int64_t node = 0;     // coordinates [B][n]
+  int64_t quad = 0;     // thickness, dC/dt [B][n_quads]
+  int64_t stage = 0;    // staged element blocks [B][36 n_staged]
+  int64_t nnz = 0;      // CSR values [B][nnz]
+  int64_t dof = 0;      // vectors [B][6 n]
+  int64_t partial = 0;  // per-CTA partials [B][..]
+  int64_t slot = 0;     // gradient slot partials [B][3 n_slots]
+};
+
 // Launch wrappers (implemented in the .cu files).  All are stream-ordered.
 void launch_beam_elements(cudaStream_t s, int n_beams, const double* x, const double* y,
                           const double* z, const int32_t* conn, const double* A,
                           const double* Iy, const double* Iz, const double* J,
-                          const double* E, const double* G, double* stage, DevFlags* flags);
+                          const double* E, const double* G, double* stage, DevFlags* flags,
+    const BatchStrides& bs = BatchStrides());
 void launch_quad_elements(cudaStream_t s, int n_quads, const double* x, const double* y,
                           const double* z, const int32_t* conn, const double* t,
                           const double* E, const double* nu, double drill_alpha,
-                          double* stage, DevFlags* flags);
+                          double* stage, DevFlags* flags,
+    const BatchStrides& bs = BatchStrides());
 void launch_assemble(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
                      const int32_t* node_col, const int64_t* contrib_ptr,
                      const int32_t* contrib, const double* stage, const uint8_t* fixed_mask,
-                     double* vals, double* dinv, DevFlags* flags);
+                     double* vals, double* dinv, DevFlags* flags,
+    const BatchStrides& bs = BatchStrides());
 
 // PCG kernels
 int cg_grid();  // persistent grid size (multiple of the SM count)
 void launch_cg_init(cudaStream_t s, int ndof, const double* f, const uint8_t* fixed_mask,
                     const double* dinv, double* fbc, double* x, double* r, double* p,
-                    double* partial, CgState* st, int warm, const double* Kx0);
+                    double* partial, CgState* st, int warm, const double* Kx0,
+    const BatchStrides& bs = BatchStrides());
 void launch_spmv_dot(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
                      const int32_t* node_col, const double* vals, const double* p,
-                     double* q, double* partial, CgState* st);
+                     double* q, double* partial, CgState* st,
+    const BatchStrides& bs = BatchStrides());
 void launch_cg_update(cudaStream_t s, int ndof, const double* dinv, double* x, double* r,
-                      const double* p, const double* q, double* partial, CgState* st);
+                      const double* p, const double* q, double* partial, CgState* st,
+    const BatchStrides& bs = BatchStrides());
 void launch_cg_pupdate(cudaStream_t s, int ndof, const double* dinv, const double* r,
-                       double* p, CgState* st);
+                       double* p, CgState* st,
+    const BatchStrides& bs = BatchStrides());
 void launch_spmv(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
-                 const int32_t* node_col, const double* vals, const double* x, double* y);
+                 const int32_t* node_col, const double* vals, const double* x, double* y,
+    const BatchStrides& bs = BatchStrides());
 void launch_residual_norm(cudaStream_t s, int ndof, const double* f, const double* Kx,
-                          double* partial, unsigned int* ticket, double* out);
-void launch_zero_fixed(cudaStream_t s, int ndof, const uint8_t* fixed_mask, double* x);
+                          double* partial, CgState* st,
+    const BatchStrides& bs = BatchStrides());
+void launch_zero_fixed(cudaStream_t s, int ndof, const uint8_t* fixed_mask, double* x,
+    const BatchStrides& bs = BatchStrides());
 
 // Partitioned-solve helpers
 enum ScalarPhase { PH_INIT = 0, PH_ALPHA = 1, PH_BETA = 2 };
@@ -115,21 +139,24 @@ void launch_allreduce_parts(cudaStream_t s, CgState* const* sts, int n_parts, in
 void launch_gather(cudaStream_t s, int n, const int32_t* idx, const double* src, double* dst);
 void launch_scatter(cudaStream_t s, int n, const int32_t* idx, const double* src, double* dst);
 void launch_dot_local(cudaStream_t s, int n, const double* a, const double* b, double* partial,
-                      unsigned int* ticket, double* out);
+                      CgState* st,
+    const BatchStrides& bs = BatchStrides());
 
 // Gradient kernels
 void launch_beam_grad(cudaStream_t s, int n_beams, const double* x, const double* y,
                       const double* z, const int32_t* conn, const double* A,
                       const double* Iy, const double* Iz, const double* J, const double* E,
-                      const double* G, const double* u, double scale, double* slot_partial);
+                      const double* G, const double* u, double scale, double* slot_partial,
+    const BatchStrides& bs = BatchStrides());
 void launch_quad_grad(cudaStream_t s, int n_beams, int n_quads, const double* x,
                       const double* y, const double* z, const int32_t* conn, const double* t,
                       const double* E, const double* nu, double drill_alpha, const double* u,
-                      double scale, double* slot_partial, double* dC_dt);
+                      double scale, double* slot_partial, double* dC_dt,
+    const BatchStrides& bs = BatchStrides());
 void launch_node_reduce(cudaStream_t s, int n_nodes, const int64_t* inc_ptr,
-                        const int32_t* inc_slot, const double* slot_partial, double* dC_dxyz);
-void launch_dot(cudaStream_t s, int n, const double* a, const double* b, double scale,
-                double* partial, unsigned int* ticket, double* out);
+                        const int32_t* inc_slot, const double* slot_partial, double* dC_dxyz,
+    const BatchStrides& bs = BatchStrides());
+
 
 extern long long g_launches;  // launch counter (per process; handles add their own deltas)
 

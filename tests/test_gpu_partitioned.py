@@ -99,3 +99,32 @@ def test_partitioned_c3_family_iterations(sso):
     u4, i4 = m4.solve(P["f"])
     assert abs(i1["iters"] - i4["iters"]) <= 2
     assert np.linalg.norm(u4 - u1) <= 1e-8 * np.linalg.norm(u1)
+
+
+def test_batched_designs_match_single(sso):
+    """C5-style batch: B designs sharing connectivity run in the same
+    kernels with their own CG scalars; each equals an independent single-design run."""
+    B = 5
+    designs = [W.config5_design(b, n=20) for b in range(B)]
+    P0 = designs[0]
+    mb = sso.Model(P0, rtol=1e-12, batch=B)
+    mb.set_design(z=np.stack([d["z"] for d in designs]), t=np.stack([d["t"] for d in designs]))
+    mb.assemble()
+    F = np.stack([d["f"] for d in designs])
+    U, infos = mb.solve(F)
+    Cb, dXb, dTb = mb.grad()
+    Ug = W.random_state(len(P0["x"]), 3)
+    Cg, dXg, dTg = mb.grad_at(F, np.stack([Ug] * B))
+    for b, d in enumerate(designs):
+        m1 = sso.Model(d, rtol=1e-12)
+        m1.assemble()
+        u1, i1 = m1.solve(d["f"])
+        assert infos[b]["status"] == 0
+        assert abs(infos[b]["iters"] - i1["iters"]) <= max(2, 0.03 * i1["iters"])
+        assert np.linalg.norm(U[b] - u1) <= 1e-10 * np.linalg.norm(u1)
+        C1, dX1, dT1 = m1.grad()
+        assert Cb[b] == pytest.approx(C1, rel=1e-10)
+        C1g, dX1g, dT1g = m1.grad_at(d["f"], Ug)
+        assert np.array_equal(dXg[b], dX1g) and np.array_equal(dTg[b], dT1g)
+    uref, _, _ = OG.evaluate(designs[2])
+    assert np.linalg.norm(U[2] - uref) <= 1e-9 * np.linalg.norm(uref)
