@@ -374,6 +374,83 @@ def run_gpu(args):
     return out
 
 
+def run_batch(args):
+    """C5 (BASELINE.json configs[4]): 64 seeded 50x50 shell designs per GPU sharing one
+    connectivity, evaluated together (compliance + gradients) — weak scaling, no
+    collective: rank r evaluates designs [64 r, 64 (r + 1))."""
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    import paper_2407_20026_b200 as sso
+    import workloads as W
+    B = args.batch
+    designs = [W.config5_design(rank * B + b) for b in range(B)]
+    stream = torch.cuda.current_stream()
+    m = sso.Model(designs[0], rtol=RTOL, batch=B, stream=stream.cuda_stream, device=dev.index)
+    Z = torch.from_numpy(np.stack([d["z"] for d in designs])).to(dev)
+    T = torch.from_numpy(np.stack([d["t"] for d in designs])).to(dev)
+    F = torch.from_numpy(np.stack([d["f"] for d in designs])).to(dev)
+    U = torch.zeros_like(F)
+    Cb = torch.zeros(B, dtype=torch.float64, device=dev)
+    dX = torch.zeros(B * 3 * m.n_nodes, dtype=torch.float64, device=dev)
+    dT = torch.zeros(B * m.n_quads, dtype=torch.float64, device=dev)
+
+    def step():
+        m.set_design(z=Z, t=T)
+        m.assemble()
+        _, infos = m.solve(F, U)
+        m.grad(sso.OBJ_COMPLIANCE, out=(Cb, dX, dT))
+        return infos
+
+    for _ in range(args.warmup):
+        step()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    l0 = m.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            infos = step()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    its = [i["iters"] for i in infos]
+    value = world * B * args.steps / (ms / 1000.0)
+    if rank == 0:
+        print(json.dumps({"metric": "C5 batched shell design evaluations (solve + adjoint gradient) per second",
+                          "value": value, "unit": "designs/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                          "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic (workloads.config5_design, seeded)",
+                          "config": {"workload": f"C5: {B} designs/GPU x 50x50 MITC-4 quads (15 606 DOF each)",
+                                     "rtol": RTOL, "cg_iters_max": max(its), "cg_iters_min": min(its),
+                                     "parallelism": f"{world} GPU(s) x {B} designs, no collective"},
+                          "gpu_launches": m.launch_count() - l0, "clocks": clk.summary()}))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    m.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -383,6 +460,8 @@ def main():
     ap.add_argument("--cg-iters", type=int, default=None,
                     help="CG iteration count used to extrapolate the oracle (reference arm)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="C3b", choices=["C3b", "C5"])
+    ap.add_argument("--batch", type=int, default=64, help="C5 designs per GPU")
     ap.add_argument("--virtual-parts", type=int, default=1,
                     help="run the partitioned (strip) algorithm with P strips on one GPU")
     args = ap.parse_args()
@@ -391,6 +470,8 @@ def main():
             p = os.path.join(ROOT, "profiles", "cg_iters_c3b.json")
             args.cg_iters = json.load(open(p))["cg_iters"] if os.path.exists(p) else 10000
         run_reference(args)
+    elif args.workload == "C5":
+        run_batch(args)
     else:
         run_gpu(args)
 

@@ -127,6 +127,11 @@ typedef struct {
    * [B][6 n_nodes], info [B]; sso_grad C [B], dC_dxyz [B][3][n_nodes], dC_dt
    * [B][n_quads]; sso_grad_at / sso_spmv [B][6 n_nodes].  Exports show design 0. */
   int32_t batch;
+  /* Residual reliability (reading c10): 0 = plain recurrence; 1 (default) = when the
+   * recurrence residual meets rtol, recompute f - K u and restart CG (p = z, at most
+   * twice) if the true residual exceeds 2 rtol, unless it sits at the fp64 floor of
+   * K u; 2 = also replace r by f - K u each time |r|^2 fell 1e4x (reliable updates). */
+  int32_t reliable;
 } sso_options;
 
 typedef struct {

@@ -134,6 +134,7 @@ struct sso_ctx {
   int warm_start = 0;
   int check_every = 64;
   int batch = 1;  // designs per handle
+  int reliable = 1;  // 0 plain CG, 1 final true-residual restart, 2 + periodic replacement
 
   // global problem sizes and what this handle's user buffers cover
   int32_t g_nodes = 0, g_beams = 0, g_quads = 0;
@@ -407,21 +408,27 @@ int reset_flags(sso_ctx* h) {
 // SpMV (events of that slot): a live sample of the SpMV launch duration.
 constexpr int PROF_EVERY = 16;
 
-// One CG iteration on stream s (captured into the chunk graphs).  Single part:
-// alpha / beta are formed by the kernels' last CTAs.  Partitioned: halo of p,
-// SpMV + local p^T q, allreduce, alpha; update + local r^T z / r^T r, allreduce,
-// beta and the convergence test; p update.  `rec` brackets part 0's SpMV with
+// One CG iteration on stream s (captured into the chunk graphs), ordered
+// p update -> SpMV -> x / r update so that residual replacements between chunks
+// land before p is formed (init sets p = z and beta = 0, so the first p update is
+// a no-op).  Single part: alpha / beta are formed by the kernels' last CTAs.
+// Partitioned: p update, halo of p, SpMV + local p^T q, allreduce, alpha; update +
+// local r^T z / r^T r, allreduce, beta and the convergence test.  `rec` brackets part 0's SpMV with
 // the event pair ev[0], ev[1].
 int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev) {
   int rc;
   if (!h->distributed()) {
     Part& P = h->P0();
+    launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st, P.bs);
     if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
     launch_spmv_dot(s, P.n_own, P.node_ptr, P.node_col, P.vals, P.p, P.q, P.partial, P.st, P.bs);
     if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
     launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st, P.bs);
-    launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st, P.bs);
     return SSO_OK;
+  }
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st, P.bs);
   }
   if ((rc = exchange(h, V_P, s))) return rc;
   bool first = true;
@@ -439,11 +446,7 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev) {
     launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st, P.bs);
   }
   if ((rc = allreduce(h, 2, s))) return rc;
-  for (auto& pp : h->parts) {
-    Part& P = *pp;
-    launch_cg_scalar(s, P.st, PH_BETA);
-    launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st, P.bs);
-  }
+  for (auto& pp : h->parts) launch_cg_scalar(s, pp->st, PH_BETA);
   return SSO_OK;
 }
 
@@ -780,6 +783,7 @@ int sso_options_default(sso_options* o) {
   o->rank = 0;
   o->nccl_unique_id = nullptr;
   o->batch = 1;
+  o->reliable = 1;
   return SSO_OK;
 }
 
@@ -856,6 +860,7 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
   h->nranks = o.nranks;
   h->rank = o.rank;
   h->batch = o.batch;
+  h->reliable = o.reliable;
   h->g_nodes = mesh->n_nodes;
   h->g_beams = mesh->n_beams;
   h->g_quads = mesh->n_quads;
@@ -974,8 +979,35 @@ int sso_assemble(sso_handle h) {
   return SSO_OK;
 }
 
+// Reliable update of the residual (SURVEY.md §7 "parity at 1e-9 through CG"):
+// r = f_bc - K x for the designs cg_check selects; REPL_FINAL also restarts p = z.
+static int replace_step(sso_ctx* h, int mode) {
+  int rc;
+  long long g0 = g_launches;
+  if ((rc = exchange(h, V_X))) return rc;
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    launch_spmv(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.xs, P.tmp, P.bs);
+    launch_cg_true_res(h->stream, (int)P.ndof_own, P.fbc, P.tmp, P.partial, P.st, P.bs);
+  }
+  if ((rc = allreduce(h, 1))) return rc;
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    launch_cg_check(h->stream, P.st, mode, P.B);
+    launch_cg_replace(h->stream, (int)P.ndof_own, P.fbc, P.tmp, P.dinv, P.r, P.p, P.partial, P.st, mode, P.bs);
+  }
+  if (h->distributed()) {
+    if ((rc = allreduce(h, 2))) return rc;
+    for (auto& pp : h->parts)
+      launch_cg_scalar(h->stream, pp->st, mode == REPL_FINAL ? PH_REPLACED + 1 : PH_REPLACED);
+  }
+  h->launches += g_launches - g0;
+  return SSO_OK;
+}
+
 // CG loop as replays of captured chunks of check_every iterations (single part
-// and partitioned alike).
+// and partitioned alike), with reliable residual updates between chunks and a
+// final true-residual check that restarts CG when the recurrence has drifted.
 static int solve_chunks(sso_ctx* h) {
   Part& P = h->P0();
   int rc;
@@ -993,44 +1025,55 @@ static int solve_chunks(sso_ctx* h) {
   // profiling on, slot-alternating graphs carry event nodes around every 16th
   // SpMV and the elapsed times of the sampled iterations that ran are accumulated.
   const int64_t max_chunks = (h->max_iter + h->check_every - 1) / h->check_every + 1;
-  int64_t launched = 0;
-  auto launch_chunk = [&](int slot) -> int {
-    CK(h, cudaGraphLaunch(prof ? h->prof_exec[slot] : h->chunk_exec, h->stream));
-    h->launches += h->kernels_per_chunk;
-    CK(h, cudaMemcpyAsync(&h->h_chunk[slot * P.B], P.st, P.B * sizeof(CgState), cudaMemcpyDeviceToHost,
-                          h->stream));
-    CK(h, cudaEventRecord(h->ev_done[slot], h->stream));
-    ++launched;
-    return SSO_OK;
-  };
   long long iters_before = 0;
-  if ((rc = launch_chunk(0))) return rc;
-  for (int64_t k = 0;; ++k) {
-    const int slot = (int)(k & 1);
-    if (launched < max_chunks && (rc = launch_chunk(1 - slot))) return rc;
-    CK(h, cudaEventSynchronize(h->ev_done[slot]));
-    // batch: the chunk's kernels ran while any design was active
-    bool all_done = true;
-    long long it_max = 0;
-    bool not_spd = false;
-    for (int bd = 0; bd < P.B; ++bd) {
-      const CgState& Sb = h->h_chunk[slot * P.B + bd];
-      all_done &= Sb.done != 0;
-      it_max = std::max<long long>(it_max, Sb.iter);
-      not_spd |= Sb.done && Sb.status == SSO_E_NOT_SPD;
-    }
-    if (prof) {
-      long long ran = it_max - iters_before;
-      if (not_spd && ran < h->check_every) ran += 1;
-      iters_before = it_max;
-      for (long long i = 0; i < std::min<long long>(ran, h->check_every); i += PROF_EVERY) {
-        float ms = 0.f;
-        CK(h, cudaEventElapsedTime(&ms, h->chunk_ev[slot][2 * i], h->chunk_ev[slot][2 * i + 1]));
-        h->tm.total_ms[F_SPMV] += ms;
-        h->tm.launches[F_SPMV] += 1;
+  for (int pass = 0; pass <= MAX_RESTARTS; ++pass) {
+    int64_t launched = 0;
+    auto launch_chunk = [&](int slot) -> int {
+      CK(h, cudaGraphLaunch(prof ? h->prof_exec[slot] : h->chunk_exec, h->stream));
+      h->launches += h->kernels_per_chunk;
+      CK(h, cudaMemcpyAsync(&h->h_chunk[slot * P.B], P.st, P.B * sizeof(CgState), cudaMemcpyDeviceToHost,
+                            h->stream));
+      CK(h, cudaEventRecord(h->ev_done[slot], h->stream));
+      ++launched;
+      return SSO_OK;
+    };
+    if ((rc = launch_chunk(0))) return rc;
+    for (int64_t k = 0;; ++k) {
+      const int slot = (int)(k & 1);
+      if (launched < max_chunks && (rc = launch_chunk(1 - slot))) return rc;
+      CK(h, cudaEventSynchronize(h->ev_done[slot]));
+      // batch: the chunk's kernels ran while any design was active
+      bool all_done = true, want_repl = false, not_spd = false;
+      long long it_max = 0;
+      for (int bd = 0; bd < P.B; ++bd) {
+        const CgState& Sb = h->h_chunk[slot * P.B + bd];
+        all_done &= Sb.done != 0;
+        it_max = std::max<long long>(it_max, Sb.iter);
+        not_spd |= Sb.done && Sb.status == SSO_E_NOT_SPD;
+        want_repl |= !Sb.done && !Sb.floor && Sb.rr < REPL_FACTOR * Sb.rr_ref;
       }
+      if (prof) {
+        long long ran = it_max - iters_before;
+        if (not_spd && ran < h->check_every) ran += 1;
+        iters_before = it_max;
+        for (long long i = 0; i < std::min<long long>(ran, h->check_every); i += PROF_EVERY) {
+          float ms = 0.f;
+          CK(h, cudaEventElapsedTime(&ms, h->chunk_ev[slot][2 * i], h->chunk_ev[slot][2 * i + 1]));
+          h->tm.total_ms[F_SPMV] += ms;
+          h->tm.launches[F_SPMV] += 1;
+        }
+      }
+      if (all_done || launched == k + 1) break;
+      if (h->reliable >= 2 && want_repl && (rc = replace_step(h, REPL_PERIODIC))) return rc;
     }
-    if (all_done || launched == k + 1) break;
+    // converged by the recurrence: check the true residual, restart if it drifted
+    if (h->reliable == 0) break;
+    if ((rc = replace_step(h, REPL_FINAL))) return rc;
+    CK(h, cudaMemcpyAsync(h->h_chunk, P.st, P.B * sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
+    if ((rc = sync(h))) return rc;
+    bool restarted = false;
+    for (int bd = 0; bd < P.B; ++bd) restarted |= h->h_chunk[bd].done == 0;
+    if (!restarted) break;
   }
   return SSO_OK;
 }

@@ -371,6 +371,7 @@ __global__ void __launch_bounds__(256) cg_update_kernel(int ndof, const double* 
     }
     const double rz_new = v[0];
     st->beta = rz_new / st->rz;
+    st->rz_prev = st->rz;
     st->rz = rz_new;
     st->rr = v[1];
     st->iter += 1;
@@ -469,6 +470,7 @@ __global__ void __launch_bounds__(256) cg_init_kernel(int ndof, const double* __
     st->done = (v[2] <= st->tol2 * v[0] || v[0] == 0.0) ? 1 : 0;
     st->tol2 = st->tol2 * v[0];  // host passes rtol^2 in tol2; becomes rtol^2 |f_bc|^2
     st->alpha = st->beta = 0.0;
+    st->rr_ref = v[2];
   }
 }
 
@@ -515,6 +517,18 @@ __global__ void cg_scalar_kernel(CgState* st, int phase) {
     st->done = (rr <= st->tol2 * ff || ff == 0.0) ? 1 : 0;
     st->tol2 = st->tol2 * ff;
     st->alpha = st->beta = 0.0;
+    st->rr_ref = rr;
+    return;
+  }
+  if (phase == PH_REPLACED || phase == PH_REPLACED + 1) {  // after the allreduce of the replaced r
+    if (st->act) {
+      st->rz = st->red[0];
+      st->rr = st->red[1];
+      st->rr_ref = st->red[1];
+      // restart (final): p = z; periodic: beta from the replaced r^T z
+      st->beta = (phase == PH_REPLACED + 1) ? 0.0 : st->red[0] / st->rz_prev;
+      st->act = 0;
+    }
     return;
   }
   if (st->done) return;
@@ -530,6 +544,7 @@ __global__ void cg_scalar_kernel(CgState* st, int phase) {
   } else {
     const double rz_new = st->red[0];
     st->beta = rz_new / st->rz;
+    st->rz_prev = st->rz;
     st->rz = rz_new;
     st->rr = st->red[1];
     st->iter += 1;
@@ -539,6 +554,101 @@ __global__ void cg_scalar_kernel(CgState* st, int phase) {
     } else if (st->iter >= st->max_iter) {
       st->done = 1;
       st->status = SSO_E_NOT_CONVERGED;
+    }
+  }
+}
+
+// |f_bc - K x|^2 (local part) into red[0]; design from blockIdx.y.
+__global__ void __launch_bounds__(256) cg_true_res_kernel(int ndof, const double* __restrict__ fbc,
+                                                          const double* __restrict__ Kx,
+                                                          double* __restrict__ partial, CgState* st,
+                                                          BatchStrides bs) {
+  __shared__ double sm[32];
+  {
+    const int bd = blockIdx.y;
+    fbc += bd * bs.dof;
+    Kx += bd * bs.dof;
+    partial += bd * bs.partial;
+    st += bd;
+  }
+  double v[1] = {0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndof; i += stride) {
+    const double d = fbc[i] - Kx[i];
+    v[0] += d * d;
+  }
+  if (grid_sum<1>(v, partial, &st->ticket[3], sm) && threadIdx.x == 0) st->red[0] = v[0];
+}
+
+// Decide the residual replacement of every design (thread per design) from global values.
+__global__ void cg_check_kernel(CgState* st, int mode, int B) {
+  const int bd = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bd >= B) return;
+  CgState* S = st + bd;
+  // red[0] holds the global true |f_bc - K x|^2 of the current iterate
+  const double tt = S->red[0];
+  const bool drifted = tt > REPL_DRIFT * REPL_DRIFT * S->rr;
+  if (mode == REPL_PERIODIC) {
+    S->act = 0;
+    if (!S->done && !S->floor && S->rr < REPL_FACTOR * S->rr_ref) {
+      if (drifted) S->floor = 1;
+      else S->act = 1;
+    }
+  } else {
+    S->act = 0;
+    if (S->done && S->status == SSO_OK && !S->floor && tt > 4.0 * S->tol2 &&
+        S->restarts < MAX_RESTARTS) {
+      if (drifted && tt > 1e4 * S->tol2) {
+        S->floor = 1;  // far from rtol because of the K x floor: restarting cannot help
+      } else {
+        S->act = 1;
+        S->done = 0;
+        S->restarts += 1;
+      }
+    }
+  }
+}
+
+// r = f_bc - K x for designs selected by cg_check; local r^T z, r^T r to red[]
+// (partitioned) or straight into the state, with beta for the following p update
+// (an iteration is p update -> SpMV -> x / r update, so r is replaced before p is formed).
+__global__ void __launch_bounds__(256) cg_replace_kernel(int ndof, const double* __restrict__ fbc,
+                                                         const double* __restrict__ Kx,
+                                                         const double* __restrict__ dinv,
+                                                         double* __restrict__ r, double* __restrict__ p,
+                                                         double* __restrict__ partial, CgState* st,
+                                                         int mode, BatchStrides bs) {
+  __shared__ double sm[64];
+  {
+    const int bd = blockIdx.y;
+    fbc += bd * bs.dof;
+    Kx += bd * bs.dof;
+    dinv += bd * bs.dof;
+    r += bd * bs.dof;
+    p += bd * bs.dof;
+    partial += bd * bs.partial;
+    st += bd;
+  }
+  if (!st->act) return;
+  double v[2] = {0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndof; i += stride) {
+    const double ri = fbc[i] - Kx[i];
+    const double zi = dinv[i] * ri;
+    r[i] = ri;
+    v[0] += ri * zi;
+    v[1] += ri * ri;
+  }
+  if (grid_sum<2>(v, partial, &st->ticket[1], sm) && threadIdx.x == 0) {
+    st->red[0] = v[0];
+    st->red[1] = v[1];
+    if (!st->dist) {
+      st->rz = v[0];
+      st->rr = v[1];
+      st->rr_ref = v[1];
+      // the next p update forms p = z + beta p: restart (final) -> beta = 0
+      st->beta = (mode == REPL_FINAL) ? 0.0 : v[0] / st->rz_prev;
+      st->act = 0;
     }
   }
 }
@@ -597,6 +707,24 @@ int vec_grid(int64_t n, int B = 1) {
 }
 
 }  // namespace
+
+void launch_cg_true_res(cudaStream_t s, int ndof, const double* fbc, const double* Kx, double* partial,
+                        CgState* st, const BatchStrides& bs) {
+  cg_true_res_kernel<<<dim3(vec_grid(ndof, bs.B), bs.B), 256, 0, s>>>(ndof, fbc, Kx, partial, st, bs);
+  SSO_POST_LAUNCH("cg_true_res_kernel");
+}
+
+void launch_cg_check(cudaStream_t s, CgState* st, int mode, int B) {
+  cg_check_kernel<<<(B + 127) / 128, 128, 0, s>>>(st, mode, B);
+  SSO_POST_LAUNCH("cg_check_kernel");
+}
+
+void launch_cg_replace(cudaStream_t s, int ndof, const double* fbc, const double* Kx, const double* dinv,
+                       double* r, double* p, double* partial, CgState* st, int mode, const BatchStrides& bs) {
+  cg_replace_kernel<<<dim3(vec_grid(ndof, bs.B), bs.B), 256, 0, s>>>(ndof, fbc, Kx, dinv, r, p, partial, st,
+                                                                     mode, bs);
+  SSO_POST_LAUNCH("cg_replace_kernel");
+}
 
 void launch_cg_scalar(cudaStream_t s, CgState* st, int phase) {
   cg_scalar_kernel<<<1, 32, 0, s>>>(st, phase);

@@ -53,8 +53,13 @@ struct CgState {
   unsigned int ticket[4];  // last-block-done counters (one per reduction site)
   int dist;         // 1 = partitioned: kernels write local sums to red[], a scalar
                     //     kernel forms alpha / beta after the cross-part allreduce
-  int pad_;
+  int act;         // residual replacement selected for this design (see cg_check)
   double red[4];    // local (then global) reduction values
+  double rr_ref;    // r^T r at the last residual replacement
+  double rz_prev;   // r^T z of the previous iteration (beta after a replacement)
+  int restarts;     // final true-residual restarts used
+  int floor;        // 1 = the true residual sits far above the recurrence (fp64 floor):
+                    //     no further replacements / restarts
 };
 
 // error flags written by device kernels (atomicMin on the offending index)
@@ -132,7 +137,22 @@ void launch_zero_fixed(cudaStream_t s, int ndof, const uint8_t* fixed_mask, doub
     const BatchStrides& bs = BatchStrides());
 
 // Partitioned-solve helpers
-enum ScalarPhase { PH_INIT = 0, PH_ALPHA = 1, PH_BETA = 2 };
+enum ScalarPhase { PH_INIT = 0, PH_ALPHA = 1, PH_BETA = 2, PH_REPLACED = 3 };
+// Reliable updates (residual replacement): REPL_PERIODIC replaces r by f - K x for
+// active designs whose r^T r fell below REPL_FACTOR * rr_ref; REPL_FINAL restarts
+// (r = f - K x, p = z) converged designs whose TRUE residual exceeds 2 rtol.  Both
+// only while |f - K x| <= REPL_DRIFT |r| (else the iterate has reached the fp64
+// accuracy floor of K x and the design is marked `floor`: plain CG from then on).
+enum ReplMode { REPL_PERIODIC = 0, REPL_FINAL = 1 };
+constexpr double REPL_FACTOR = 1e-4;
+constexpr int MAX_RESTARTS = 2;
+constexpr double REPL_DRIFT = 10.0;
+void launch_cg_true_res(cudaStream_t s, int ndof, const double* fbc, const double* Kx, double* partial,
+                        CgState* st, const BatchStrides& bs = BatchStrides());
+void launch_cg_check(cudaStream_t s, CgState* st, int mode, int B);
+void launch_cg_replace(cudaStream_t s, int ndof, const double* fbc, const double* Kx,
+                       const double* dinv, double* r, double* p, double* partial, CgState* st, int mode,
+                       const BatchStrides& bs = BatchStrides());
 void launch_cg_scalar(cudaStream_t s, CgState* st, int phase);
 void launch_pack(cudaStream_t s, int count, const int32_t* idx, const double* vec, double* buf);
 void launch_allreduce_parts(cudaStream_t s, CgState* const* sts, int n_parts, int nvals);

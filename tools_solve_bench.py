@@ -6,8 +6,10 @@ import torch
 import workloads as W
 import paper_2407_20026_b200 as sso
 n = int(os.environ.get("N", "408"))
-P = W.shell_config3(n, cfg=3)
-m = sso.Model(P, rtol=1e-10)
+sup = os.environ.get("SUP", "clamped_edges")
+P = W.shell_config3(n, cfg=4 if sup == "c4" else 3, supports=sup)
+m = sso.Model(P, rtol=1e-10, n_parts=int(os.environ.get("PARTS", "1")),
+              reliable=int(os.environ.get("REL", "1")))
 m.assemble()
 f = torch.from_numpy(P["f"]).cuda()
 u = torch.zeros_like(f)
@@ -15,14 +17,15 @@ m.solve(f, u)
 m.profile_enable(True)
 m.profile_reset()
 ts = []
-for _ in range(3):
+for _ in range(int(os.environ.get("REPS", "3"))):
     _, info = m.solve(f, u)
     ts.append(info["ms"])
 ms, cnt = m.profile_read("spmv")
 ndof, nnz, nb = m.sizes()
 byts = 8 * nnz + 4 * nb + 8 * (m.n_nodes + 1) + 16 * ndof
 avg = ms / max(cnt, 1)
-print(json.dumps({"variant": os.environ.get("SSO_SPMV_VARIANT", "0"), "n": n, "iters": info["iters"],
+print(json.dumps({"variant": os.environ.get("SSO_SPMV_VARIANT", "0"), "rel": os.environ.get("REL", "1"),
+                  "sup": sup, "n": n, "iters": info["iters"],
                   "solve_ms": min(ts), "us_per_iter": 1000 * min(ts) / info["iters"],
                   "spmv_us": 1000 * avg, "spmv_GBs": byts / (avg / 1000) / 1e9,
                   "true_rel_res": info["true_rel_res"]}))
