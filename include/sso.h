@@ -132,6 +132,10 @@ typedef struct {
    * twice) if the true residual exceeds 2 rtol, unless it sits at the fp64 floor of
    * K u; 2 = also replace r by f - K u each time |r|^2 fell 1e4x (reliable updates). */
   int32_t reliable;
+  /* 0 (default) = element stiffness and assembly fused in one pass (no staged element
+   * matrices) when the mesh is quad-only with node degree <= 10; 1 = always the staged
+   * path (element kernel, then the segmented-sum gather). */
+  int32_t assembly;
 } sso_options;
 
 typedef struct {

@@ -7,7 +7,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsso.so")
-SOURCES = ["api.cu", "elements.cu", "assemble.cu", "pcg.cu", "grad.cu", "pattern.cpp"]
+SOURCES = ["api.cu", "elements.cu", "assemble.cu", "assemble_fused.cu", "pcg.cu", "grad.cu",
+           "pattern.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -36,7 +37,8 @@ def nvcc():
 
 def build(verbose=False, force=False):
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    hdrs = [os.path.join(CSRC, "sso_internal.h"), os.path.join(ROOT, "include", "sso.h")]
+    hdrs = [os.path.join(CSRC, "sso_internal.h"), os.path.join(CSRC, "shell_math.cuh"),
+            os.path.join(ROOT, "include", "sso.h")]
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(p) < t for p in srcs + hdrs):

@@ -114,6 +114,9 @@ struct Part {
   double* scal = nullptr;
   double *slot_partial = nullptr, *dxyz = nullptr, *dt = nullptr, *dt_own = nullptr;
   // partition maps
+  int32_t* block_rank = nullptr;      // quads [n_quads][16] (fused assembly)
+  int max_inc = 0, max_deg = 0;       // over owned nodes
+  bool fused = false;                 // element + assembly in one pass (quad-only meshes)
   int32_t* own_quad_local = nullptr;  // [n_own_quads]
   int32_t* own_quad_gid = nullptr;    // [n_own_quads] global quad ids (virtual parts)
   int32_t* send_idx = nullptr;        // concatenated send lists (local owned node ids)
@@ -135,6 +138,7 @@ struct sso_ctx {
   int check_every = 64;
   int batch = 1;  // designs per handle
   int reliable = 1;  // 0 plain CG, 1 final true-residual restart, 2 + periodic replacement
+  int assembly = 0;  // 0 auto (fused when the mesh allows), 1 staged
 
   // global problem sizes and what this handle's user buffers cover
   int32_t g_nodes = 0, g_beams = 0, g_quads = 0;
@@ -500,7 +504,7 @@ void free_part(Part& P) {
                   P.fixed_mask, P.node_ptr, P.node_col, P.contrib_ptr, P.contrib, P.inc_ptr,
                   P.inc_slot, P.stage, P.vals, P.dinv, P.f, P.fbc, P.xs, P.r, P.p, P.q, P.tmp, P.gu,
                   P.gf, P.partial, P.st, P.flags, P.tickets, P.scal, P.slot_partial, P.dxyz, P.dt,
-                  P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf};
+                  P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -604,6 +608,11 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   P.n_staged = P.pat.n_staged_blocks();
   P.n_slots = 2 * (int64_t)P.n_beams + 4 * (int64_t)P.n_quads;
   P.nnz = 36 * (P.pat.node_ptr[P.n_own]);  // owned rows only
+  for (int32_t n = 0; n < P.n_own; ++n) {
+    P.max_inc = std::max<int>(P.max_inc, (int)(P.pat.inc_ptr[n + 1] - P.pat.inc_ptr[n]));
+    P.max_deg = std::max<int>(P.max_deg, (int)(P.pat.node_ptr[n + 1] - P.pat.node_ptr[n]));
+  }
+  P.fused = h->assembly == 0 && P.n_beams == 0 && P.n_quads > 0 && P.max_deg <= fused_max_degree();
   const int64_t ne = (int64_t)P.n_beams + P.n_quads;
   const int B = P.B = h->batch;
   P.bs.B = B;
@@ -678,6 +687,7 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   UP(contrib, P.pat.contrib.data(), P.n_staged);
   UP(inc_ptr, P.pat.inc_ptr.data(), P.n_nodes + 1);
   UP(inc_slot, P.pat.inc_slot.data(), P.n_slots);
+  if (P.fused) UP(block_rank, P.pat.block_rank.data(), 16 * (int64_t)P.n_quads);
   UP(own_quad_local, L.own_quad_local.data(), P.n_own_quads);
   UP(own_quad_gid, own_gid.data(), P.n_own_quads);
   UP(send_idx, send.data(), P.n_send);
@@ -784,6 +794,7 @@ int sso_options_default(sso_options* o) {
   o->nccl_unique_id = nullptr;
   o->batch = 1;
   o->reliable = 1;
+  o->assembly = 0;
   return SSO_OK;
 }
 
@@ -861,6 +872,7 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
   h->rank = o.rank;
   h->batch = o.batch;
   h->reliable = o.reliable;
+  h->assembly = o.assembly;
   h->g_nodes = mesh->n_nodes;
   h->g_beams = mesh->n_beams;
   h->g_quads = mesh->n_quads;
@@ -957,6 +969,14 @@ int sso_assemble(sso_handle h) {
   if (rc) return rc;
   for (auto& pp : h->parts) {
     Part& P = *pp;
+    if (P.fused) {
+      Scope sc(h, F_ASSEMBLE);
+      launch_quad_assemble_fused(h->stream, P.n_own, P.max_inc, P.node_ptr, P.node_col, P.inc_ptr, P.inc_slot,
+                                 P.block_rank, P.x, P.y, P.z, P.quad_conn, P.t, P.E + P.n_beams,
+                                 P.nu + P.n_beams, h->drill_alpha, P.fixed_mask, P.vals, P.dinv, P.flags,
+                                 P.bs);
+      continue;
+    }
     {
       Scope sc(h, F_ELEMENT);
       launch_beam_elements(h->stream, P.n_beams, P.x, P.y, P.z, P.beam_conn, P.A, P.Iy, P.Iz, P.J, P.E,
@@ -1357,6 +1377,14 @@ int sso_export_ke(sso_handle h, int64_t first, int64_t count, double* ke) {
   const int64_t ne = (int64_t)P.n_beams + P.n_quads;
   if (first < 0 || count < 0 || first + count > ne) FAIL(h, SSO_E_INVALID, "element range out of bounds");
   if (!h->assembled) FAIL(h, SSO_E_STATE, "export of K_e before sso_assemble");
+  // the fused path keeps no element matrices: form them (debug export only)
+  launch_beam_elements(h->stream, P.n_beams, P.x, P.y, P.z, P.beam_conn, P.A, P.Iy, P.Iz, P.J, P.E, P.G,
+                       P.stage, P.flags, P.bs);
+  launch_quad_elements(h->stream, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.E + P.n_beams,
+                       P.nu + P.n_beams, h->drill_alpha, P.stage + 36 * 4 * (int64_t)P.n_beams, P.flags, P.bs);
+  CKL(h);
+  int rc0 = sync(h);
+  if (rc0) return rc0;
   double* out = ke;
   std::vector<double> blk;
   for (int64_t e = first; e < first + count; ++e) {

@@ -111,6 +111,16 @@ void launch_assemble(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
                      double* vals, double* dinv, DevFlags* flags,
     const BatchStrides& bs = BatchStrides());
 
+// Fused element stiffness + assembly for quad-only meshes (no staging).
+int fused_max_degree();
+void launch_quad_assemble_fused(cudaStream_t s, int n_own, int max_inc, const int64_t* node_ptr,
+                                const int32_t* node_col, const int64_t* inc_ptr, const int32_t* inc_slot,
+                                const int32_t* block_rank, const double* x, const double* y,
+                                const double* z, const int32_t* conn, const double* t, const double* E,
+                                const double* nu, double drill_alpha, const uint8_t* fixed_mask,
+                                double* vals, double* dinv, DevFlags* flags,
+                                const BatchStrides& bs = BatchStrides());
+
 // PCG kernels
 int cg_grid();  // persistent grid size (multiple of the SM count)
 void launch_cg_init(cudaStream_t s, int ndof, const double* f, const uint8_t* fixed_mask,
