@@ -245,6 +245,7 @@ def run_gpu(args):
         parallelism = "single GPU"
     t_create = time.perf_counter() - t0
     ndof, nnz, nblocks = m.sizes()
+    stored_vals, stored_blocks, symmetric = m.storage_info()
     n_nodes, nq = m.n_nodes, m.n_quads
     f_own = P["f"][6 * m.own_node_begin: 6 * (m.own_node_begin + n_nodes)]
     f_dev = torch.from_numpy(np.ascontiguousarray(f_own)).to(dev)
@@ -327,10 +328,16 @@ def run_gpu(args):
 
     # ---- roofline of the dominant kernel (SpMV inside PCG) --------------------
     peak, peak_src = measured_peaks()
-    spmv_bytes = 8 * nnz + 4 * nblocks + 8 * (n_nodes + 1) + 16 * ndof  # this rank's rows
+    # algorithmic bytes of the stored format: values + block column ids + node_ptr + x read,
+    # y written; symmetric storage adds the transpose slots (written and read back once)
+    spmv_bytes = 8 * stored_vals + 4 * stored_blocks + 8 * (n_nodes + 1) + 16 * ndof
+    if symmetric:
+        spmv_bytes += 2 * 48 * (stored_blocks - n_nodes) + 8 * (n_nodes + 1) + 4 * (stored_blocks - n_nodes)
     spmv_avg_ms = spmv_ms / max(spmv_n, 1)
     achieved = spmv_bytes / (spmv_avg_ms / 1000.0) / 1e9 if spmv_n else None
-    roofline = {"bound": "hbm", "kernel": "spmv_dot (CG q = K p, p^T q)",
+    roofline = {"bound": "hbm",
+                "kernel": ("spmv_sym pass1+pass2 (upper-block K, CG q = K p, p^T q)" if symmetric
+                           else "spmv_dot (CG q = K p, p^T q)"),
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(),
                 "algorithmic_bytes_per_launch": spmv_bytes, "avg_launch_ms": spmv_avg_ms,

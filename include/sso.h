@@ -136,6 +136,12 @@ typedef struct {
    * matrices) when the mesh is quad-only with node degree <= 10; 1 = always the staged
    * path (element kernel, then the segmented-sum gather). */
   int32_t assembly;
+  /* 0 (default) or 1 = full CSR storage.  2 = single-strip handles keep only the
+   * upper node blocks (n, m >= n) of the symmetric K_bc (44 % fewer value bytes on
+   * shell grids); pass 1 of the SpMV forms the upper row sums, the transpose
+   * contributions (sender-ordered slots) and p^T K p, the x / r update adds each
+   * node's incoming slots in ascending source order.  Exports return the full CSR. */
+  int32_t storage;
 } sso_options;
 
 typedef struct {
@@ -203,6 +209,10 @@ int sso_export_csr(sso_handle h, int64_t* row_ptr, int32_t* col_idx, double* val
 int sso_export_scatter(sso_handle h, int32_t* block_rank);
 int sso_export_ke(sso_handle h, int64_t first, int64_t count, double* ke);
 int sso_export_dinv(sso_handle h, double* dinv);
+
+/* Device storage of the assembled matrix: stored values / node blocks (owned rows) and
+ * whether the upper-block symmetric layout is in use. */
+int sso_storage_info(sso_handle h, int64_t* stored_values, int64_t* stored_blocks, int32_t* symmetric);
 
 /* Partition of this handle: number of strips held, first owned global node, owned
  * node count and owned quad count (the extents of the caller's f / u / gradients). */

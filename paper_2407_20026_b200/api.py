@@ -62,7 +62,8 @@ class sso_options(C.Structure):
                 ("cuda_stream", C.c_void_p), ("device", C.c_int32),
                 ("n_parts", C.c_int32), ("part_ranges", _ip), ("nranks", C.c_int32),
                 ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p), ("batch", C.c_int32),
-                ("reliable", C.c_int32), ("assembly", C.c_int32)]
+                ("reliable", C.c_int32), ("assembly", C.c_int32),
+                ("storage", C.c_int32)]
 
 
 class sso_solve_info(C.Structure):
@@ -96,6 +97,7 @@ _sig = {
     "sso_profile_reset": (C.c_int, [_H]),
     "sso_launch_count": (C.c_int64, [_H]),
     "sso_part_info": (C.c_int, [_H, _ip, _ip, _ip, _ip]),
+    "sso_storage_info": (C.c_int, [_H, _lp, _lp, _ip]),
     "sso_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "sso_local_pattern": (C.c_int, [C.POINTER(sso_mesh), _ip, C.c_int32, C.c_int32, _lp, C.c_void_p, C.c_void_p]),
     "sso_halo_plan": (C.c_int, [C.POINTER(sso_mesh), _ip, C.c_int32, C.c_int32, _ip, C.c_void_p, _ip,
@@ -142,7 +144,7 @@ class Model:
 
     def __init__(self, problem, rtol=1e-10, max_iter=200000, drill_alpha=1e-3, check_every=64,
                  warm_start=False, stream=None, device=-1, n_parts=1, part_ranges=None,
-                 nranks=1, rank=0, nccl_id=None, batch=1, reliable=1, assembly=0):
+                 nranks=1, rank=0, nccl_id=None, batch=1, reliable=1, assembly=0, storage=0):
         P = problem
         self._keep = []
         x, y, z = (_np(P[k], np.float64) for k in ("x", "y", "z"))
@@ -172,7 +174,7 @@ class Model:
         opt.mem = MEM_HOST
         opt.cuda_stream = stream
         opt.n_parts, opt.nranks, opt.rank, opt.batch = n_parts, nranks, rank, batch
-        opt.reliable, opt.assembly = reliable, assembly
+        opt.reliable, opt.assembly, opt.storage = reliable, assembly, storage
         if part_ranges is not None:
             pr = np.ascontiguousarray(part_ranges, np.int32)
             self._keep.append(pr)
@@ -232,6 +234,11 @@ class Model:
         a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
         self._check(_lib.sso_sizes(self.h, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
+
+    def storage_info(self):
+        v, b, s = C.c_int64(), C.c_int64(), C.c_int32()
+        self._check(_lib.sso_storage_info(self.h, C.byref(v), C.byref(b), C.byref(s)))
+        return v.value, b.value, bool(s.value)
 
     def set_design(self, x=None, y=None, z=None, t=None):
         dev = self._mode(x, y, z, t)

@@ -114,7 +114,13 @@ struct Part {
   double* scal = nullptr;
   double *slot_partial = nullptr, *dxyz = nullptr, *dt = nullptr, *dt_own = nullptr;
   // partition maps
-  int32_t* block_rank = nullptr;      // quads [n_quads][16] (fused assembly)
+  int32_t* block_rank = nullptr;      // quads [n_quads][16] (fused assembly; upper ranks when sym)
+  bool sym = false;                   // upper-block (symmetric) storage, single-strip handles
+  UpperPattern up;
+  int64_t* lptr = nullptr;            // sym: incoming transpose slots per node
+  int32_t* lslot = nullptr;
+  double* tbuf = nullptr;             // sym: transpose contributions [B][6 n_tslots]
+  int64_t stored_blocks = 0;          // node blocks kept on the device for the owned rows
   int max_inc = 0, max_deg = 0;       // over owned nodes
   bool fused = false;                 // element + assembly in one pass (quad-only meshes)
   int32_t* own_quad_local = nullptr;  // [n_own_quads]
@@ -139,6 +145,7 @@ struct sso_ctx {
   int batch = 1;  // designs per handle
   int reliable = 1;  // 0 plain CG, 1 final true-residual restart, 2 + periodic replacement
   int assembly = 0;  // 0 auto (fused when the mesh allows), 1 staged
+  int storage = 0;   // 0 / 1 full CSR storage, 2 symmetric upper blocks (single-strip handles)
 
   // global problem sizes and what this handle's user buffers cover
   int32_t g_nodes = 0, g_beams = 0, g_quads = 0;
@@ -306,6 +313,21 @@ double* vec_of(Part& P, int v) {
   }
 }
 
+// y = K x for the part's owned rows (full or symmetric storage); with st also
+// p^T q and alpha (CG) -- for symmetric storage the CG form leaves y = the upper
+// row sums and the receiver sums to cg_update (launch_cg_update_sym).  x must have
+// its halo filled (partitioned handles).
+void spmv_apply(cudaStream_t s, Part& P, const double* x, double* y, CgState* st) {
+  if (P.sym && st)
+    launch_spmv_sym_cg(s, P.n_own, P.node_ptr, P.node_col, P.vals, x, y, P.tbuf, P.partial, st, P.bs);
+  else if (P.sym)
+    launch_spmv_sym(s, P.n_own, P.node_ptr, P.node_col, P.vals, x, y, P.tbuf, P.lptr, P.lslot, P.bs);
+  else if (st)
+    launch_spmv_dot(s, P.n_own, P.node_ptr, P.node_col, P.vals, x, y, P.partial, st, P.bs);
+  else
+    launch_spmv(s, P.n_own, P.node_ptr, P.node_col, P.vals, x, y, P.bs);
+}
+
 int exchange(sso_ctx* h, int v, cudaStream_t s = nullptr) {
   if (!h->distributed()) return SSO_OK;
   if (!s) s = h->stream;
@@ -425,9 +447,13 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev) {
     Part& P = h->P0();
     launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st, P.bs);
     if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
-    launch_spmv_dot(s, P.n_own, P.node_ptr, P.node_col, P.vals, P.p, P.q, P.partial, P.st, P.bs);
+    spmv_apply(s, P, P.p, P.q, P.st);
     if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
-    launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st, P.bs);
+    if (P.sym)
+      launch_cg_update_sym(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.tbuf, P.lptr, P.lslot, P.partial,
+                           P.st, P.bs);
+    else
+      launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st, P.bs);
     return SSO_OK;
   }
   for (auto& pp : h->parts) {
@@ -439,7 +465,7 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     if (ev && first) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
-    launch_spmv_dot(s, P.n_own, P.node_ptr, P.node_col, P.vals, P.p, P.q, P.partial, P.st, P.bs);
+    spmv_apply(s, P, P.p, P.q, P.st);
     if (ev && first) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
     first = false;
   }
@@ -504,7 +530,8 @@ void free_part(Part& P) {
                   P.fixed_mask, P.node_ptr, P.node_col, P.contrib_ptr, P.contrib, P.inc_ptr,
                   P.inc_slot, P.stage, P.vals, P.dinv, P.f, P.fbc, P.xs, P.r, P.p, P.q, P.tmp, P.gu,
                   P.gf, P.partial, P.st, P.flags, P.tickets, P.scal, P.slot_partial, P.dxyz, P.dt,
-                  P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank};
+                  P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
+                  P.lptr, P.lslot, P.tbuf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -613,13 +640,17 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
     P.max_deg = std::max<int>(P.max_deg, (int)(P.pat.node_ptr[n + 1] - P.pat.node_ptr[n]));
   }
   P.fused = h->assembly == 0 && P.n_beams == 0 && P.n_quads > 0 && P.max_deg <= fused_max_degree();
+  P.sym = h->storage == 2 && L.n_parts == 1 && h->nranks == 1 && P.n_own == P.n_nodes;
+  if (P.sym) build_upper(P.pat, L.beam_conn.data(), L.quad_conn.data(), P.up);
+  P.stored_blocks = P.sym ? P.up.uptr[P.n_own] : P.pat.node_ptr[P.n_own];
   const int64_t ne = (int64_t)P.n_beams + P.n_quads;
   const int B = P.B = h->batch;
   P.bs.B = B;
   P.bs.node = P.n_nodes;
   P.bs.quad = P.n_quads;
   P.bs.stage = 36 * P.n_staged;
-  P.bs.nnz = 36 * P.n_blocks;
+  P.bs.nnz = 36 * (P.sym ? P.up.n_ublocks() : P.n_blocks);
+  P.bs.tbuf = 6 * std::max<int64_t>(P.sym ? P.up.n_tslots : 0, 1);
   P.bs.dof = P.ndof;
   P.bs.partial = 16 * (int64_t)cg_grid();
   P.bs.slot = 3 * std::max<int64_t>(P.n_slots, 1);
@@ -681,13 +712,23 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   UP(nu, nu.data(), ne);
   UP(G, G.data(), ne);
   UP(fixed_mask, mask.data(), P.n_nodes);
-  UP(node_ptr, P.pat.node_ptr.data(), P.n_nodes + 1);
-  UP(node_col, P.pat.node_col.data(), P.n_blocks);
-  UP(contrib_ptr, P.pat.contrib_ptr.data(), P.n_blocks + 1);
-  UP(contrib, P.pat.contrib.data(), P.n_staged);
+  if (P.sym) {  // the device works on the upper graph; the full one stays on the host for exports
+    UP(node_ptr, P.up.uptr.data(), P.n_nodes + 1);
+    UP(node_col, P.up.ucol.data(), P.up.n_ublocks());
+    UP(contrib_ptr, P.up.ucontrib_ptr.data(), P.up.n_ublocks() + 1);
+    UP(contrib, P.up.ucontrib.data(), (int64_t)P.up.ucontrib.size());
+    UP(lptr, P.up.lptr.data(), P.n_nodes + 1);
+    UP(lslot, P.up.lslot.data(), (int64_t)P.up.lslot.size());
+    AL(tbuf, B * P.bs.tbuf);
+  } else {
+    UP(node_ptr, P.pat.node_ptr.data(), P.n_nodes + 1);
+    UP(node_col, P.pat.node_col.data(), P.n_blocks);
+    UP(contrib_ptr, P.pat.contrib_ptr.data(), P.n_blocks + 1);
+    UP(contrib, P.pat.contrib.data(), P.n_staged);
+  }
   UP(inc_ptr, P.pat.inc_ptr.data(), P.n_nodes + 1);
   UP(inc_slot, P.pat.inc_slot.data(), P.n_slots);
-  if (P.fused) UP(block_rank, P.pat.block_rank.data(), 16 * (int64_t)P.n_quads);
+  if (P.fused) UP(block_rank, (P.sym ? P.up.urank : P.pat.block_rank).data(), 16 * (int64_t)P.n_quads);
   UP(own_quad_local, L.own_quad_local.data(), P.n_own_quads);
   UP(own_quad_gid, own_gid.data(), P.n_own_quads);
   UP(send_idx, send.data(), P.n_send);
@@ -724,6 +765,10 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   CK(h, cudaMemset(P.f, 0, B * P.ndof * sizeof(double)));
   P.pat.contrib.clear();  // only needed on the device
   P.pat.contrib.shrink_to_fit();
+  P.up.ucontrib.clear();
+  P.up.ucontrib.shrink_to_fit();
+  P.up.lslot.clear();
+  P.up.lslot.shrink_to_fit();
   P.pat.inc_slot.clear();
   P.pat.inc_slot.shrink_to_fit();
   return SSO_OK;
@@ -795,6 +840,7 @@ int sso_options_default(sso_options* o) {
   o->batch = 1;
   o->reliable = 1;
   o->assembly = 0;
+  o->storage = 0;
   return SSO_OK;
 }
 
@@ -873,6 +919,7 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
   h->batch = o.batch;
   h->reliable = o.reliable;
   h->assembly = o.assembly;
+  h->storage = o.storage;
   h->g_nodes = mesh->n_nodes;
   h->g_beams = mesh->n_beams;
   h->g_quads = mesh->n_quads;
@@ -1007,7 +1054,7 @@ static int replace_step(sso_ctx* h, int mode) {
   if ((rc = exchange(h, V_X))) return rc;
   for (auto& pp : h->parts) {
     Part& P = *pp;
-    launch_spmv(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.xs, P.tmp, P.bs);
+    spmv_apply(h->stream, P, P.xs, P.tmp, nullptr);
     launch_cg_true_res(h->stream, (int)P.ndof_own, P.fbc, P.tmp, P.partial, P.st, P.bs);
   }
   if ((rc = allreduce(h, 1))) return rc;
@@ -1118,7 +1165,7 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
     for (auto& pp : h->parts) {
       Part& P = *pp;
       Scope sc(h, F_SPMV);
-      launch_spmv(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.xs, P.tmp, P.bs);
+      spmv_apply(h->stream, P, P.xs, P.tmp, nullptr);
     }
   }
   std::memset(h->h_st, 0, h->batch * sizeof(CgState));
@@ -1152,7 +1199,7 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     long long g1 = g_launches;
-    launch_spmv(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.xs, P.tmp, P.bs);
+    spmv_apply(h->stream, P, P.xs, P.tmp, nullptr);
     launch_residual_norm(h->stream, (int)P.ndof_own, P.fbc, P.tmp, P.partial, P.st, P.bs);
     h->launches += g_launches - g1;
   }
@@ -1292,7 +1339,7 @@ int sso_spmv(sso_handle h, const double* xin, double* yout) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     Scope sc(h, F_SPMV);
-    launch_spmv(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.gu, P.tmp, P.bs);
+    spmv_apply(h->stream, P, P.gu, P.tmp, nullptr);
   }
   CKL(h);
   if ((rc = vec_out(h, yout, &Part::tmp))) return rc;
@@ -1310,6 +1357,21 @@ int sso_sizes(sso_handle h, int64_t* ndof, int64_t* nnz, int64_t* n_blocks) {
   if (ndof) *ndof = d;
   if (nnz) *nnz = z;
   if (n_blocks) *n_blocks = b;
+  return SSO_OK;
+}
+
+int sso_storage_info(sso_handle h, int64_t* stored_values, int64_t* stored_blocks, int32_t* symmetric) {
+  if (!h) return SSO_E_INVALID;
+  int64_t v = 0, b = 0;
+  bool sym = true;
+  for (auto& pp : h->parts) {
+    v += 36 * pp->stored_blocks;
+    b += pp->stored_blocks;
+    sym &= pp->sym;
+  }
+  if (stored_values) *stored_values = v;
+  if (stored_blocks) *stored_blocks = b;
+  if (symmetric) *symmetric = sym ? 1 : 0;
   return SSO_OK;
 }
 
@@ -1335,9 +1397,27 @@ int sso_export_csr(sso_handle h, int64_t* row_ptr, int32_t* col_idx, double* val
     Part& P = *pp;
     const HostPattern& T = P.pat;
     if (vals) {
-      pv.resize((size_t)P.nnz);
-      CK(h, cudaMemcpy(pv.data(), P.vals, (size_t)P.nnz * sizeof(double), cudaMemcpyDeviceToHost));
+      pv.resize((size_t)(36 * P.stored_blocks));
+      CK(h, cudaMemcpy(pv.data(), P.vals, pv.size() * sizeof(double), cudaMemcpyDeviceToHost));
     }
+    // value (a, b) of block (n, k-th full neighbour): symmetric storage keeps the
+    // blocks (n, m >= n); a lower block is the transpose of the stored (m, n)
+    auto value = [&](int32_t n, int64_t k, int a, int b) -> double {
+      const int64_t b0 = T.node_ptr[n];
+      const int64_t deg = T.node_ptr[n + 1] - b0;
+      if (!P.sym) return pv[36 * b0 + 6 * a * deg + 6 * k + b];
+      const int32_t m = T.node_col[b0 + k];
+      const UpperPattern& U = P.up;
+      if (m >= n) {
+        const int64_t ud = U.uptr[n + 1] - U.uptr[n];
+        const int64_t ku = k - (deg - ud);
+        return pv[36 * U.uptr[n] + 6 * a * ud + 6 * ku + b];
+      }
+      const int64_t ud = U.uptr[m + 1] - U.uptr[m];
+      const int32_t* c0 = U.ucol.data() + U.uptr[m];
+      const int64_t ku = std::lower_bound(c0, c0 + ud, n) - c0;
+      return pv[36 * U.uptr[m] + 6 * b * ud + 6 * ku + a];
+    };
     for (int32_t n = 0; n < P.n_own; ++n) {
       const int64_t b0 = T.node_ptr[n];
       const int64_t deg = T.node_ptr[n + 1] - b0;
@@ -1351,7 +1431,7 @@ int sso_export_csr(sso_handle h, int64_t* row_ptr, int32_t* col_idx, double* val
           const int32_t gcol = cols[kk].first, k = cols[kk].second;
           for (int b = 0; b < 6; ++b) {
             if (col_idx) col_idx[start + 6 * kk + b] = 6 * gcol + b;
-            if (vals) vals[start + 6 * kk + b] = pv[36 * b0 + 6 * a * deg + 6 * k + b];
+            if (vals) vals[start + 6 * kk + b] = value(n, k, a, b);
           }
         }
       }

@@ -226,7 +226,10 @@ __global__ void __launch_bounds__(128, 4) quad_assemble_fused_kernel(
     for (int a = 0; a < 6; ++a)
 #pragma unroll
       for (int b = 0; b < 6; ++b) K[a][b] = 0.0;
-    if (has) {
+    // symmetric storage keeps only blocks (n, m >= n): rank < 0 marks a skipped block
+    const int rank = has ? block_rank[16 * q + 4 * il + j] : -1;
+    const bool blk = has && rank >= 0;
+    if (blk) {
       const int bi = il, bj = j;
       const double Em = G[G_EM], Eb = G[G_EB], ds = G[G_DS], cs = G[G_CS], nu = G[G_NU];
       double gxi_i[3], geta_i[3], gxi_j[3], geta_j[3];
@@ -302,10 +305,9 @@ __global__ void __launch_bounds__(128, 4) quad_assemble_fused_kernel(
       transform_block(K, R, G[G_H + bi], G[G_H + bj]);
     }
     // ---- ordered accumulation into the node's CSR run (ascending element) ----
-    const int rank = has ? block_rank[16 * q + 4 * il + j] : 0;
 #pragma unroll
     for (int kk2 = 0; kk2 < 4; ++kk2) {
-      if (has && k == kk2) {
+      if (blk && k == kk2) {
 #pragma unroll
         for (int a = 0; a < 6; ++a)
 #pragma unroll

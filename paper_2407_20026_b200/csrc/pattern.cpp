@@ -137,6 +137,75 @@ std::string build_pattern(int32_t n_nodes, int32_t n_beams, const int32_t* beam_
   return std::string();
 }
 
+void build_upper(const HostPattern& P, const int32_t* beam_conn, const int32_t* quad_conn,
+                 UpperPattern& U) {
+  const int32_t nn = P.n_nodes;
+  U = UpperPattern();
+  U.uptr.assign((size_t)nn + 1, 0);
+  std::vector<int32_t> first_upper((size_t)nn);  // position of n itself in adj(n)
+  for (int32_t n = 0; n < nn; ++n) {
+    const int64_t b0 = P.node_ptr[n], b1 = P.node_ptr[n + 1];
+    int64_t k = b0;
+    while (k < b1 && P.node_col[k] < n) ++k;
+    first_upper[n] = (int32_t)(k - b0);
+    U.uptr[n + 1] = U.uptr[n] + (b1 - k);
+  }
+  U.ucol.resize((size_t)U.uptr[nn]);
+  for (int32_t n = 0; n < nn; ++n) {
+    const int64_t src = P.node_ptr[n] + first_upper[n];
+    std::copy(P.node_col.begin() + src, P.node_col.begin() + P.node_ptr[n + 1], U.ucol.begin() + U.uptr[n]);
+  }
+  U.n_tslots = U.uptr[nn] - nn;
+  // element block ranks in the upper lists, and the upper contributor lists
+  U.urank.resize(P.block_rank.size());
+  U.ucontrib_ptr.assign((size_t)U.uptr[nn] + 1, 0);
+  auto elem = [&](int64_t e, int& k, const int32_t*& c, int64_t& base) {
+    if (e < P.n_beams) { k = 2; c = beam_conn + 2 * e; base = 4 * e; }
+    else { const int64_t q = e - P.n_beams; k = 4; c = quad_conn + 4 * q; base = 4 * (int64_t)P.n_beams + 16 * q; }
+  };
+  const int64_t ne = (int64_t)P.n_beams + P.n_quads;
+  for (int64_t e = 0; e < ne; ++e) {
+    int k; const int32_t* c; int64_t base;
+    elem(e, k, c, base);
+    for (int i = 0; i < k; ++i)
+      for (int jj = 0; jj < k; ++jj) {
+        const int32_t ni = c[i], nj = c[jj];
+        int32_t r = -1;
+        if (nj >= ni) {
+          r = P.block_rank[base + i * k + jj] - first_upper[ni];
+          U.ucontrib_ptr[U.uptr[ni] + r + 1]++;
+        }
+        U.urank[base + i * k + jj] = r;
+      }
+  }
+  for (int64_t b = 0; b < U.uptr[nn]; ++b) U.ucontrib_ptr[b + 1] += U.ucontrib_ptr[b];
+  U.ucontrib.resize((size_t)U.ucontrib_ptr[U.uptr[nn]]);
+  {
+    std::vector<int64_t> fill(U.ucontrib_ptr.begin(), U.ucontrib_ptr.end() - 1);
+    for (int64_t e = 0; e < ne; ++e) {
+      int k; const int32_t* c; int64_t base;
+      elem(e, k, c, base);
+      for (int i = 0; i < k; ++i)
+        for (int jj = 0; jj < k; ++jj) {
+          const int32_t r = U.urank[base + i * k + jj];
+          if (r >= 0) U.ucontrib[fill[U.uptr[c[i]] + r]++] = (int32_t)(base + i * k + jj);
+        }
+    }
+  }
+  // incoming sender slots per node, ascending source node
+  U.lptr.assign((size_t)nn + 1, 0);
+  for (int32_t n = 0; n < nn; ++n)
+    for (int64_t k = U.uptr[n] + 1; k < U.uptr[n + 1]; ++k) U.lptr[U.ucol[k] + 1]++;
+  for (int32_t n = 0; n < nn; ++n) U.lptr[n + 1] += U.lptr[n];
+  U.lslot.resize((size_t)U.lptr[nn]);
+  {
+    std::vector<int64_t> fill(U.lptr.begin(), U.lptr.end() - 1);
+    for (int32_t n = 0; n < nn; ++n)
+      for (int64_t k = U.uptr[n] + 1; k < U.uptr[n + 1]; ++k)
+        U.lslot[fill[U.ucol[k]]++] = (int32_t)(U.uptr[n] - n + (k - U.uptr[n]) - 1);
+  }
+}
+
 }  // namespace sso
 
 namespace sso {

@@ -188,22 +188,21 @@ __device__ __forceinline__ double node_rows(const double* base, int64_t b0, int 
 #pragma unroll
   for (int a = 0; a < 8; ++a) acc[a] = 0.0;
   if (deg <= 32) {
+    // two adjacent row positions per lane (same 6x6 block: positions are even and 6
+    // is even): 128-bit shared loads of the values and one 128-bit gather of x
     for (int r0 = 0; r0 < rowlen; r0 += 64) {
-      // two row positions per lane in flight: gathers first, then the 12 products
-      const int ra = r0 + lane, rb = r0 + 32 + lane;
-      const bool aa = ra < rowlen, ab = rb < rowlen;
-      const int ka = aa ? ra / 6 : 0, kb = ab ? rb / 6 : 0;
+      const int ra = r0 + 2 * lane;
+      const bool aa = ra < rowlen;
+      const int ka = aa ? ra / 6 : 0;
       const int ma = __shfl_sync(0xffffffffu, ncol, ka);
-      const int mb = __shfl_sync(0xffffffffu, ncol, kb);
-      const double xa = aa ? x[6 * (int64_t)ma + (ra - 6 * ka)] : 0.0;
-      const double xb = ab ? x[6 * (int64_t)mb + (rb - 6 * kb)] : 0.0;
+      double2 xv = make_double2(0.0, 0.0);
+      if (aa) xv = *reinterpret_cast<const double2*>(x + 6 * (int64_t)ma + (ra - 6 * ka));
       if (aa) {
 #pragma unroll
-        for (int a = 0; a < 6; ++a) acc[a] += base[a * rowlen + ra] * xa;
-      }
-      if (ab) {
-#pragma unroll
-        for (int a = 0; a < 6; ++a) acc[a] += base[a * rowlen + rb] * xb;
+        for (int a = 0; a < 6; ++a) {
+          const double2 v = *reinterpret_cast<const double2*>(base + a * rowlen + ra);
+          acc[a] = fma(v.y, xv.y, fma(v.x, xv.x, acc[a]));
+        }
       }
     }
   } else {
@@ -216,6 +215,332 @@ __device__ __forceinline__ double node_rows(const double* base, int64_t b0, int 
     }
   }
   return reduce6(acc, lane);
+}
+
+// ---------------------------------------------------------------------------
+// Symmetric (upper-block) storage SpMV.  Pass 1, warp-independent TMA rings as
+// above, two nodes per step: for node n the upper row sums y_n = sum_{m >= n}
+// K_nm x_m, and per off-diagonal upper block the transpose contribution
+// t = K_nm^T x_n written to its receiver-ordered slot.  In the CG form (DOT) the
+// same values give p^T K p = sum_n (2 p_n . y_n - p_n^T K_nn p_n): the diagonal
+// term is sum over the lanes holding block 0 of t_b p_n[b], so alpha is formed
+// at the end of pass 1 and the receiver sums move into the x / r update.
+// ---------------------------------------------------------------------------
+
+// v[i] for a lane-dependent i without forcing v into local memory
+__device__ __forceinline__ double pick6(const double (&v)[6], int i) {
+  double r = v[0];
+  r = (i == 1) ? v[1] : r;
+  r = (i == 2) ? v[2] : r;
+  r = (i == 3) ? v[3] : r;
+  r = (i == 4) ? v[4] : r;
+  r = (i == 5) ? v[5] : r;
+  return r;
+}
+
+// One node (general degree): row sums + transpose slots; returns y[vi(lane)] and adds
+// the lane's share of -p_n^T K_nn p_n to *dq (DOT).
+__device__ __forceinline__ double node_rows_sym(const double* base, int deg, int ncol,
+                                                const double* __restrict__ x, const double (&xn)[6],
+                                                double* __restrict__ tn, double* dq, int lane) {
+  const int rowlen = 6 * deg;
+  double acc[8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a) acc[a] = 0.0;
+  for (int r0 = 0; r0 < rowlen; r0 += 32) {
+    const int rem = r0 + lane;
+    const bool act = rem < rowlen;
+    const int k = act ? rem / 6 : 0;
+    const int m = __shfl_sync(0xffffffffu, ncol, k);
+    if (act) {
+      const int b = rem - 6 * k;
+      const double xv = x[6 * (int64_t)m + b];
+      double t = 0.0;
+#pragma unroll
+      for (int a = 0; a < 6; ++a) {
+        const double v = base[a * rowlen + rem];
+        acc[a] += v * xv;
+        t += v * xn[a];
+      }
+      if (k > 0) tn[rem - 6] = t;
+      else *dq -= t * pick6(xn, b);
+    }
+  }
+  return reduce6(acc, lane);
+}
+
+template <bool DOT, int SPMV_STAGES, int SLOT_DEG, int MINB>
+__global__ void __launch_bounds__(SPMV_WARPS * 32, MINB) spmv_sym_pass1_kernel(
+    int n_nodes, int nodes_per_warp, const int64_t* __restrict__ uptr,
+    const int32_t* __restrict__ ucol, const double* __restrict__ vals,
+    const double* __restrict__ p, double* __restrict__ q, double* __restrict__ tbuf,
+    double* __restrict__ partial, CgState* st, BatchStrides bs) {
+  constexpr int SLOT_DOUBLES = 36 * SLOT_DEG;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar[SPMV_WARPS][SPMV_STAGES];
+  __shared__ double sm[32];
+  {
+    const int bd = blockIdx.y;
+    vals += bd * bs.nnz;
+    p += bd * bs.dof;
+    q += bd * bs.dof;
+    tbuf += bd * bs.tbuf;
+    if (DOT) {
+      partial += bd * bs.partial;
+      st += bd;
+    }
+  }
+  if (DOT && st->done) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * SPMV_WARPS + warp;
+  const int64_t nb = gw * nodes_per_warp;
+  const int64_t left = (int64_t)n_nodes - nb;
+  const int cnt = left <= 0 ? 0 : (int)(left < nodes_per_warp ? left : nodes_per_warp);
+  double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * SPMV_STAGES * SLOT_DOUBLES;
+  uint64_t* wbar = bar[warp];
+  uint64_t pol = 0;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < SPMV_STAGES; ++s) mbar_init(&wbar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    pol = evict_first_policy();
+  }
+  __syncwarp();
+  auto issue = [&](int k) {  // lane 0 only
+    const int64_t n = nb + k;
+    const int s = k % SPMV_STAGES;
+    const int64_t b0 = uptr[n], b1 = uptr[n + 1];
+    if (b1 - b0 <= SLOT_DEG) {
+      const unsigned bytes = (unsigned)(288 * (b1 - b0));
+      mbar_arrive_expect_tx(&wbar[s], bytes);
+      bulk_g2s(ring + (size_t)s * SLOT_DOUBLES, vals + 36 * b0, bytes, &wbar[s], pol);
+    } else {
+      mbar_arrive(&wbar[s]);
+    }
+  };
+  // pairs of nodes per step: nodes k, k+1 are consumed while k+2 .. k+S-1 stream in
+  if (lane == 0)
+    for (int k = 0; k < min(SPMV_STAGES - 2, cnt); ++k) issue(k);
+  const int vi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  const bool writer = ((lane & 3) == 0) && vi < 6;
+  double dq = 0.0;  // this lane's share of p^T K p
+  int64_t b0n = 0;
+  int degn = 0, ncoln = 0;
+  if (cnt > 0) {
+    b0n = uptr[nb];
+    degn = (int)(uptr[nb + 1] - b0n);
+    ncoln = (lane < degn) ? __ldg(ucol + b0n + lane) : 0;
+  }
+  for (int k = 0; k < cnt; k += 2) {
+    const bool twoB = k + 1 < cnt;
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (k + SPMV_STAGES - 2 < cnt) issue(k + SPMV_STAGES - 2);
+      if (k + SPMV_STAGES - 1 < cnt) issue(k + SPMV_STAGES - 1);
+    }
+    const int64_t nA = nb + k, nB = nA + 1;
+    const int64_t bA = b0n;
+    const int degA = degn, ncolA = ncoln;
+    int64_t bB = 0;
+    int degB = 0, ncolB = 0;
+    if (twoB) {
+      bB = uptr[nB];
+      degB = (int)(uptr[nB + 1] - bB);
+      ncolB = (lane < degB) ? __ldg(ucol + bB + lane) : 0;
+    }
+    if (k + 2 < cnt) {
+      b0n = uptr[nA + 2];
+      degn = (int)(uptr[nA + 3] - b0n);
+      ncoln = (lane < degn) ? __ldg(ucol + b0n + lane) : 0;
+    }
+    double* tA = tbuf + 6 * (bA - nA);  // sender-ordered slots of node A
+    double* tB = tbuf + 6 * (bB - nB);
+    double xA[6], xB[6];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+      xA[a] = p[6 * nA + a];
+      xB[a] = twoB ? p[6 * nB + a] : 0.0;
+    }
+    const int sA = k % SPMV_STAGES, sB = (k + 1) % SPMV_STAGES;
+    double yA = 0.0, yB = 0.0;
+    if (degA <= 5 && degB <= 5) {
+      // common case (at most 5 upper blocks: <= 30 row positions, one per lane)
+      const int rlA = 6 * degA, rlB = 6 * degB;
+      const bool aA = lane < rlA, aB = lane < rlB;
+      const int kA = aA ? lane / 6 : 0, kB = aB ? lane / 6 : 0;
+      const int mA = __shfl_sync(0xffffffffu, ncolA, kA);
+      const int mB = __shfl_sync(0xffffffffu, ncolB, kB);
+      const int cA = lane - 6 * kA, cB = lane - 6 * kB;
+      const double xgA = aA ? p[6 * (int64_t)mA + cA] : 0.0;
+      const double xgB = aB ? p[6 * (int64_t)mB + cB] : 0.0;
+      mbar_wait(&wbar[sA], (unsigned)((k / SPMV_STAGES) & 1));
+      if (twoB) mbar_wait(&wbar[sB], (unsigned)(((k + 1) / SPMV_STAGES) & 1));
+      const double* baseA = ring + (size_t)sA * SLOT_DOUBLES;
+      const double* baseB = ring + (size_t)sB * SLOT_DOUBLES;
+      double accA[8], accB[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) accA[a] = accB[a] = 0.0;
+      if (aA) {
+        double t = 0.0;
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+          const double v = baseA[a * rlA + lane];
+          accA[a] = v * xgA;
+          t += v * xA[a];
+        }
+        if (kA > 0) tA[lane - 6] = t;
+        else dq -= t * p[6 * nA + cA];
+      }
+      if (aB) {
+        double t = 0.0;
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+          const double v = baseB[a * rlB + lane];
+          accB[a] = v * xgB;
+          t += v * xB[a];
+        }
+        if (kB > 0) tB[lane - 6] = t;
+        else dq -= t * p[6 * nB + cB];
+      }
+      yA = reduce6(accA, lane);
+      yB = reduce6(accB, lane);
+    } else {
+      // general degree: one node at a time
+      for (int h2 = 0; h2 < (twoB ? 2 : 1); ++h2) {
+        const int64_t b0 = h2 ? bB : bA;
+        const int deg = h2 ? degB : degA;
+        const int s = h2 ? sB : sA;
+        mbar_wait(&wbar[s], (unsigned)(((k + h2) / SPMV_STAGES) & 1));
+        const double* base = (deg <= SLOT_DEG) ? ring + (size_t)s * SLOT_DOUBLES : vals + 36 * b0;
+        double y;
+        if (deg <= 32) {
+          y = node_rows_sym(base, deg, h2 ? ncolB : ncolA, p, h2 ? xB : xA, h2 ? tB : tA, &dq, lane);
+        } else {
+          const int rowlen = 6 * deg;
+          double acc[8];
+#pragma unroll
+          for (int a = 0; a < 8; ++a) acc[a] = 0.0;
+          for (int rem = lane; rem < rowlen; rem += 32) {
+            const int kk = rem / 6, b = rem - 6 * (rem / 6);
+            const int m = __ldg(ucol + b0 + kk);
+            const double xv = p[6 * (int64_t)m + b];
+            double t = 0.0;
+#pragma unroll
+            for (int a = 0; a < 6; ++a) {
+              const double v = base[a * rowlen + rem];
+              acc[a] += v * xv;
+              t += v * (h2 ? xB[a] : xA[a]);
+            }
+            if (kk > 0) (h2 ? tB : tA)[rem - 6] = t;
+            else dq -= t * pick6(h2 ? xB : xA, b);
+          }
+          y = reduce6(acc, lane);
+        }
+        if (h2) yB = y; else yA = y;
+      }
+    }
+    if (writer) {
+      q[6 * nA + vi] = yA;
+      if (DOT) dq += 2.0 * p[6 * nA + vi] * yA;
+      if (twoB) {
+        q[6 * nB + vi] = yB;
+        if (DOT) dq += 2.0 * p[6 * nB + vi] * yB;
+      }
+    }
+    __syncwarp();
+  }
+  if (DOT) {
+    double v[1] = {dq};
+    if (grid_sum<1>(v, partial, &st->ticket[0], sm) && threadIdx.x == 0) {
+      if (st->dist) {
+        st->red[0] = v[0];
+        return;
+      }
+      st->pq = v[0];
+      if (!(v[0] > 0.0)) {
+        st->status = SSO_E_NOT_SPD;
+        st->done = 1;
+      } else {
+        st->alpha = st->rz / v[0];
+      }
+    }
+  }
+}
+
+// Symmetric storage, pass 2 (plain SpMV): y[d] += node d/6's incoming slots (contiguous).
+__global__ void __launch_bounds__(256) spmv_sym_pass2_kernel(int ndof, const int64_t* __restrict__ lptr,
+                                                             const int32_t* __restrict__ lslot,
+                                                             const double* __restrict__ tbuf,
+                                                             double* __restrict__ y, BatchStrides bs) {
+  tbuf += blockIdx.y * bs.tbuf;
+  y += blockIdx.y * bs.dof;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < ndof; d += stride) {
+    const int64_t m = d / 6;
+    const int b = (int)(d - 6 * m);
+    double v = y[d];
+    for (int64_t l = lptr[m]; l < lptr[m + 1]; ++l) v += tbuf[6 * (int64_t)lslot[l] + b];
+    y[d] = v;
+  }
+}
+
+// CG x / r update with the symmetric receiver sums folded in: q = y_up + incoming slots.
+__global__ void __launch_bounds__(256) cg_update_sym_kernel(int ndof, const double* __restrict__ dinv,
+                                                            double* __restrict__ x, double* __restrict__ r,
+                                                            const double* __restrict__ p,
+                                                            const double* __restrict__ yup,
+                                                            const double* __restrict__ tbuf,
+                                                            const int64_t* __restrict__ lptr,
+                                                            const int32_t* __restrict__ lslot,
+                                                            double* __restrict__ partial, CgState* st,
+                                                            BatchStrides bs) {
+  __shared__ double sm[64];
+  {
+    const int bd = blockIdx.y;
+    dinv += bd * bs.dof;
+    x += bd * bs.dof;
+    r += bd * bs.dof;
+    p += bd * bs.dof;
+    yup += bd * bs.dof;
+    tbuf += bd * bs.tbuf;
+    partial += bd * bs.partial;
+    st += bd;
+  }
+  if (st->done) return;
+  const double alpha = st->alpha;
+  double v[2] = {0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < ndof; d += stride) {
+    const int64_t m = d / 6;
+    const int b = (int)(d - 6 * m);
+    double q = yup[d];
+    for (int64_t l = lptr[m]; l < lptr[m + 1]; ++l) q += tbuf[6 * (int64_t)lslot[l] + b];
+    x[d] += alpha * p[d];
+    const double ri = r[d] - alpha * q;
+    r[d] = ri;
+    v[0] += ri * (dinv[d] * ri);
+    v[1] += ri * ri;
+  }
+  if (grid_sum<2>(v, partial, &st->ticket[1], sm) && threadIdx.x == 0) {
+    if (st->dist) {
+      st->red[0] = v[0];
+      st->red[1] = v[1];
+      return;
+    }
+    const double rz_new = v[0];
+    st->beta = rz_new / st->rz;
+    st->rz_prev = st->rz;
+    st->rz = rz_new;
+    st->rr = v[1];
+    st->iter += 1;
+    if (v[1] <= st->tol2) {
+      st->done = 1;
+      st->status = SSO_OK;
+    } else if (st->iter >= st->max_iter) {
+      st->done = 1;
+      st->status = SSO_E_NOT_CONVERGED;
+    }
+  }
 }
 
 // q = K p; with DOT also p^T q -> alpha (CG) and an early exit once `done`.
@@ -792,6 +1117,8 @@ struct SpmvVariant {
   void (*plain)(int, int, const int64_t*, const int32_t*, const double*, const double*, double*,
                 double*, CgState*, BatchStrides);
 };
+// symmetric pass 1: 4-slot ring (two nodes consumed per step), <= 5 upper blocks per slot
+constexpr int SYM_STAGES = 4, SYM_SLOT_DEG = 5, SYM_MINB = 2;
 #define SPMV_VARIANT(S, D, M) \
   { S, D, M, spmv_tma_kernel<true, S, D, M>, spmv_tma_kernel<false, S, D, M> }
 static const SpmvVariant kSpmvVariants[] = {
@@ -809,6 +1136,12 @@ static const SpmvVariant& spmv_variant() {
     const int smem = SPMV_WARPS * V.stages * 36 * V.slot_deg * 8;
     cudaFuncSetAttribute(V.dot, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(V.plain, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(spmv_sym_pass1_kernel<true, SYM_STAGES, SYM_SLOT_DEG, SYM_MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SPMV_WARPS * SYM_STAGES * 36 * SYM_SLOT_DEG * 8);
+    cudaFuncSetAttribute(spmv_sym_pass1_kernel<false, SYM_STAGES, SYM_SLOT_DEG, SYM_MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SPMV_WARPS * SYM_STAGES * 36 * SYM_SLOT_DEG * 8);
   }
   return kSpmvVariants[v];
 }
@@ -832,6 +1165,48 @@ void launch_spmv_dot(cudaStream_t s, int n_nodes, const int64_t* node_ptr, const
   spmv_variant().dot<<<dim3(grid, bs.B), SPMV_WARPS * 32, smem, s>>>(n_nodes, npw, node_ptr, node_col, vals,
                                                                      p, q, partial, st, bs);
   SSO_POST_LAUNCH("spmv_dot_kernel");
+}
+
+static void sym_config(int n_nodes, int B, int* grid, int* npw, int* smem) {
+  spmv_variant();  // kernel attributes
+  const int ctas = std::max(1, SYM_MINB * (cg_grid() / 4) / B);
+  const int64_t warps = (int64_t)ctas * SPMV_WARPS;
+  int per = (int)((n_nodes + warps - 1) / warps);
+  if (per < 1) per = 1;
+  *npw = per;
+  *grid = (int)std::max<int64_t>(1, (((int64_t)n_nodes + per - 1) / per + SPMV_WARPS - 1) / SPMV_WARPS);
+  *smem = SPMV_WARPS * SYM_STAGES * 36 * SYM_SLOT_DEG * 8;
+}
+
+void launch_spmv_sym(cudaStream_t s, int n_nodes, const int64_t* uptr, const int32_t* ucol,
+                     const double* vals, const double* x, double* y, double* tbuf,
+                     const int64_t* lptr, const int32_t* lslot, const BatchStrides& bs) {
+  int grid, npw, smem;
+  sym_config(n_nodes, bs.B, &grid, &npw, &smem);
+  spmv_sym_pass1_kernel<false, SYM_STAGES, SYM_SLOT_DEG, SYM_MINB><<<dim3(grid, bs.B), SPMV_WARPS * 32, smem, s>>>(
+      n_nodes, npw, uptr, ucol, vals, x, y, tbuf, nullptr, nullptr, bs);
+  SSO_POST_LAUNCH("spmv_sym_pass1_kernel");
+  const int ndof = 6 * n_nodes;
+  spmv_sym_pass2_kernel<<<dim3(vec_grid(ndof, bs.B), bs.B), 256, 0, s>>>(ndof, lptr, lslot, tbuf, y, bs);
+  SSO_POST_LAUNCH("spmv_sym_pass2_kernel");
+}
+
+void launch_spmv_sym_cg(cudaStream_t s, int n_nodes, const int64_t* uptr, const int32_t* ucol,
+                        const double* vals, const double* p, double* y, double* tbuf,
+                        double* partial, CgState* st, const BatchStrides& bs) {
+  int grid, npw, smem;
+  sym_config(n_nodes, bs.B, &grid, &npw, &smem);
+  spmv_sym_pass1_kernel<true, SYM_STAGES, SYM_SLOT_DEG, SYM_MINB><<<dim3(grid, bs.B), SPMV_WARPS * 32, smem, s>>>(
+      n_nodes, npw, uptr, ucol, vals, p, y, tbuf, partial, st, bs);
+  SSO_POST_LAUNCH("spmv_sym_pass1_kernel");
+}
+
+void launch_cg_update_sym(cudaStream_t s, int ndof, const double* dinv, double* x, double* r,
+                          const double* p, const double* yup, const double* tbuf, const int64_t* lptr,
+                          const int32_t* lslot, double* partial, CgState* st, const BatchStrides& bs) {
+  cg_update_sym_kernel<<<dim3(vec_grid(ndof, bs.B), bs.B), 256, 0, s>>>(ndof, dinv, x, r, p, yup, tbuf, lptr,
+                                                                        lslot, partial, st, bs);
+  SSO_POST_LAUNCH("cg_update_sym_kernel");
 }
 
 void launch_spmv(cudaStream_t s, int n_nodes, const int64_t* node_ptr, const int32_t* node_col,

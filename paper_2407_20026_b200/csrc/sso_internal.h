@@ -32,6 +32,25 @@ struct HostPattern {
   int64_t n_staged_blocks() const { return 4 * (int64_t)n_beams + 16 * (int64_t)n_quads; }
 };
 
+// Upper-triangular (symmetric) node-block storage: node n keeps only the blocks
+// (n, m) with m >= n (the diagonal block first).  The transpose contribution
+// K_nm^T x_n of the k-th (k >= 1) upper block of node n is written to the
+// sender-ordered slot uptr[n] - n + k - 1 (contiguous per sender); node m sums
+// its incoming slots lslot[lptr[m] ..] in ascending source node.
+struct UpperPattern {
+  std::vector<int64_t> uptr;          // [n_nodes+1]
+  std::vector<int32_t> ucol;          // [n_ublocks]
+  std::vector<int32_t> urank;         // beams [Eb][4], quads [Eq][16]: rank in ucol(node_i) or -1
+  std::vector<int64_t> ucontrib_ptr;  // [n_ublocks+1]
+  std::vector<int32_t> ucontrib;      // staged block ids of upper blocks, ascending (e, i, j)
+  std::vector<int64_t> lptr;          // [n_nodes+1]
+  std::vector<int32_t> lslot;         // incoming sender slots, ascending source node
+  int64_t n_ublocks() const { return (int64_t)ucol.size(); }
+  int64_t n_tslots = 0;
+};
+void build_upper(const HostPattern& P, const int32_t* beam_conn, const int32_t* quad_conn,
+                 UpperPattern& U);
+
 // Builds the pattern; returns empty string on success, else an error message.
 std::string build_pattern(int32_t n_nodes, int32_t n_beams, const int32_t* beam_conn,
                           int32_t n_quads, const int32_t* quad_conn, HostPattern& P);
@@ -92,6 +111,7 @@ struct BatchStrides {
   int64_t dof = 0;      // vectors [B][6 n]
   int64_t partial = 0;  // per-CTA partials [B][..]
   int64_t slot = 0;     // gradient slot partials [B][3 n_slots]
+  int64_t tbuf = 0;     // symmetric-storage transpose slots [B][6 n_tslots]
 };
 
 // Launch wrappers (implemented in the .cu files).  All are stream-ordered.
@@ -137,6 +157,23 @@ void launch_cg_update(cudaStream_t s, int ndof, const double* dinv, double* x, d
 void launch_cg_pupdate(cudaStream_t s, int ndof, const double* dinv, const double* r,
                        double* p, CgState* st,
     const BatchStrides& bs = BatchStrides());
+// Symmetric (upper-block) storage SpMV: pass 1 streams the upper runs (TMA ring),
+// writes the upper row sums to y and the transpose contributions K_nm^T x_n to
+// tbuf; pass 2 adds each node's incoming slots (ascending source node) and, with
+// st != nullptr, forms p^T q and alpha like launch_spmv_dot.
+void launch_spmv_sym(cudaStream_t s, int n_nodes, const int64_t* uptr, const int32_t* ucol,
+                     const double* vals, const double* x, double* y, double* tbuf,
+                     const int64_t* lptr, const int32_t* lslot, const BatchStrides& bs = BatchStrides());
+// CG with symmetric storage: pass 1 only (upper row sums -> y, transpose slots,
+// p^T K p and alpha); the receiver sums are folded into launch_cg_update_sym.
+void launch_spmv_sym_cg(cudaStream_t s, int n_nodes, const int64_t* uptr, const int32_t* ucol,
+                        const double* vals, const double* p, double* y,
+                        double* tbuf, double* partial, CgState* st,
+                        const BatchStrides& bs = BatchStrides());
+void launch_cg_update_sym(cudaStream_t s, int ndof, const double* dinv, double* x, double* r,
+                          const double* p, const double* yup, const double* tbuf, const int64_t* lptr,
+                          const int32_t* lslot, double* partial, CgState* st,
+                          const BatchStrides& bs = BatchStrides());
 void launch_spmv(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
                  const int32_t* node_col, const double* vals, const double* x, double* y,
     const BatchStrides& bs = BatchStrides());

@@ -269,3 +269,30 @@ def test_fused_assembly_matches_staged(sso, make):
         seg = slice(rp[r], rp[r + 1])
         assert np.abs(vf[seg] - vs[seg]).max() <= 1e-14 * np.abs(vs[seg]).max()
     assert np.allclose(mf.export_dinv(), ms.export_dinv(), rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("make", [W.config2, mixed, W.config1, lambda: W.shell_config3(40, cfg=3)])
+def test_symmetric_storage_matches_full(sso, make):
+    """Upper-block (symmetric) storage with the two-pass transpose SpMV (default for
+    single-strip handles) reproduces the full-storage operator, solve and gradient."""
+    P = make()
+    ms = sso.Model(P, rtol=1e-12, storage=2)
+    mf = sso.Model(P, rtol=1e-12, storage=1)
+    assert ms.storage_info()[2] and not mf.storage_info()[2]
+    assert ms.storage_info()[1] < mf.storage_info()[1]
+    ms.assemble()
+    mf.assemble()
+    rp, ci, vs = ms.export_csr()
+    _, _, vf = mf.export_csr()
+    for r in range(len(rp) - 1):
+        seg = slice(rp[r], rp[r + 1])
+        assert np.abs(vs[seg] - vf[seg]).max() <= 1e-14 * np.abs(vf[seg]).max()
+    x = np.random.default_rng(4).standard_normal(ms.ndof)
+    ys, yf = ms.spmv(x), mf.spmv(x)
+    assert np.abs(ys - yf).max() <= 1e-13 * np.abs(yf).max()
+    us, i_s = ms.solve(P["f"])
+    uf, i_f = mf.solve(P["f"])
+    assert np.linalg.norm(us - uf) <= 1e-9 * np.linalg.norm(uf)
+    Cs, dXs, _ = ms.grad()
+    Cf, dXf, _ = mf.grad()
+    assert Cs == pytest.approx(Cf, rel=1e-10)
