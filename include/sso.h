@@ -192,6 +192,29 @@ int sso_grad(sso_handle h, sso_objective obj, double* C, double* dC_dxyz, double
 int sso_grad_at(sso_handle h, sso_objective obj, const double* f, const double* u,
                 double* C, double* dC_dxyz, double* dC_dt);
 
+/* General objective g(u, p) (Eq. 5-6):
+ * sso_adjoint_solve solves K_bc^T lambda = dg/du (K symmetric; entries at constrained
+ * DOFs ignored, lambda = 0 there) with the same Jacobi-PCG and options as sso_solve,
+ * keeping the primal state (u, f) of the last solve.  dg_du, lambda [6 n_nodes].
+ * sso_grad_adjoint then returns the Eq. 6 term -lambda^T (dK/dp) u at the primal u
+ * (df/dp = 0, reading c3) for p = coordinates dg_dxyz [3][n_nodes], thicknesses
+ * dg_dt [n_quads] and moduli dg_dE [n_beams + n_quads] (any may be NULL); the caller
+ * adds the explicit dg/dp.  Single-strip, single-design handles. */
+int sso_adjoint_solve(sso_handle h, const double* dg_du, double* lambda, sso_solve_info* info);
+int sso_grad_adjoint(sso_handle h, const double* lambda, double* dg_dxyz, double* dg_dt, double* dg_dE);
+
+/* SIMP / material design variable (Eq. 12):
+ * dC_dE [batch][n_beams + n_quads] = -s u_e^T (dK_e/dE_e) u_e at the last solve, where the
+ * element's whole elastic tensor scales with E_e (a given G scales with it).  With
+ * E_e = rho_e^P E0_e the caller forms dC/drho = dC/dE * P rho^(P-1) E0.  Single-strip
+ * handles.  Errors: SSO_E_STATE (no solve yet). */
+int sso_grad_E(sso_handle h, sso_objective obj, double* dC_dE);
+
+/* Replace the element moduli E [n_beams + n_quads] (shared by a batch; pointer kind per
+ * mem); G follows (derived G recomputed, given G scaled).  Invalidates the assembly.
+ * Single-strip handles.  Errors: SSO_E_INVALID (E <= 0). */
+int sso_set_material(sso_handle h, const double* E);
+
 /* y = K_bc x with the assembled matrix (x, y [6 n_nodes]; pointer kind per mem). */
 int sso_spmv(sso_handle h, const double* x, double* y);
 

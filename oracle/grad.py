@@ -112,6 +112,37 @@ def element_grad(P, e, u, s=1.0, X=None):
     return out, g_t
 
 
+def element_dK_dE(P, e, X=None):
+    """dK_e / dE_e by complex step (any element).  The whole elastic tensor of the
+    element scales with E_e (SIMP, Eq. 12): an explicitly given G scales by
+    the same factor."""
+    Pc = dict(P)
+    Pc["E"] = P["E"].astype(np.complex128)
+    Pc["E"][e] += 1j * H_CS
+    if P.get("G") is not None:
+        Pc["G"] = P["G"].astype(np.complex128)
+        Pc["G"][e] *= Pc["E"][e] / P["E"][e]
+    return np.imag(A.element_K(Pc, e, X)) / H_CS
+
+
+def material_gradient(P, u, s=1.0):
+    """dC/dE_e = -s u_e^T (dK_e/dE_e) u_e for every element (beams first, then quads):
+    the adjoint gradient of PAPER.md Eq. 6 with respect to the element modulus, the
+    design variable of SIMP (Eq. 12: E_j = p_T,j^P E_*,j)."""
+    nb, nq = A.n_beams(P), A.n_quads(P)
+    X = A.coords(P)
+    out = np.zeros(nb + nq)
+    for e in range(nb + nq):
+        ue = u[A.element_dofs(A.element_nodes(P, e))]
+        out[e] = -s * float(ue @ element_dK_dE(P, e, X) @ ue)
+    return out
+
+
+def simp_gradient(dC_dE, rho, E0, penal):
+    """SIMP chain rule (Eq. 12): E = rho^P E0 -> dC/drho = dC/dE * P rho^(P-1) E0."""
+    return dC_dE * penal * rho ** (penal - 1.0) * E0
+
+
 def _solve_C(P, X, t, s):
     nd = 6 * len(P["x"])
     dok = A.assemble_dok(P, X, t)
@@ -126,15 +157,21 @@ def _solve_C(P, X, t, s):
 
 
 def global_complex_step(P, kind, index, s=1.0):
-    """dC/dp for p = coordinate (kind='xyz', index=(node, axis)) or thickness
-    (kind='t', index=quad) by perturbing p with i h, re-assembling and solving
-    the complex system with dense LU (loads held fixed, reading c3)."""
+    """dC/dp for p = coordinate (kind='xyz', index=(node, axis)), thickness
+    (kind='t', index=quad) or modulus (kind='E', index=element) by perturbing p with
+    i h, re-assembling and solving the complex system with dense LU (loads held
+    fixed, reading c3)."""
     X = A.coords(P).astype(np.complex128)
     t = P["t"].astype(np.complex128)
     if kind == "xyz":
         X[index[0], index[1]] += 1j * H_CS
-    else:
+    elif kind == "t":
         t[index] += 1j * H_CS
+    else:
+        Pc = dict(P)
+        Pc["E"] = P["E"].astype(np.complex128)
+        Pc["E"][index] += 1j * H_CS
+        return float(np.imag(_solve_C(Pc, X, t, s)) / H_CS)
     return float(np.imag(_solve_C(P, X, t, s)) / H_CS)
 
 
@@ -156,3 +193,53 @@ def central_fd(P, kind, index, s=1.0, rel_step=1e-6):
             tp[index] = p0 + sgn * hstep
         vals.append(float(np.real(_solve_C(P, Xp, tp, s))))
     return (vals[0] - vals[1]) / (2 * hstep)
+
+
+def adjoint_general(P, u, lam):
+    """General-objective adjoint term of PAPER.md Eq. 6 with df/dp = 0 (reading c3):
+    -lambda^T (dK/dp) u, where K^T lambda = dg/du (Eq. 5) is solved by the caller.
+    Returns (d[3, n_nodes] for coordinates, d[n_quads] for thickness, d[n_elems] for E),
+    element contributions summed in ascending element order."""
+    nn = len(P["x"])
+    nb, nq = A.n_beams(P), A.n_quads(P)
+    X = A.coords(P)
+    dX = np.zeros((3, nn))
+    dt = np.zeros(nq)
+    dE = np.zeros(nb + nq)
+    for e in range(nb + nq):
+        nodes = A.element_nodes(P, e)
+        dofs = A.element_dofs(nodes)
+        ue, le = u[dofs], lam[dofs]
+        for il, n in enumerate(nodes):
+            for axis in range(3):
+                dX[axis, n] += -float(le @ element_dK_dcoord(P, e, il, axis, X) @ ue)
+        if e >= nb:
+            dt[e - nb] = -float(le @ element_dK_dt(P, e, X) @ ue)
+        dE[e] = -float(le @ element_dK_dE(P, e, X) @ ue)
+    return dX, dt, dE
+
+
+def global_complex_step_linear(P, c, kind, index):
+    """d(c^T u)/dp by complex step of the full solve (the pin of adjoint_general)."""
+    X = A.coords(P).astype(np.complex128)
+    t = P["t"].astype(np.complex128)
+    Pc = P
+    if kind == "xyz":
+        X[index[0], index[1]] += 1j * H_CS
+    elif kind == "t":
+        t[index] += 1j * H_CS
+    else:
+        Pc = dict(P)
+        Pc["E"] = P["E"].astype(np.complex128)
+        Pc["E"][index] += 1j * H_CS
+        if P.get("G") is not None:
+            Pc["G"] = P["G"].astype(np.complex128)
+            Pc["G"][index] *= Pc["E"][index] / P["E"][index]
+    nd = 6 * len(P["x"])
+    K = A.dense_from_dok(A.assemble_dok(Pc, X, t), nd, dtype=np.complex128)
+    fixed = A.fixed_dofs(P)
+    Kbc, fbc = A.apply_supports_dense(K, P["f"].astype(np.complex128), fixed)
+    free = np.nonzero(~fixed)[0]
+    u = np.zeros(nd, dtype=np.complex128)
+    u[free] = S.solve_dense_lu(Kbc[np.ix_(free, free)], fbc[free])
+    return float(np.imag(np.dot(c, u)) / H_CS)

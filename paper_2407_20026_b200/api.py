@@ -87,6 +87,10 @@ _sig = {
     "sso_grad": (C.c_int, [_H, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sso_grad_at": (C.c_int, [_H, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sso_spmv": (C.c_int, [_H, C.c_void_p, C.c_void_p]),
+    "sso_grad_E": (C.c_int, [_H, C.c_int, C.c_void_p]),
+    "sso_adjoint_solve": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.POINTER(sso_solve_info)]),
+    "sso_grad_adjoint": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sso_set_material": (C.c_int, [_H, C.c_void_p]),
     "sso_sizes": (C.c_int, [_H, _lp, _lp, _lp]),
     "sso_export_csr": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sso_export_scatter": (C.c_int, [_H, C.c_void_p]),
@@ -305,6 +309,40 @@ class Model:
             return Cv, dX.reshape(B, 3, self.n_nodes), dT.reshape(B, -1)[:, : self.n_quads]
         C0 = float(Cv[0]) if not dev else Cv
         return C0, dX.reshape(3, self.n_nodes), dT[: self.n_quads]
+
+    def grad_E(self, objective=OBJ_COMPLIANCE):
+        """dC/dE per element (beams first, then quads), [batch, n_elems] or [n_elems]."""
+        ne = self.n_beams + self.g_quads
+        out = np.zeros(self.batch * ne)
+        self._mode()
+        self._check(_lib.sso_grad_E(self.h, objective, out.ctypes.data))
+        return out.reshape(self.batch, ne) if self.batch > 1 else out
+
+    def adjoint_solve(self, dg_du):
+        """lambda with K lambda = dg/du (primal state kept).  Returns (lambda, info)."""
+        self._mode()
+        g = _np(dg_du, np.float64)
+        lam = np.zeros(self.ndof)
+        info = sso_solve_info()
+        self._check(_lib.sso_adjoint_solve(self.h, g.ctypes.data, lam.ctypes.data, C.byref(info)))
+        return lam, info.as_dict()
+
+    def grad_adjoint(self, lam):
+        """(-lambda^T dK/dX u [3, n], -lambda^T dK/dt u [n_quads], -lambda^T dK/dE u [n_elems])."""
+        self._mode()
+        lam = _np(lam, np.float64)
+        dX = np.zeros(3 * self.n_nodes)
+        dT = np.zeros(max(self.n_quads, 1))
+        dE = np.zeros(self.n_beams + self.g_quads)
+        self._check(_lib.sso_grad_adjoint(self.h, lam.ctypes.data, dX.ctypes.data, dT.ctypes.data,
+                                          dE.ctypes.data))
+        return dX.reshape(3, self.n_nodes), dT[: self.n_quads], dE
+
+    def set_material(self, E):
+        dev = self._mode(E)
+        if not dev:
+            E = _np(E, np.float64)
+        self._check(_lib.sso_set_material(self.h, _ptr(E, np.float64)))
 
     def spmv(self, x):
         dev = self._mode(x)

@@ -112,7 +112,12 @@ struct Part {
   DevFlags* flags = nullptr;
   unsigned int* tickets = nullptr;
   double* scal = nullptr;
-  double *slot_partial = nullptr, *dxyz = nullptr, *dt = nullptr, *dt_own = nullptr;
+  double *slot_partial = nullptr, *dxyz = nullptr, *dt = nullptr, *dt_own = nullptr, *dE = nullptr;
+  // general-objective adjoint (sso_adjoint_solve / sso_grad_adjoint): primal backups,
+  // lambda and the second polarization pass (allocated on first use)
+  double *ub = nullptr, *fb = nullptr, *lam = nullptr, *dxyz2 = nullptr, *dt2 = nullptr, *dE2 = nullptr;
+  std::vector<double> h_nu;             // host copies for sso_set_material
+  std::vector<char> g_derived;          // G = E / (2 (1 + nu)) when G was not given
   // partition maps
   int32_t* block_rank = nullptr;      // quads [n_quads][16] (fused assembly; upper ranks when sym)
   bool sym = false;                   // upper-block (symmetric) storage, single-strip handles
@@ -531,7 +536,8 @@ void free_part(Part& P) {
                   P.inc_slot, P.stage, P.vals, P.dinv, P.f, P.fbc, P.xs, P.r, P.p, P.q, P.tmp, P.gu,
                   P.gf, P.partial, P.st, P.flags, P.tickets, P.scal, P.slot_partial, P.dxyz, P.dt,
                   P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
-                  P.lptr, P.lslot, P.tbuf};
+                  P.lptr, P.lslot, P.tbuf, P.dE,
+                  P.ub, P.fb, P.lam, P.dxyz2, P.dt2, P.dE2};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -754,6 +760,9 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   AL(dxyz, 3 * (int64_t)B * P.n_nodes);
   AL(dt, (int64_t)B * std::max<int32_t>(P.n_quads, 1));
   AL(dt_own, std::max<int32_t>(P.n_own_quads, 1));
+  AL(dE, (int64_t)B * std::max<int64_t>(ne, 1));
+  P.h_nu = nu;
+  P.g_derived.assign((size_t)ne, mat->G ? 0 : 1);
 #undef UP
 #undef AL
   CK(h, cudaMemset(P.tickets, 0, 16 * sizeof(unsigned)));
@@ -1243,7 +1252,7 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
 
 // Objective + gradient at the parts' (fv, uvec) state (owned entries set; halos exchanged here).
 static int grad_impl(sso_ctx* h, sso_objective obj, double* Part::*fv, int uvec, double* C,
-                     double* dC_dxyz, double* dC_dt) {
+                     double* dC_dxyz, double* dC_dt, double* dC_dE = nullptr) {
   const double s = (obj == SSO_OBJ_STRAIN_ENERGY) ? 0.5 : 1.0;
   int rc;
   if ((rc = exchange(h, uvec))) return rc;
@@ -1256,10 +1265,11 @@ static int grad_impl(sso_ctx* h, sso_objective obj, double* Part::*fv, int uvec,
     }
     {
       Scope sc(h, F_GRAD);
+      double* dE = dC_dE ? P.dE : nullptr;
       launch_beam_grad(h->stream, P.n_beams, P.x, P.y, P.z, P.beam_conn, P.A, P.Iy, P.Iz, P.J, P.E, P.G,
-                       U, s, P.slot_partial, P.bs);
+                       U, s, P.slot_partial, dE, P.n_beams + P.n_quads, P.bs);
       launch_quad_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.E, P.nu,
-                       h->drill_alpha, U, s, P.slot_partial, P.dt, P.bs);
+                       h->drill_alpha, U, s, P.slot_partial, P.dt, dE, P.bs);
     }
     {
       Scope sc(h, F_REDUCE);
@@ -1280,6 +1290,11 @@ static int grad_impl(sso_ctx* h, sso_objective obj, double* Part::*fv, int uvec,
                               P.dxyz + (int64_t)a * P.n_own, (size_t)P.n_own * sizeof(double), kind_out(h),
                               h->stream));
     }
+  }
+  if (dC_dE) {
+    Part& P = h->P0();
+    CK(h, cudaMemcpyAsync(dC_dE, P.dE, (size_t)h->batch * (P.n_beams + P.n_quads) * sizeof(double), kind_out(h),
+                          h->stream));
   }
   if (dC_dt && h->user_quads > 0) {
     if (!h->distributed()) {
@@ -1328,6 +1343,120 @@ int sso_grad_at(sso_handle h, sso_objective obj, const double* f, const double* 
   if ((rc = vec_in(h, f, &Part::gf))) return rc;
   if ((rc = vec_in(h, u, &Part::gu))) return rc;
   return grad_impl(h, obj, &Part::gf, V_GU, C, dC_dxyz, dC_dt);
+}
+
+// Gradient kernels at state U with scale s into P.dxyz (owned nodes), P.dt, P.dE.
+static int grad_pass(sso_ctx* h, Part& P, const double* U, double s) {
+  launch_beam_grad(h->stream, P.n_beams, P.x, P.y, P.z, P.beam_conn, P.A, P.Iy, P.Iz, P.J, P.E, P.G, U, s,
+                   P.slot_partial, P.dE, P.n_beams + P.n_quads, P.bs);
+  launch_quad_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.E, P.nu, h->drill_alpha,
+                   U, s, P.slot_partial, P.dt, P.dE, P.bs);
+  launch_node_reduce(h->stream, P.n_own, P.inc_ptr, P.inc_slot, P.slot_partial, P.dxyz, P.bs);
+  CKL(h);
+  return SSO_OK;
+}
+
+int sso_adjoint_solve(sso_handle h, const double* dg_du, double* lambda, sso_solve_info* info) {
+  if (!h || !dg_du || !lambda) return SSO_E_INVALID;
+  if (h->distributed() || h->batch > 1) FAIL(h, SSO_E_INVALID, "sso_adjoint_solve is defined for single-strip, single-design handles");
+  if (!h->assembled) FAIL(h, SSO_E_STATE, "sso_adjoint_solve before sso_assemble");
+  Part& P = h->P0();
+  int r;
+  if (!P.ub && (r = dalloc(h, &P.ub, P.ndof))) return r;
+  if (!P.fb && (r = dalloc(h, &P.fb, P.ndof))) return r;
+  const bool was_solved = h->solved;
+  // keep the primal (u, f): the adjoint reuses the CG buffers
+  CK(h, cudaMemcpyAsync(P.ub, P.xs, P.ndof * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(P.fb, P.f, P.ndof * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  const int rc = sso_solve(h, dg_du, lambda, info);  // K symmetric: K^T lambda = K lambda
+  CK(h, cudaMemcpyAsync(P.xs, P.ub, P.ndof * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(P.f, P.fb, P.ndof * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  int rs = sync(h);
+  if (rs) return rs;
+  h->solved = was_solved;
+  return rc;
+}
+
+int sso_grad_adjoint(sso_handle h, const double* lambda, double* dg_dxyz, double* dg_dt, double* dg_dE) {
+  if (!h || !lambda) return SSO_E_INVALID;
+  if (h->distributed() || h->batch > 1) FAIL(h, SSO_E_INVALID, "sso_grad_adjoint is defined for single-strip, single-design handles");
+  if (!h->solved) FAIL(h, SSO_E_STATE, "sso_grad_adjoint before a successful sso_solve");
+  Part& P = h->P0();
+  const int64_t ne = (int64_t)P.n_beams + P.n_quads;
+  int r;
+  if (!P.lam && (r = dalloc(h, &P.lam, P.ndof))) return r;
+  if (!P.dxyz2 && (r = dalloc(h, &P.dxyz2, 3 * (int64_t)P.n_nodes))) return r;
+  if (!P.dt2 && (r = dalloc(h, &P.dt2, std::max<int32_t>(P.n_quads, 1)))) return r;
+  if (!P.dE2 && (r = dalloc(h, &P.dE2, std::max<int64_t>(ne, 1)))) return r;
+  if ((r = vec_in(h, lambda, &Part::lam))) return r;
+  // polarization: lambda^T K u = [(u + c l)^T K (u + c l) - (u - c l)^T K (u - c l)] / (4 c),
+  // c = |u| / |lambda| balances the two states (bilinear result, quadratic kernels)
+  {
+    Scope sc(h, F_REDUCE);
+    launch_dot_local(h->stream, (int)P.ndof, P.xs, P.xs, P.partial, P.st, P.bs);
+    CK(h, cudaMemcpyAsync(&h->h_scal[0], &P.st->red[0], sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    launch_dot_local(h->stream, (int)P.ndof, P.lam, P.lam, P.partial, P.st, P.bs);
+    CK(h, cudaMemcpyAsync(&h->h_scal[1], &P.st->red[0], sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  }
+  if ((r = sync(h))) return r;
+  const double uu = h->h_scal[0], ll = h->h_scal[1];
+  const double c = (uu > 0.0 && ll > 0.0) ? std::sqrt(uu / ll) : 1.0;
+  {
+    Scope sc(h, F_GRAD);
+    launch_lincomb(h->stream, P.ndof, 1.0, P.xs, -c, P.lam, P.gu);  // u - c lambda
+    if ((r = grad_pass(h, P, P.gu, 0.25))) return r;
+    CK(h, cudaMemcpyAsync(P.dxyz2, P.dxyz, 3 * (size_t)P.n_nodes * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(P.dt2, P.dt, std::max<int32_t>(P.n_quads, 1) * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(P.dE2, P.dE, std::max<int64_t>(ne, 1) * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    launch_lincomb(h->stream, P.ndof, 1.0, P.xs, c, P.lam, P.gu);   // u + c lambda
+    if ((r = grad_pass(h, P, P.gu, 0.25))) return r;
+    // -(1/4)[dE(w+) - dE(w-)] / c  ==  -lambda^T (dK/dp) u
+    launch_lincomb(h->stream, 3 * (int64_t)P.n_nodes, 1.0 / c, P.dxyz, -1.0 / c, P.dxyz2, P.dxyz);
+    launch_lincomb(h->stream, P.n_quads, 1.0 / c, P.dt, -1.0 / c, P.dt2, P.dt);
+    launch_lincomb(h->stream, ne, 1.0 / c, P.dE, -1.0 / c, P.dE2, P.dE);
+  }
+  CKL(h);
+  if (dg_dxyz)
+    CK(h, cudaMemcpyAsync(dg_dxyz, P.dxyz, 3 * (size_t)P.n_nodes * sizeof(double), kind_out(h), h->stream));
+  if (dg_dt && P.n_quads)
+    CK(h, cudaMemcpyAsync(dg_dt, P.dt, (size_t)P.n_quads * sizeof(double), kind_out(h), h->stream));
+  if (dg_dE) CK(h, cudaMemcpyAsync(dg_dE, P.dE, (size_t)ne * sizeof(double), kind_out(h), h->stream));
+  return sync(h);
+}
+
+int sso_grad_E(sso_handle h, sso_objective obj, double* dC_dE) {
+  if (!h || !dC_dE) return SSO_E_INVALID;
+  if (obj != SSO_OBJ_COMPLIANCE && obj != SSO_OBJ_STRAIN_ENERGY) FAIL(h, SSO_E_INVALID, "unknown objective");
+  if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_grad_E is defined for single-strip handles");
+  if (!h->solved) FAIL(h, SSO_E_STATE, "sso_grad_E before a successful sso_solve");
+  return grad_impl(h, obj, &Part::f, V_X, nullptr, nullptr, nullptr, dC_dE);
+}
+
+int sso_set_material(sso_handle h, const double* E) {
+  if (!h || !E) return SSO_E_INVALID;
+  if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_set_material is defined for single-strip handles");
+  Part& P = h->P0();
+  const int64_t ne = (int64_t)P.n_beams + P.n_quads;
+  std::vector<double> e((size_t)ne), g((size_t)ne);
+  CK(h, cudaMemcpy(e.data(), E, ne * sizeof(double),
+                   h->mem == SSO_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(g.data(), P.G, ne * sizeof(double), cudaMemcpyDeviceToHost));
+  std::vector<double> eold((size_t)ne);
+  CK(h, cudaMemcpy(eold.data(), P.E, ne * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int64_t k = 0; k < ne; ++k) {
+    if (!(e[k] > 0.0) || !std::isfinite(e[k])) {
+      char buf[96];
+      snprintf(buf, sizeof buf, "element %lld: E <= 0 or non-finite", (long long)k);
+      FAIL(h, SSO_E_INVALID, buf);
+    }
+    // the whole elastic tensor scales with E (SIMP): a derived G follows E, a given G scales
+    g[k] = P.g_derived[k] ? e[k] / (2.0 * (1.0 + P.h_nu[k])) : g[k] * (e[k] / eold[k]);
+  }
+  CK(h, cudaMemcpy(P.E, e.data(), ne * sizeof(double), cudaMemcpyHostToDevice));
+  CK(h, cudaMemcpy(P.G, g.data(), ne * sizeof(double), cudaMemcpyHostToDevice));
+  h->assembled = false;
+  h->solved = false;
+  return SSO_OK;
 }
 
 int sso_spmv(sso_handle h, const double* xin, double* yout) {

@@ -197,7 +197,8 @@ __global__ void __launch_bounds__(128) quad_grad_kernel(
     const double* __restrict__ gz, const int32_t* __restrict__ conn,
     const double* __restrict__ gt, const double* __restrict__ gE,
     const double* __restrict__ gnu, double drill_alpha, const double* __restrict__ u,
-    double scale, double* __restrict__ slot_partial, double* __restrict__ dC_dt, BatchStrides bs) {
+    double scale, double* __restrict__ slot_partial, double* __restrict__ dC_dt,
+    double* __restrict__ dC_dE, int n_elems, BatchStrides bs) {
   {  // design of a batch (blockIdx.y)
     const int bd = blockIdx.y;
     gx += bd * bs.node;
@@ -207,6 +208,7 @@ __global__ void __launch_bounds__(128) quad_grad_kernel(
     u += bd * bs.dof;
     slot_partial += bd * bs.slot;
     dC_dt += bd * bs.quad;
+    if (dC_dE) dC_dE += bd * (int64_t)n_elems;
   }
   const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4;
   const int p = threadIdx.x & 15;
@@ -232,12 +234,16 @@ __global__ void __launch_bounds__(128) quad_grad_kernel(
   } else {
     t.d = 1.0;
   }
-  const Dual en = quad_energy(X, t, __ldg(gE + n_beams + q), __ldg(gnu + n_beams + q), drill_alpha, ue);
+  const double Eq = __ldg(gE + n_beams + q);
+  const Dual en = quad_energy(X, t, Eq, __ldg(gnu + n_beams + q), drill_alpha, ue);
   const double g = -scale * en.d;
-  if (p < 12)
+  if (p < 12) {
     slot_partial[(2 * (int64_t)n_beams + 4 * q + p / 3) * 3 + (p % 3)] = g;
-  else
+  } else {
     dC_dt[q] = g;
+    // K_e is linear in E_e (SIMP scales the whole elastic tensor): dC/dE = -s u^T K u / E
+    if (dC_dE) dC_dE[n_beams + q] = -scale * en.v / Eq;
+  }
 }
 
 // u_e^T K_e u_e of a 3D frame element (reading C1): d_l = T u_e, energy = d_l^T k_loc d_l.
@@ -247,7 +253,8 @@ __global__ void __launch_bounds__(128) beam_grad_kernel(
     const double* __restrict__ gA, const double* __restrict__ gIy,
     const double* __restrict__ gIz, const double* __restrict__ gJ,
     const double* __restrict__ gE, const double* __restrict__ gG, const double* __restrict__ u,
-    double scale, double* __restrict__ slot_partial, BatchStrides bs) {
+    double scale, double* __restrict__ slot_partial, double* __restrict__ dC_dE, int n_elems,
+    BatchStrides bs) {
   {  // design of a batch (blockIdx.y)
     const int bd = blockIdx.y;
     gx += bd * bs.node;
@@ -255,6 +262,7 @@ __global__ void __launch_bounds__(128) beam_grad_kernel(
     gz += bd * bs.node;
     u += bd * bs.dof;
     slot_partial += bd * bs.slot;
+    if (dC_dE) dC_dE += bd * (int64_t)n_elems;
   }
   const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
   const int p = threadIdx.x & 7;
@@ -315,6 +323,7 @@ __global__ void __launch_bounds__(128) beam_grad_kernel(
   const double g = -scale * en.d;
   const int node_local = (p < 3) ? 0 : 1;
   slot_partial[(2 * e + node_local) * 3 + (p % 3)] = g;
+  if (dC_dE && p == 0) dC_dE[e] = -scale * en.v / E;
 }
 
 __global__ void __launch_bounds__(256) node_reduce_kernel(int n_nodes, const int64_t* __restrict__ inc_ptr,
@@ -343,24 +352,25 @@ __global__ void __launch_bounds__(256) node_reduce_kernel(int n_nodes, const int
 void launch_quad_grad(cudaStream_t s, int n_beams, int n_quads, const double* x, const double* y,
                       const double* z, const int32_t* conn, const double* t, const double* E,
                       const double* nu, double drill_alpha, const double* u, double scale,
-                      double* slot_partial, double* dC_dt, const BatchStrides& bs) {
+                      double* slot_partial, double* dC_dt, double* dC_dE, const BatchStrides& bs) {
   if (n_quads <= 0) return;
   const int64_t threads = 16 * (int64_t)n_quads;
   const dim3 grid((unsigned)((threads + 127) / 128), bs.B);
   quad_grad_kernel<<<grid, 128, 0, s>>>(n_beams, n_quads, x, y, z, conn, t, E, nu, drill_alpha, u,
-                                        scale, slot_partial, dC_dt, bs);
+                                        scale, slot_partial, dC_dt, dC_dE, n_beams + n_quads, bs);
   SSO_POST_LAUNCH("quad_grad_kernel");
 }
 
 void launch_beam_grad(cudaStream_t s, int n_beams, const double* x, const double* y,
                       const double* z, const int32_t* conn, const double* A, const double* Iy,
                       const double* Iz, const double* J, const double* E, const double* G,
-                      const double* u, double scale, double* slot_partial, const BatchStrides& bs) {
+                      const double* u, double scale, double* slot_partial, double* dC_dE, int n_elems,
+                      const BatchStrides& bs) {
   if (n_beams <= 0) return;
   const int64_t threads = 8 * (int64_t)n_beams;
   const dim3 grid((unsigned)((threads + 127) / 128), bs.B);
   beam_grad_kernel<<<grid, 128, 0, s>>>(n_beams, x, y, z, conn, A, Iy, Iz, J, E, G, u, scale,
-                                        slot_partial, bs);
+                                        slot_partial, dC_dE, n_elems, bs);
   SSO_POST_LAUNCH("beam_grad_kernel");
 }
 

@@ -1051,6 +1051,20 @@ void launch_cg_replace(cudaStream_t s, int ndof, const double* fbc, const double
   SSO_POST_LAUNCH("cg_replace_kernel");
 }
 
+namespace {
+__global__ void lincomb_kernel(int64_t n, double a, const double* __restrict__ x, double b,
+                               const double* __restrict__ y, double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a * x[i] + b * y[i];
+}
+}  // namespace
+
+void launch_lincomb(cudaStream_t s, int64_t n, double a, const double* x, double b, const double* y, double* out) {
+  if (n <= 0) return;
+  lincomb_kernel<<<vec_grid(n), 256, 0, s>>>(n, a, x, b, y, out);
+  SSO_POST_LAUNCH("lincomb_kernel");
+}
+
 void launch_cg_scalar(cudaStream_t s, CgState* st, int phase) {
   cg_scalar_kernel<<<1, 32, 0, s>>>(st, phase);
   SSO_POST_LAUNCH("cg_scalar_kernel");

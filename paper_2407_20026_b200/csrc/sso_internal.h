@@ -203,6 +203,8 @@ void launch_cg_replace(cudaStream_t s, int ndof, const double* fbc, const double
 void launch_cg_scalar(cudaStream_t s, CgState* st, int phase);
 void launch_pack(cudaStream_t s, int count, const int32_t* idx, const double* vec, double* buf);
 void launch_allreduce_parts(cudaStream_t s, CgState* const* sts, int n_parts, int nvals);
+// out = a x + b y (elementwise, n doubles)
+void launch_lincomb(cudaStream_t s, int64_t n, double a, const double* x, double b, const double* y, double* out);
 void launch_gather(cudaStream_t s, int n, const int32_t* idx, const double* src, double* dst);
 void launch_scatter(cudaStream_t s, int n, const int32_t* idx, const double* src, double* dst);
 void launch_dot_local(cudaStream_t s, int n, const double* a, const double* b, double* partial,
@@ -214,12 +216,12 @@ void launch_beam_grad(cudaStream_t s, int n_beams, const double* x, const double
                       const double* z, const int32_t* conn, const double* A,
                       const double* Iy, const double* Iz, const double* J, const double* E,
                       const double* G, const double* u, double scale, double* slot_partial,
-    const BatchStrides& bs = BatchStrides());
+                      double* dC_dE, int n_elems, const BatchStrides& bs = BatchStrides());
 void launch_quad_grad(cudaStream_t s, int n_beams, int n_quads, const double* x,
                       const double* y, const double* z, const int32_t* conn, const double* t,
                       const double* E, const double* nu, double drill_alpha, const double* u,
-                      double scale, double* slot_partial, double* dC_dt,
-    const BatchStrides& bs = BatchStrides());
+                      double scale, double* slot_partial, double* dC_dt, double* dC_dE,
+                      const BatchStrides& bs = BatchStrides());
 void launch_node_reduce(cudaStream_t s, int n_nodes, const int64_t* inc_ptr,
                         const int32_t* inc_slot, const double* slot_partial, double* dC_dxyz,
     const BatchStrides& bs = BatchStrides());

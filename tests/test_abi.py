@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "sso.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(sso_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(sso_[A-Za-z_]+)\s*\(", src)))
 
 
 def test_library_exports_every_header_symbol():

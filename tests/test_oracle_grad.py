@@ -100,3 +100,59 @@ def test_compliance_identities():
     P3["f"] = P["f"] * 2.5
     u3, _, _ = Gd.evaluate(P3)
     assert Gd.compliance(P3["f"], u3) == pytest.approx(C * 6.25, rel=1e-10)
+
+
+@pytest.mark.parametrize("make", [lambda: W.tiny_shell(2, 3), lambda: W.tiny_beam_grid(2)])
+def test_material_gradient(make):
+    """dC/dE_e (SIMP design variable, Eq. 12) against the global complex step,
+    and the degree-1 homogeneity of K in E: sum_e E_e dC/dE_e = -C."""
+    P = make()
+    u, _, _ = Gd.evaluate(P)
+    C = Gd.compliance(P["f"], u)
+    g = Gd.material_gradient(P, u, 1.0)
+    for e in (0, len(g) // 2, len(g) - 1):
+        ref = Gd.global_complex_step(P, "E", e, 1.0)
+        assert abs(g[e] - ref) <= 1e-10 * max(abs(ref), 1e-6 * np.abs(g).max())
+    assert float(np.dot(P["E"], g)) == pytest.approx(-C, rel=1e-10)
+    # SIMP chain rule vs complex step through rho (E = rho^P E0)
+    rho = np.random.default_rng(1).uniform(0.3, 1.0, len(g))
+    E0, penal = P["E"].copy(), 3.0
+    Q = dict(P, E=rho ** penal * E0)
+    uq, _, _ = Gd.evaluate(Q)
+    gq = Gd.simp_gradient(Gd.material_gradient(Q, uq), rho, E0, penal)
+    e = 1
+    rc = rho.astype(np.complex128)
+    rc[e] += 1e-30j
+    Qc = dict(P, E=rc ** penal * E0)
+    ref = float(np.imag(Gd._solve_C(Qc, A.coords(P).astype(np.complex128),
+                                    P["t"].astype(np.complex128), 1.0)) / 1e-30)
+    assert gq[e] == pytest.approx(ref, rel=1e-9)
+
+
+@pytest.mark.parametrize("make", [lambda: W.tiny_shell(2, 4), lambda: W.tiny_beam_grid(3)])
+def test_general_adjoint(make):
+    """Eq. 5-6 for a non-self-adjoint objective g = c^T u (e.g. a displacement, the
+    constraint term of PAPER.md Eq. 9): K lambda = c, dg/dp = -lambda^T (dK/dp) u, checked
+    against the complex step of the full solve."""
+    P = make()
+    u, Kb, fb = Gd.evaluate(P)
+    fixed = A.fixed_dofs(P)
+    c = np.random.default_rng(8).standard_normal(len(u))
+    c[fixed] = 0.0
+    free = np.nonzero(~fixed)[0]
+    lam = np.zeros_like(u)
+    lam[free] = np.linalg.solve(Kb[np.ix_(free, free)], c[free])
+    dX, dt, dE = Gd.adjoint_general(P, u, lam)
+    nn = len(P["x"])
+    for (n, axis) in [(nn // 2, 2), (1, 0), (nn - 2, 1)]:
+        ref = Gd.global_complex_step_linear(P, c, "xyz", (n, axis))
+        assert abs(dX[axis, n] - ref) <= 1e-9 * max(abs(ref), 1e-6 * np.abs(dX).max())
+    if len(dt):
+        ref = Gd.global_complex_step_linear(P, c, "t", 1)
+        assert abs(dt[1] - ref) <= 1e-9 * max(abs(ref), 1e-6 * np.abs(dt).max())
+    ref = Gd.global_complex_step_linear(P, c, "E", 2)
+    assert abs(dE[2] - ref) <= 1e-9 * max(abs(ref), 1e-6 * np.abs(dE).max())
+    # self-adjoint special case: c = f gives lambda = u and the compliance gradient
+    dXc, dtc, _ = Gd.adjoint_general(P, u, u)
+    gX, gT = Gd.adjoint_gradient(P, u, 1.0)
+    assert np.allclose(dXc, gX, rtol=1e-12, atol=1e-12 * np.abs(gX).max())
