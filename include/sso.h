@@ -215,6 +215,19 @@ int sso_grad_E(sso_handle h, sso_objective obj, double* dC_dE);
  * Single-strip handles.  Errors: SSO_E_INVALID (E <= 0). */
 int sso_set_material(sso_handle h, const double* E);
 
+/* Hat filter of sensitivities ("a standard hat filter with a
+ * radius of r"; reading c16 in DESIGN.md):
+ *     out_i = sum_j w_ij in_j / sum_j w_ij,   w_ij = max(0, radius - |X_i - X_j|),
+ * X = the current node coordinates (on_elements = 0; n = n_nodes) or the element
+ * centroids, beams then quads, each the mean of its nodes (on_elements != 0;
+ * n = n_beams + n_quads).  in, out: [ncomp][n] fp64, ncomp in 1..3 (e.g. the three rows of
+ * dC/dxyz), pointer kind per mem; out may not alias in.  The neighbour cell grid is
+ * cached per (kind, radius) and rebuilt after sso_set_design changes coordinates.
+ * Single-strip, batch-1 handles.  Errors: SSO_E_INVALID (radius <= 0 or non-finite,
+ * ncomp out of range, NULL pointers, partitioned / batched handle). */
+int sso_hat_filter(sso_handle h, int32_t on_elements, double radius, int32_t ncomp, const double* in,
+                   double* out);
+
 /* y = K_bc x with the assembled matrix (x, y [6 n_nodes]; pointer kind per mem). */
 int sso_spmv(sso_handle h, const double* x, double* y);
 

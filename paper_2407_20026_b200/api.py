@@ -91,6 +91,7 @@ _sig = {
     "sso_adjoint_solve": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.POINTER(sso_solve_info)]),
     "sso_grad_adjoint": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sso_set_material": (C.c_int, [_H, C.c_void_p]),
+    "sso_hat_filter": (C.c_int, [_H, C.c_int32, C.c_double, C.c_int32, C.c_void_p, C.c_void_p]),
     "sso_sizes": (C.c_int, [_H, _lp, _lp, _lp]),
     "sso_export_csr": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sso_export_scatter": (C.c_int, [_H, C.c_void_p]),
@@ -343,6 +344,22 @@ class Model:
         if not dev:
             E = _np(E, np.float64)
         self._check(_lib.sso_set_material(self.h, _ptr(E, np.float64)))
+
+    def hat_filter(self, values, radius, on_elements=False):
+        """Hat filter of sensitivities (include/sso.h sso_hat_filter): values [n] or
+        [ncomp<=3, n] over nodes (n_nodes) or element centroids (n_beams + n_quads)."""
+        dev = self._mode(values)
+        if dev:
+            import torch
+            v = values.contiguous()
+            out = torch.empty_like(v)
+        else:
+            v = _np(values, np.float64)
+            out = np.empty_like(v)
+        ncomp = 1 if v.ndim == 1 else int(v.shape[0])
+        self._check(_lib.sso_hat_filter(self.h, 1 if on_elements else 0, float(radius), ncomp,
+                                        _ptr(v, np.float64), _ptr(out, np.float64)))
+        return out
 
     def spmv(self, x):
         dev = self._mode(x)

@@ -174,6 +174,18 @@ struct sso_ctx {
   std::vector<cudaEvent_t> chunk_ev[2];
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_done[2] = {nullptr, nullptr};
 
+  // hat filter neighbour grids (sso_hat_filter), one per point kind, rebuilt when the
+  // radius or the geometry changes
+  struct FilterGrid {
+    bool valid = false;
+    double radius = 0.0;
+    int32_t n = 0;
+    int gx = 1, gy = 1, gz = 1;
+    double *px = nullptr, *py = nullptr, *pz = nullptr, *io = nullptr;  // io: [2][3][n] host-mem staging
+    int32_t *cell_of = nullptr, *perm = nullptr;
+    int64_t* cell_start = nullptr;
+  } fgrid[2];
+
   Timers tm;
   long long launches = 0;
   std::string err;
@@ -542,7 +554,15 @@ void free_part(Part& P) {
     if (p) cudaFree(p);
 }
 
+void free_filter_grid(sso_ctx::FilterGrid& g) {
+  void* ptrs[] = {g.px, g.py, g.pz, g.io, g.cell_of, g.perm, g.cell_start};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  g = sso_ctx::FilterGrid();
+}
+
 void free_all(sso_ctx* h) {
+  for (auto& g : h->fgrid) free_filter_grid(g);
   for (auto& pp : h->parts) free_part(*pp);
   h->parts.clear();
   if (h->d_sts) cudaFree(h->d_sts);
@@ -1014,6 +1034,8 @@ int sso_set_design(sso_handle h, const double* x, const double* y, const double*
   if (y && (rc = design_in(h, y, h->g_nodes, &Part::y, false))) return rc;
   if (z && (rc = design_in(h, z, h->g_nodes, &Part::z, false))) return rc;
   if (t && (rc = design_in(h, t, h->g_quads, &Part::t, true))) return rc;
+  if (x || y || z)
+    for (auto& g : h->fgrid) g.valid = false;
   h->assembled = false;
   h->solved = false;
   return sync(h);
@@ -1457,6 +1479,124 @@ int sso_set_material(sso_handle h, const double* E) {
   h->assembled = false;
   h->solved = false;
   return SSO_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Hat filter (filter.cu).  The cell grid is built here on the host from the current
+// design-0 coordinates: cubic cells of edge >= radius, so every point within the
+// radius lies in the 27 cells around a point's own cell.
+int build_filter_grid(sso_ctx* h, int on_elements, double radius) {
+  sso_ctx::FilterGrid& g = h->fgrid[on_elements ? 1 : 0];
+  if (g.valid && g.radius == radius) return SSO_OK;
+  free_filter_grid(g);
+  Part& P = h->P0();
+  const int64_t nn = P.n_nodes;
+  std::vector<double> X(nn), Y(nn), Z(nn);
+  CK(h, cudaMemcpyAsync(X.data(), P.x, nn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaMemcpyAsync(Y.data(), P.y, nn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaMemcpyAsync(Z.data(), P.z, nn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  std::vector<double> px, py, pz;
+  if (!on_elements) {
+    px = X, py = Y, pz = Z;
+  } else {  // element centroids, beams then quads (mean of the element's nodes)
+    auto add = [&](const std::vector<int32_t>& conn, int k) {
+      for (size_t e = 0; e < conn.size() / k; ++e) {
+        double a = 0, b = 0, c = 0;
+        for (int j = 0; j < k; ++j) {
+          const int32_t n = conn[e * k + j];
+          a += X[n], b += Y[n], c += Z[n];
+        }
+        px.push_back(a / k), py.push_back(b / k), pz.push_back(c / k);
+      }
+    };
+    add(P.lm.beam_conn, 2);
+    add(P.lm.quad_conn, 4);
+  }
+  const int64_t n = (int64_t)px.size();
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = 0; i < n; ++i) {
+    const double v[3] = {px[i], py[i], pz[i]};
+    for (int a = 0; a < 3; ++a) lo[a] = std::min(lo[a], v[a]), hi[a] = std::max(hi[a], v[a]);
+  }
+  double cell = radius;
+  int64_t dims[3];
+  const int64_t max_cells = std::max<int64_t>(8 * n, 1 << 16);
+  for (;;) {
+    for (int a = 0; a < 3; ++a) dims[a] = (n ? (int64_t)std::floor((hi[a] - lo[a]) / cell) : 0) + 1;
+    if (dims[0] * dims[1] * dims[2] <= max_cells) break;
+    cell *= 1.5;  // larger cells stay correct (edge >= radius), only less selective
+  }
+  const int64_t ncell = dims[0] * dims[1] * dims[2];
+  std::vector<int32_t> cid(n), cell_of(2 * n), perm(n);
+  std::vector<int64_t> start(ncell + 1, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t c3[3];
+    const double v[3] = {px[i], py[i], pz[i]};
+    for (int a = 0; a < 3; ++a)
+      c3[a] = std::min<int64_t>(dims[a] - 1, (int64_t)std::floor((v[a] - lo[a]) / cell));
+    cid[i] = (int32_t)((c3[2] * dims[1] + c3[1]) * dims[0] + c3[0]);
+    ++start[cid[i] + 1];
+  }
+  for (int64_t c = 0; c < ncell; ++c) start[c + 1] += start[c];
+  std::vector<int64_t> fill(start.begin(), start.end() - 1);
+  std::vector<double> sx(n), sy(n), sz(n);
+  for (int64_t i = 0; i < n; ++i) {  // stable: ascending original index within a cell
+    const int64_t k = fill[cid[i]]++;
+    perm[k] = (int32_t)i;
+    cell_of[i] = (int32_t)k;
+    cell_of[n + i] = cid[i];
+    sx[k] = px[i], sy[k] = py[i], sz[k] = pz[i];
+  }
+  int rc;
+  if ((rc = upload(h, &g.px, sx.data(), n)) || (rc = upload(h, &g.py, sy.data(), n)) ||
+      (rc = upload(h, &g.pz, sz.data(), n)) || (rc = upload(h, &g.cell_of, cell_of.data(), 2 * n)) ||
+      (rc = upload(h, &g.perm, perm.data(), n)) || (rc = upload(h, &g.cell_start, start.data(), ncell + 1)) ||
+      (rc = dalloc(h, &g.io, 6 * n))) {
+    free_filter_grid(g);
+    return rc;
+  }
+  g.n = (int32_t)n;
+  g.gx = (int)dims[0], g.gy = (int)dims[1], g.gz = (int)dims[2];
+  g.radius = radius;
+  g.valid = true;
+  return SSO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sso_hat_filter(sso_handle h, int32_t on_elements, double radius, int32_t ncomp, const double* in,
+                   double* out) {
+  if (!h || !in || !out) return SSO_E_INVALID;
+  if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_hat_filter is defined for single-strip handles");
+  if (h->batch != 1) FAIL(h, SSO_E_INVALID, "sso_hat_filter is defined for batch 1 handles");
+  if (!(radius > 0.0) || !std::isfinite(radius)) FAIL(h, SSO_E_INVALID, "radius must be positive and finite");
+  if (ncomp < 1 || ncomp > 3) FAIL(h, SSO_E_INVALID, "ncomp must be 1, 2 or 3");
+  int rc = build_filter_grid(h, on_elements != 0, radius);
+  if (rc) return rc;
+  sso_ctx::FilterGrid& g = h->fgrid[on_elements ? 1 : 0];
+  const int64_t n = g.n;
+  if (n == 0) return SSO_OK;
+  const double* din = in;
+  double* dout = out;
+  if (h->mem == SSO_MEM_HOST) {
+    CK(h, cudaMemcpyAsync(g.io, in, ncomp * n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    din = g.io;
+    dout = g.io + 3 * n;
+  }
+  const long long g0 = g_launches;
+  launch_hat_filter(h->stream, (int)n, ncomp, g.px, g.py, g.pz, g.cell_of, g.perm, g.cell_start, g.gx, g.gy,
+                    g.gz, radius, din, dout);
+  CKL(h);
+  h->launches += g_launches - g0;
+  if (h->mem == SSO_MEM_HOST)
+    CK(h, cudaMemcpyAsync(out, dout, ncomp * n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  return sync(h);
 }
 
 int sso_spmv(sso_handle h, const double* xin, double* yout) {

@@ -211,6 +211,13 @@ void launch_dot_local(cudaStream_t s, int n, const double* a, const double* b, d
                       CgState* st,
     const BatchStrides& bs = BatchStrides());
 
+// Hat filter (filter.cu): points sorted by cell (px, py, pz, perm: sorted -> original),
+// cell_of [2n]: sorted position of point i, then its cell id; cell_start [cells + 1].
+void launch_hat_filter(cudaStream_t s, int n, int ncomp, const double* px, const double* py,
+                       const double* pz, const int32_t* cell_of, const int32_t* perm,
+                       const int64_t* cell_start, int gx, int gy, int gz, double radius,
+                       const double* in, double* out);
+
 // Gradient kernels
 void launch_beam_grad(cudaStream_t s, int n_beams, const double* x, const double* y,
                       const double* z, const int32_t* conn, const double* A,
