@@ -19,6 +19,8 @@ Modules (each function cites the passage it follows):
     assembly  DOK assembly, CSR pattern, scatter map, supports
     solve     dense Cholesky, Lagrange-multiplier LU, Jacobi-PCG
     grad      compliance and adjoint gradient
+    filter    hat filter of sensitivities (reading c16)
+    loads     design-dependent area loads, 2 u^T df/dp term (reading c17)
 
 Pins (tests/test_oracle_*.py, run with -m "not gpu") tie every function to
 something other than itself: closed-form cantilever results, the Navier plate
@@ -27,4 +29,4 @@ Lagrange-vs-elimination equivalence, global complex-step and central finite
 differences, homogeneity identities and the paper's barrel-arch numbers.
 Functions without such a pin say "parity unpinned" in their docstring.
 """
-from . import beam, shell, assembly, solve, grad  # noqa: F401
+from . import beam, shell, assembly, solve, grad, filter, loads  # noqa: F401
