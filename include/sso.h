@@ -215,6 +215,22 @@ int sso_grad_E(sso_handle h, sso_objective obj, double* dC_dE);
  * Single-strip handles.  Errors: SSO_E_INVALID (E <= 0). */
 int sso_set_material(sso_handle h, const double* E);
 
+/* Design-dependent area loads (Eq. 6 with
+ * df/dp != 0; reading c17 in DESIGN.md).  Every quad e carries the load per unit area
+ * (q[e] + w[e] t_e) in the direction dir[3], lumped equally to its 4 nodes with
+ * A_e = 1/2 |(X3 - X1) x (X4 - X2)| at the CURRENT design:
+ *     f_n[0:3] += dir (q[e] + w[e] t_e) A_e / 4.
+ * q: pressure-like load per unit area, w: unit weight (rho g; w t is self-weight); both
+ * [n_quads] global, pointer kind per mem (either may be NULL = zeros; both NULL switches
+ * the area load off); dir: HOST pointer, 3 doubles, not normalised.  While active:
+ *   - sso_solve adds the area load to f (f may then be NULL = no nodal loads);
+ *   - sso_grad / sso_grad_at return dC/dp = s (2 u^T df/dp - u^T dK/dp u) (sso_grad_at
+ *     expects the f it is given to include the area load);
+ *   - sso_grad_adjoint returns -lambda^T (dK/dp u - df/dp);
+ *   - sso_adjoint_solve solves with dg/du alone.
+ * Beams carry no area load.  Errors: SSO_E_INVALID (non-finite values, dir NULL). */
+int sso_set_area_load(sso_handle h, const double* q, const double* w, const double* dir);
+
 /* Hat filter of sensitivities ("a standard hat filter with a
  * radius of r"; reading c16 in DESIGN.md):
  *     out_i = sum_j w_ij in_j / sum_j w_ij,   w_ij = max(0, radius - |X_i - X_j|),

@@ -91,6 +91,7 @@ _sig = {
     "sso_adjoint_solve": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.POINTER(sso_solve_info)]),
     "sso_grad_adjoint": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sso_set_material": (C.c_int, [_H, C.c_void_p]),
+    "sso_set_area_load": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sso_hat_filter": (C.c_int, [_H, C.c_int32, C.c_double, C.c_int32, C.c_void_p, C.c_void_p]),
     "sso_sizes": (C.c_int, [_H, _lp, _lp, _lp]),
     "sso_export_csr": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -344,6 +345,17 @@ class Model:
         if not dev:
             E = _np(E, np.float64)
         self._check(_lib.sso_set_material(self.h, _ptr(E, np.float64)))
+
+    def set_area_load(self, q=None, w=None, direction=(0.0, 0.0, -1.0)):
+        """Design-dependent area load (include/sso.h sso_set_area_load): per-quad load per
+        unit area q and unit weight w (self-weight w t) along `direction`; q = w = None
+        switches it off."""
+        dev = self._mode(q, w)
+        if not dev:
+            q, w = _np(q, np.float64), _np(w, np.float64)
+        d = np.ascontiguousarray(direction, dtype=np.float64)
+        assert d.shape == (3,)
+        self._check(_lib.sso_set_area_load(self.h, _ptr(q, np.float64), _ptr(w, np.float64), d.ctypes.data))
 
     def hat_filter(self, values, radius, on_elements=False):
         """Hat filter of sensitivities (include/sso.h sso_hat_filter): values [n] or

@@ -116,6 +116,9 @@ struct Part {
   // general-objective adjoint (sso_adjoint_solve / sso_grad_adjoint): primal backups,
   // lambda and the second polarization pass (allocated on first use)
   double *ub = nullptr, *fb = nullptr, *lam = nullptr, *dxyz2 = nullptr, *dt2 = nullptr, *dE2 = nullptr;
+  // design-dependent area loads (sso_set_area_load): local per-quad q, w and the
+  // per-quad lumped value a = (q + w t) A / 4 [B][n_quads]
+  double *ld_q = nullptr, *ld_w = nullptr, *ld_a = nullptr;
   std::vector<double> h_nu;             // host copies for sso_set_material
   std::vector<char> g_derived;          // G = E / (2 (1 + nu)) when G was not given
   // partition maps
@@ -151,6 +154,9 @@ struct sso_ctx {
   int reliable = 1;  // 0 plain CG, 1 final true-residual restart, 2 + periodic replacement
   int assembly = 0;  // 0 auto (fused when the mesh allows), 1 staged
   int storage = 0;   // 0 / 1 full CSR storage, 2 symmetric upper blocks (single-strip handles)
+  bool area_load = false;  // design-dependent area loads active (sso_set_area_load)
+  bool skip_load = false;  // adjoint solves: the right-hand side is dg/du only
+  double ld_dir[3] = {0.0, 0.0, 0.0};
 
   // global problem sizes and what this handle's user buffers cover
   int32_t g_nodes = 0, g_beams = 0, g_quads = 0;
@@ -549,7 +555,7 @@ void free_part(Part& P) {
                   P.gf, P.partial, P.st, P.flags, P.tickets, P.scal, P.slot_partial, P.dxyz, P.dt,
                   P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
                   P.lptr, P.lslot, P.tbuf, P.dE,
-                  P.ub, P.fb, P.lam, P.dxyz2, P.dt2, P.dE2};
+                  P.ub, P.fb, P.lam, P.dxyz2, P.dt2, P.dE2, P.ld_q, P.ld_w, P.ld_a};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -1177,14 +1183,29 @@ static int solve_chunks(sso_ctx* h) {
 }
 
 int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
-  if (!h || !f || !u) {
+  const bool add_load = h && h->area_load && !h->skip_load;
+  if (!h || (!f && !add_load) || !u) {
     if (h) h->err = "null argument";
     return SSO_E_INVALID;
   }
   if (!h->assembled) FAIL(h, SSO_E_STATE, "sso_solve before sso_assemble");
   int rc;
   const bool dist = h->distributed();
-  if ((rc = vec_in(h, f, &Part::f))) return rc;
+  if (f) {
+    if ((rc = vec_in(h, f, &Part::f))) return rc;
+  } else {
+    for (auto& pp : h->parts)
+      CK(h, cudaMemsetAsync(pp->f, 0, (size_t)pp->B * pp->ndof * sizeof(double), h->stream));
+  }
+  if (add_load) {
+    for (auto& pp : h->parts) {
+      Part& P = *pp;
+      Scope sc(h, F_REDUCE);
+      launch_area_load(h->stream, P.n_own, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.ld_q, P.ld_w,
+                       h->ld_dir, P.inc_ptr, P.inc_slot, P.ld_a, P.f, P.bs);
+    }
+    CKL(h);
+  }
   const int warm = h->warm_start ? 1 : 0;
   if (warm) {
     if ((rc = vec_in(h, u, &Part::xs))) return rc;
@@ -1292,6 +1313,10 @@ static int grad_impl(sso_ctx* h, sso_objective obj, double* Part::*fv, int uvec,
                        U, s, P.slot_partial, dE, P.n_beams + P.n_quads, P.bs);
       launch_quad_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.E, P.nu,
                        h->drill_alpha, U, s, P.slot_partial, P.dt, dE, P.bs);
+      // design-dependent load: dC/dp += 2 s u^T df/dp (reading c17)
+      if (h->area_load)
+        launch_area_load_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.ld_q, P.ld_w,
+                              h->ld_dir, U, 2.0 * s, P.slot_partial, P.dt, P.bs);
     }
     {
       Scope sc(h, F_REDUCE);
@@ -1373,6 +1398,10 @@ static int grad_pass(sso_ctx* h, Part& P, const double* U, double s) {
                    P.slot_partial, P.dE, P.n_beams + P.n_quads, P.bs);
   launch_quad_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.E, P.nu, h->drill_alpha,
                    U, s, P.slot_partial, P.dt, P.dE, P.bs);
+  // + lambda^T df/dp through the same polarization: (1/c)[T(u + c l) - T(u - c l)] = 2 T(l), T = 1/2 v^T df/dp
+  if (h->area_load)
+    launch_area_load_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.ld_q, P.ld_w,
+                          h->ld_dir, U, 0.5, P.slot_partial, P.dt, P.bs);
   launch_node_reduce(h->stream, P.n_own, P.inc_ptr, P.inc_slot, P.slot_partial, P.dxyz, P.bs);
   CKL(h);
   return SSO_OK;
@@ -1390,7 +1419,9 @@ int sso_adjoint_solve(sso_handle h, const double* dg_du, double* lambda, sso_sol
   // keep the primal (u, f): the adjoint reuses the CG buffers
   CK(h, cudaMemcpyAsync(P.ub, P.xs, P.ndof * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   CK(h, cudaMemcpyAsync(P.fb, P.f, P.ndof * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  h->skip_load = true;
   const int rc = sso_solve(h, dg_du, lambda, info);  // K symmetric: K^T lambda = K lambda
+  h->skip_load = false;
   CK(h, cudaMemcpyAsync(P.xs, P.ub, P.ndof * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   CK(h, cudaMemcpyAsync(P.f, P.fb, P.ndof * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   int rs = sync(h);
@@ -1452,6 +1483,46 @@ int sso_grad_E(sso_handle h, sso_objective obj, double* dC_dE) {
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_grad_E is defined for single-strip handles");
   if (!h->solved) FAIL(h, SSO_E_STATE, "sso_grad_E before a successful sso_solve");
   return grad_impl(h, obj, &Part::f, V_X, nullptr, nullptr, nullptr, dC_dE);
+}
+
+int sso_set_area_load(sso_handle h, const double* q, const double* w, const double* dir) {
+  if (!h) return SSO_E_INVALID;
+  if (!q && !w) {
+    h->area_load = false;
+    h->solved = false;
+    return SSO_OK;
+  }
+  if (!dir) FAIL(h, SSO_E_INVALID, "sso_set_area_load: dir is NULL");
+  for (int a = 0; a < 3; ++a)
+    if (!std::isfinite(dir[a])) FAIL(h, SSO_E_INVALID, "sso_set_area_load: non-finite direction");
+  const int64_t nq = h->g_quads;
+  std::vector<double> hq(nq, 0.0), hw(nq, 0.0);
+  const cudaMemcpyKind kh = h->mem == SSO_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost;
+  if (nq > 0 && q) CK(h, cudaMemcpy(hq.data(), q, nq * sizeof(double), kh));
+  if (nq > 0 && w) CK(h, cudaMemcpy(hw.data(), w, nq * sizeof(double), kh));
+  for (int64_t e = 0; e < nq; ++e)
+    if (!std::isfinite(hq[e]) || !std::isfinite(hw[e])) FAIL(h, SSO_E_INVALID, "sso_set_area_load: non-finite load");
+  int r;
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    const int64_t nl = std::max<int64_t>(P.n_quads, 1);
+    if (!P.ld_q && (r = dalloc(h, &P.ld_q, nl))) return r;
+    if (!P.ld_w && (r = dalloc(h, &P.ld_w, nl))) return r;
+    if (!P.ld_a && (r = dalloc(h, &P.ld_a, (int64_t)P.B * nl))) return r;
+    std::vector<double> lq(P.n_quads), lw(P.n_quads);
+    for (int32_t k = 0; k < P.n_quads; ++k) {
+      const int32_t g = P.lm.quad_gid.empty() ? k : P.lm.quad_gid[k];
+      lq[k] = hq[g], lw[k] = hw[g];
+    }
+    if (P.n_quads > 0) {
+      CK(h, cudaMemcpy(P.ld_q, lq.data(), P.n_quads * sizeof(double), cudaMemcpyHostToDevice));
+      CK(h, cudaMemcpy(P.ld_w, lw.data(), P.n_quads * sizeof(double), cudaMemcpyHostToDevice));
+    }
+  }
+  for (int a = 0; a < 3; ++a) h->ld_dir[a] = dir[a];
+  h->area_load = true;
+  h->solved = false;
+  return SSO_OK;
 }
 
 int sso_set_material(sso_handle h, const double* E) {

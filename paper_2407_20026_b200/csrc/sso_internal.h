@@ -218,6 +218,17 @@ void launch_hat_filter(cudaStream_t s, int n, int ncomp, const double* px, const
                        const int64_t* cell_start, int gx, int gy, int gz, double radius,
                        const double* in, double* out);
 
+// Design-dependent area loads (loads.cu): f += d (q + w t) A / 4 at the owned nodes; and
+// slot_partial / dt += coef * v^T df/dp.
+void launch_area_load(cudaStream_t s, int n_own, int n_beams, int n_quads, const double* x, const double* y,
+                      const double* z, const int32_t* conn, const double* t, const double* lq, const double* lw,
+                      const double dir[3], const int64_t* inc_ptr, const int32_t* inc_slot, double* a, double* f,
+                      const BatchStrides& bs);
+void launch_area_load_grad(cudaStream_t s, int n_beams, int n_quads, const double* x, const double* y,
+                           const double* z, const int32_t* conn, const double* t, const double* lq,
+                           const double* lw, const double dir[3], const double* v, double coef,
+                           double* slot_partial, double* dt, const BatchStrides& bs);
+
 // Gradient kernels
 void launch_beam_grad(cudaStream_t s, int n_beams, const double* x, const double* y,
                       const double* z, const int32_t* conn, const double* A,
