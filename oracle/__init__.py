@@ -21,6 +21,7 @@ Modules (each function cites the passage it follows):
     grad      compliance and adjoint gradient
     filter    hat filter of sensitivities (reading c16)
     loads     design-dependent area loads, 2 u^T df/dp term (reading c17)
+    prescribed  non-zero support displacements V u = b via the Lagrange system (reading c18)
 
 Pins (tests/test_oracle_*.py, run with -m "not gpu") tie every function to
 something other than itself: closed-form cantilever results, the Navier plate
@@ -29,4 +30,4 @@ Lagrange-vs-elimination equivalence, global complex-step and central finite
 differences, homogeneity identities and the paper's barrel-arch numbers.
 Functions without such a pin say "parity unpinned" in their docstring.
 """
-from . import beam, shell, assembly, solve, grad, filter, loads  # noqa: F401
+from . import beam, shell, assembly, solve, grad, filter, loads, prescribed  # noqa: F401
