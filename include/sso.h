@@ -215,6 +215,18 @@ int sso_grad_E(sso_handle h, sso_objective obj, double* dC_dE);
  * Single-strip handles.  Errors: SSO_E_INVALID (E <= 0). */
 int sso_set_material(sso_handle h, const double* E);
 
+/* Prescribed support displacements (Eqs. 2-3
+ * V u = b with b != 0; reading c18 in DESIGN.md).  b: [6 n_nodes] fp64, pointer kind per
+ * mem; only the entries of constrained DOFs are used (the rest ignored); NULL switches
+ * them off.  Solved by lifting: K_ff u_f = f_f - K_fc b, u_c = b (K_fc b from one extra
+ * unconstrained assembly + SpMV inside the next sso_assemble, which this call requires).
+ * While active, sso_grad / sso_grad_E return the compliance gradient C = s f^T u,
+ * dC/dp = -lambda^T dK/dp u + (lambda + s u)^T df/dp with lambda = s u_hom (the same loads
+ * with b = 0: one more PCG solve inside sso_grad); sso_grad_at is refused.
+ * Single-strip, batch-1 handles.  Errors: SSO_E_INVALID (non-finite b, partitioned or
+ * batched handle). */
+int sso_set_prescribed(sso_handle h, const double* b);
+
 /* Design-dependent area loads (Eq. 6 with
  * df/dp != 0; reading c17 in DESIGN.md).  Every quad e carries the load per unit area
  * (q[e] + w[e] t_e) in the direction dir[3], lumped equally to its 4 nodes with

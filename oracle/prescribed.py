@@ -58,8 +58,21 @@ def gradient(P, u, s=1.0):
     return dX, dt, dE
 
 
-def global_complex_step(P, b_full, kind, index, s=1.0):
-    """dC/dp by complex step of the augmented solve (b and f fixed)."""
+def gradient_with_loads(P, u, q, w, d, s=1.0):
+    """With design-dependent area loads as well (oracle/loads.py, reading c17), f the total
+    load: dC/dp = -lambda^T dK/dp u + (lambda + s u)^T df/dp, lambda = s u_hom(f)."""
+    from . import loads as L
+    f = P["f"] + L.area_load(P, q, w, d)
+    u_hom = solve(P, np.zeros(6 * len(P["x"])), f)
+    lam = s * u_hom
+    dX, dt, dE = Gd.adjoint_general(P, u, lam)
+    lX, lt = L.load_gradient_term(P, lam + s * u, q, w, d)
+    return dX + lX, dt + lt, dE
+
+
+def global_complex_step(P, b_full, kind, index, s=1.0, load=None):
+    """dC/dp by complex step of the augmented solve (b fixed; f fixed, or recomputed
+    from the area load model when load = (q, w, d))."""
     X = A.coords(P).astype(np.complex128)
     t = P["t"].astype(np.complex128)
     h = Gd.H_CS
@@ -67,5 +80,9 @@ def global_complex_step(P, b_full, kind, index, s=1.0):
         X[index[0], index[1]] += 1j * h
     else:
         t[index] += 1j * h
-    u = solve(P, b_full, None, X, t)
-    return float(np.imag(s * np.dot(P["f"], u)) / h)
+    f = P["f"].astype(np.complex128)
+    if load is not None:
+        from . import loads as L
+        f = f + L.area_load(P, *load, X, t)
+    u = solve(P, b_full, f, X, t)
+    return float(np.imag(s * np.dot(f, u)) / h)

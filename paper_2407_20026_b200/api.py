@@ -91,6 +91,7 @@ _sig = {
     "sso_adjoint_solve": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.POINTER(sso_solve_info)]),
     "sso_grad_adjoint": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sso_set_material": (C.c_int, [_H, C.c_void_p]),
+    "sso_set_prescribed": (C.c_int, [_H, C.c_void_p]),
     "sso_set_area_load": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sso_hat_filter": (C.c_int, [_H, C.c_int32, C.c_double, C.c_int32, C.c_void_p, C.c_void_p]),
     "sso_sizes": (C.c_int, [_H, _lp, _lp, _lp]),
@@ -345,6 +346,14 @@ class Model:
         if not dev:
             E = _np(E, np.float64)
         self._check(_lib.sso_set_material(self.h, _ptr(E, np.float64)))
+
+    def set_prescribed(self, b):
+        """Prescribed support displacements b [6 n_nodes] (constrained entries used);
+        None switches them off.  Requires a new assemble()."""
+        dev = self._mode(b)
+        if b is not None and not dev:
+            b = _np(b, np.float64)
+        self._check(_lib.sso_set_prescribed(self.h, _ptr(b, np.float64)))
 
     def set_area_load(self, q=None, w=None, direction=(0.0, 0.0, -1.0)):
         """Design-dependent area load (include/sso.h sso_set_area_load): per-quad load per

@@ -119,6 +119,10 @@ struct Part {
   // design-dependent area loads (sso_set_area_load): local per-quad q, w and the
   // per-quad lumped value a = (q + w t) A / 4 [B][n_quads]
   double *ld_q = nullptr, *ld_w = nullptr, *ld_a = nullptr;
+  // prescribed support displacements (sso_set_prescribed): b on the constrained DOFs
+  // (0 elsewhere), K_full b, the CG right-hand side f - K_full b, an all-free mask
+  double *pb = nullptr, *kb = nullptr, *feff = nullptr;
+  uint8_t* free_mask = nullptr;
   std::vector<double> h_nu;             // host copies for sso_set_material
   std::vector<char> g_derived;          // G = E / (2 (1 + nu)) when G was not given
   // partition maps
@@ -155,7 +159,8 @@ struct sso_ctx {
   int assembly = 0;  // 0 auto (fused when the mesh allows), 1 staged
   int storage = 0;   // 0 / 1 full CSR storage, 2 symmetric upper blocks (single-strip handles)
   bool area_load = false;  // design-dependent area loads active (sso_set_area_load)
-  bool skip_load = false;  // adjoint solves: the right-hand side is dg/du only
+  bool skip_load = false;  // adjoint solves: the right-hand side is dg/du only, b = 0
+  bool prescribed = false; // non-zero support displacements active (sso_set_prescribed)
   double ld_dir[3] = {0.0, 0.0, 0.0};
 
   // global problem sizes and what this handle's user buffers cover
@@ -555,7 +560,7 @@ void free_part(Part& P) {
                   P.gf, P.partial, P.st, P.flags, P.tickets, P.scal, P.slot_partial, P.dxyz, P.dt,
                   P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
                   P.lptr, P.lslot, P.tbuf, P.dE,
-                  P.ub, P.fb, P.lam, P.dxyz2, P.dt2, P.dE2, P.ld_q, P.ld_w, P.ld_a};
+                  P.ub, P.fb, P.lam, P.dxyz2, P.dt2, P.dE2, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -1047,17 +1052,15 @@ int sso_set_design(sso_handle h, const double* x, const double* y, const double*
   return sync(h);
 }
 
-int sso_assemble(sso_handle h) {
-  if (!h) return SSO_E_INVALID;
-  int rc = reset_flags(h);
-  if (rc) return rc;
+static int assemble_pass(sso_ctx* h, bool unconstrained) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
+    const uint8_t* mask = unconstrained ? P.free_mask : P.fixed_mask;
     if (P.fused) {
       Scope sc(h, F_ASSEMBLE);
       launch_quad_assemble_fused(h->stream, P.n_own, P.max_inc, P.node_ptr, P.node_col, P.inc_ptr, P.inc_slot,
                                  P.block_rank, P.x, P.y, P.z, P.quad_conn, P.t, P.E + P.n_beams,
-                                 P.nu + P.n_beams, h->drill_alpha, P.fixed_mask, P.vals, P.dinv, P.flags,
+                                 P.nu + P.n_beams, h->drill_alpha, mask, P.vals, P.dinv, P.flags,
                                  P.bs);
       continue;
     }
@@ -1072,10 +1075,28 @@ int sso_assemble(sso_handle h) {
     {
       Scope sc(h, F_ASSEMBLE);
       launch_assemble(h->stream, P.n_own, P.node_ptr, P.node_col, P.contrib_ptr, P.contrib, P.stage,
-                      P.fixed_mask, P.vals, P.dinv, P.flags, P.bs);
+                      mask, P.vals, P.dinv, P.flags, P.bs);
     }
   }
   CKL(h);
+  return SSO_OK;
+}
+
+int sso_assemble(sso_handle h) {
+  if (!h) return SSO_E_INVALID;
+  int rc = reset_flags(h);
+  if (rc) return rc;
+  if (h->prescribed) {
+    // lifting (reading c18): K_full b with the unconstrained matrix, then the real one
+    if ((rc = assemble_pass(h, true))) return rc;
+    Part& P = h->P0();
+    {
+      Scope sc(h, F_SPMV);
+      spmv_apply(h->stream, P, P.pb, P.kb, nullptr);
+    }
+    CKL(h);
+  }
+  if ((rc = assemble_pass(h, false))) return rc;
   rc = check_flags(h);
   if (rc) return rc;
   h->assembled = true;
@@ -1230,11 +1251,17 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
     CK(h, cudaMemcpyAsync(pp->st, h->h_st, pp->B * sizeof(CgState), cudaMemcpyHostToDevice, h->stream));
   // the pinned staging struct is reused below: make the uploads complete first
   if ((rc = sync(h))) return rc;
+  const bool lift = h->prescribed && !h->skip_load;
+  if (lift) {  // K_ff u_f = f_f - K_fc b (reading c18)
+    Part& P = h->P0();
+    Scope sc(h, F_UPDATE);
+    launch_lincomb(h->stream, P.ndof, 1.0, P.f, -1.0, P.kb, P.feff);
+  }
   CK(h, cudaEventRecord(h->ev_a, h->stream));
   for (auto& pp : h->parts) {
     Part& P = *pp;
     Scope sc(h, F_UPDATE);
-    launch_cg_init(h->stream, (int)P.ndof_own, P.f, P.fixed_mask, P.dinv, P.fbc, P.xs, P.r, P.p,
+    launch_cg_init(h->stream, (int)P.ndof_own, lift ? P.feff : P.f, P.fixed_mask, P.dinv, P.fbc, P.xs, P.r, P.p,
                    P.partial, P.st, warm, P.tmp, P.bs);
   }
   if (dist) {
@@ -1258,6 +1285,11 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
   if ((rc = allreduce(h, 1))) return rc;
   CK(h, cudaMemcpyAsync(h->h_st, h->P0().st, h->batch * sizeof(CgState), cudaMemcpyDeviceToHost,
                         h->stream));
+  if (lift) {  // u = u_f + b
+    Part& P = h->P0();
+    Scope sc(h, F_UPDATE);
+    launch_lincomb(h->stream, P.ndof, 1.0, P.xs, 1.0, P.pb, P.xs);
+  }
   if ((rc = vec_out(h, u, &Part::xs))) return rc;
   if ((rc = sync(h))) return rc;
   CKL(h);
@@ -1375,10 +1407,14 @@ static int grad_impl(sso_ctx* h, sso_objective obj, double* Part::*fv, int uvec,
   return SSO_OK;
 }
 
+static int grad_prescribed(sso_ctx* h, sso_objective obj, double* C, double* dC_dxyz, double* dC_dt,
+                           double* dC_dE);
+
 int sso_grad(sso_handle h, sso_objective obj, double* C, double* dC_dxyz, double* dC_dt) {
   if (!h) return SSO_E_INVALID;
   if (obj != SSO_OBJ_COMPLIANCE && obj != SSO_OBJ_STRAIN_ENERGY) FAIL(h, SSO_E_INVALID, "unknown objective");
   if (!h->solved) FAIL(h, SSO_E_STATE, "sso_grad before a successful sso_solve");
+  if (h->prescribed) return grad_prescribed(h, obj, C, dC_dxyz, dC_dt, nullptr);
   return grad_impl(h, obj, &Part::f, V_X, C, dC_dxyz, dC_dt);
 }
 
@@ -1386,6 +1422,7 @@ int sso_grad_at(sso_handle h, sso_objective obj, const double* f, const double* 
                 double* dC_dxyz, double* dC_dt) {
   if (!h || !f || !u) return SSO_E_INVALID;
   if (obj != SSO_OBJ_COMPLIANCE && obj != SSO_OBJ_STRAIN_ENERGY) FAIL(h, SSO_E_INVALID, "unknown objective");
+  if (h->prescribed) FAIL(h, SSO_E_INVALID, "sso_grad_at is not defined with prescribed displacements (use sso_grad)");
   int rc;
   if ((rc = vec_in(h, f, &Part::gf))) return rc;
   if ((rc = vec_in(h, u, &Part::gu))) return rc;
@@ -1393,7 +1430,7 @@ int sso_grad_at(sso_handle h, sso_objective obj, const double* f, const double* 
 }
 
 // Gradient kernels at state U with scale s into P.dxyz (owned nodes), P.dt, P.dE.
-static int grad_pass(sso_ctx* h, Part& P, const double* U, double s) {
+static int grad_pass(sso_ctx* h, Part& P, const double* U, double s, double u_load_coef = 0.0) {
   launch_beam_grad(h->stream, P.n_beams, P.x, P.y, P.z, P.beam_conn, P.A, P.Iy, P.Iz, P.J, P.E, P.G, U, s,
                    P.slot_partial, P.dE, P.n_beams + P.n_quads, P.bs);
   launch_quad_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.E, P.nu, h->drill_alpha,
@@ -1402,6 +1439,9 @@ static int grad_pass(sso_ctx* h, Part& P, const double* U, double s) {
   if (h->area_load)
     launch_area_load_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.ld_q, P.ld_w,
                           h->ld_dir, U, 0.5, P.slot_partial, P.dt, P.bs);
+  if (h->area_load && u_load_coef != 0.0)
+    launch_area_load_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.ld_q, P.ld_w,
+                          h->ld_dir, P.xs, u_load_coef, P.slot_partial, P.dt, P.bs);
   launch_node_reduce(h->stream, P.n_own, P.inc_ptr, P.inc_slot, P.slot_partial, P.dxyz, P.bs);
   CKL(h);
   return SSO_OK;
@@ -1430,18 +1470,15 @@ int sso_adjoint_solve(sso_handle h, const double* dg_du, double* lambda, sso_sol
   return rc;
 }
 
-int sso_grad_adjoint(sso_handle h, const double* lambda, double* dg_dxyz, double* dg_dt, double* dg_dE) {
-  if (!h || !lambda) return SSO_E_INVALID;
-  if (h->distributed() || h->batch > 1) FAIL(h, SSO_E_INVALID, "sso_grad_adjoint is defined for single-strip, single-design handles");
-  if (!h->solved) FAIL(h, SSO_E_STATE, "sso_grad_adjoint before a successful sso_solve");
+// -lambda^T (dK/dp u - df/dp) [+ s u^T df/dp when u_load_s != 0] at the primal state, lambda in
+// P.lam, into P.dxyz / P.dt / P.dE (single strip, batch 1).
+static int adjoint_grad_dev(sso_ctx* h, double u_load_s) {
   Part& P = h->P0();
   const int64_t ne = (int64_t)P.n_beams + P.n_quads;
   int r;
-  if (!P.lam && (r = dalloc(h, &P.lam, P.ndof))) return r;
   if (!P.dxyz2 && (r = dalloc(h, &P.dxyz2, 3 * (int64_t)P.n_nodes))) return r;
   if (!P.dt2 && (r = dalloc(h, &P.dt2, std::max<int32_t>(P.n_quads, 1)))) return r;
   if (!P.dE2 && (r = dalloc(h, &P.dE2, std::max<int64_t>(ne, 1)))) return r;
-  if ((r = vec_in(h, lambda, &Part::lam))) return r;
   // polarization: lambda^T K u = [(u + c l)^T K (u + c l) - (u - c l)^T K (u - c l)] / (4 c),
   // c = |u| / |lambda| balances the two states (bilinear result, quadratic kernels)
   {
@@ -1462,13 +1499,27 @@ int sso_grad_adjoint(sso_handle h, const double* lambda, double* dg_dxyz, double
     CK(h, cudaMemcpyAsync(P.dt2, P.dt, std::max<int32_t>(P.n_quads, 1) * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
     CK(h, cudaMemcpyAsync(P.dE2, P.dE, std::max<int64_t>(ne, 1) * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
     launch_lincomb(h->stream, P.ndof, 1.0, P.xs, c, P.lam, P.gu);   // u + c lambda
-    if ((r = grad_pass(h, P, P.gu, 0.25))) return r;
+    // the "+" pass also carries c * s u^T df/dp, which the 1/c below turns into s u^T df/dp
+    if ((r = grad_pass(h, P, P.gu, 0.25, c * u_load_s))) return r;
     // -(1/4)[dE(w+) - dE(w-)] / c  ==  -lambda^T (dK/dp) u
     launch_lincomb(h->stream, 3 * (int64_t)P.n_nodes, 1.0 / c, P.dxyz, -1.0 / c, P.dxyz2, P.dxyz);
     launch_lincomb(h->stream, P.n_quads, 1.0 / c, P.dt, -1.0 / c, P.dt2, P.dt);
     launch_lincomb(h->stream, ne, 1.0 / c, P.dE, -1.0 / c, P.dE2, P.dE);
   }
   CKL(h);
+  return SSO_OK;
+}
+
+int sso_grad_adjoint(sso_handle h, const double* lambda, double* dg_dxyz, double* dg_dt, double* dg_dE) {
+  if (!h || !lambda) return SSO_E_INVALID;
+  if (h->distributed() || h->batch > 1) FAIL(h, SSO_E_INVALID, "sso_grad_adjoint is defined for single-strip, single-design handles");
+  if (!h->solved) FAIL(h, SSO_E_STATE, "sso_grad_adjoint before a successful sso_solve");
+  Part& P = h->P0();
+  const int64_t ne = (int64_t)P.n_beams + P.n_quads;
+  int r;
+  if (!P.lam && (r = dalloc(h, &P.lam, P.ndof))) return r;
+  if ((r = vec_in(h, lambda, &Part::lam))) return r;
+  if ((r = adjoint_grad_dev(h, 0.0))) return r;
   if (dg_dxyz)
     CK(h, cudaMemcpyAsync(dg_dxyz, P.dxyz, 3 * (size_t)P.n_nodes * sizeof(double), kind_out(h), h->stream));
   if (dg_dt && P.n_quads)
@@ -1477,12 +1528,90 @@ int sso_grad_adjoint(sso_handle h, const double* lambda, double* dg_dxyz, double
   return sync(h);
 }
 
+// Compliance gradient with prescribed displacements (reading c18): C = s f^T u,
+// lambda = s u_hom (the same loads with b = 0, one more PCG solve),
+// dC/dp = -lambda^T dK/dp u + (lambda + s u)^T df/dp.
+static int grad_prescribed(sso_ctx* h, sso_objective obj, double* C, double* dC_dxyz, double* dC_dt,
+                           double* dC_dE) {
+  const double s = (obj == SSO_OBJ_STRAIN_ENERGY) ? 0.5 : 1.0;
+  Part& P = h->P0();
+  const int64_t ne = (int64_t)P.n_beams + P.n_quads;
+  int r;
+  if (!P.lam && (r = dalloc(h, &P.lam, P.ndof))) return r;
+  if (!P.gf && (r = dalloc(h, &P.gf, P.ndof))) return r;
+  CK(h, cudaMemcpyAsync(P.gf, P.f, P.ndof * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  // the adjoint solve through the public entry, with device pointers for the call
+  const sso_mem mem = h->mem;
+  h->mem = SSO_MEM_DEVICE;
+  r = sso_adjoint_solve(h, P.gf, P.lam, nullptr);
+  h->mem = mem;
+  if (r) return r;
+  {
+    Scope sc(h, F_UPDATE);
+    launch_lincomb(h->stream, P.ndof, s, P.lam, 0.0, P.lam, P.lam);
+  }
+  if ((r = adjoint_grad_dev(h, s))) return r;
+  {
+    Scope sc(h, F_REDUCE);
+    launch_dot_local(h->stream, (int)P.ndof, P.f, P.xs, P.partial, P.st, P.bs);
+    CK(h, cudaMemcpyAsync(&h->h_scal[2], &P.st->red[0], sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  }
+  if (dC_dxyz)
+    CK(h, cudaMemcpyAsync(dC_dxyz, P.dxyz, 3 * (size_t)P.n_nodes * sizeof(double), kind_out(h), h->stream));
+  if (dC_dt && P.n_quads)
+    CK(h, cudaMemcpyAsync(dC_dt, P.dt, (size_t)P.n_quads * sizeof(double), kind_out(h), h->stream));
+  if (dC_dE) CK(h, cudaMemcpyAsync(dC_dE, P.dE, (size_t)ne * sizeof(double), kind_out(h), h->stream));
+  if ((r = sync(h))) return r;
+  if (C) {
+    const double v = s * h->h_scal[2];
+    if (h->mem == SSO_MEM_HOST) *C = v;
+    else CK(h, cudaMemcpy(C, &v, sizeof(double), cudaMemcpyHostToDevice));
+  }
+  return SSO_OK;
+}
+
 int sso_grad_E(sso_handle h, sso_objective obj, double* dC_dE) {
   if (!h || !dC_dE) return SSO_E_INVALID;
   if (obj != SSO_OBJ_COMPLIANCE && obj != SSO_OBJ_STRAIN_ENERGY) FAIL(h, SSO_E_INVALID, "unknown objective");
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_grad_E is defined for single-strip handles");
   if (!h->solved) FAIL(h, SSO_E_STATE, "sso_grad_E before a successful sso_solve");
+  if (h->prescribed) return grad_prescribed(h, obj, nullptr, nullptr, nullptr, dC_dE);
   return grad_impl(h, obj, &Part::f, V_X, nullptr, nullptr, nullptr, dC_dE);
+}
+
+int sso_set_prescribed(sso_handle h, const double* b) {
+  if (!h) return SSO_E_INVALID;
+  if (!b) {
+    if (h->prescribed) h->assembled = false;
+    h->prescribed = false;
+    h->solved = false;
+    return SSO_OK;
+  }
+  if (h->distributed() || h->batch > 1)
+    FAIL(h, SSO_E_INVALID, "sso_set_prescribed is defined for single-strip, single-design handles");
+  Part& P = h->P0();
+  int r;
+  if (!P.pb && (r = dalloc(h, &P.pb, P.ndof))) return r;
+  if (!P.kb && (r = dalloc(h, &P.kb, P.ndof))) return r;
+  if (!P.feff && (r = dalloc(h, &P.feff, P.ndof))) return r;
+  if (!P.free_mask) {  // per-node support bitmasks, all clear
+    if ((r = dalloc(h, &P.free_mask, P.n_nodes))) return r;
+    CK(h, cudaMemsetAsync(P.free_mask, 0, P.n_nodes, h->stream));
+  }
+  std::vector<double> hb(P.ndof);
+  CK(h, cudaMemcpy(hb.data(), b, P.ndof * sizeof(double),
+                   h->mem == SSO_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost));
+  std::vector<uint8_t> mask(P.n_nodes);
+  CK(h, cudaMemcpy(mask.data(), P.fixed_mask, P.n_nodes, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < P.ndof; ++i) {
+    if (!std::isfinite(hb[i])) FAIL(h, SSO_E_INVALID, "sso_set_prescribed: non-finite value");
+    if (!((mask[i / 6] >> (i % 6)) & 1)) hb[i] = 0.0;  // only the constrained DOFs carry b
+  }
+  CK(h, cudaMemcpy(P.pb, hb.data(), P.ndof * sizeof(double), cudaMemcpyHostToDevice));
+  h->prescribed = true;
+  h->assembled = false;  // K_full b is formed by the next sso_assemble
+  h->solved = false;
+  return SSO_OK;
 }
 
 int sso_set_area_load(sso_handle h, const double* q, const double* w, const double* dir) {

@@ -56,3 +56,22 @@ def test_rigid_translation_prescribed_everywhere_is_exact():
     u = PR.solve(P, b)
     ref = b.copy()
     assert np.allclose(u, ref, rtol=0, atol=1e-14)
+
+
+def test_gradient_with_area_loads_vs_complex_step():
+    from oracle import loads as L
+    P = W.tiny_shell(3, 4)
+    rng = np.random.default_rng(5)
+    nq = len(P["quad_conn"])
+    load = (rng.uniform(1e3, 3e3, nq), rng.uniform(2e4, 3e4, nq), np.array([0.1, 0.3, -1.0]))
+    b = _b(P, 7)
+    s = 0.5
+    f = P["f"] + L.area_load(P, *load)
+    u = PR.solve(P, b, f)
+    dX, dt, _ = PR.gradient_with_loads(P, u, *load, s)
+    nn = len(P["x"])
+    for (n, a) in [(nn // 2, 2), (2, 0), (nn - 3, 1)]:
+        ref = PR.global_complex_step(P, b, "xyz", (n, a), s, load)
+        assert abs(dX[a, n] - ref) <= 1e-9 * max(abs(ref), 1e-6 * np.abs(dX).max())
+    ref = PR.global_complex_step(P, b, "t", 2, s, load)
+    assert abs(dt[2] - ref) <= 1e-9 * max(abs(ref), 1e-6 * np.abs(dt).max())
