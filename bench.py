@@ -241,7 +241,7 @@ def run_gpu(args):
                       n_parts=args.virtual_parts)
         parallelism = f"{args.virtual_parts} node strips on 1 GPU (in-process transport)"
     else:
-        m = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index)
+        m = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index, storage=args.storage)
         parallelism = "single GPU"
     t_create = time.perf_counter() - t0
     ndof, nnz, nblocks = m.sizes()
@@ -331,13 +331,16 @@ def run_gpu(args):
     # algorithmic bytes of the stored format: values + block column ids + node_ptr + x read,
     # y written; symmetric storage adds the transpose slots (written and read back once)
     spmv_bytes = 8 * stored_vals + 4 * stored_blocks + 8 * (n_nodes + 1) + 16 * ndof
-    if symmetric:
+    if symmetric == 2:
         spmv_bytes += 2 * 48 * (stored_blocks - n_nodes) + 8 * (n_nodes + 1) + 4 * (stored_blocks - n_nodes)
+    elif symmetric == 3:  # pull lists: lptr + one (source node, block) pair per pulled block
+        spmv_bytes += 8 * (n_nodes + 1) + 8 * (stored_blocks - n_nodes)
     spmv_avg_ms = spmv_ms / max(spmv_n, 1)
     achieved = spmv_bytes / (spmv_avg_ms / 1000.0) / 1e9 if spmv_n else None
     roofline = {"bound": "hbm",
-                "kernel": ("spmv_sym pass1+pass2 (upper-block K, CG q = K p, p^T q)" if symmetric
-                           else "spmv_dot (CG q = K p, p^T q)"),
+                "kernel": {0: "spmv_dot (CG q = K p, p^T q)",
+                           2: "spmv_sym pass1+pass2 (upper-block K, CG q = K p, p^T q)",
+                           3: "spmv_pull_dot (upper-block K, one-pass pull, CG q = K p, p^T q)"}[symmetric],
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(),
                 "algorithmic_bytes_per_launch": spmv_bytes, "avg_launch_ms": spmv_avg_ms,
@@ -467,6 +470,8 @@ def main():
     ap.add_argument("--cg-iters", type=int, default=None,
                     help="CG iteration count used to extrapolate the oracle (reference arm)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--storage", type=int, default=0,
+                    help="sso_options.storage for single-GPU C3b (0 = library default)")
     ap.add_argument("--workload", default="C3b", choices=["C3b", "C5"])
     ap.add_argument("--batch", type=int, default=64, help="C5 designs per GPU")
     ap.add_argument("--virtual-parts", type=int, default=1,

@@ -140,7 +140,14 @@ typedef struct {
    * upper node blocks (n, m >= n) of the symmetric K_bc (44 % fewer value bytes on
    * shell grids); pass 1 of the SpMV forms the upper row sums, the transpose
    * contributions (sender-ordered slots) and p^T K p, the x / r update adds each
-   * node's incoming slots in ascending source order.  Exports return the full CSR. */
+   * node's incoming slots in ascending source order.  3 = upper node blocks, each
+   * node's run stored column-major (every 6x6 block one contiguous 288-byte chunk),
+   * and a ONE-pass "pull" SpMV: the warp owning row node m streams its upper run and
+   * the stored blocks (n, m) of its lower neighbours n < m (an L2 hit: nodes are
+   * dealt round-robin, so the owner streams them in the same window) and forms
+   * y_m = sum_{j>=m} K_mj x_j + sum_{n<m} K_nm^T x_n; no transpose buffer.  Storage
+   * 2 and 3 apply to single-strip handles (partitioned handles keep full storage).
+   * Exports return the full CSR.  Other values -> SSO_E_INVALID. */
   int32_t storage;
 } sso_options;
 
@@ -275,7 +282,8 @@ int sso_export_ke(sso_handle h, int64_t first, int64_t count, double* ke);
 int sso_export_dinv(sso_handle h, double* dinv);
 
 /* Device storage of the assembled matrix: stored values / node blocks (owned rows) and
- * whether the upper-block symmetric layout is in use. */
+ * the layout in use: *symmetric = 0 full storage, 2 upper blocks with the two-pass
+ * transpose SpMV, 3 upper blocks (column-major runs) with the one-pass pull SpMV. */
 int sso_storage_info(sso_handle h, int64_t* stored_values, int64_t* stored_blocks, int32_t* symmetric);
 
 /* Partition of this handle: number of strips held, first owned global node, owned

@@ -245,7 +245,7 @@ class Model:
     def storage_info(self):
         v, b, s = C.c_int64(), C.c_int64(), C.c_int32()
         self._check(_lib.sso_storage_info(self.h, C.byref(v), C.byref(b), C.byref(s)))
-        return v.value, b.value, bool(s.value)
+        return v.value, b.value, s.value  # 0 full, 2 two-pass symmetric, 3 pull symmetric
 
     def set_design(self, x=None, y=None, z=None, t=None):
         dev = self._mode(x, y, z, t)

@@ -128,6 +128,10 @@ struct Part {
   // partition maps
   int32_t* block_rank = nullptr;      // quads [n_quads][16] (fused assembly; upper ranks when sym)
   bool sym = false;                   // upper-block (symmetric) storage, single-strip handles
+  bool pull = false;                  // sym with the one-pass pull SpMV (storage 3, column-major runs)
+  int32_t* lpull = nullptr;           // pull: (source node, upper block) per incoming block
+  int32_t* pdesc = nullptr;           // pull: 16-int per-node descriptors (build_pull_desc)
+  CUtensorMap pull_tmap;              // pull: [B n_ublocks][36] view of vals for the gather4 TMA
   UpperPattern up;
   int64_t* lptr = nullptr;            // sym: incoming transpose slots per node
   int32_t* lslot = nullptr;
@@ -346,7 +350,10 @@ double* vec_of(Part& P, int v) {
 // row sums and the receiver sums to cg_update (launch_cg_update_sym).  x must have
 // its halo filled (partitioned handles).
 void spmv_apply(cudaStream_t s, Part& P, const double* x, double* y, CgState* st) {
-  if (P.sym && st)
+  if (P.pull)
+    launch_spmv_pull(s, &P.pull_tmap, P.n_own, (int)(P.bs.nnz / 36), P.pdesc, P.node_col, P.lpull, P.vals, x, y,
+                     st ? P.partial : nullptr, st, P.bs);
+  else if (P.sym && st)
     launch_spmv_sym_cg(s, P.n_own, P.node_ptr, P.node_col, P.vals, x, y, P.tbuf, P.partial, st, P.bs);
   else if (P.sym)
     launch_spmv_sym(s, P.n_own, P.node_ptr, P.node_col, P.vals, x, y, P.tbuf, P.lptr, P.lslot, P.bs);
@@ -477,7 +484,7 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev) {
     if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
     spmv_apply(s, P, P.p, P.q, P.st);
     if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
-    if (P.sym)
+    if (P.sym && !P.pull)
       launch_cg_update_sym(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.tbuf, P.lptr, P.lslot, P.partial,
                            P.st, P.bs);
     else
@@ -559,7 +566,7 @@ void free_part(Part& P) {
                   P.inc_slot, P.stage, P.vals, P.dinv, P.f, P.fbc, P.xs, P.r, P.p, P.q, P.tmp, P.gu,
                   P.gf, P.partial, P.st, P.flags, P.tickets, P.scal, P.slot_partial, P.dxyz, P.dt,
                   P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
-                  P.lptr, P.lslot, P.tbuf, P.dE,
+                  P.lptr, P.lslot, P.lpull, P.pdesc, P.tbuf, P.dE,
                   P.ub, P.fb, P.lam, P.dxyz2, P.dt2, P.dE2, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -677,7 +684,12 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
     P.max_deg = std::max<int>(P.max_deg, (int)(P.pat.node_ptr[n + 1] - P.pat.node_ptr[n]));
   }
   P.fused = h->assembly == 0 && P.n_beams == 0 && P.n_quads > 0 && P.max_deg <= fused_max_degree();
-  P.sym = h->storage == 2 && L.n_parts == 1 && h->nranks == 1 && P.n_own == P.n_nodes;
+  P.sym = (h->storage == 2 || h->storage == 3) && L.n_parts == 1 && h->nranks == 1 && P.n_own == P.n_nodes;
+  P.pull = P.sym && h->storage == 3;
+  if (P.pull && P.pat.node_ptr[P.n_nodes] >= INT32_MAX / 36) {  // 32-bit block offsets in the pull kernel
+    h->err = "storage 3: too many node blocks for 32-bit offsets";
+    return SSO_E_INVALID;
+  }
   if (P.sym) build_upper(P.pat, L.beam_conn.data(), L.quad_conn.data(), P.up);
   P.stored_blocks = P.sym ? P.up.uptr[P.n_own] : P.pat.node_ptr[P.n_own];
   const int64_t ne = (int64_t)P.n_beams + P.n_quads;
@@ -687,7 +699,7 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   P.bs.quad = P.n_quads;
   P.bs.stage = 36 * P.n_staged;
   P.bs.nnz = 36 * (P.sym ? P.up.n_ublocks() : P.n_blocks);
-  P.bs.tbuf = 6 * std::max<int64_t>(P.sym ? P.up.n_tslots : 0, 1);
+  P.bs.tbuf = 6 * std::max<int64_t>(P.sym && !P.pull ? P.up.n_tslots : 0, 1);
   P.bs.dof = P.ndof;
   P.bs.partial = 16 * (int64_t)cg_grid();
   P.bs.slot = 3 * std::max<int64_t>(P.n_slots, 1);
@@ -755,8 +767,15 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
     UP(contrib_ptr, P.up.ucontrib_ptr.data(), P.up.n_ublocks() + 1);
     UP(contrib, P.up.ucontrib.data(), (int64_t)P.up.ucontrib.size());
     UP(lptr, P.up.lptr.data(), P.n_nodes + 1);
-    UP(lslot, P.up.lslot.data(), (int64_t)P.up.lslot.size());
-    AL(tbuf, B * P.bs.tbuf);
+    if (P.pull) {
+      UP(lpull, P.up.lpull.data(), (int64_t)P.up.lpull.size());
+      std::vector<int32_t> desc;
+      build_pull_desc(P.up, desc);
+      UP(pdesc, desc.data(), (int64_t)desc.size());
+    } else {
+      UP(lslot, P.up.lslot.data(), (int64_t)P.up.lslot.size());
+      AL(tbuf, B * P.bs.tbuf);
+    }
   } else {
     UP(node_ptr, P.pat.node_ptr.data(), P.n_nodes + 1);
     UP(node_col, P.pat.node_col.data(), P.n_blocks);
@@ -772,6 +791,10 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   AL(sendbuf, 6 * std::max<int64_t>(P.n_send, 1));
   AL(stage, B * P.bs.stage);
   AL(vals, B * P.bs.nnz);
+  if (P.pull && make_pull_tmap(P.vals, B * P.bs.nnz / 36, &P.pull_tmap)) {
+    h->err = "storage 3: cuTensorMapEncodeTiled failed";
+    return SSO_E_CUDA;
+  }
   AL(dinv, B * P.ndof);
   AL(f, B * P.ndof);
   AL(fbc, B * P.ndof);
@@ -809,6 +832,8 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   P.up.ucontrib.shrink_to_fit();
   P.up.lslot.clear();
   P.up.lslot.shrink_to_fit();
+  P.up.lpull.clear();
+  P.up.lpull.shrink_to_fit();
   P.pat.inc_slot.clear();
   P.pat.inc_slot.shrink_to_fit();
   return SSO_OK;
@@ -930,6 +955,10 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
     }
   if (o.batch < 1 || (o.batch > 1 && (o.n_parts > 1 || o.nranks > 1))) {
     g_create_err = "options: batch >= 1, and batch > 1 needs n_parts == nranks == 1";
+    return SSO_E_INVALID;
+  }
+  if (o.storage < 0 || o.storage > 3) {
+    g_create_err = "options: storage must be 0, 1, 2 or 3";
     return SSO_E_INVALID;
   }
   if (o.nranks > 1 && !o.nccl_unique_id) {
@@ -1061,7 +1090,7 @@ static int assemble_pass(sso_ctx* h, bool unconstrained) {
       launch_quad_assemble_fused(h->stream, P.n_own, P.max_inc, P.node_ptr, P.node_col, P.inc_ptr, P.inc_slot,
                                  P.block_rank, P.x, P.y, P.z, P.quad_conn, P.t, P.E + P.n_beams,
                                  P.nu + P.n_beams, h->drill_alpha, mask, P.vals, P.dinv, P.flags,
-                                 P.bs);
+                                 P.bs, P.pull ? 1 : 0);
       continue;
     }
     {
@@ -1075,7 +1104,7 @@ static int assemble_pass(sso_ctx* h, bool unconstrained) {
     {
       Scope sc(h, F_ASSEMBLE);
       launch_assemble(h->stream, P.n_own, P.node_ptr, P.node_col, P.contrib_ptr, P.contrib, P.stage,
-                      mask, P.vals, P.dinv, P.flags, P.bs);
+                      mask, P.vals, P.dinv, P.flags, P.bs, P.pull ? 1 : 0);
     }
   }
   CKL(h);
@@ -1832,15 +1861,16 @@ int sso_sizes(sso_handle h, int64_t* ndof, int64_t* nnz, int64_t* n_blocks) {
 int sso_storage_info(sso_handle h, int64_t* stored_values, int64_t* stored_blocks, int32_t* symmetric) {
   if (!h) return SSO_E_INVALID;
   int64_t v = 0, b = 0;
-  bool sym = true;
+  bool sym = true, pull = true;
   for (auto& pp : h->parts) {
     v += 36 * pp->stored_blocks;
     b += pp->stored_blocks;
     sym &= pp->sym;
+    pull &= pp->pull;
   }
   if (stored_values) *stored_values = v;
   if (stored_blocks) *stored_blocks = b;
-  if (symmetric) *symmetric = sym ? 1 : 0;
+  if (symmetric) *symmetric = sym ? (pull ? 3 : 2) : 0;
   return SSO_OK;
 }
 
@@ -1877,15 +1907,19 @@ int sso_export_csr(sso_handle h, int64_t* row_ptr, int32_t* col_idx, double* val
       if (!P.sym) return pv[36 * b0 + 6 * a * deg + 6 * k + b];
       const int32_t m = T.node_col[b0 + k];
       const UpperPattern& U = P.up;
+      // run position of (row a, column 6 ku + b): row-major (storage 2) or column-major (3)
+      auto at = [&](int64_t ud, int64_t ku, int ra, int cb) {
+        return P.pull ? 6 * (6 * ku + cb) + ra : 6 * ra * ud + 6 * ku + cb;
+      };
       if (m >= n) {
         const int64_t ud = U.uptr[n + 1] - U.uptr[n];
         const int64_t ku = k - (deg - ud);
-        return pv[36 * U.uptr[n] + 6 * a * ud + 6 * ku + b];
+        return pv[36 * U.uptr[n] + at(ud, ku, a, b)];
       }
       const int64_t ud = U.uptr[m + 1] - U.uptr[m];
       const int32_t* c0 = U.ucol.data() + U.uptr[m];
       const int64_t ku = std::lower_bound(c0, c0 + ud, n) - c0;
-      return pv[36 * U.uptr[m] + 6 * b * ud + 6 * ku + a];
+      return pv[36 * U.uptr[m] + at(ud, ku, b, a)];
     };
     for (int32_t n = 0; n < P.n_own; ++n) {
       const int64_t b0 = T.node_ptr[n];

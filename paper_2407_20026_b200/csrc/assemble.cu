@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(
     int n_nodes, const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ node_col,
     const int64_t* __restrict__ contrib_ptr, const int32_t* __restrict__ contrib,
     const double* __restrict__ stage, const uint8_t* __restrict__ fixed_mask,
-    double* __restrict__ vals, double* __restrict__ dinv, DevFlags* flags, BatchStrides bs) {
+    double* __restrict__ vals, double* __restrict__ dinv, DevFlags* flags, BatchStrides bs, int cm) {
   {  // design of a batch (blockIdx.y)
     const int bd = blockIdx.y;
     stage += bd * bs.stage;
@@ -44,8 +44,9 @@ __global__ void __launch_bounds__(256) assemble_kernel(
     const uint8_t mrow = fixed_mask[n];
     double* out = vals + 36 * b0;
     for (int v = lane; v < total; v += 32) {
-      const int a = v / rowlen;
-      const int rem = v - a * rowlen;
+      // storage order of the run: row-major (a, rem) or column-major (rem, a)
+      const int a = cm ? v % 6 : v / rowlen;
+      const int rem = cm ? v / 6 : v - a * rowlen;
       const int k = rem / 6;
       const int b = rem - 6 * k;
       const int64_t blk = b0 + k;
@@ -78,14 +79,14 @@ __global__ void __launch_bounds__(256) assemble_kernel(
 void launch_assemble(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
                      const int32_t* node_col, const int64_t* contrib_ptr,
                      const int32_t* contrib, const double* stage, const uint8_t* fixed_mask,
-                     double* vals, double* dinv, DevFlags* flags, const BatchStrides& bs) {
+                     double* vals, double* dinv, DevFlags* flags, const BatchStrides& bs, int cm) {
   if (n_nodes <= 0) return;
   const int warps_per_cta = 8;
   int64_t need = ((int64_t)n_nodes + warps_per_cta - 1) / warps_per_cta;
   const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)cg_grid() * 4 / bs.B)), bs.B);
   assemble_kernel<<<grid, 32 * warps_per_cta, 0, s>>>(n_nodes, node_ptr, node_col, contrib_ptr,
                                                        contrib, stage, fixed_mask, vals, dinv,
-                                                       flags, bs);
+                                                       flags, bs, cm);
   SSO_POST_LAUNCH("assemble_kernel");
 }
 

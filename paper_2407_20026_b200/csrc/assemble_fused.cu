@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(128, 4) quad_assemble_fused_kernel(
     const double* __restrict__ gz, const int32_t* __restrict__ conn, const double* __restrict__ gt,
     const double* __restrict__ gE, const double* __restrict__ gnu, double drill_alpha,
     const uint8_t* __restrict__ fixed_mask, double* __restrict__ vals, double* __restrict__ dinv,
-    DevFlags* flags, BatchStrides bs) {
+    DevFlags* flags, BatchStrides bs, int cm) {
   __shared__ double geo[NPC * 4 * GS];
   __shared__ double buf[NPC * 36 * MAXDEG];
   {  // design of a batch (blockIdx.y)
@@ -322,12 +322,13 @@ __global__ void __launch_bounds__(128, 4) quad_assemble_fused_kernel(
     const uint8_t mrow = fixed_mask[n];
     double* out = vals + 36 * b0;
     for (int v = t16; v < 36 * deg; v += 16) {
-      const int a = v / rowlen;
-      const int rem = v - a * rowlen;
+      // v walks the run in its storage order: row-major (a, rem) or column-major (rem, a)
+      const int a = cm ? v % 6 : v / rowlen;
+      const int rem = cm ? v / 6 : v - a * rowlen;
       const int kb = rem / 6;
       const int b = rem - 6 * kb;
       const int m = node_col[b0 + kb];
-      double s = nbuf[v];
+      double s = nbuf[a * rowlen + rem];
       const bool diag = (m == n) && (a == b);
       const bool rfix = (mrow >> a) & 1;
       const bool cfix = (fixed_mask[m] >> b) & 1;
@@ -356,12 +357,13 @@ void launch_quad_assemble_fused(cudaStream_t s, int n_own, int max_inc, const in
                                 const int32_t* block_rank, const double* x, const double* y,
                                 const double* z, const int32_t* conn, const double* t, const double* E,
                                 const double* nu, double drill_alpha, const uint8_t* fixed_mask,
-                                double* vals, double* dinv, DevFlags* flags, const BatchStrides& bs) {
+                                double* vals, double* dinv, DevFlags* flags, const BatchStrides& bs,
+                                int cm) {
   if (n_own <= 0) return;
   const dim3 grid((n_own + NPC - 1) / NPC, bs.B);
   quad_assemble_fused_kernel<<<grid, 128, 0, s>>>(n_own, max_inc, node_ptr, node_col, inc_ptr, inc_slot,
                                                   block_rank, x, y, z, conn, t, E, nu, drill_alpha,
-                                                  fixed_mask, vals, dinv, flags, bs);
+                                                  fixed_mask, vals, dinv, flags, bs, cm);
   SSO_POST_LAUNCH("quad_assemble_fused_kernel");
 }
 

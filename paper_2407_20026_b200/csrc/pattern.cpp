@@ -204,6 +204,17 @@ void build_upper(const HostPattern& P, const int32_t* beam_conn, const int32_t* 
       for (int64_t k = U.uptr[n] + 1; k < U.uptr[n + 1]; ++k)
         U.lslot[fill[U.ucol[k]]++] = (int32_t)(U.uptr[n] - n + (k - U.uptr[n]) - 1);
   }
+  // pull lists (storage 3): the same incoming blocks as (source node, upper block index)
+  U.lpull.resize(2 * (size_t)U.lptr[nn]);
+  {
+    std::vector<int64_t> fill(U.lptr.begin(), U.lptr.end() - 1);
+    for (int32_t n = 0; n < nn; ++n)
+      for (int64_t k = U.uptr[n] + 1; k < U.uptr[n + 1]; ++k) {
+        const int64_t at = fill[U.ucol[k]]++;
+        U.lpull[2 * at] = n;
+        U.lpull[2 * at + 1] = (int32_t)k;
+      }
+  }
 }
 
 }  // namespace sso

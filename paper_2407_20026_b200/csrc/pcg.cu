@@ -22,6 +22,9 @@
 // coalesced value streams); a 9-shuffle transposed butterfly reduces the six
 // row sums.  Column indices are read per 6x6 block (4 B / 36 values) instead
 // of per value (4 B / value): 8.1 B per non-zero instead of 12.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -646,6 +649,279 @@ __global__ void __launch_bounds__(SPMV_WARPS * 32, MINB) spmv_tma_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Symmetric "pull" SpMV (storage 3).  Only the upper node blocks (n, m >= n)
+// are stored, each node's run COLUMN-major: value (a, c) of node n's upper run
+// (row 6n + a, run column c = 6k + b of upper block k) sits at 36 uptr[n] + 6c + a,
+// so every 6x6 block is one contiguous 288-byte chunk and every column of it six
+// contiguous values.  The warp that owns row node m streams, into one ring slot,
+// its own upper run AND the upper blocks (n, m) of its lower neighbours n < m
+// (one TMA bulk copy each; their location comes from the pull list), so
+//   y_m = sum_{j >= m} K_mj x_j + sum_{n < m} K_nm^T x_n
+// is formed in one pass with no transpose buffer, no atomics and a fixed order.
+// Nodes are dealt to warps round-robin (warp w takes w, w + NW, ...): at any time
+// the GPU works on one window of ~NW consecutive nodes, so a pulled block was
+// streamed by its owner (or is about to be) within one window -- it is an L2
+// hit, and DRAM sees each stored value once (~0.56 of the full-storage bytes on
+// shell grids).  Lane <-> one column slot per pass: own column c: acc[a] +=
+// v[a] x_{m(c)}[b]; pulled column b of block j: acc[b] += sum_a v[a] x_n[a].
+// ---------------------------------------------------------------------------
+// Per-node pull descriptor (16 int32, built on the host, SSO pattern order):
+//   d[0] = first upper block of the node (its run starts at 36 d[0]),
+//   d[1] = udeg | ldeg << 8 | fits << 16,
+//   fits:  d[2 .. 2+udeg) upper block columns, then (source node, upper block) of each
+//          pulled block at d[2+udeg+2j], d[3+udeg+2j];
+//   !fits: d[2] = first pull-list entry (lptr) -- the node takes the general path.
+// A node fits the ring slot when udeg <= PULL_MAX_UDEG and ldeg <= 4.  Slot layout
+// (128-byte aligned): the pulled blocks, fetched by ONE TMA tile::gather4 of 4 rows of
+// the [blocks][36] view of the values (padding rows repeat the node's own first block),
+// then the own upper run (one bulk copy).
+constexpr int PULL_DESC = 16;
+constexpr int PULL_MAX_UDEG = 5;
+constexpr int PULL_SLOT_DOUBLES = 336;  // 4 pulled + 5 own blocks = 324 doubles, rounded to 128 B
+constexpr int PULL_OWN_OFF = 144;       // doubles: own run after the 4 gathered rows
+
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int r0, int r1, int r2, int r3,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+      "l"(policy)
+      : "memory");
+}
+
+template <bool DOT, int STAGES, int MINB>
+__global__ void __launch_bounds__(SPMV_WARPS * 32, MINB) spmv_pull_kernel(
+    const __grid_constant__ CUtensorMap tmap, int n_nodes, int rows_per_design, const int32_t* __restrict__ pdesc,
+    const int32_t* __restrict__ ucol, const int2* __restrict__ lpull, const double* __restrict__ vals,
+    const double* __restrict__ p, double* __restrict__ q, double* __restrict__ partial, CgState* st,
+    BatchStrides bs) {
+  constexpr int SLOT_DOUBLES = PULL_SLOT_DOUBLES;
+  const int row0 = blockIdx.y * rows_per_design;  // this design's first row of the gather view
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bar[SPMV_WARPS][STAGES];
+  __shared__ double2 red_all[SPMV_WARPS][32];  // per-warp row-pair partials of the current node
+  __shared__ double sm[32];
+  {  // design of a batch (blockIdx.y)
+    const int bd = blockIdx.y;
+    vals += bd * bs.nnz;
+    p += bd * bs.dof;
+    q += bd * bs.dof;
+    if (DOT) {
+      partial += bd * bs.partial;
+      st += bd;
+    }
+  }
+  if (DOT && st->done) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * SPMV_WARPS + warp;
+  const int64_t NW = (int64_t)gridDim.x * SPMV_WARPS;
+  const int cnt = gw < n_nodes ? (int)(((int64_t)n_nodes - 1 - gw) / NW + 1) : 0;
+  double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * STAGES * SLOT_DOUBLES;
+  uint64_t* wbar = bar[warp];
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(&wbar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const uint64_t pol = evict_first_policy();
+  __syncwarp();
+  // descriptor word `lane` of node k (lanes >= 16 and k >= cnt: 0)
+  auto desc = [&](int k) -> int {
+    return (k < cnt && lane < PULL_DESC) ? __ldg(pdesc + PULL_DESC * (gw + (int64_t)k * NW) + lane) : 0;
+  };
+  // warp-collective: node k's pulled blocks (one gather4) and own upper run (one bulk copy)
+  // into ring slot k % STAGES; lane 0 issues both
+  auto issue = [&](int k, int d) {
+    const int s = k % STAGES;
+    const int b0 = __shfl_sync(FULL, d, 0), fl = __shfl_sync(FULL, d, 1);
+    const int udeg = fl & 255, ldeg = (fl >> 8) & 255;
+    const bool fits = (fl >> 16) & 1;
+    int r[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int g = __shfl_sync(FULL, d, min(3 + udeg + 2 * i, PULL_DESC - 1));
+      r[i] = row0 + (i < ldeg ? g : b0);
+    }
+    double* dst = ring + (size_t)s * SLOT_DOUBLES;
+    // the slot was last read by node k - STAGES (before the previous loop-end __syncwarp)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (lane == 0) {
+      if (fits) {
+        mbar_arrive_expect_tx(&wbar[s], (unsigned)(288 * udeg + (ldeg ? 1152 : 0)));
+        if (ldeg) tma_gather4(dst, &tmap, r[0], r[1], r[2], r[3], &wbar[s], pol);
+        bulk_g2s(dst + PULL_OWN_OFF, vals + 36 * (int64_t)b0, (unsigned)(288 * udeg), &wbar[s], pol);
+      } else {
+        mbar_arrive(&wbar[s]);  // general node: read from global, keep the phase sequence
+      }
+    }
+  };
+  // Lane plan (fits): lane = 3 j + h (lane < 27) owns block j of the slot (own upper blocks
+  // first, then the pulled ones) and output rows 2h, 2h+1 of the node:
+  //   own K_mj:    t_e = sum_b K_mj[2h+e][b] x_j[b]      (column-major: pairs at 6b + 2h)
+  //   pulled K_nm: t_e = sum_a K_nm[a][2h+e] x_n[a]      (columns 2h, 2h+1: 12 contiguous)
+  // (t0, t1) go to a per-warp reduction row red[j][h]; lanes a < 6 then sum column a over
+  // the blocks in ascending j: y[a] (fixed order, no shuffles of doubles).
+  const int jl = lane / 3, hl = lane - 3 * jl;
+  double2* red = red_all[warp];
+  auto xnode = [&](int d) -> int {  // node whose x this lane gathers (own: column node, pulled: source)
+    const int fl = __shfl_sync(FULL, d, 1);
+    const int udeg = fl & 255;
+    const int src = jl < udeg ? 2 + jl : 2 + 2 * jl - udeg;
+    return __shfl_sync(FULL, d, min(src, PULL_DESC - 1));
+  };
+  auto gather = [&](int d, int node, double2& x0, double2& x1, double2& x2) {
+    const int fl = __shfl_sync(FULL, d, 1);
+    const int nb = (fl & 255) + ((fl >> 8) & 255);
+    if (((fl >> 16) & 1) && jl < nb) {
+      const double2* xp = reinterpret_cast<const double2*>(p + 6 * (int64_t)node);
+      x0 = xp[0];
+      x1 = xp[1];
+      x2 = xp[2];
+    }
+  };
+  double pq[1] = {0.0};
+  // Software pipeline: node k computes while nodes k+1 .. k+STAGES-1 stream into the ring,
+  // the descriptors of the nodes up to k+P are in flight and the x operands of node k+1 are
+  // being gathered.  The loop is unrolled by the descriptor period P (a ring of P registers,
+  // P even so the x operands ping-pong) so no in-flight register is ever moved.
+  constexpr int P = (STAGES + 2) & ~1;  // even, >= STAGES + 1
+  int dd[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) dd[j] = desc(j);
+#pragma unroll
+  for (int j = 0; j < STAGES - 1; ++j)
+    if (j < cnt) issue(j, dd[j]);
+  double2 xs[2][3];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) xs[h][j] = make_double2(0.0, 0.0);
+  gather(dd[0], xnode(dd[0]), xs[0][0], xs[0][1], xs[0][2]);
+#pragma unroll 1
+  for (int k0 = 0; k0 < cnt; k0 += P) {
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      const int k = k0 + u;
+      if (k >= cnt) break;
+      const int cu = u & 1, nu = cu ^ 1;  // x operands of node k / node k+1
+      if (k + STAGES - 1 < cnt) issue(k + STAGES - 1, dd[(u + STAGES - 1) % P]);
+      if (k + 1 < cnt) {  // x operands of node k+1
+        const int d1 = dd[(u + 1) % P];
+        gather(d1, xnode(d1), xs[nu][0], xs[nu][1], xs[nu][2]);
+      }
+      // ---- node k ----
+      const int s = k % STAGES;
+      const int64_t n = gw + (int64_t)k * NW;
+      const int dk = dd[u];
+      const int flc = __shfl_sync(FULL, dk, 1);
+      const int b0c = __shfl_sync(FULL, dk, 0), l0c = __shfl_sync(FULL, dk, 2);
+      const double2 xa0 = xs[cu][0], xa1 = xs[cu][1], xa2 = xs[cu][2];
+      dd[u] = desc(k + P);  // node k's descriptor is fully read above
+      const int udeg = flc & 255, ldeg = (flc >> 8) & 255, nb = udeg + ldeg;
+      mbar_wait(&wbar[s], (unsigned)((k / STAGES) & 1));
+      double y = 0.0;
+      if ((flc >> 16) & 1) {
+        if (jl < nb) {
+          const double* blk = ring + (size_t)s * SLOT_DOUBLES + (jl < udeg ? PULL_OWN_OFF + 36 * jl : 36 * (jl - udeg));
+          double t0, t1;
+          if (jl < udeg) {
+            const double* r = blk + 2 * hl;
+            const double2 v0 = *reinterpret_cast<const double2*>(r);
+            const double2 v1 = *reinterpret_cast<const double2*>(r + 6);
+            const double2 v2 = *reinterpret_cast<const double2*>(r + 12);
+            const double2 v3 = *reinterpret_cast<const double2*>(r + 18);
+            const double2 v4 = *reinterpret_cast<const double2*>(r + 24);
+            const double2 v5 = *reinterpret_cast<const double2*>(r + 30);
+            t0 = v0.x * xa0.x;
+            t1 = v0.y * xa0.x;
+            t0 = fma(v1.x, xa0.y, t0);
+            t1 = fma(v1.y, xa0.y, t1);
+            t0 = fma(v2.x, xa1.x, t0);
+            t1 = fma(v2.y, xa1.x, t1);
+            t0 = fma(v3.x, xa1.y, t0);
+            t1 = fma(v3.y, xa1.y, t1);
+            t0 = fma(v4.x, xa2.x, t0);
+            t1 = fma(v4.y, xa2.x, t1);
+            t0 = fma(v5.x, xa2.y, t0);
+            t1 = fma(v5.y, xa2.y, t1);
+          } else {
+            const double* c = blk + 12 * hl;
+            const double2 a01 = *reinterpret_cast<const double2*>(c);
+            const double2 a23 = *reinterpret_cast<const double2*>(c + 2);
+            const double2 a45 = *reinterpret_cast<const double2*>(c + 4);
+            const double2 b01 = *reinterpret_cast<const double2*>(c + 6);
+            const double2 b23 = *reinterpret_cast<const double2*>(c + 8);
+            const double2 b45 = *reinterpret_cast<const double2*>(c + 10);
+            t0 = a01.x * xa0.x;
+            t1 = b01.x * xa0.x;
+            t0 = fma(a01.y, xa0.y, t0);
+            t1 = fma(b01.y, xa0.y, t1);
+            t0 = fma(a23.x, xa1.x, t0);
+            t1 = fma(b23.x, xa1.x, t1);
+            t0 = fma(a23.y, xa1.y, t0);
+            t1 = fma(b23.y, xa1.y, t1);
+            t0 = fma(a45.x, xa2.x, t0);
+            t1 = fma(b45.x, xa2.x, t1);
+            t0 = fma(a45.y, xa2.y, t0);
+            t1 = fma(b45.y, xa2.y, t1);
+          }
+          red[lane] = make_double2(t0, t1);
+        }
+        __syncwarp();
+        if (lane < 6) {
+          const double* rd = reinterpret_cast<const double*>(red) + lane;  // red[3 j + a/2].(a&1)
+          for (int j = 0; j < nb; ++j) y += rd[6 * j];
+        }
+      } else {
+        // general node (degree beyond the slot or the descriptor): from global memory, lane
+        // a < 6 forms row a over the own blocks, then the pulled blocks, in ascending order
+        if (lane < 6) {
+          const int a = lane;
+          for (int kb = 0; kb < udeg; ++kb) {
+            const int m = __ldg(ucol + b0c + kb);
+            const double* blk = vals + 36 * ((int64_t)b0c + kb);
+            double t = 0.0;
+#pragma unroll
+            for (int b = 0; b < 6; ++b) t = fma(blk[6 * b + a], p[6 * (int64_t)m + b], t);
+            y += t;
+          }
+          for (int jp = 0; jp < ldeg; ++jp) {
+            const int2 e = __ldg(lpull + l0c + jp);
+            const double* blk = vals + 36 * (int64_t)e.y;
+            double t = 0.0;
+#pragma unroll
+            for (int b = 0; b < 6; ++b) t = fma(blk[6 * a + b], p[6 * (int64_t)e.x + b], t);
+            y += t;
+          }
+        }
+      }
+      if (lane < 6) {
+        q[6 * n + lane] = y;
+        if (DOT) pq[0] += p[6 * n + lane] * y;
+      }
+      __syncwarp();
+    }
+  }
+  if (DOT) {
+    if (grid_sum<1>(pq, partial, &st->ticket[0], sm) && threadIdx.x == 0) {
+      if (st->dist) {
+        st->red[0] = pq[0];
+        return;
+      }
+      st->pq = pq[0];
+      if (!(pq[0] > 0.0)) {
+        st->status = SSO_E_NOT_SPD;
+        st->done = 1;
+      } else {
+        st->alpha = st->rz / pq[0];
+      }
+    }
+  }
+}
+
 // x += alpha p, r -= alpha q, z = dinv r; partial r^T z, r^T r.  double2 streams
 // (ndof = 6 n is even; cudaMalloc buffers are 256 B aligned).
 __global__ void __launch_bounds__(256) cg_update_kernel(int ndof, const double* __restrict__ dinv,
@@ -1221,6 +1497,94 @@ void launch_cg_update_sym(cudaStream_t s, int ndof, const double* dinv, double* 
   cg_update_sym_kernel<<<dim3(vec_grid(ndof, bs.B), bs.B), 256, 0, s>>>(ndof, dinv, x, r, p, yup, tbuf, lptr,
                                                                         lslot, partial, st, bs);
   SSO_POST_LAUNCH("cg_update_sym_kernel");
+}
+
+// pull SpMV (storage 3): rings of PULL_SLOT_DOUBLES slots (4 gathered + 5 own blocks);
+// SSO_PULL_VARIANT selects (stages, CTAs per SM): 0 -> (3, 3), 1 -> (2, 4), 2 -> (4, 2)
+struct PullVariant {
+  int stages, minb;
+  void (*dot)(const CUtensorMap, int, int, const int32_t*, const int32_t*, const int2*, const double*,
+              const double*, double*, double*, CgState*, BatchStrides);
+  void (*plain)(const CUtensorMap, int, int, const int32_t*, const int32_t*, const int2*, const double*,
+                const double*, double*, double*, CgState*, BatchStrides);
+};
+#define PULL_VARIANT(S, M) \
+  { S, M, spmv_pull_kernel<true, S, M>, spmv_pull_kernel<false, S, M> }
+static const PullVariant kPullVariants[] = {PULL_VARIANT(3, 3), PULL_VARIANT(2, 4), PULL_VARIANT(4, 2)};
+
+static const PullVariant& pull_variant(int* smem) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SSO_PULL_VARIANT");
+    v = e ? atoi(e) : 0;
+    if (v < 0 || v >= (int)(sizeof(kPullVariants) / sizeof(kPullVariants[0]))) v = 0;
+    *smem = SPMV_WARPS * kPullVariants[v].stages * PULL_SLOT_DOUBLES * 8;
+    cudaFuncSetAttribute(kPullVariants[v].dot, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem);
+    cudaFuncSetAttribute(kPullVariants[v].plain, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem);
+  }
+  *smem = SPMV_WARPS * kPullVariants[v].stages * PULL_SLOT_DOUBLES * 8;
+  return kPullVariants[v];
+}
+
+void build_pull_desc(const UpperPattern& U, std::vector<int32_t>& d) {
+  const int64_t nn = (int64_t)U.uptr.size() - 1;
+  d.assign((size_t)(PULL_DESC * nn), 0);
+  for (int64_t m = 0; m < nn; ++m) {
+    int32_t* o = d.data() + PULL_DESC * m;
+    const int64_t b0 = U.uptr[m], l0 = U.lptr[m];
+    const int udeg = (int)(U.uptr[m + 1] - b0), ldeg = (int)(U.lptr[m + 1] - l0);
+    const bool fits = udeg <= PULL_MAX_UDEG && ldeg <= 4;
+    o[0] = (int32_t)b0;
+    o[1] = (std::min(udeg, 255)) | (std::min(ldeg, 255) << 8) | ((fits ? 1 : 0) << 16);
+    if (!fits) {
+      o[2] = (int32_t)l0;
+      continue;
+    }
+    for (int k = 0; k < udeg; ++k) o[2 + k] = U.ucol[b0 + k];
+    for (int j = 0; j < ldeg; ++j) {
+      o[2 + udeg + 2 * j] = U.lpull[2 * (l0 + j)];
+      o[3 + udeg + 2 * j] = U.lpull[2 * (l0 + j) + 1];
+    }
+  }
+}
+
+int make_pull_tmap(const double* vals, int64_t rows, CUtensorMap* out) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess || !fn)
+      return 1;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  // [rows][36] fp64 view of the values; a box is one 288-byte row, gather4 fetches four
+  cuuint64_t dims[2] = {36, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {288};
+  cuuint32_t box[2] = {36, 1};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(vals), dims, strides,
+                            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : 2;
+}
+
+void launch_spmv_pull(cudaStream_t s, const CUtensorMap* tmap, int n_nodes, int rows_per_design,
+                      const int32_t* pdesc, const int32_t* ucol, const int32_t* lpull, const double* vals,
+                      const double* x, double* y, double* partial, CgState* st, const BatchStrides& bs) {
+  if (n_nodes <= 0) return;
+  int smem;
+  const PullVariant& V = pull_variant(&smem);
+  const int ctas = std::max(1, V.minb * (cg_grid() / 4) / bs.B);  // persistent: minb CTAs per SM in total
+  const int grid = std::max(1, std::min(ctas, (n_nodes + SPMV_WARPS - 1) / SPMV_WARPS));
+  const int2* lp = reinterpret_cast<const int2*>(lpull);
+  if (st)
+    V.dot<<<dim3(grid, bs.B), SPMV_WARPS * 32, smem, s>>>(*tmap, n_nodes, rows_per_design, pdesc, ucol, lp, vals,
+                                                         x, y, partial, st, bs);
+  else
+    V.plain<<<dim3(grid, bs.B), SPMV_WARPS * 32, smem, s>>>(*tmap, n_nodes, rows_per_design, pdesc, ucol, lp,
+                                                           vals, x, y, nullptr, nullptr, bs);
+  SSO_POST_LAUNCH(st ? "spmv_pull_dot_kernel" : "spmv_pull_kernel");
 }
 
 void launch_spmv(cudaStream_t s, int n_nodes, const int64_t* node_ptr, const int32_t* node_col,

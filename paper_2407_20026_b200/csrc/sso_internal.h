@@ -1,6 +1,7 @@
 // Internal declarations of the B200 JAX-SSO hot-path library (not part of the ABI).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -45,6 +46,7 @@ struct UpperPattern {
   std::vector<int32_t> ucontrib;      // staged block ids of upper blocks, ascending (e, i, j)
   std::vector<int64_t> lptr;          // [n_nodes+1]
   std::vector<int32_t> lslot;         // incoming sender slots, ascending source node
+  std::vector<int32_t> lpull;         // [2 * incoming]: (source node n, upper block index of (n, m))
   int64_t n_ublocks() const { return (int64_t)ucol.size(); }
   int64_t n_tslots = 0;
 };
@@ -129,7 +131,7 @@ void launch_assemble(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
                      const int32_t* node_col, const int64_t* contrib_ptr,
                      const int32_t* contrib, const double* stage, const uint8_t* fixed_mask,
                      double* vals, double* dinv, DevFlags* flags,
-    const BatchStrides& bs = BatchStrides());
+    const BatchStrides& bs = BatchStrides(), int cm = 0);
 
 // Fused element stiffness + assembly for quad-only meshes (no staging).
 int fused_max_degree();
@@ -139,7 +141,7 @@ void launch_quad_assemble_fused(cudaStream_t s, int n_own, int max_inc, const in
                                 const double* z, const int32_t* conn, const double* t, const double* E,
                                 const double* nu, double drill_alpha, const uint8_t* fixed_mask,
                                 double* vals, double* dinv, DevFlags* flags,
-                                const BatchStrides& bs = BatchStrides());
+                                const BatchStrides& bs = BatchStrides(), int cm = 0);
 
 // PCG kernels
 int cg_grid();  // persistent grid size (multiple of the SM count)
@@ -174,6 +176,18 @@ void launch_cg_update_sym(cudaStream_t s, int ndof, const double* dinv, double* 
                           const double* p, const double* yup, const double* tbuf, const int64_t* lptr,
                           const int32_t* lslot, double* partial, CgState* st,
                           const BatchStrides& bs = BatchStrides());
+// Symmetric pull SpMV (storage 3): upper node blocks stored column-major per run;
+// the row-owner warp streams its upper run and the upper blocks (n, m) of its lower
+// neighbours (pull list lpull = [(n, upper block index)] per node, via lptr) and
+// forms y = K x in one pass.  With st != nullptr also p^T q and alpha (CG).
+void launch_spmv_pull(cudaStream_t s, const CUtensorMap* tmap, int n_nodes, int rows_per_design,
+                      const int32_t* pdesc, const int32_t* ucol, const int32_t* lpull, const double* vals,
+                      const double* x, double* y, double* partial, CgState* st,
+                      const BatchStrides& bs = BatchStrides());
+// 16-int per-node descriptors of the pull SpMV (see pcg.cu)
+void build_pull_desc(const UpperPattern& U, std::vector<int32_t>& desc);
+// TMA map of the [rows][36] fp64 view of the values (gather4 of pulled blocks); 0 on success
+int make_pull_tmap(const double* vals, int64_t rows, CUtensorMap* out);
 void launch_spmv(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
                  const int32_t* node_col, const double* vals, const double* x, double* y,
     const BatchStrides& bs = BatchStrides());

@@ -271,12 +271,14 @@ def test_fused_assembly_matches_staged(sso, make):
     assert np.allclose(mf.export_dinv(), ms.export_dinv(), rtol=1e-14, atol=0)
 
 
+@pytest.mark.parametrize("storage", [2, 3])
 @pytest.mark.parametrize("make", [W.config2, mixed, W.config1, lambda: W.shell_config3(40, cfg=3)])
-def test_symmetric_storage_matches_full(sso, make):
-    """Upper-block (symmetric) storage with the two-pass transpose SpMV (default for
-    single-strip handles) reproduces the full-storage operator, solve and gradient."""
+def test_symmetric_storage_matches_full(sso, make, storage):
+    """Upper-block (symmetric) storage -- two-pass transpose SpMV (2) or one-pass pull
+    SpMV over column-major runs (3) -- reproduces the full-storage operator, solve and
+    gradient."""
     P = make()
-    ms = sso.Model(P, rtol=1e-12, storage=2)
+    ms = sso.Model(P, rtol=1e-12, storage=storage)
     mf = sso.Model(P, rtol=1e-12, storage=1)
     assert ms.storage_info()[2] and not mf.storage_info()[2]
     assert ms.storage_info()[1] < mf.storage_info()[1]
@@ -352,3 +354,46 @@ def test_general_objective_adjoint(sso, make):
     for got, ref in ((dX, rX), (dE, rE)) + (((dT, rT),) if len(rT) else ()):
         fl = 1e-3 * np.abs(ref).max()
         assert np.all(np.abs(got - ref) <= 1e-6 * np.maximum(np.abs(ref), fl))
+
+
+@pytest.mark.parametrize("name", ["C2", "ragged", "mixed", "beamgrid"])
+def test_pull_storage_against_oracle(sso, cases, name):
+    """Storage 3 (upper blocks, pull SpMV) against the oracle directly: CSR values with
+    supports, dinv, u (Cholesky), C and the gradient through the solved state."""
+    c = oracle_case(cases, name)
+    P = c["P"]
+    m = sso.Model(P, rtol=1e-12, storage=3)
+    assert m.storage_info()[2] == 3
+    m.assemble()
+    _, _, v = m.export_csr()
+    rp, ref = c["rp"], c["vbc"]
+    for r in range(len(rp) - 1):
+        seg = slice(rp[r], rp[r + 1])
+        assert np.abs(v[seg] - ref[seg]).max() <= TOL_VAL * np.abs(ref[seg]).max(), r
+    u, info = m.solve(P["f"])
+    assert info["status"] == 0
+    uref = c["u"]
+    assert np.linalg.norm(u - uref) <= TOL_U * np.linalg.norm(uref)
+    Cv, dX, _ = m.grad(sso.OBJ_COMPLIANCE)
+    assert abs(Cv - OG.compliance(P["f"], uref)) <= TOL_C * abs(OG.compliance(P["f"], uref))
+    gX, _ = OG.adjoint_gradient(P, uref, 1.0)
+    floor = 1e-3 * np.abs(gX).max()
+    assert np.all(np.abs(dX - gX) <= 1e-6 * np.maximum(np.abs(gX), floor))
+
+
+def test_pull_storage_batched(sso):
+    """Storage 3 with a batch of designs (grid.y) equals full storage per design."""
+    B = 3
+    designs = [W.config5_design(b, n=12) for b in range(B)]
+    F = np.stack([d["f"] for d in designs])
+    out = {}
+    for st in (1, 3):
+        m = sso.Model(designs[0], rtol=1e-12, batch=B, storage=st)
+        m.set_design(z=np.stack([d["z"] for d in designs]), t=np.stack([d["t"] for d in designs]))
+        m.assemble()
+        U, infos = m.solve(F)
+        assert all(i["status"] == 0 for i in infos)
+        out[st] = (U, m.grad()[0])
+    for b in range(B):
+        assert np.linalg.norm(out[3][0][b] - out[1][0][b]) <= 1e-9 * np.linalg.norm(out[1][0][b])
+        assert out[3][1][b] == pytest.approx(out[1][1][b], rel=1e-10)
