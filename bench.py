@@ -361,6 +361,8 @@ def run_gpu(args):
                           "n_nodes": n_nodes, "n_quads": nq, "ndof": ndof, "nnz": nnz,
                           "rtol": RTOL, "cg_iters": cg_iters,
                           "parallelism": parallelism,
+                          "storage": {0: "full node-block CSR", 2: "upper blocks, two-pass SpMV",
+                                      3: "upper blocks (column-major runs), one-pass pull SpMV"}[symmetric],
                           "l2": "working set > L2 (CSR values alone 432 MB vs 126 MB L2); no flush",
                           "pattern_build_s": t_create},
                "roofline": roofline,

@@ -136,7 +136,8 @@ typedef struct {
    * matrices) when the mesh is quad-only with node degree <= 10; 1 = always the staged
    * path (element kernel, then the segmented-sum gather). */
   int32_t assembly;
-  /* 0 (default) or 1 = full CSR storage.  2 = single-strip handles keep only the
+  /* 0 (default) = storage 3 for single-strip handles (partitioned handles always use
+   * full storage).  1 = full CSR storage.  2 = single-strip handles keep only the
    * upper node blocks (n, m >= n) of the symmetric K_bc (44 % fewer value bytes on
    * shell grids); pass 1 of the SpMV forms the upper row sums, the transpose
    * contributions (sender-ordered slots) and p^T K p, the x / r update adds each

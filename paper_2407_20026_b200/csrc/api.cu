@@ -988,7 +988,7 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
   h->batch = o.batch;
   h->reliable = o.reliable;
   h->assembly = o.assembly;
-  h->storage = o.storage;
+  h->storage = o.storage == 0 ? 3 : o.storage;  // default: upper blocks + pull SpMV (single-strip handles)
   h->g_nodes = mesh->n_nodes;
   h->g_beams = mesh->n_beams;
   h->g_quads = mesh->n_quads;

@@ -922,6 +922,296 @@ __global__ void __launch_bounds__(SPMV_WARPS * 32, MINB) spmv_pull_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pull SpMV, warp-specialised chunk form (storage 3, the default pull kernel).
+// The per-node bookkeeping that made the warp-per-node form issue-bound (descriptor
+// shuffles, two TMA issues per node) is done lane-parallel by a PRODUCER warp: a
+// CTA takes chunks of C consecutive nodes (chunks dealt round-robin over the CTAs,
+// so the GPU sweeps one window of nodes and pulled blocks stay L2 hits); producer
+// lane i loads node i's descriptor into shared memory and issues that node's
+// gather4 of pulled blocks, lane 0 issues ONE bulk copy of the chunk's own upper
+// runs (consecutive nodes' runs are contiguous).  NB buffers with full / empty
+// mbarriers; CONSUMER warps (PULL_CONSUMERS) each take C / PULL_CONSUMERS nodes of
+// a chunk with no CTA-wide barrier: lane 3j + h forms (t_2h, t_2h+1) of block j
+// (own upper blocks, then pulled) as in the warp form, a per-warp shared row sums
+// them in ascending j.  Chunks holding a node that does not fit (udeg > 5 or
+// ldeg > 4) take a general path reading the values from global memory.
+// ---------------------------------------------------------------------------
+constexpr int PULL_CONSUMERS = 8;
+
+template <int C>
+struct PullChunkSmem {
+  static constexpr int PULL = 36 * 4 * C;          // doubles: 4 gathered rows per node (1152 B each)
+  static constexpr int OWN = 36 * 5 * C;           // doubles: own upper runs (<= 5 blocks per node)
+  static constexpr int DESC = PULL_DESC * C / 2;   // doubles holding the C descriptors (16 int32 each)
+  static constexpr int BUF = PULL + OWN + DESC;    // per buffer (PULL first: 128-byte aligned rows)
+  static constexpr int NPW = C / PULL_CONSUMERS;   // nodes per consumer warp per chunk
+  static constexpr int RED = 2 * 27 * NPW;         // doubles per consumer warp
+};
+
+template <bool DOT, int C, int NB, int MINB>
+__global__ void __launch_bounds__(32 * (PULL_CONSUMERS + 1), MINB) spmv_pull_cta_kernel(
+    const __grid_constant__ CUtensorMap tmap, int n_nodes, int rows_per_design, const int32_t* __restrict__ pdesc,
+    const int32_t* __restrict__ ucol, const int2* __restrict__ lpull, const double* __restrict__ vals,
+    const double* __restrict__ p, double* __restrict__ q, double* __restrict__ partial, CgState* st,
+    BatchStrides bs) {
+  using S = PullChunkSmem<C>;
+  constexpr int NPW = S::NPW;
+  constexpr unsigned FULL = 0xffffffffu;
+  static_assert(C <= 32 && C % PULL_CONSUMERS == 0, "chunk size");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[NB];   // chunk data landed (bulk copy + gathers)
+  __shared__ __align__(8) uint64_t desc_bar[NB];   // chunk descriptors written (x gathers may start)
+  __shared__ __align__(8) uint64_t empty_bar[NB];  // consumers done with the buffer
+  __shared__ int chunk_fits[NB];
+  __shared__ double sm[32];
+  const int row0 = blockIdx.y * rows_per_design;
+  {  // design of a batch (blockIdx.y)
+    const int bd = blockIdx.y;
+    vals += bd * bs.nnz;
+    p += bd * bs.dof;
+    q += bd * bs.dof;
+    if (DOT) {
+      partial += bd * bs.partial;
+      st += bd;
+    }
+  }
+  if (DOT && st->done) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_chunks = (n_nodes + C - 1) / C;
+  const int cnt = (int)blockIdx.x < n_chunks ? (n_chunks - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  double* sbase = reinterpret_cast<double*>(smem_raw);
+  double* red_base = sbase + (size_t)NB * S::BUF;
+  if (tid == 0) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&full_bar[b], 1);
+      mbar_init(&desc_bar[b], 1);
+      mbar_init(&empty_bar[b], PULL_CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double pq[1] = {0.0};
+  if (warp == PULL_CONSUMERS) {
+    // ---------------- producer ----------------
+    const uint64_t pol = evict_first_policy();
+    for (int k = 0; k < cnt; ++k) {
+      const int b = k % NB;
+      if (k >= NB) mbar_wait(&empty_bar[b], (unsigned)(((k / NB) - 1) & 1));
+      double* buf = sbase + (size_t)b * S::BUF;
+      int32_t* D = reinterpret_cast<int32_t*>(buf + S::PULL + S::OWN);
+      const int first = ((int)blockIdx.x + k * (int)gridDim.x) * C;
+      const int nc = min(C, n_nodes - first);
+      int4 d0 = make_int4(0, 0, 0, 0), d1 = d0, d2 = d0, d3 = d0;
+      if (lane < nc) {
+        const int4* src = reinterpret_cast<const int4*>(pdesc + PULL_DESC * ((int64_t)first + lane));
+        d0 = __ldg(src);
+        d1 = __ldg(src + 1);
+        d2 = __ldg(src + 2);
+        d3 = __ldg(src + 3);
+        int4* dst = reinterpret_cast<int4*>(D + PULL_DESC * lane);
+        dst[0] = d0;
+        dst[1] = d1;
+        dst[2] = d2;
+        dst[3] = d3;
+      }
+      const int fl = d0.y;
+      const int udeg = fl & 255, ldeg = (fl >> 8) & 255;
+      const bool all_fit = __all_sync(FULL, lane >= nc || ((fl >> 16) & 1));
+      const unsigned has_pull = __ballot_sync(FULL, lane < nc && ldeg > 0);
+      const int b_first = __shfl_sync(FULL, d0.x, 0);
+      const int b_end = __shfl_sync(FULL, d0.x + udeg, nc - 1);
+      // generic reads of buffer b by the consumers of chunk k - NB precede the async writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        chunk_fits[b] = all_fit ? 1 : 0;
+        mbar_arrive(&desc_bar[b]);  // release: descriptors and the fit flag are visible
+        if (all_fit) {
+          mbar_arrive_expect_tx(&full_bar[b], (unsigned)(288 * (b_end - b_first) + 1152 * __popc(has_pull)));
+          bulk_g2s(buf + S::PULL, vals + 36 * (int64_t)b_first, (unsigned)(288 * (b_end - b_first)), &full_bar[b],
+                   pol);
+        } else {
+          mbar_arrive(&full_bar[b]);  // release: the descriptors written above are visible
+        }
+      }
+      __syncwarp();  // expect_tx registered before the gathers complete
+      if (all_fit && lane < nc && ldeg > 0) {
+        // pulled block i of the node: (source, block) at d[2 + udeg + 2i] (re-read from this lane's
+        // own shared-memory copy of the descriptor); pad with the own first block
+        const int32_t* Dl = D + PULL_DESC * lane + 3 + udeg;
+        int r[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) r[i] = row0 + (i < ldeg ? Dl[2 * i] : d0.x);
+        tma_gather4(buf + 144 * lane, &tmap, r[0], r[1], r[2], r[3], &full_bar[b], pol);
+      }
+    }
+  } else {
+    // ---------------- consumers ----------------
+    double2* red = reinterpret_cast<double2*>(red_base) + (size_t)warp * 27 * NPW;
+    const int jl = lane / 3, hl = lane - 3 * jl;
+    for (int k = 0; k < cnt; ++k) {
+      const int b = k % NB;
+      const double* buf = sbase + (size_t)b * S::BUF;
+      const double* own = buf + S::PULL;
+      const int32_t* D = reinterpret_cast<const int32_t*>(buf + S::PULL + S::OWN);
+      const int first = ((int)blockIdx.x + k * (int)gridDim.x) * C;
+      const int nc = min(C, n_nodes - first);
+      mbar_wait(&desc_bar[b], (unsigned)((k / NB) & 1));
+      if (chunk_fits[b]) {
+        const int b_first = D[0];
+        const double* blk[NPW];
+        double2 xv[NPW][3];
+        bool act[NPW];
+        int nbs[NPW];
+#pragma unroll
+        for (int e = 0; e < NPW; ++e) {  // node i = warp + 8 e of the chunk: operands first
+          const int i = warp + PULL_CONSUMERS * e;
+          const int* Di = D + PULL_DESC * (i < nc ? i : 0);
+          const int fl = Di[1];
+          const int udeg = fl & 255, nb = udeg + ((fl >> 8) & 255);
+          nbs[e] = i < nc ? nb : 0;
+          act[e] = i < nc && jl < nb;
+          blk[e] = own;
+          if (act[e]) {
+            int xn;
+            if (jl < udeg) {
+              blk[e] = own + 36 * (Di[0] - b_first + jl) + 2 * hl;
+              xn = Di[2 + jl];
+            } else {
+              blk[e] = buf + 144 * i + 36 * (jl - udeg) + 12 * hl;
+              xn = Di[2 + 2 * jl - udeg];
+            }
+            const double2* xp = reinterpret_cast<const double2*>(p + 6 * (int64_t)xn);
+            xv[e][0] = xp[0];
+            xv[e][1] = xp[1];
+            xv[e][2] = xp[2];
+          }
+        }
+        mbar_wait(&full_bar[b], (unsigned)((k / NB) & 1));  // x gathers overlap the chunk's data
+#pragma unroll
+        for (int e = 0; e < NPW; ++e) {
+          if (!act[e]) continue;
+          const int i = warp + PULL_CONSUMERS * e;
+          const int udeg = D[PULL_DESC * i + 1] & 255;
+          const double* r = blk[e];
+          const double2 x0 = xv[e][0], x1 = xv[e][1], x2 = xv[e][2];
+          double t0, t1;
+          if (jl < udeg) {  // own K_mj, column-major: pairs (K[2h][b], K[2h+1][b]) at 6b + 2h
+            const double2 v0 = *reinterpret_cast<const double2*>(r);
+            const double2 v1 = *reinterpret_cast<const double2*>(r + 6);
+            const double2 v2 = *reinterpret_cast<const double2*>(r + 12);
+            const double2 v3 = *reinterpret_cast<const double2*>(r + 18);
+            const double2 v4 = *reinterpret_cast<const double2*>(r + 24);
+            const double2 v5 = *reinterpret_cast<const double2*>(r + 30);
+            t0 = v0.x * x0.x;
+            t1 = v0.y * x0.x;
+            t0 = fma(v1.x, x0.y, t0);
+            t1 = fma(v1.y, x0.y, t1);
+            t0 = fma(v2.x, x1.x, t0);
+            t1 = fma(v2.y, x1.x, t1);
+            t0 = fma(v3.x, x1.y, t0);
+            t1 = fma(v3.y, x1.y, t1);
+            t0 = fma(v4.x, x2.x, t0);
+            t1 = fma(v4.y, x2.x, t1);
+            t0 = fma(v5.x, x2.y, t0);
+            t1 = fma(v5.y, x2.y, t1);
+          } else {  // pulled K_nm: columns 2h, 2h+1 (12 contiguous) against x_n
+            const double2 a01 = *reinterpret_cast<const double2*>(r);
+            const double2 a23 = *reinterpret_cast<const double2*>(r + 2);
+            const double2 a45 = *reinterpret_cast<const double2*>(r + 4);
+            const double2 b01 = *reinterpret_cast<const double2*>(r + 6);
+            const double2 b23 = *reinterpret_cast<const double2*>(r + 8);
+            const double2 b45 = *reinterpret_cast<const double2*>(r + 10);
+            t0 = a01.x * x0.x;
+            t1 = b01.x * x0.x;
+            t0 = fma(a01.y, x0.y, t0);
+            t1 = fma(b01.y, x0.y, t1);
+            t0 = fma(a23.x, x1.x, t0);
+            t1 = fma(b23.x, x1.x, t1);
+            t0 = fma(a23.y, x1.y, t0);
+            t1 = fma(b23.y, x1.y, t1);
+            t0 = fma(a45.x, x2.x, t0);
+            t1 = fma(b45.x, x2.x, t1);
+            t0 = fma(a45.y, x2.y, t0);
+            t1 = fma(b45.y, x2.y, t1);
+          }
+          red[27 * e + lane] = make_double2(t0, t1);
+        }
+        __syncwarp();
+        // lane 6 e + a (< 6 NPW): row a of node e, blocks in ascending j
+        if (lane < 6 * NPW) {
+          const int e = lane / 6, a = lane - 6 * e;
+          const int i = warp + PULL_CONSUMERS * e;
+          int nb = 0;
+#pragma unroll
+          for (int t = 0; t < NPW; ++t)
+            if (t == e) nb = nbs[t];
+          if (i < nc) {
+            const double* rd = reinterpret_cast<const double*>(red + 27 * e) + a;
+            double y = 0.0;
+            for (int j = 0; j < nb; ++j) y += rd[6 * j];
+            const int64_t row = 6 * ((int64_t)first + i) + a;
+            q[row] = y;
+            if (DOT) pq[0] += p[row] * y;
+          }
+        }
+      } else if (lane < 6 * NPW) {
+        mbar_wait(&full_bar[b], (unsigned)((k / NB) & 1));  // (no data: keeps the phase sequence)
+        // general chunk: lane (node e, row a) sums its row from global memory, own blocks then
+        // pulled blocks in ascending order (the order of the fast path)
+        const int e = lane / 6, a = lane - 6 * e;
+        const int i = warp + PULL_CONSUMERS * e;
+        if (i < nc) {
+          const int* Di = D + PULL_DESC * i;
+          const int b0 = Di[0], fl = Di[1];
+          const int udeg = fl & 255, ldeg = (fl >> 8) & 255;
+          const bool fitn = (fl >> 16) & 1;
+          const int l0 = fitn ? 0 : Di[2];
+          double y = 0.0;
+          for (int kb = 0; kb < udeg; ++kb) {
+            const int m = fitn ? Di[2 + kb] : __ldg(ucol + b0 + kb);
+            const double* bk = vals + 36 * ((int64_t)b0 + kb);
+            double t = 0.0;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) t = fma(bk[6 * c + a], p[6 * (int64_t)m + c], t);
+            y += t;
+          }
+          for (int jp = 0; jp < ldeg; ++jp) {
+            const int2 e2 = fitn ? make_int2(Di[2 + udeg + 2 * jp], Di[3 + udeg + 2 * jp]) : __ldg(lpull + l0 + jp);
+            const double* bk = vals + 36 * (int64_t)e2.y;
+            double t = 0.0;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) t = fma(bk[6 * a + c], p[6 * (int64_t)e2.x + c], t);
+            y += t;
+          }
+          const int64_t row = 6 * ((int64_t)first + i) + a;
+          q[row] = y;
+          if (DOT) pq[0] += p[row] * y;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[b]);  // this warp is done with buffer b
+    }
+  }
+  if (DOT) {
+    if (grid_sum<1>(pq, partial, &st->ticket[0], sm) && threadIdx.x == 0) {
+      if (st->dist) {
+        st->red[0] = pq[0];
+        return;
+      }
+      st->pq = pq[0];
+      if (!(pq[0] > 0.0)) {
+        st->status = SSO_E_NOT_SPD;
+        st->done = 1;
+      } else {
+        st->alpha = st->rz / pq[0];
+      }
+    }
+  }
+}
+
 // x += alpha p, r -= alpha q, z = dinv r; partial r^T z, r^T r.  double2 streams
 // (ndof = 6 n is even; cudaMalloc buffers are 256 B aligned).
 __global__ void __launch_bounds__(256) cg_update_kernel(int ndof, const double* __restrict__ dinv,
@@ -1499,31 +1789,43 @@ void launch_cg_update_sym(cudaStream_t s, int ndof, const double* dinv, double* 
   SSO_POST_LAUNCH("cg_update_sym_kernel");
 }
 
-// pull SpMV (storage 3): rings of PULL_SLOT_DOUBLES slots (4 gathered + 5 own blocks);
-// SSO_PULL_VARIANT selects (stages, CTAs per SM): 0 -> (3, 3), 1 -> (2, 4), 2 -> (4, 2)
+// pull SpMV (storage 3).  SSO_PULL_VARIANT selects (chunk nodes, buffers, CTAs per SM) of the
+// warp-specialised form: 0 (default) (16, 2, 2), 1 (8, 2, 3), 2 (8, 3, 3), 3 (16, 3, 1); 4-5 the
+// warp-per-node form (stages, CTAs per SM) = (3, 3), (2, 4)
 struct PullVariant {
-  int stages, minb;
+  int smem;
+  int minb;
+  int threads;
+  int chunk;  // nodes per CTA chunk (0: warp per node)
   void (*dot)(const CUtensorMap, int, int, const int32_t*, const int32_t*, const int2*, const double*,
               const double*, double*, double*, CgState*, BatchStrides);
   void (*plain)(const CUtensorMap, int, int, const int32_t*, const int32_t*, const int2*, const double*,
                 const double*, double*, double*, CgState*, BatchStrides);
 };
+#define PULL_CTA_VARIANT(C, NB, M)                                                                       \
+  {                                                                                                      \
+    (NB * PullChunkSmem<C>::BUF + PULL_CONSUMERS * PullChunkSmem<C>::RED) * 8, M, 32 * (PULL_CONSUMERS + 1), \
+        C, spmv_pull_cta_kernel<true, C, NB, M>, spmv_pull_cta_kernel<false, C, NB, M>                   \
+  }
 #define PULL_VARIANT(S, M) \
-  { S, M, spmv_pull_kernel<true, S, M>, spmv_pull_kernel<false, S, M> }
-static const PullVariant kPullVariants[] = {PULL_VARIANT(3, 3), PULL_VARIANT(2, 4), PULL_VARIANT(4, 2)};
+  { SPMV_WARPS * S * PULL_SLOT_DOUBLES * 8, M, 32 * SPMV_WARPS, 0, spmv_pull_kernel<true, S, M>, spmv_pull_kernel<false, S, M> }
+static const PullVariant kPullVariants[] = {PULL_CTA_VARIANT(16, 2, 2), PULL_CTA_VARIANT(8, 2, 3),
+                                            PULL_CTA_VARIANT(8, 3, 3),  PULL_CTA_VARIANT(16, 3, 1),
+                                            PULL_VARIANT(3, 3),         PULL_VARIANT(2, 4)};
+static int g_pull_v = -1;
 
 static const PullVariant& pull_variant(int* smem) {
-  static int v = -1;
-  if (v < 0) {
+  if (g_pull_v < 0) {
     const char* e = getenv("SSO_PULL_VARIANT");
-    v = e ? atoi(e) : 0;
+    int v = e ? atoi(e) : 0;
     if (v < 0 || v >= (int)(sizeof(kPullVariants) / sizeof(kPullVariants[0]))) v = 0;
-    *smem = SPMV_WARPS * kPullVariants[v].stages * PULL_SLOT_DOUBLES * 8;
-    cudaFuncSetAttribute(kPullVariants[v].dot, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem);
-    cudaFuncSetAttribute(kPullVariants[v].plain, cudaFuncAttributeMaxDynamicSharedMemorySize, *smem);
+    cudaFuncSetAttribute(kPullVariants[v].dot, cudaFuncAttributeMaxDynamicSharedMemorySize, kPullVariants[v].smem);
+    cudaFuncSetAttribute(kPullVariants[v].plain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kPullVariants[v].smem);
+    g_pull_v = v;
   }
-  *smem = SPMV_WARPS * kPullVariants[v].stages * PULL_SLOT_DOUBLES * 8;
-  return kPullVariants[v];
+  *smem = kPullVariants[g_pull_v].smem;
+  return kPullVariants[g_pull_v];
 }
 
 void build_pull_desc(const UpperPattern& U, std::vector<int32_t>& d) {
@@ -1576,13 +1878,15 @@ void launch_spmv_pull(cudaStream_t s, const CUtensorMap* tmap, int n_nodes, int 
   int smem;
   const PullVariant& V = pull_variant(&smem);
   const int ctas = std::max(1, V.minb * (cg_grid() / 4) / bs.B);  // persistent: minb CTAs per SM in total
-  const int grid = std::max(1, std::min(ctas, (n_nodes + SPMV_WARPS - 1) / SPMV_WARPS));
+  const int chunk = V.chunk;
+  const int units = chunk ? (n_nodes + chunk - 1) / chunk : (n_nodes + SPMV_WARPS - 1) / SPMV_WARPS;
+  const int grid = std::max(1, std::min(ctas, units));
   const int2* lp = reinterpret_cast<const int2*>(lpull);
   if (st)
-    V.dot<<<dim3(grid, bs.B), SPMV_WARPS * 32, smem, s>>>(*tmap, n_nodes, rows_per_design, pdesc, ucol, lp, vals,
+    V.dot<<<dim3(grid, bs.B), V.threads, smem, s>>>(*tmap, n_nodes, rows_per_design, pdesc, ucol, lp, vals,
                                                          x, y, partial, st, bs);
   else
-    V.plain<<<dim3(grid, bs.B), SPMV_WARPS * 32, smem, s>>>(*tmap, n_nodes, rows_per_design, pdesc, ucol, lp,
+    V.plain<<<dim3(grid, bs.B), V.threads, smem, s>>>(*tmap, n_nodes, rows_per_design, pdesc, ucol, lp,
                                                            vals, x, y, nullptr, nullptr, bs);
   SSO_POST_LAUNCH(st ? "spmv_pull_dot_kernel" : "spmv_pull_kernel");
 }
