@@ -241,7 +241,8 @@ def run_gpu(args):
                       n_parts=args.virtual_parts)
         parallelism = f"{args.virtual_parts} node strips on 1 GPU (in-process transport)"
     else:
-        m = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index, storage=args.storage)
+        m = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index, storage=args.storage,
+                      precond=args.precond)
         parallelism = "single GPU"
     t_create = time.perf_counter() - t0
     ndof, nnz, nblocks = m.sizes()
@@ -350,6 +351,31 @@ def run_gpu(args):
     asm_ms = (el_ms + as_ms) / max(args.steps, 1)
     clocks = clk.summary()
 
+    # ---- the same evaluation with the node-block Jacobi preconditioner (reading c17) ----
+    alt = None
+    if world == 1 and args.precond == 0 and args.virtual_parts == 1 and not args.no_alt:
+        mb = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index, storage=args.storage,
+                       precond=1)
+
+        def step_b():
+            mb.assemble()
+            _, ib = mb.solve(f_dev, u_dev)
+            mb.grad(sso.OBJ_COMPLIANCE, out=(Cb, dXb, dTb))
+            return ib
+        step_b()
+        nb = max(1, min(args.steps, 3))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        for _ in range(nb):
+            ib = step_b()
+        e1.record(stream)
+        barrier()
+        tb = e0.elapsed_time(e1)
+        alt = {"precond": "node-block Jacobi (sso_options.precond = 1)", "value": nb / (tb / 1000.0),
+               "unit": UNIT, "ms_per_step": tb / nb, "cg_iters": int(ib["iters"]), "steps": nb, "warmup": 1}
+        mb.close()
+
     out = None
     if rank == 0:
         cpu = cpu_baseline_obj(P, cg_iters) if (world == 1 and not args.no_cpu) else None
@@ -361,6 +387,7 @@ def run_gpu(args):
                           "n_nodes": n_nodes, "n_quads": nq, "ndof": ndof, "nnz": nnz,
                           "rtol": RTOL, "cg_iters": cg_iters,
                           "parallelism": parallelism,
+                          "precond": {0: "point Jacobi", 1: "node-block Jacobi"}[args.precond if world == 1 else 0],
                           "storage": {0: "full node-block CSR", 2: "upper blocks, two-pass SpMV",
                                       3: "upper blocks (column-major runs), one-pass pull SpMV"}[symmetric],
                           "l2": "working set > L2 (CSR values alone 432 MB vs 126 MB L2); no flush",
@@ -376,7 +403,8 @@ def run_gpu(args):
                          "assemble_gather_ms": as_ms / max(args.steps, 1),
                          "grad_ms": gr_ms / max(args.steps, 1),
                          "cg_iters_per_s": cg_iters / (ms_step / 1000.0),
-                         "spmv_ms_per_step_est": spmv_avg_ms * (cg_iters + 1)}}
+                         "spmv_ms_per_step_est": spmv_avg_ms * (cg_iters + 1),
+                         "block_jacobi": alt}}
         print(json.dumps(out))
     if world > 1:
         import torch.distributed as dist
@@ -472,6 +500,9 @@ def main():
     ap.add_argument("--cg-iters", type=int, default=None,
                     help="CG iteration count used to extrapolate the oracle (reference arm)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip the node-block Jacobi comparison run")
+    ap.add_argument("--precond", type=int, default=0,
+                    help="sso_options.precond for single-GPU C3b: 0 point Jacobi (north star), 1 node-block")
     ap.add_argument("--storage", type=int, default=0,
                     help="sso_options.storage for single-GPU C3b (0 = library default)")
     ap.add_argument("--workload", default="C3b", choices=["C3b", "C5"])

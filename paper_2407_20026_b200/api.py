@@ -63,7 +63,7 @@ class sso_options(C.Structure):
                 ("n_parts", C.c_int32), ("part_ranges", _ip), ("nranks", C.c_int32),
                 ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p), ("batch", C.c_int32),
                 ("reliable", C.c_int32), ("assembly", C.c_int32),
-                ("storage", C.c_int32)]
+                ("storage", C.c_int32), ("precond", C.c_int32)]
 
 
 class sso_solve_info(C.Structure):
@@ -151,7 +151,8 @@ class Model:
 
     def __init__(self, problem, rtol=1e-10, max_iter=200000, drill_alpha=1e-3, check_every=64,
                  warm_start=False, stream=None, device=-1, n_parts=1, part_ranges=None,
-                 nranks=1, rank=0, nccl_id=None, batch=1, reliable=1, assembly=0, storage=0):
+                 nranks=1, rank=0, nccl_id=None, batch=1, reliable=1, assembly=0, storage=0,
+                 precond=0):
         P = problem
         self._keep = []
         x, y, z = (_np(P[k], np.float64) for k in ("x", "y", "z"))
@@ -182,6 +183,7 @@ class Model:
         opt.cuda_stream = stream
         opt.n_parts, opt.nranks, opt.rank, opt.batch = n_parts, nranks, rank, batch
         opt.reliable, opt.assembly, opt.storage = reliable, assembly, storage
+        opt.precond = precond
         if part_ranges is not None:
             pr = np.ascontiguousarray(part_ranges, np.int32)
             self._keep.append(pr)

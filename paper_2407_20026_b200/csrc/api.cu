@@ -131,6 +131,8 @@ struct Part {
   bool pull = false;                  // sym with the one-pass pull SpMV (storage 3, column-major runs)
   int32_t* lpull = nullptr;           // pull: (source node, upper block) per incoming block
   int32_t* pdesc = nullptr;           // pull: 16-int per-node descriptors (build_pull_desc)
+  double* binv = nullptr;             // precond 1: [B][21][n_own] packed (K_nn)^-1
+  double* zb = nullptr;               // precond 1: z = M^-1 r [B][ndof]
   CUtensorMap pull_tmap;              // pull: [B n_ublocks][36] view of vals for the gather4 TMA
   UpperPattern up;
   int64_t* lptr = nullptr;            // sym: incoming transpose slots per node
@@ -162,6 +164,7 @@ struct sso_ctx {
   int reliable = 1;  // 0 plain CG, 1 final true-residual restart, 2 + periodic replacement
   int assembly = 0;  // 0 auto (fused when the mesh allows), 1 staged
   int storage = 0;   // 0 / 1 full CSR storage, 2 symmetric upper blocks (single-strip handles)
+  int precond = 0;   // 0 point Jacobi, 1 node-block Jacobi (block_jacobi.cu)
   bool area_load = false;  // design-dependent area loads active (sso_set_area_load)
   bool skip_load = false;  // adjoint solves: the right-hand side is dg/du only, b = 0
   bool prescribed = false; // non-zero support displacements active (sso_set_prescribed)
@@ -480,11 +483,16 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev) {
   int rc;
   if (!h->distributed()) {
     Part& P = h->P0();
-    launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st, P.bs);
+    if (P.binv)
+      launch_cg_pupdate_z(s, (int)P.ndof_own, P.zb, P.p, P.st, P.bs);
+    else
+      launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st, P.bs);
     if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
     spmv_apply(s, P, P.p, P.q, P.st);
     if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
-    if (P.sym && !P.pull)
+    if (P.binv)
+      launch_cg_update_block(s, P.n_own, P.binv, P.xs, P.r, P.p, P.q, P.zb, P.partial, P.st, P.bs);
+    else if (P.sym && !P.pull)
       launch_cg_update_sym(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.tbuf, P.lptr, P.lslot, P.partial,
                            P.st, P.bs);
     else
@@ -493,7 +501,10 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev) {
   }
   for (auto& pp : h->parts) {
     Part& P = *pp;
-    launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st, P.bs);
+    if (P.binv)
+      launch_cg_pupdate_z(s, (int)P.ndof_own, P.zb, P.p, P.st, P.bs);
+    else
+      launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st, P.bs);
   }
   if ((rc = exchange(h, V_P, s))) return rc;
   bool first = true;
@@ -508,7 +519,10 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     launch_cg_scalar(s, P.st, PH_ALPHA);
-    launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st, P.bs);
+    if (P.binv)
+      launch_cg_update_block(s, P.n_own, P.binv, P.xs, P.r, P.p, P.q, P.zb, P.partial, P.st, P.bs);
+    else
+      launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st, P.bs);
   }
   if ((rc = allreduce(h, 2, s))) return rc;
   for (auto& pp : h->parts) launch_cg_scalar(s, pp->st, PH_BETA);
@@ -566,7 +580,7 @@ void free_part(Part& P) {
                   P.inc_slot, P.stage, P.vals, P.dinv, P.f, P.fbc, P.xs, P.r, P.p, P.q, P.tmp, P.gu,
                   P.gf, P.partial, P.st, P.flags, P.tickets, P.scal, P.slot_partial, P.dxyz, P.dt,
                   P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
-                  P.lptr, P.lslot, P.lpull, P.pdesc, P.tbuf, P.dE,
+                  P.lptr, P.lslot, P.lpull, P.pdesc, P.binv, P.zb, P.tbuf, P.dE,
                   P.ub, P.fb, P.lam, P.dxyz2, P.dt2, P.dE2, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -796,6 +810,10 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
     return SSO_E_CUDA;
   }
   AL(dinv, B * P.ndof);
+  if (h->precond == 1) {
+    AL(binv, 21 * (int64_t)B * std::max<int32_t>(P.n_own, 1));
+    AL(zb, B * P.ndof);
+  }
   AL(f, B * P.ndof);
   AL(fbc, B * P.ndof);
   AL(xs, B * P.ndof);
@@ -906,6 +924,7 @@ int sso_options_default(sso_options* o) {
   o->reliable = 1;
   o->assembly = 0;
   o->storage = 0;
+  o->precond = 0;
   return SSO_OK;
 }
 
@@ -957,6 +976,10 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
     g_create_err = "options: batch >= 1, and batch > 1 needs n_parts == nranks == 1";
     return SSO_E_INVALID;
   }
+  if (o.precond < 0 || o.precond > 1 || (o.precond == 1 && o.storage == 2)) {
+    g_create_err = "options: precond must be 0 or 1 (1 needs storage 0, 1 or 3)";
+    return SSO_E_INVALID;
+  }
   if (o.storage < 0 || o.storage > 3) {
     g_create_err = "options: storage must be 0, 1, 2 or 3";
     return SSO_E_INVALID;
@@ -988,7 +1011,8 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
   h->batch = o.batch;
   h->reliable = o.reliable;
   h->assembly = o.assembly;
-  h->storage = o.storage == 0 ? 3 : o.storage;  // default: upper blocks + pull SpMV (single-strip handles)
+  h->storage = o.storage == 0 ? 3 : o.storage;
+  h->precond = o.precond;  // default: upper blocks + pull SpMV (single-strip handles)
   h->g_nodes = mesh->n_nodes;
   h->g_beams = mesh->n_beams;
   h->g_quads = mesh->n_quads;
@@ -1126,6 +1150,15 @@ int sso_assemble(sso_handle h) {
     CKL(h);
   }
   if ((rc = assemble_pass(h, false))) return rc;
+  if (h->precond == 1) {
+    for (auto& pp : h->parts) {
+      Part& P = *pp;
+      Scope sc(h, F_ASSEMBLE);
+      launch_block_inverse(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.pull ? 3 : (P.sym ? 2 : 0), P.binv,
+                           P.flags, P.bs);
+    }
+    CKL(h);
+  }
   rc = check_flags(h);
   if (rc) return rc;
   h->assembled = true;
@@ -1148,7 +1181,10 @@ static int replace_step(sso_ctx* h, int mode) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     launch_cg_check(h->stream, P.st, mode, P.B);
-    launch_cg_replace(h->stream, (int)P.ndof_own, P.fbc, P.tmp, P.dinv, P.r, P.p, P.partial, P.st, mode, P.bs);
+    if (P.binv)
+      launch_cg_replace_block(h->stream, P.n_own, P.fbc, P.tmp, P.binv, P.r, P.zb, P.partial, P.st, mode, P.bs);
+    else
+      launch_cg_replace(h->stream, (int)P.ndof_own, P.fbc, P.tmp, P.dinv, P.r, P.p, P.partial, P.st, mode, P.bs);
   }
   if (h->distributed()) {
     if ((rc = allreduce(h, 2))) return rc;
@@ -1290,8 +1326,12 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     Scope sc(h, F_UPDATE);
-    launch_cg_init(h->stream, (int)P.ndof_own, lift ? P.feff : P.f, P.fixed_mask, P.dinv, P.fbc, P.xs, P.r, P.p,
-                   P.partial, P.st, warm, P.tmp, P.bs);
+    if (P.binv)
+      launch_cg_init_block(h->stream, P.n_own, lift ? P.feff : P.f, P.fixed_mask, P.binv, P.fbc, P.xs, P.r, P.p,
+                           P.zb, P.partial, P.st, warm, P.tmp, P.bs);
+    else
+      launch_cg_init(h->stream, (int)P.ndof_own, lift ? P.feff : P.f, P.fixed_mask, P.dinv, P.fbc, P.xs, P.r,
+                     P.p, P.partial, P.st, warm, P.tmp, P.bs);
   }
   if (dist) {
     if ((rc = allreduce(h, 3))) return rc;

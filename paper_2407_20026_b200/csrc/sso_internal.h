@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -191,6 +192,24 @@ int make_pull_tmap(const double* vals, int64_t rows, CUtensorMap* out);
 void launch_spmv(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
                  const int32_t* node_col, const double* vals, const double* x, double* y,
     const BatchStrides& bs = BatchStrides());
+// Node-block Jacobi preconditioner (sso_options.precond = 1, block_jacobi.cu).  binv
+// [B][21][n] packed upper triangles of (K_nn)^-1; layout 0 full runs, 2 upper row-major
+// runs, 3 upper column-major runs.
+void launch_block_inverse(cudaStream_t s, int n_nodes, const int64_t* node_ptr, const int32_t* node_col,
+                          const double* vals, int layout, double* binv, DevFlags* flags,
+                          const BatchStrides& bs = BatchStrides());
+void launch_cg_init_block(cudaStream_t s, int n_nodes, const double* f, const uint8_t* fixed_mask,
+                          const double* binv, double* fbc, double* x, double* r, double* p, double* z,
+                          double* partial, CgState* st, int warm, const double* Kx0,
+                          const BatchStrides& bs = BatchStrides());
+void launch_cg_update_block(cudaStream_t s, int n_nodes, const double* binv, double* x, double* r,
+                            const double* p, const double* q, double* z, double* partial, CgState* st,
+                            const BatchStrides& bs = BatchStrides());
+void launch_cg_pupdate_z(cudaStream_t s, int ndof, const double* z, double* p, CgState* st,
+                         const BatchStrides& bs = BatchStrides());
+void launch_cg_replace_block(cudaStream_t s, int n_nodes, const double* fbc, const double* Kx, const double* binv,
+                             double* r, double* z, double* partial, CgState* st, int mode,
+                             const BatchStrides& bs = BatchStrides());
 void launch_residual_norm(cudaStream_t s, int ndof, const double* f, const double* Kx,
                           double* partial, CgState* st,
     const BatchStrides& bs = BatchStrides());

@@ -397,3 +397,62 @@ def test_pull_storage_batched(sso):
     for b in range(B):
         assert np.linalg.norm(out[3][0][b] - out[1][0][b]) <= 1e-9 * np.linalg.norm(out[1][0][b])
         assert out[3][1][b] == pytest.approx(out[1][1][b], rel=1e-10)
+
+
+@pytest.mark.parametrize("storage", [1, 3])
+@pytest.mark.parametrize("name", ["C2", "ragged", "mixed", "beamgrid", "tiny3edge"])
+def test_block_jacobi_against_oracle(sso, cases, name, storage):
+    """precond = 1 (node-block Jacobi, reading c17): u equals the oracle's Cholesky u,
+    C and the gradient follow, and the iteration count tracks the oracle's block PCG."""
+    import scipy.sparse as sps
+    from oracle import solve as OS
+    c = oracle_case(cases, name)
+    P = c["P"]
+    m = sso.Model(P, rtol=1e-12, storage=storage, precond=1)
+    m.assemble()
+    u, info = m.solve(P["f"])
+    assert info["status"] == 0 and info["true_rel_res"] < 1e-11
+    uref = c["u"]
+    assert np.linalg.norm(u - uref) <= TOL_U * np.linalg.norm(uref)
+    Cv, dX, _ = m.grad(sso.OBJ_COMPLIANCE)
+    Cref = OG.compliance(P["f"], uref)
+    assert abs(Cv - Cref) <= TOL_C * abs(Cref)
+    nd = 6 * len(P["x"])
+    Kb = sps.csr_matrix((c["vbc"], c["ci"], c["rp"]), shape=(nd, nd))
+    fb = P["f"].copy()
+    fb[list(c["fixed"])] = 0.0
+    _, oi = OS.pcg_block(Kb, fb, rtol=1e-12)
+    assert abs(info["iters"] - oi["iters"]) <= max(3, 0.05 * oi["iters"])
+
+
+def test_block_jacobi_batched_and_partitioned(sso):
+    """precond = 1 with a batch of designs and with in-process strips equals precond = 1
+    single runs (and the oracle)."""
+    designs = [W.config5_design(b, n=12) for b in range(3)]
+    mb = sso.Model(designs[0], rtol=1e-12, batch=3, precond=1)
+    mb.set_design(z=np.stack([d["z"] for d in designs]), t=np.stack([d["t"] for d in designs]))
+    mb.assemble()
+    U, infos = mb.solve(np.stack([d["f"] for d in designs]))
+    for b, d in enumerate(designs):
+        uref, _, _ = OG.evaluate(d)
+        assert infos[b]["status"] == 0
+        assert np.linalg.norm(U[b] - uref) <= TOL_U * np.linalg.norm(uref)
+    P = W.config2()
+    mp = sso.Model(P, rtol=1e-12, n_parts=3, precond=1)
+    mp.assemble()
+    up, ip = mp.solve(P["f"])
+    m1 = sso.Model(P, rtol=1e-12, precond=1, storage=1)
+    m1.assemble()
+    u1, i1 = m1.solve(P["f"])
+    assert ip["status"] == 0 and abs(ip["iters"] - i1["iters"]) <= 2
+    uref, _, _ = OG.evaluate(P)
+    assert np.linalg.norm(up - uref) <= TOL_U * np.linalg.norm(uref)
+    # point vs block: fewer iterations with the node blocks on a shell
+    m0 = sso.Model(P, rtol=1e-12, precond=0)
+    m0.assemble()
+    _, i0 = m0.solve(P["f"])
+    assert i1["iters"] < i0["iters"]
+    with pytest.raises(Exception):
+        sso.Model(P, precond=1, storage=2)
+    with pytest.raises(Exception):
+        sso.Model(P, precond=2)
