@@ -42,12 +42,14 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """dram bytes per SpMV launch from the committed ncu --set full summary, if any."""
+def ncu_traffic(storage_kind):
+    """dram bytes per SpMV launch of the kernel this storage kind runs, from the committed
+    ncu --set full capture (profiles/spmv_traffic.json), if any."""
     p = os.path.join(ROOT, "profiles", "spmv_traffic.json")
     if os.path.exists(p):
         with open(p) as fh:
-            return json.load(fh).get("dram_bytes_per_launch")
+            e = json.load(fh).get("by_storage", {}).get(str(storage_kind))
+        return e.get("dram_bytes_per_launch") if e else None
     return None
 
 
@@ -343,7 +345,7 @@ def run_gpu(args):
                            2: "spmv_sym pass1+pass2 (upper-block K, CG q = K p, p^T q)",
                            3: "spmv_pull_dot (upper-block K, one-pass pull, CG q = K p, p^T q)"}[symmetric],
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(),
+                "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(symmetric),
                 "algorithmic_bytes_per_launch": spmv_bytes, "avg_launch_ms": spmv_avg_ms,
                 "launches": spmv_n, "peak_source": peak_src,
                 "share_of_step": (spmv_avg_ms * (cg_iters + 1) * args.steps / ms_total) if spmv_n else None,
