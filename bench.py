@@ -353,7 +353,7 @@ def run_gpu(args):
     asm_ms = (el_ms + as_ms) / max(args.steps, 1)
     clocks = clk.summary()
 
-    # ---- the same evaluation with the node-block Jacobi preconditioner (reading c17) ----
+    # ---- the same evaluation with the node-block Jacobi preconditioner (reading c19) ----
     alt = None
     if world == 1 and args.precond == 0 and args.virtual_parts == 1 and not args.no_alt:
         mb = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index, storage=args.storage,

@@ -150,7 +150,7 @@ typedef struct {
    * 2 and 3 apply to single-strip handles (partitioned handles keep full storage).
    * Exports return the full CSR.  Other values -> SSO_E_INVALID. */
   int32_t storage;
-  /* Preconditioner of the CG (reading c10 / c17): 0 (default) = point Jacobi, M =
+  /* Preconditioner of the CG (reading c10 / c19): 0 (default) = point Jacobi, M =
    * diag(K_bc) (the north star's); 1 = node-block Jacobi, M = blockdiag(K_nn) of the 6x6
    * diagonal block of every node (inverted once per sso_assemble; about 30 % fewer
    * iterations on shells).  precond 1 with storage 2 -> SSO_E_INVALID. */

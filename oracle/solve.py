@@ -11,7 +11,7 @@ SURVEY.md §8(c) C5 (reading c10):
     stop when |r|_2 <= rtol |f|_2;
     beta = r_new.z_new / r_old.z_old;  p = z + beta p.
 
-The node-block variant (reading c17, `sso_options.precond = 1`) is
+The node-block variant (reading c19, `sso_options.precond = 1`) is
 the same algorithm with M = blockdiag(K_nn), the 6x6 diagonal block of every
 node of K_bc (a Jacobi preconditioner over the node DOF blocks): z = M^-1 r
 by a 6x6 solve per node.
@@ -103,7 +103,7 @@ def node_blocks(K, ndof):
 
 def pcg_block(K, f, rtol=1e-12, max_iter=100000):
     """Textbook node-block Jacobi PCG: the loop of pcg() with z = M^-1 r,
-    M = blockdiag(K_nn) (reading c17).  Returns (x, info) like pcg()."""
+    M = blockdiag(K_nn) (reading c19).  Returns (x, info) like pcg()."""
     nd = f.shape[0]
     B = node_blocks(K, nd)
 

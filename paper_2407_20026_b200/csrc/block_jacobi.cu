@@ -1,6 +1,6 @@
 // A3 variant — node-block Jacobi preconditioner for the PCG (sm_100a).
 //
-// sso_options.precond = 1 (reading c17): M = blockdiag(K_nn), the 6x6
+// sso_options.precond = 1 (reading c19): M = blockdiag(K_nn), the 6x6
 // diagonal block of every node of K_bc, instead of diag(K_bc).  The CG loop is
 // the one of pcg.cu (reading c10) with z = M^-1 r; oracle: oracle/solve.py
 // pcg_block.  Shell nodes couple translations and rotations inside the node

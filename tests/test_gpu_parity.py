@@ -402,7 +402,7 @@ def test_pull_storage_batched(sso):
 @pytest.mark.parametrize("storage", [1, 3])
 @pytest.mark.parametrize("name", ["C2", "ragged", "mixed", "beamgrid", "tiny3edge"])
 def test_block_jacobi_against_oracle(sso, cases, name, storage):
-    """precond = 1 (node-block Jacobi, reading c17): u equals the oracle's Cholesky u,
+    """precond = 1 (node-block Jacobi, reading c19): u equals the oracle's Cholesky u,
     C and the gradient follow, and the iteration count tracks the oracle's block PCG."""
     import scipy.sparse as sps
     from oracle import solve as OS

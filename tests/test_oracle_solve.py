@@ -4,7 +4,7 @@
     Lagrange-multiplier system (PAPER.md Eq. 2-3) solved by dense LU;
   * the textbook Jacobi-PCG u equals the Cholesky u;
   * the Lanczos Ritz values bracket inside the true spectrum of D^-1/2 K D^-1/2;
-  * node-block Jacobi PCG (reading c17): u equals the Cholesky u; one iteration
+  * node-block Jacobi PCG (reading c19): u equals the Cholesky u; one iteration
     on a block-diagonal K (M = K exactly); the point PCG's iterates when every
     diagonal block is diagonal.
 """
