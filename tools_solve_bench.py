@@ -9,7 +9,8 @@ n = int(os.environ.get("N", "408"))
 sup = os.environ.get("SUP", "clamped_edges")
 P = W.shell_config3(n, cfg=4 if sup == "c4" else 3, supports=sup)
 m = sso.Model(P, rtol=1e-10, n_parts=int(os.environ.get("PARTS", "1")),
-              reliable=int(os.environ.get("REL", "1")), storage=int(os.environ.get("STORAGE", "0")))
+              reliable=int(os.environ.get("REL", "1")), storage=int(os.environ.get("STORAGE", "0")),
+              precond=int(os.environ.get("PRECOND", "0")))
 m.assemble()
 f = torch.from_numpy(P["f"]).cuda()
 u = torch.zeros_like(f)
@@ -22,9 +23,10 @@ for _ in range(int(os.environ.get("REPS", "3"))):
     ts.append(info["ms"])
 ms, cnt = m.profile_read("spmv")
 ndof, nnz, nb = m.sizes()
-byts = 8 * nnz + 4 * nb + 8 * (m.n_nodes + 1) + 16 * ndof
+sv, sb, kind = m.storage_info()
+byts = 8 * sv + 4 * sb + 8 * (m.n_nodes + 1) + 16 * ndof if kind != 3 else 8 * sv + 4 * sb + 64 * m.n_nodes + 16 * ndof
 avg = ms / max(cnt, 1)
-print(json.dumps({"variant": os.environ.get("SSO_SPMV_VARIANT", "0"), "rel": os.environ.get("REL", "1"), "storage": os.environ.get("STORAGE", "0"),
+print(json.dumps({"precond": os.environ.get("PRECOND", "0"), "variant": os.environ.get("SSO_SPMV_VARIANT", "0"), "rel": os.environ.get("REL", "1"), "storage": os.environ.get("STORAGE", "0"),
                   "sup": sup, "n": n, "iters": info["iters"],
                   "solve_ms": min(ts), "us_per_iter": 1000 * min(ts) / info["iters"],
                   "spmv_us": 1000 * avg, "spmv_GBs": byts / (avg / 1000) / 1e9,
