@@ -9,6 +9,6 @@ python bench.py --workload C5 --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_c
 python bench.py --steps 1 --warmup 0 --no-cpu --no-alt > gpurun_out/plain_launch.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 1 --warmup 0 --no-cpu --no-alt > gpurun_out/ncu_launch.log 2>&1; echo "ncu list rc=$?"
-python tools_ncu_target.py > gpurun_out/plain_target.log 2>&1 && \
+python tools/ncu_target.py > gpurun_out/plain_target.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"spmv_pull|cg_update|cg_pupdate|quad_assemble|quad_grad" -s 6 -c 8 \
-    -o gpurun_out/prof_round python tools_ncu_target.py > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+    -o gpurun_out/prof_round python tools/ncu_target.py > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"

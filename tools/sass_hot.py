@@ -1,5 +1,5 @@
 """Summarise an ncu source page (SASS) CSV: per-opcode executed instructions and stall samples,
-and the hottest instructions.  Usage: ncu -i rep --page source --csv | python tools_sass_hot.py [N]"""
+and the hottest instructions.  Usage: ncu -i rep --page source --csv | python tools/sass_hot.py [N]"""
 import csv
 import sys
 from collections import defaultdict
