@@ -136,8 +136,7 @@ typedef struct {
    * matrices) when the mesh is quad-only with node degree <= 10; 1 = always the staged
    * path (element kernel, then the segmented-sum gather). */
   int32_t assembly;
-  /* 0 (default) = storage 3 for single-strip handles (partitioned handles always use
-   * full storage).  1 = full CSR storage.  2 = single-strip handles keep only the
+  /* 0 (default) = storage 3.  1 = full CSR storage.  2 = single-strip handles keep only the
    * upper node blocks (n, m >= n) of the symmetric K_bc (44 % fewer value bytes on
    * shell grids); pass 1 of the SpMV forms the upper row sums, the transpose
    * contributions (sender-ordered slots) and p^T K p, the x / r update adds each
@@ -147,7 +146,8 @@ typedef struct {
    * the stored blocks (n, m) of its lower neighbours n < m (an L2 hit: nodes are
    * dealt round-robin, so the owner streams them in the same window) and forms
    * y_m = sum_{j>=m} K_mj x_j + sum_{n<m} K_nm^T x_n; no transpose buffer.  Storage
-   * 2 and 3 apply to single-strip handles (partitioned handles keep full storage).
+   * 3 also applies to strips (owned nodes precede halo nodes locally, so lower
+   * neighbours are owned); storage 2 is single-strip only (else full storage).
    * Exports return the full CSR.  Other values -> SSO_E_INVALID. */
   int32_t storage;
   /* Preconditioner of the CG (reading c10 / c19): 0 (default) = point Jacobi, M =

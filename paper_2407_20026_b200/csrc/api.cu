@@ -698,7 +698,11 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
     P.max_deg = std::max<int>(P.max_deg, (int)(P.pat.node_ptr[n + 1] - P.pat.node_ptr[n]));
   }
   P.fused = h->assembly == 0 && P.n_beams == 0 && P.n_quads > 0 && P.max_deg <= fused_max_degree();
-  P.sym = (h->storage == 2 || h->storage == 3) && L.n_parts == 1 && h->nranks == 1 && P.n_own == P.n_nodes;
+  // Storage 3 works on strips too: owned nodes come first in the local numbering, so every
+  // lower neighbour (n < m) of an owned row m is owned and stores the block (n, m) itself, and
+  // halo neighbours are always upper.  Storage 2 (receiver slots) stays single-strip.
+  P.sym = (h->storage == 3) ||
+          (h->storage == 2 && L.n_parts == 1 && h->nranks == 1 && P.n_own == P.n_nodes);
   P.pull = P.sym && h->storage == 3;
   if (P.pull && P.pat.node_ptr[P.n_nodes] >= INT32_MAX / 36) {  // 32-bit block offsets in the pull kernel
     h->err = "storage 3: too many node blocks for 32-bit offsets";
