@@ -354,7 +354,7 @@ double* vec_of(Part& P, int v) {
 // its halo filled (partitioned handles).
 void spmv_apply(cudaStream_t s, Part& P, const double* x, double* y, CgState* st) {
   if (P.pull)
-    launch_spmv_pull(s, &P.pull_tmap, P.n_own, (int)(P.bs.nnz / 36), P.pdesc, P.node_col, P.lpull, P.vals, x, y,
+    launch_spmv_pull(s, &P.pull_tmap, P.n_own, (int)(P.bs.nnz / PULL_BLOCK), P.pdesc, P.node_col, P.lpull, P.vals, x, y,
                      st ? P.partial : nullptr, st, P.bs);
   else if (P.sym && st)
     launch_spmv_sym_cg(s, P.n_own, P.node_ptr, P.node_col, P.vals, x, y, P.tbuf, P.partial, st, P.bs);
@@ -716,7 +716,7 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   P.bs.node = P.n_nodes;
   P.bs.quad = P.n_quads;
   P.bs.stage = 36 * P.n_staged;
-  P.bs.nnz = 36 * (P.sym ? P.up.n_ublocks() : P.n_blocks);
+  P.bs.nnz = P.pull ? PULL_BLOCK * P.up.n_ublocks() : 36 * (P.sym ? P.up.n_ublocks() : P.n_blocks);
   P.bs.tbuf = 6 * std::max<int64_t>(P.sym && !P.pull ? P.up.n_tslots : 0, 1);
   P.bs.dof = P.ndof;
   P.bs.partial = 16 * (int64_t)cg_grid();
@@ -809,7 +809,8 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   AL(sendbuf, 6 * std::max<int64_t>(P.n_send, 1));
   AL(stage, B * P.bs.stage);
   AL(vals, B * P.bs.nnz);
-  if (P.pull && make_pull_tmap(P.vals, B * P.bs.nnz / 36, &P.pull_tmap)) {
+  if (P.pull) CK(h, cudaMemset(P.vals, 0, B * P.bs.nnz * sizeof(double)));  // record pads stay zero
+  if (P.pull && make_pull_tmap(P.vals, B * P.bs.nnz / PULL_BLOCK, &P.pull_tmap)) {
     h->err = "storage 3: cuTensorMapEncodeTiled failed";
     return SSO_E_CUDA;
   }
@@ -1940,7 +1941,7 @@ int sso_export_csr(sso_handle h, int64_t* row_ptr, int32_t* col_idx, double* val
     Part& P = *pp;
     const HostPattern& T = P.pat;
     if (vals) {
-      pv.resize((size_t)(36 * P.stored_blocks));
+      pv.resize((size_t)((P.pull ? PULL_BLOCK : 36) * P.stored_blocks));
       CK(h, cudaMemcpy(pv.data(), P.vals, pv.size() * sizeof(double), cudaMemcpyDeviceToHost));
     }
     // value (a, b) of block (n, k-th full neighbour): symmetric storage keeps the
@@ -1952,18 +1953,19 @@ int sso_export_csr(sso_handle h, int64_t* row_ptr, int32_t* col_idx, double* val
       const int32_t m = T.node_col[b0 + k];
       const UpperPattern& U = P.up;
       // run position of (row a, column 6 ku + b): row-major (storage 2) or column-major (3)
-      auto at = [&](int64_t ud, int64_t ku, int ra, int cb) {
-        return P.pull ? 6 * (6 * ku + cb) + ra : 6 * ra * ud + 6 * ku + cb;
+      // (storage 2) row-major runs; (storage 3) PULL_BLOCK records, column-major values
+      auto at = [&](int64_t u0, int64_t ud, int64_t ku, int ra, int cb) {
+        return P.pull ? PULL_BLOCK * (u0 + ku) + 6 * cb + ra : 36 * u0 + 6 * ra * ud + 6 * ku + cb;
       };
       if (m >= n) {
         const int64_t ud = U.uptr[n + 1] - U.uptr[n];
         const int64_t ku = k - (deg - ud);
-        return pv[36 * U.uptr[n] + at(ud, ku, a, b)];
+        return pv[at(U.uptr[n], ud, ku, a, b)];
       }
       const int64_t ud = U.uptr[m + 1] - U.uptr[m];
       const int32_t* c0 = U.ucol.data() + U.uptr[m];
       const int64_t ku = std::lower_bound(c0, c0 + ud, n) - c0;
-      return pv[36 * U.uptr[m] + at(ud, ku, b, a)];
+      return pv[at(U.uptr[m], ud, ku, b, a)];
     };
     for (int32_t n = 0; n < P.n_own; ++n) {
       const int64_t b0 = T.node_ptr[n];

@@ -320,13 +320,15 @@ __global__ void __launch_bounds__(128, 4) quad_assemble_fused_kernel(
   // ---- supports (elimination), Jacobi diagonal, one coalesced write ----------
   if (node_ok) {
     const uint8_t mrow = fixed_mask[n];
-    double* out = vals + 36 * b0;
+    // run layout: row-major (a, rem) runs of 36 deg values, or (cm) one PULL_BLOCK record per
+    // block with the values column-major; v walks the values in storage order
+    double* out = vals + (cm ? PULL_BLOCK : 36) * b0;
     for (int v = t16; v < 36 * deg; v += 16) {
-      // v walks the run in its storage order: row-major (a, rem) or column-major (rem, a)
       const int a = cm ? v % 6 : v / rowlen;
       const int rem = cm ? v / 6 : v - a * rowlen;
       const int kb = rem / 6;
       const int b = rem - 6 * kb;
+      const int dst = cm ? PULL_BLOCK * kb + 6 * b + a : v;
       const int m = node_col[b0 + kb];
       double s = nbuf[a * rowlen + rem];
       const bool diag = (m == n) && (a == b);
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(128, 4) quad_assemble_fused_kernel(
           s = 0.0;
         }
       }
-      out[v] = s;
+      out[dst] = s;
       if (diag) {
         if (!(s > 0.0)) atomicMin(&flags->singular_dof, (int)(6 * n + a));
         dinv[6 * n + a] = 1.0 / s;

@@ -99,7 +99,7 @@ __device__ __forceinline__ bool grid_sum(double (&v)[NV], double* partial, unsig
 
 // (K_nn)^-1 of every owned node from the assembled values.  Run layout: 0 full storage
 // (row-major runs, diagonal block at its rank in the node's column list), 2 upper blocks
-// row-major (diagonal block first), 3 upper blocks column-major (diagonal block first).
+// row-major (diagonal block first), 3 upper-block records (PULL_BLOCK, column-major; diagonal first).
 __global__ void __launch_bounds__(128) block_inverse_kernel(int n_nodes, const int64_t* __restrict__ node_ptr,
                                                             const int32_t* __restrict__ node_col,
                                                             const double* __restrict__ vals, int layout,
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(128) block_inverse_kernel(int n_nodes, const i
     rs = 6 * deg;
     cs = 1;
   } else {
-    off = 36 * b0;
+    off = PULL_BLOCK * b0;
     rs = 1;
     cs = 6;
   }

@@ -650,36 +650,32 @@ __global__ void __launch_bounds__(SPMV_WARPS * 32, MINB) spmv_tma_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// Symmetric "pull" SpMV (storage 3).  Only the upper node blocks (n, m >= n)
-// are stored, each node's run COLUMN-major: value (a, c) of node n's upper run
-// (row 6n + a, run column c = 6k + b of upper block k) sits at 36 uptr[n] + 6c + a,
-// so every 6x6 block is one contiguous 288-byte chunk and every column of it six
-// contiguous values.  The warp that owns row node m streams, into one ring slot,
-// its own upper run AND the upper blocks (n, m) of its lower neighbours n < m
-// (one TMA bulk copy each; their location comes from the pull list), so
-//   y_m = sum_{j >= m} K_mj x_j + sum_{n < m} K_nm^T x_n
-// is formed in one pass with no transpose buffer, no atomics and a fixed order.
-// Nodes are dealt to warps round-robin (warp w takes w, w + NW, ...): at any time
-// the GPU works on one window of ~NW consecutive nodes, so a pulled block was
-// streamed by its owner (or is about to be) within one window -- it is an L2
-// hit, and DRAM sees each stored value once (~0.56 of the full-storage bytes on
-// shell grids).  Lane <-> one column slot per pass: own column c: acc[a] +=
-// v[a] x_{m(c)}[b]; pulled column b of block j: acc[b] += sum_a v[a] x_n[a].
+// Symmetric "pull" SpMV (storage 3).  Only the upper node blocks (n, m >= n) are
+// stored.  Each block is one contiguous record of PULL_BLOCK = 38 doubles: the 6x6
+// values COLUMN-major (K[a][b] at 6b + a) followed by 2 zero pad doubles.  The pad
+// makes the record stride 19 16-byte words (odd), which spreads the 16-byte
+// shared-memory reads of the consumers over all bank groups (an 18-word stride
+// keeps them on even groups: 2-way conflicts).  A node's upper run is its records
+// for k = 0 .. udeg-1 (block k at PULL_BLOCK (uptr[n] + k)).  The row node m needs
+//   y_m = sum_{j >= m} K_mj x_j + sum_{n < m} K_nm^T x_n:
+// its own run (contiguous) and the records (n, m) of its lower neighbours n < m,
+// formed in one pass with no transpose buffer, no atomics and a fixed order.
+// Nodes are processed in round-robin chunks, so at any time the GPU works on one
+// window of consecutive nodes and a pulled record was streamed by its owner (or is
+// about to be) within that window -- an L2 hit: DRAM sees each stored value once
+// (~0.56 of the full-storage bytes on shell grids).
 // ---------------------------------------------------------------------------
 // Per-node pull descriptor (16 int32, built on the host, SSO pattern order):
-//   d[0] = first upper block of the node (its run starts at 36 d[0]),
+//   d[0] = first upper block of the node (its run starts at PULL_BLOCK d[0]),
 //   d[1] = udeg | ldeg << 8 | fits << 16,
 //   fits:  d[2 .. 2+udeg) upper block columns, then (source node, upper block) of each
 //          pulled block at d[2+udeg+2j], d[3+udeg+2j];
 //   !fits: d[2] = first pull-list entry (lptr) -- the node takes the general path.
-// A node fits the ring slot when udeg <= PULL_MAX_UDEG and ldeg <= 4.  Slot layout
-// (128-byte aligned): the pulled blocks, fetched by ONE TMA tile::gather4 of 4 rows of
-// the [blocks][36] view of the values (padding rows repeat the node's own first block),
-// then the own upper run (one bulk copy).
+// A node fits when udeg <= PULL_MAX_UDEG and ldeg <= 4: its pulled records come with
+// ONE TMA tile::gather4 of 4 rows of the [blocks][PULL_BLOCK] view of the values
+// (padding rows repeat the node's own first block).
 constexpr int PULL_DESC = 16;
 constexpr int PULL_MAX_UDEG = 5;
-constexpr int PULL_SLOT_DOUBLES = 336;  // 4 pulled + 5 own blocks = 324 doubles, rounded to 128 B
-constexpr int PULL_OWN_OFF = 144;       // doubles: own run after the 4 gathered rows
 
 __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int r0, int r1, int r2, int r3,
                                             uint64_t* bar, uint64_t policy) {
@@ -691,237 +687,6 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-template <bool DOT, int STAGES, int MINB>
-__global__ void __launch_bounds__(SPMV_WARPS * 32, MINB) spmv_pull_kernel(
-    const __grid_constant__ CUtensorMap tmap, int n_nodes, int rows_per_design, const int32_t* __restrict__ pdesc,
-    const int32_t* __restrict__ ucol, const int2* __restrict__ lpull, const double* __restrict__ vals,
-    const double* __restrict__ p, double* __restrict__ q, double* __restrict__ partial, CgState* st,
-    BatchStrides bs) {
-  constexpr int SLOT_DOUBLES = PULL_SLOT_DOUBLES;
-  const int row0 = blockIdx.y * rows_per_design;  // this design's first row of the gather view
-  constexpr unsigned FULL = 0xffffffffu;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t bar[SPMV_WARPS][STAGES];
-  __shared__ double2 red_all[SPMV_WARPS][32];  // per-warp row-pair partials of the current node
-  __shared__ double sm[32];
-  {  // design of a batch (blockIdx.y)
-    const int bd = blockIdx.y;
-    vals += bd * bs.nnz;
-    p += bd * bs.dof;
-    q += bd * bs.dof;
-    if (DOT) {
-      partial += bd * bs.partial;
-      st += bd;
-    }
-  }
-  if (DOT && st->done) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * SPMV_WARPS + warp;
-  const int64_t NW = (int64_t)gridDim.x * SPMV_WARPS;
-  const int cnt = gw < n_nodes ? (int)(((int64_t)n_nodes - 1 - gw) / NW + 1) : 0;
-  double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * STAGES * SLOT_DOUBLES;
-  uint64_t* wbar = bar[warp];
-  if (lane == 0) {
-#pragma unroll
-    for (int s = 0; s < STAGES; ++s) mbar_init(&wbar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  const uint64_t pol = evict_first_policy();
-  __syncwarp();
-  // descriptor word `lane` of node k (lanes >= 16 and k >= cnt: 0)
-  auto desc = [&](int k) -> int {
-    return (k < cnt && lane < PULL_DESC) ? __ldg(pdesc + PULL_DESC * (gw + (int64_t)k * NW) + lane) : 0;
-  };
-  // warp-collective: node k's pulled blocks (one gather4) and own upper run (one bulk copy)
-  // into ring slot k % STAGES; lane 0 issues both
-  auto issue = [&](int k, int d) {
-    const int s = k % STAGES;
-    const int b0 = __shfl_sync(FULL, d, 0), fl = __shfl_sync(FULL, d, 1);
-    const int udeg = fl & 255, ldeg = (fl >> 8) & 255;
-    const bool fits = (fl >> 16) & 1;
-    int r[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int g = __shfl_sync(FULL, d, min(3 + udeg + 2 * i, PULL_DESC - 1));
-      r[i] = row0 + (i < ldeg ? g : b0);
-    }
-    double* dst = ring + (size_t)s * SLOT_DOUBLES;
-    // the slot was last read by node k - STAGES (before the previous loop-end __syncwarp)
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (lane == 0) {
-      if (fits) {
-        mbar_arrive_expect_tx(&wbar[s], (unsigned)(288 * udeg + (ldeg ? 1152 : 0)));
-        if (ldeg) tma_gather4(dst, &tmap, r[0], r[1], r[2], r[3], &wbar[s], pol);
-        bulk_g2s(dst + PULL_OWN_OFF, vals + 36 * (int64_t)b0, (unsigned)(288 * udeg), &wbar[s], pol);
-      } else {
-        mbar_arrive(&wbar[s]);  // general node: read from global, keep the phase sequence
-      }
-    }
-  };
-  // Lane plan (fits): lane = 3 j + h (lane < 27) owns block j of the slot (own upper blocks
-  // first, then the pulled ones) and output rows 2h, 2h+1 of the node:
-  //   own K_mj:    t_e = sum_b K_mj[2h+e][b] x_j[b]      (column-major: pairs at 6b + 2h)
-  //   pulled K_nm: t_e = sum_a K_nm[a][2h+e] x_n[a]      (columns 2h, 2h+1: 12 contiguous)
-  // (t0, t1) go to a per-warp reduction row red[j][h]; lanes a < 6 then sum column a over
-  // the blocks in ascending j: y[a] (fixed order, no shuffles of doubles).
-  const int jl = lane / 3, hl = lane - 3 * jl;
-  double2* red = red_all[warp];
-  auto xnode = [&](int d) -> int {  // node whose x this lane gathers (own: column node, pulled: source)
-    const int fl = __shfl_sync(FULL, d, 1);
-    const int udeg = fl & 255;
-    const int src = jl < udeg ? 2 + jl : 2 + 2 * jl - udeg;
-    return __shfl_sync(FULL, d, min(src, PULL_DESC - 1));
-  };
-  auto gather = [&](int d, int node, double2& x0, double2& x1, double2& x2) {
-    const int fl = __shfl_sync(FULL, d, 1);
-    const int nb = (fl & 255) + ((fl >> 8) & 255);
-    if (((fl >> 16) & 1) && jl < nb) {
-      const double2* xp = reinterpret_cast<const double2*>(p + 6 * (int64_t)node);
-      x0 = xp[0];
-      x1 = xp[1];
-      x2 = xp[2];
-    }
-  };
-  double pq[1] = {0.0};
-  // Software pipeline: node k computes while nodes k+1 .. k+STAGES-1 stream into the ring,
-  // the descriptors of the nodes up to k+P are in flight and the x operands of node k+1 are
-  // being gathered.  The loop is unrolled by the descriptor period P (a ring of P registers,
-  // P even so the x operands ping-pong) so no in-flight register is ever moved.
-  constexpr int P = (STAGES + 2) & ~1;  // even, >= STAGES + 1
-  int dd[P];
-#pragma unroll
-  for (int j = 0; j < P; ++j) dd[j] = desc(j);
-#pragma unroll
-  for (int j = 0; j < STAGES - 1; ++j)
-    if (j < cnt) issue(j, dd[j]);
-  double2 xs[2][3];
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) xs[h][j] = make_double2(0.0, 0.0);
-  gather(dd[0], xnode(dd[0]), xs[0][0], xs[0][1], xs[0][2]);
-#pragma unroll 1
-  for (int k0 = 0; k0 < cnt; k0 += P) {
-#pragma unroll
-    for (int u = 0; u < P; ++u) {
-      const int k = k0 + u;
-      if (k >= cnt) break;
-      const int cu = u & 1, nu = cu ^ 1;  // x operands of node k / node k+1
-      if (k + STAGES - 1 < cnt) issue(k + STAGES - 1, dd[(u + STAGES - 1) % P]);
-      if (k + 1 < cnt) {  // x operands of node k+1
-        const int d1 = dd[(u + 1) % P];
-        gather(d1, xnode(d1), xs[nu][0], xs[nu][1], xs[nu][2]);
-      }
-      // ---- node k ----
-      const int s = k % STAGES;
-      const int64_t n = gw + (int64_t)k * NW;
-      const int dk = dd[u];
-      const int flc = __shfl_sync(FULL, dk, 1);
-      const int b0c = __shfl_sync(FULL, dk, 0), l0c = __shfl_sync(FULL, dk, 2);
-      const double2 xa0 = xs[cu][0], xa1 = xs[cu][1], xa2 = xs[cu][2];
-      dd[u] = desc(k + P);  // node k's descriptor is fully read above
-      const int udeg = flc & 255, ldeg = (flc >> 8) & 255, nb = udeg + ldeg;
-      mbar_wait(&wbar[s], (unsigned)((k / STAGES) & 1));
-      double y = 0.0;
-      if ((flc >> 16) & 1) {
-        if (jl < nb) {
-          const double* blk = ring + (size_t)s * SLOT_DOUBLES + (jl < udeg ? PULL_OWN_OFF + 36 * jl : 36 * (jl - udeg));
-          double t0, t1;
-          if (jl < udeg) {
-            const double* r = blk + 2 * hl;
-            const double2 v0 = *reinterpret_cast<const double2*>(r);
-            const double2 v1 = *reinterpret_cast<const double2*>(r + 6);
-            const double2 v2 = *reinterpret_cast<const double2*>(r + 12);
-            const double2 v3 = *reinterpret_cast<const double2*>(r + 18);
-            const double2 v4 = *reinterpret_cast<const double2*>(r + 24);
-            const double2 v5 = *reinterpret_cast<const double2*>(r + 30);
-            t0 = v0.x * xa0.x;
-            t1 = v0.y * xa0.x;
-            t0 = fma(v1.x, xa0.y, t0);
-            t1 = fma(v1.y, xa0.y, t1);
-            t0 = fma(v2.x, xa1.x, t0);
-            t1 = fma(v2.y, xa1.x, t1);
-            t0 = fma(v3.x, xa1.y, t0);
-            t1 = fma(v3.y, xa1.y, t1);
-            t0 = fma(v4.x, xa2.x, t0);
-            t1 = fma(v4.y, xa2.x, t1);
-            t0 = fma(v5.x, xa2.y, t0);
-            t1 = fma(v5.y, xa2.y, t1);
-          } else {
-            const double* c = blk + 12 * hl;
-            const double2 a01 = *reinterpret_cast<const double2*>(c);
-            const double2 a23 = *reinterpret_cast<const double2*>(c + 2);
-            const double2 a45 = *reinterpret_cast<const double2*>(c + 4);
-            const double2 b01 = *reinterpret_cast<const double2*>(c + 6);
-            const double2 b23 = *reinterpret_cast<const double2*>(c + 8);
-            const double2 b45 = *reinterpret_cast<const double2*>(c + 10);
-            t0 = a01.x * xa0.x;
-            t1 = b01.x * xa0.x;
-            t0 = fma(a01.y, xa0.y, t0);
-            t1 = fma(b01.y, xa0.y, t1);
-            t0 = fma(a23.x, xa1.x, t0);
-            t1 = fma(b23.x, xa1.x, t1);
-            t0 = fma(a23.y, xa1.y, t0);
-            t1 = fma(b23.y, xa1.y, t1);
-            t0 = fma(a45.x, xa2.x, t0);
-            t1 = fma(b45.x, xa2.x, t1);
-            t0 = fma(a45.y, xa2.y, t0);
-            t1 = fma(b45.y, xa2.y, t1);
-          }
-          red[lane] = make_double2(t0, t1);
-        }
-        __syncwarp();
-        if (lane < 6) {
-          const double* rd = reinterpret_cast<const double*>(red) + lane;  // red[3 j + a/2].(a&1)
-          for (int j = 0; j < nb; ++j) y += rd[6 * j];
-        }
-      } else {
-        // general node (degree beyond the slot or the descriptor): from global memory, lane
-        // a < 6 forms row a over the own blocks, then the pulled blocks, in ascending order
-        if (lane < 6) {
-          const int a = lane;
-          for (int kb = 0; kb < udeg; ++kb) {
-            const int m = __ldg(ucol + b0c + kb);
-            const double* blk = vals + 36 * ((int64_t)b0c + kb);
-            double t = 0.0;
-#pragma unroll
-            for (int b = 0; b < 6; ++b) t = fma(blk[6 * b + a], p[6 * (int64_t)m + b], t);
-            y += t;
-          }
-          for (int jp = 0; jp < ldeg; ++jp) {
-            const int2 e = __ldg(lpull + l0c + jp);
-            const double* blk = vals + 36 * (int64_t)e.y;
-            double t = 0.0;
-#pragma unroll
-            for (int b = 0; b < 6; ++b) t = fma(blk[6 * a + b], p[6 * (int64_t)e.x + b], t);
-            y += t;
-          }
-        }
-      }
-      if (lane < 6) {
-        q[6 * n + lane] = y;
-        if (DOT) pq[0] += p[6 * n + lane] * y;
-      }
-      __syncwarp();
-    }
-  }
-  if (DOT) {
-    if (grid_sum<1>(pq, partial, &st->ticket[0], sm) && threadIdx.x == 0) {
-      if (st->dist) {
-        st->red[0] = pq[0];
-        return;
-      }
-      st->pq = pq[0];
-      if (!(pq[0] > 0.0)) {
-        st->status = SSO_E_NOT_SPD;
-        st->done = 1;
-      } else {
-        st->alpha = st->rz / pq[0];
-      }
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Pull SpMV, warp-specialised chunk form (storage 3, the default pull kernel).
 // The per-node bookkeeping that made the warp-per-node form issue-bound (descriptor
@@ -931,34 +696,40 @@ __global__ void __launch_bounds__(SPMV_WARPS * 32, MINB) spmv_pull_kernel(
 // lane i loads node i's descriptor into shared memory and issues that node's
 // gather4 of pulled blocks, lane 0 issues ONE bulk copy of the chunk's own upper
 // runs (consecutive nodes' runs are contiguous).  NB buffers with full / empty
-// mbarriers; CONSUMER warps (PULL_CONSUMERS) each take C / PULL_CONSUMERS nodes of
+// mbarriers; W CONSUMER warps each take C / W nodes of
 // a chunk with no CTA-wide barrier: lane 3j + h forms (t_2h, t_2h+1) of block j
 // (own upper blocks, then pulled) as in the warp form, a per-warp shared row sums
 // them in ascending j.  Chunks holding a node that does not fit (udeg > 5 or
 // ldeg > 4) take a general path reading the values from global memory.
 // ---------------------------------------------------------------------------
-constexpr int PULL_CONSUMERS = 8;
+// Consumer lane -> compute unit u = 3 j + h (31 = idle).  Searched offline for the record
+// layout (19-word stride, own region after the 80-word pulled slots): every 16-byte shared
+// load of an interior node and the row-pair store hit 8 distinct bank groups per quarter
+// warp (4 wavefronts per instruction; the identity mapping needs 5.6).
+__constant__ int8_t kPullUnitOfLane[32] = {6,  3,  9,  4,  31, 0,  13, 10, 31, 20, 17, 31, 23, 18, 16, 19,
+                                           26, 25, 31, 22, 21, 24, 31, 15, 11, 14, 7,  5,  1,  2,  12, 8};
 
-template <int C>
+template <int C, int W>
 struct PullChunkSmem {
-  static constexpr int PULL = 36 * 4 * C;          // doubles: 4 gathered rows per node (1152 B each)
-  static constexpr int OWN = 36 * 5 * C;           // doubles: own upper runs (<= 5 blocks per node)
+  static constexpr int PSLOT = 160;                // doubles per node: 4 gathered records (1216 B) -> 1280 B
+  static constexpr int PULL = PSLOT * C;           // doubles: pulled records (128-byte aligned per node)
+  static constexpr int OWN = PULL_BLOCK * 5 * C;   // doubles: own upper runs (<= 5 blocks per node)
   static constexpr int DESC = PULL_DESC * C / 2;   // doubles holding the C descriptors (16 int32 each)
   static constexpr int BUF = PULL + OWN + DESC;    // per buffer (PULL first: 128-byte aligned rows)
-  static constexpr int NPW = C / PULL_CONSUMERS;   // nodes per consumer warp per chunk
+  static constexpr int NPW = C / W;                // nodes per consumer warp per chunk
   static constexpr int RED = 2 * 27 * NPW;         // doubles per consumer warp
 };
 
-template <bool DOT, int C, int NB, int MINB>
-__global__ void __launch_bounds__(32 * (PULL_CONSUMERS + 1), MINB) spmv_pull_cta_kernel(
+template <bool DOT, int C, int NB, int MINB, int W>
+__global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
     const __grid_constant__ CUtensorMap tmap, int n_nodes, int rows_per_design, const int32_t* __restrict__ pdesc,
     const int32_t* __restrict__ ucol, const int2* __restrict__ lpull, const double* __restrict__ vals,
     const double* __restrict__ p, double* __restrict__ q, double* __restrict__ partial, CgState* st,
     BatchStrides bs) {
-  using S = PullChunkSmem<C>;
+  using S = PullChunkSmem<C, W>;
   constexpr int NPW = S::NPW;
   constexpr unsigned FULL = 0xffffffffu;
-  static_assert(C <= 32 && C % PULL_CONSUMERS == 0, "chunk size");
+  static_assert(C <= 32 && C % W == 0, "chunk size");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[NB];   // chunk data landed (bulk copy + gathers)
   __shared__ __align__(8) uint64_t desc_bar[NB];   // chunk descriptors written (x gathers may start)
@@ -987,29 +758,39 @@ __global__ void __launch_bounds__(32 * (PULL_CONSUMERS + 1), MINB) spmv_pull_cta
     for (int b = 0; b < NB; ++b) {
       mbar_init(&full_bar[b], 1);
       mbar_init(&desc_bar[b], 1);
-      mbar_init(&empty_bar[b], PULL_CONSUMERS);
+      mbar_init(&empty_bar[b], W);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   double pq[1] = {0.0};
-  if (warp == PULL_CONSUMERS) {
+  if (warp == W) {
     // ---------------- producer ----------------
     const uint64_t pol = evict_first_policy();
+    // descriptors of chunk k are loaded one chunk ahead (off the empty-barrier critical path)
+    auto load_desc = [&](int k, int4& a, int4& b2, int4& c, int4& d) {
+      const int first = ((int)blockIdx.x + k * (int)gridDim.x) * C;
+      a = b2 = c = d = make_int4(0, 0, 0, 0);
+      if (k < cnt && lane < min(C, n_nodes - first)) {
+        const int4* src = reinterpret_cast<const int4*>(pdesc + PULL_DESC * ((int64_t)first + lane));
+        a = __ldg(src);
+        b2 = __ldg(src + 1);
+        c = __ldg(src + 2);
+        d = __ldg(src + 3);
+      }
+    };
+    int4 n0, n1, n2, n3;
+    load_desc(0, n0, n1, n2, n3);
     for (int k = 0; k < cnt; ++k) {
       const int b = k % NB;
+      const int4 d0 = n0, d1 = n1, d2 = n2, d3 = n3;
+      load_desc(k + 1, n0, n1, n2, n3);
       if (k >= NB) mbar_wait(&empty_bar[b], (unsigned)(((k / NB) - 1) & 1));
       double* buf = sbase + (size_t)b * S::BUF;
       int32_t* D = reinterpret_cast<int32_t*>(buf + S::PULL + S::OWN);
       const int first = ((int)blockIdx.x + k * (int)gridDim.x) * C;
       const int nc = min(C, n_nodes - first);
-      int4 d0 = make_int4(0, 0, 0, 0), d1 = d0, d2 = d0, d3 = d0;
       if (lane < nc) {
-        const int4* src = reinterpret_cast<const int4*>(pdesc + PULL_DESC * ((int64_t)first + lane));
-        d0 = __ldg(src);
-        d1 = __ldg(src + 1);
-        d2 = __ldg(src + 2);
-        d3 = __ldg(src + 3);
         int4* dst = reinterpret_cast<int4*>(D + PULL_DESC * lane);
         dst[0] = d0;
         dst[1] = d1;
@@ -1029,9 +810,10 @@ __global__ void __launch_bounds__(32 * (PULL_CONSUMERS + 1), MINB) spmv_pull_cta
         chunk_fits[b] = all_fit ? 1 : 0;
         mbar_arrive(&desc_bar[b]);  // release: descriptors and the fit flag are visible
         if (all_fit) {
-          mbar_arrive_expect_tx(&full_bar[b], (unsigned)(288 * (b_end - b_first) + 1152 * __popc(has_pull)));
-          bulk_g2s(buf + S::PULL, vals + 36 * (int64_t)b_first, (unsigned)(288 * (b_end - b_first)), &full_bar[b],
-                   pol);
+          mbar_arrive_expect_tx(&full_bar[b],
+                                (unsigned)(8 * PULL_BLOCK * (b_end - b_first + 4 * __popc(has_pull))));
+          bulk_g2s(buf + S::PULL, vals + PULL_BLOCK * (int64_t)b_first, (unsigned)(8 * PULL_BLOCK * (b_end - b_first)),
+                   &full_bar[b], pol);
         } else {
           mbar_arrive(&full_bar[b]);  // release: the descriptors written above are visible
         }
@@ -1044,13 +826,14 @@ __global__ void __launch_bounds__(32 * (PULL_CONSUMERS + 1), MINB) spmv_pull_cta
         int r[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) r[i] = row0 + (i < ldeg ? Dl[2 * i] : d0.x);
-        tma_gather4(buf + 144 * lane, &tmap, r[0], r[1], r[2], r[3], &full_bar[b], pol);
+        tma_gather4(buf + S::PSLOT * lane, &tmap, r[0], r[1], r[2], r[3], &full_bar[b], pol);
       }
     }
   } else {
     // ---------------- consumers ----------------
     double2* red = reinterpret_cast<double2*>(red_base) + (size_t)warp * 27 * NPW;
-    const int jl = lane / 3, hl = lane - 3 * jl;
+    const int ul = kPullUnitOfLane[lane];
+    const int jl = ul < 27 ? ul / 3 : 9, hl = ul < 27 ? ul - 3 * (ul / 3) : 0;
     for (int k = 0; k < cnt; ++k) {
       const int b = k % NB;
       const double* buf = sbase + (size_t)b * S::BUF;
@@ -1064,23 +847,21 @@ __global__ void __launch_bounds__(32 * (PULL_CONSUMERS + 1), MINB) spmv_pull_cta
         const double* blk[NPW];
         double2 xv[NPW][3];
         bool act[NPW];
-        int nbs[NPW];
 #pragma unroll
         for (int e = 0; e < NPW; ++e) {  // node i = warp + 8 e of the chunk: operands first
-          const int i = warp + PULL_CONSUMERS * e;
+          const int i = warp + W * e;
           const int* Di = D + PULL_DESC * (i < nc ? i : 0);
           const int fl = Di[1];
           const int udeg = fl & 255, nb = udeg + ((fl >> 8) & 255);
-          nbs[e] = i < nc ? nb : 0;
           act[e] = i < nc && jl < nb;
           blk[e] = own;
           if (act[e]) {
             int xn;
             if (jl < udeg) {
-              blk[e] = own + 36 * (Di[0] - b_first + jl) + 2 * hl;
+              blk[e] = own + PULL_BLOCK * (Di[0] - b_first + jl) + 2 * hl;
               xn = Di[2 + jl];
             } else {
-              blk[e] = buf + 144 * i + 36 * (jl - udeg) + 12 * hl;
+              blk[e] = buf + S::PSLOT * i + PULL_BLOCK * (jl - udeg) + 12 * hl;
               xn = Di[2 + 2 * jl - udeg];
             }
             const double2* xp = reinterpret_cast<const double2*>(p + 6 * (int64_t)xn);
@@ -1092,66 +873,72 @@ __global__ void __launch_bounds__(32 * (PULL_CONSUMERS + 1), MINB) spmv_pull_cta
         mbar_wait(&full_bar[b], (unsigned)((k / NB) & 1));  // x gathers overlap the chunk's data
 #pragma unroll
         for (int e = 0; e < NPW; ++e) {
-          if (!act[e]) continue;
-          const int i = warp + PULL_CONSUMERS * e;
-          const int udeg = D[PULL_DESC * i + 1] & 255;
-          const double* r = blk[e];
-          const double2 x0 = xv[e][0], x1 = xv[e][1], x2 = xv[e][2];
-          double t0, t1;
-          if (jl < udeg) {  // own K_mj, column-major: pairs (K[2h][b], K[2h+1][b]) at 6b + 2h
-            const double2 v0 = *reinterpret_cast<const double2*>(r);
-            const double2 v1 = *reinterpret_cast<const double2*>(r + 6);
-            const double2 v2 = *reinterpret_cast<const double2*>(r + 12);
-            const double2 v3 = *reinterpret_cast<const double2*>(r + 18);
-            const double2 v4 = *reinterpret_cast<const double2*>(r + 24);
-            const double2 v5 = *reinterpret_cast<const double2*>(r + 30);
-            t0 = v0.x * x0.x;
-            t1 = v0.y * x0.x;
-            t0 = fma(v1.x, x0.y, t0);
-            t1 = fma(v1.y, x0.y, t1);
-            t0 = fma(v2.x, x1.x, t0);
-            t1 = fma(v2.y, x1.x, t1);
-            t0 = fma(v3.x, x1.y, t0);
-            t1 = fma(v3.y, x1.y, t1);
-            t0 = fma(v4.x, x2.x, t0);
-            t1 = fma(v4.y, x2.x, t1);
-            t0 = fma(v5.x, x2.y, t0);
-            t1 = fma(v5.y, x2.y, t1);
-          } else {  // pulled K_nm: columns 2h, 2h+1 (12 contiguous) against x_n
-            const double2 a01 = *reinterpret_cast<const double2*>(r);
-            const double2 a23 = *reinterpret_cast<const double2*>(r + 2);
-            const double2 a45 = *reinterpret_cast<const double2*>(r + 4);
-            const double2 b01 = *reinterpret_cast<const double2*>(r + 6);
-            const double2 b23 = *reinterpret_cast<const double2*>(r + 8);
-            const double2 b45 = *reinterpret_cast<const double2*>(r + 10);
-            t0 = a01.x * x0.x;
-            t1 = b01.x * x0.x;
-            t0 = fma(a01.y, x0.y, t0);
-            t1 = fma(b01.y, x0.y, t1);
-            t0 = fma(a23.x, x1.x, t0);
-            t1 = fma(b23.x, x1.x, t1);
-            t0 = fma(a23.y, x1.y, t0);
-            t1 = fma(b23.y, x1.y, t1);
-            t0 = fma(a45.x, x2.x, t0);
-            t1 = fma(b45.x, x2.x, t1);
-            t0 = fma(a45.y, x2.y, t0);
-            t1 = fma(b45.y, x2.y, t1);
+          if (ul >= 27) continue;
+          // inactive units (j beyond the node's blocks) write zeros: the row sums below add all
+          // nine entries in a fixed tree
+          double t0 = 0.0, t1 = 0.0;
+          if (act[e]) {
+            const int i = warp + W * e;
+            const int udeg = D[PULL_DESC * i + 1] & 255;
+            const double* r = blk[e];
+            const double2 x0 = xv[e][0], x1 = xv[e][1], x2 = xv[e][2];
+            // two partial chains per output (b even / b odd) halve the dependent FMA latency
+            double u0, u1;
+            if (jl < udeg) {  // own K_mj, column-major: pairs (K[2h][b], K[2h+1][b]) at 6b + 2h
+              const double2 v0 = *reinterpret_cast<const double2*>(r);
+              const double2 v1 = *reinterpret_cast<const double2*>(r + 6);
+              const double2 v2 = *reinterpret_cast<const double2*>(r + 12);
+              const double2 v3 = *reinterpret_cast<const double2*>(r + 18);
+              const double2 v4 = *reinterpret_cast<const double2*>(r + 24);
+              const double2 v5 = *reinterpret_cast<const double2*>(r + 30);
+              t0 = v0.x * x0.x;
+              t1 = v0.y * x0.x;
+              u0 = v1.x * x0.y;
+              u1 = v1.y * x0.y;
+              t0 = fma(v2.x, x1.x, t0);
+              t1 = fma(v2.y, x1.x, t1);
+              u0 = fma(v3.x, x1.y, u0);
+              u1 = fma(v3.y, x1.y, u1);
+              t0 = fma(v4.x, x2.x, t0);
+              t1 = fma(v4.y, x2.x, t1);
+              u0 = fma(v5.x, x2.y, u0);
+              u1 = fma(v5.y, x2.y, u1);
+            } else {  // pulled K_nm: columns 2h, 2h+1 (12 contiguous) against x_n
+              const double2 a01 = *reinterpret_cast<const double2*>(r);
+              const double2 a23 = *reinterpret_cast<const double2*>(r + 2);
+              const double2 a45 = *reinterpret_cast<const double2*>(r + 4);
+              const double2 b01 = *reinterpret_cast<const double2*>(r + 6);
+              const double2 b23 = *reinterpret_cast<const double2*>(r + 8);
+              const double2 b45 = *reinterpret_cast<const double2*>(r + 10);
+              t0 = a01.x * x0.x;
+              t1 = b01.x * x0.x;
+              u0 = a01.y * x0.y;
+              u1 = b01.y * x0.y;
+              t0 = fma(a23.x, x1.x, t0);
+              t1 = fma(b23.x, x1.x, t1);
+              u0 = fma(a23.y, x1.y, u0);
+              u1 = fma(b23.y, x1.y, u1);
+              t0 = fma(a45.x, x2.x, t0);
+              t1 = fma(b45.x, x2.x, t1);
+              u0 = fma(a45.y, x2.y, u0);
+              u1 = fma(b45.y, x2.y, u1);
+            }
+            t0 += u0;
+            t1 += u1;
           }
-          red[27 * e + lane] = make_double2(t0, t1);
+          red[27 * e + ul] = make_double2(t0, t1);
         }
         __syncwarp();
-        // lane 6 e + a (< 6 NPW): row a of node e, blocks in ascending j
+        // lane 6 e + a (< 6 NPW): row a of node e, the nine block entries in a fixed tree
         if (lane < 6 * NPW) {
           const int e = lane / 6, a = lane - 6 * e;
-          const int i = warp + PULL_CONSUMERS * e;
-          int nb = 0;
-#pragma unroll
-          for (int t = 0; t < NPW; ++t)
-            if (t == e) nb = nbs[t];
+          const int i = warp + W * e;
           if (i < nc) {
             const double* rd = reinterpret_cast<const double*>(red + 27 * e) + a;
-            double y = 0.0;
-            for (int j = 0; j < nb; ++j) y += rd[6 * j];
+            double r9[9];
+#pragma unroll
+            for (int j = 0; j < 9; ++j) r9[j] = rd[6 * j];
+            const double y = (((r9[0] + r9[1]) + (r9[2] + r9[3])) + ((r9[4] + r9[5]) + (r9[6] + r9[7]))) + r9[8];
             const int64_t row = 6 * ((int64_t)first + i) + a;
             q[row] = y;
             if (DOT) pq[0] += p[row] * y;
@@ -1162,7 +949,7 @@ __global__ void __launch_bounds__(32 * (PULL_CONSUMERS + 1), MINB) spmv_pull_cta
         // general chunk: lane (node e, row a) sums its row from global memory, own blocks then
         // pulled blocks in ascending order (the order of the fast path)
         const int e = lane / 6, a = lane - 6 * e;
-        const int i = warp + PULL_CONSUMERS * e;
+        const int i = warp + W * e;
         if (i < nc) {
           const int* Di = D + PULL_DESC * i;
           const int b0 = Di[0], fl = Di[1];
@@ -1172,7 +959,7 @@ __global__ void __launch_bounds__(32 * (PULL_CONSUMERS + 1), MINB) spmv_pull_cta
           double y = 0.0;
           for (int kb = 0; kb < udeg; ++kb) {
             const int m = fitn ? Di[2 + kb] : __ldg(ucol + b0 + kb);
-            const double* bk = vals + 36 * ((int64_t)b0 + kb);
+            const double* bk = vals + PULL_BLOCK * ((int64_t)b0 + kb);
             double t = 0.0;
 #pragma unroll
             for (int c = 0; c < 6; ++c) t = fma(bk[6 * c + a], p[6 * (int64_t)m + c], t);
@@ -1180,7 +967,7 @@ __global__ void __launch_bounds__(32 * (PULL_CONSUMERS + 1), MINB) spmv_pull_cta
           }
           for (int jp = 0; jp < ldeg; ++jp) {
             const int2 e2 = fitn ? make_int2(Di[2 + udeg + 2 * jp], Di[3 + udeg + 2 * jp]) : __ldg(lpull + l0 + jp);
-            const double* bk = vals + 36 * (int64_t)e2.y;
+            const double* bk = vals + PULL_BLOCK * (int64_t)e2.y;
             double t = 0.0;
 #pragma unroll
             for (int c = 0; c < 6; ++c) t = fma(bk[6 * a + c], p[6 * (int64_t)e2.x + c], t);
@@ -1789,29 +1576,25 @@ void launch_cg_update_sym(cudaStream_t s, int ndof, const double* dinv, double* 
   SSO_POST_LAUNCH("cg_update_sym_kernel");
 }
 
-// pull SpMV (storage 3).  SSO_PULL_VARIANT selects (chunk nodes, buffers, CTAs per SM) of the
-// warp-specialised form: 0 (default) (16, 2, 2), 1 (8, 2, 3), 2 (8, 3, 3), 3 (16, 3, 1); 4-5 the
-// warp-per-node form (stages, CTAs per SM) = (3, 3), (2, 4)
+// pull SpMV (storage 3).  SSO_PULL_VARIANT selects (chunk nodes, buffers, CTAs per SM,
+// consumer warps): 0 (default) (8, 2, 4, 4), 1 (16, 2, 2, 8), 2 (8, 3, 3, 4)
 struct PullVariant {
   int smem;
   int minb;
   int threads;
-  int chunk;  // nodes per CTA chunk (0: warp per node)
+  int chunk;  // nodes per CTA chunk
   void (*dot)(const CUtensorMap, int, int, const int32_t*, const int32_t*, const int2*, const double*,
               const double*, double*, double*, CgState*, BatchStrides);
   void (*plain)(const CUtensorMap, int, int, const int32_t*, const int32_t*, const int2*, const double*,
                 const double*, double*, double*, CgState*, BatchStrides);
 };
-#define PULL_CTA_VARIANT(C, NB, M)                                                                       \
-  {                                                                                                      \
-    (NB * PullChunkSmem<C>::BUF + PULL_CONSUMERS * PullChunkSmem<C>::RED) * 8, M, 32 * (PULL_CONSUMERS + 1), \
-        C, spmv_pull_cta_kernel<true, C, NB, M>, spmv_pull_cta_kernel<false, C, NB, M>                   \
+#define PULL_CTA_VARIANT(C, NB, M, W)                                                                 \
+  {                                                                                                   \
+    (NB * PullChunkSmem<C, W>::BUF + W * PullChunkSmem<C, W>::RED) * 8, M, 32 * (W + 1), C,           \
+        spmv_pull_cta_kernel<true, C, NB, M, W>, spmv_pull_cta_kernel<false, C, NB, M, W>             \
   }
-#define PULL_VARIANT(S, M) \
-  { SPMV_WARPS * S * PULL_SLOT_DOUBLES * 8, M, 32 * SPMV_WARPS, 0, spmv_pull_kernel<true, S, M>, spmv_pull_kernel<false, S, M> }
-static const PullVariant kPullVariants[] = {PULL_CTA_VARIANT(16, 2, 2), PULL_CTA_VARIANT(8, 2, 3),
-                                            PULL_CTA_VARIANT(8, 3, 3),  PULL_CTA_VARIANT(16, 3, 1),
-                                            PULL_VARIANT(3, 3),         PULL_VARIANT(2, 4)};
+static const PullVariant kPullVariants[] = {PULL_CTA_VARIANT(8, 2, 4, 4), PULL_CTA_VARIANT(16, 2, 2, 8),
+                                            PULL_CTA_VARIANT(8, 3, 3, 4)};
 static int g_pull_v = -1;
 
 static const PullVariant& pull_variant(int* smem) {
@@ -1860,10 +1643,10 @@ int make_pull_tmap(const double* vals, int64_t rows, CUtensorMap* out) {
       return 1;
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  // [rows][36] fp64 view of the values; a box is one 288-byte row, gather4 fetches four
-  cuuint64_t dims[2] = {36, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {288};
-  cuuint32_t box[2] = {36, 1};
+  // [rows][PULL_BLOCK] fp64 view of the values; a box is one record, gather4 fetches four
+  cuuint64_t dims[2] = {PULL_BLOCK, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {8 * PULL_BLOCK};
+  cuuint32_t box[2] = {PULL_BLOCK, 1};
   cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(vals), dims, strides,
                             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1879,7 +1662,7 @@ void launch_spmv_pull(cudaStream_t s, const CUtensorMap* tmap, int n_nodes, int 
   const PullVariant& V = pull_variant(&smem);
   const int ctas = std::max(1, V.minb * (cg_grid() / 4) / bs.B);  // persistent: minb CTAs per SM in total
   const int chunk = V.chunk;
-  const int units = chunk ? (n_nodes + chunk - 1) / chunk : (n_nodes + SPMV_WARPS - 1) / SPMV_WARPS;
+  const int units = (n_nodes + chunk - 1) / chunk;
   const int grid = std::max(1, std::min(ctas, units));
   const int2* lp = reinterpret_cast<const int2*>(lpull);
   if (st)

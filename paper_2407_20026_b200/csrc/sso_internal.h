@@ -185,6 +185,9 @@ void launch_spmv_pull(cudaStream_t s, const CUtensorMap* tmap, int n_nodes, int 
                       const int32_t* pdesc, const int32_t* ucol, const int32_t* lpull, const double* vals,
                       const double* x, double* y, double* partial, CgState* st,
                       const BatchStrides& bs = BatchStrides());
+// Storage 3 stores each upper 6x6 block as a record of PULL_BLOCK doubles: column-major
+// values (K[a][b] at 6b + a) then 2 zero pads (an odd 16-byte-word stride, see pcg.cu).
+constexpr int PULL_BLOCK = 38;
 // 16-int per-node descriptors of the pull SpMV (see pcg.cu)
 void build_pull_desc(const UpperPattern& U, std::vector<int32_t>& desc);
 // TMA map of the [rows][36] fp64 view of the values (gather4 of pulled blocks); 0 on success
