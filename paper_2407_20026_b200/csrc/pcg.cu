@@ -705,9 +705,10 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, i
 // Consumer lane -> compute unit u = 3 j + h (31 = idle).  Searched offline for the record
 // layout (19-word stride, own region after the 80-word pulled slots): every 16-byte shared
 // load of an interior node and the row-pair store hit 8 distinct bank groups per quarter
-// warp (4 wavefronts per instruction; the identity mapping needs 5.6).
-__constant__ int8_t kPullUnitOfLane[32] = {6,  3,  9,  4,  31, 0,  13, 10, 31, 20, 17, 31, 23, 18, 16, 19,
-                                           26, 25, 31, 22, 21, 24, 31, 15, 11, 14, 7,  5,  1,  2,  12, 8};
+// warp (4 wavefronts per instruction; the identity mapping needs 5.6), and the three lanes
+// of a block (same 48-byte x gather) share a quarter warp for all blocks but one.
+__constant__ int8_t kPullUnitOfLane[32] = {17, 31, 16, 19, 15, 31, 18, 20, 11, 13, 9,  14, 7,  12, 10, 8,
+                                           0,  6,  31, 5,  2,  4,  3,  1,  31, 24, 23, 21, 31, 26, 25, 22};
 
 template <int C, int W>
 struct PullChunkSmem {
