@@ -716,7 +716,8 @@ struct PullChunkSmem {
   static constexpr int PULL = PSLOT * C;           // doubles: pulled records (128-byte aligned per node)
   static constexpr int OWN = PULL_BLOCK * 5 * C;   // doubles: own upper runs (<= 5 blocks per node)
   static constexpr int DESC = PULL_DESC * C / 2;   // doubles holding the C descriptors (16 int32 each)
-  static constexpr int BUF = PULL + OWN + DESC;    // per buffer (PULL first: 128-byte aligned rows)
+  static constexpr int BUF = (PULL + OWN + DESC + 15) / 16 * 16;  // per buffer, 128-byte multiple
+                                                                   // (PULL first: aligned gather4 rows)
   static constexpr int NPW = C / W;                // nodes per consumer warp per chunk
   static constexpr int RED = 2 * 27 * NPW;         // doubles per consumer warp
 };
@@ -1578,7 +1579,9 @@ void launch_cg_update_sym(cudaStream_t s, int ndof, const double* dinv, double* 
 }
 
 // pull SpMV (storage 3).  SSO_PULL_VARIANT selects (chunk nodes, buffers, CTAs per SM,
-// consumer warps): 0 (default) (8, 2, 4, 4), 1 (16, 2, 2, 8), 2 (8, 3, 3, 4)
+// consumer warps): 0 (default) (8, 2, 4, 4), 1 (16, 2, 2, 8), 2 (8, 3, 3, 4), 3 (4, 2, 8, 2).
+// Measured at C3b: 68.4, 72.4, 72.4, 75.9 us (finer chunks pay the producer per chunk, larger
+// ones limit the CTAs per SM).
 struct PullVariant {
   int smem;
   int minb;
@@ -1595,7 +1598,7 @@ struct PullVariant {
         spmv_pull_cta_kernel<true, C, NB, M, W>, spmv_pull_cta_kernel<false, C, NB, M, W>             \
   }
 static const PullVariant kPullVariants[] = {PULL_CTA_VARIANT(8, 2, 4, 4), PULL_CTA_VARIANT(16, 2, 2, 8),
-                                            PULL_CTA_VARIANT(8, 3, 3, 4)};
+                                            PULL_CTA_VARIANT(8, 3, 3, 4), PULL_CTA_VARIANT(4, 2, 8, 2)};
 static int g_pull_v = -1;
 
 static const PullVariant& pull_variant(int* smem) {
