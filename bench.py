@@ -333,11 +333,12 @@ def run_gpu(args):
     peak, peak_src = measured_peaks()
     # algorithmic bytes of the stored format: values + block column ids + node_ptr + x read,
     # y written; symmetric storage adds the transpose slots (written and read back once)
-    spmv_bytes = 8 * stored_vals + 4 * stored_blocks + 8 * (n_nodes + 1) + 16 * ndof
-    if symmetric == 2:
-        spmv_bytes += 2 * 48 * (stored_blocks - n_nodes) + 8 * (n_nodes + 1) + 4 * (stored_blocks - n_nodes)
-    elif symmetric == 3:  # pull lists: lptr + one (source node, block) pair per pulled block
-        spmv_bytes += 8 * (n_nodes + 1) + 8 * (stored_blocks - n_nodes)
+    if symmetric == 3:  # values once + the 64-byte node descriptor (block columns, pull list) + p, q
+        spmv_bytes = 8 * stored_vals + 64 * n_nodes + 16 * ndof
+    else:               # values + block column ids + node_ptr + p, q (+ transpose slots, storage 2)
+        spmv_bytes = 8 * stored_vals + 4 * stored_blocks + 8 * (n_nodes + 1) + 16 * ndof
+        if symmetric == 2:
+            spmv_bytes += 2 * 48 * (stored_blocks - n_nodes) + 8 * (n_nodes + 1) + 4 * (stored_blocks - n_nodes)
     spmv_avg_ms = spmv_ms / max(spmv_n, 1)
     achieved = spmv_bytes / (spmv_avg_ms / 1000.0) / 1e9 if spmv_n else None
     roofline = {"bound": "hbm",
