@@ -456,3 +456,32 @@ def test_block_jacobi_batched_and_partitioned(sso):
         sso.Model(P, precond=1, storage=2)
     with pytest.raises(Exception):
         sso.Model(P, precond=2)
+
+
+def test_pull_storage_general_nodes(sso):
+    """Nodes beyond the pull kernel's fast path (upper degree > 5 or more than 4 pulled
+    blocks) take its general branch: a 4x4 shell with a fan of beams from node 0 to every
+    other node of its first two rows, and from those to the last node.  Storage 3 equals
+    full storage and the oracle."""
+    P = W.tiny_shell(4, seed=9)
+    nn = len(P["x"])
+    fan = [[0, k] for k in range(2, 10)] + [[k, nn - 1] for k in range(2, 10)]
+    P["beam_conn"] = np.array(fan, np.int32)
+    nb = len(fan)
+    P["A"], P["Iy"], P["Iz"], P["J"] = (np.full(nb, 1e-3), np.full(nb, 2e-6), np.full(nb, 1e-6),
+                                        np.full(nb, 2e-6))
+    P["E"] = np.concatenate([np.full(nb, 210e9), P["E"]])
+    P["nu"] = np.concatenate([np.full(nb, 0.3), P["nu"]])
+    m3 = sso.Model(P, rtol=1e-12, storage=3)
+    m1 = sso.Model(P, rtol=1e-12, storage=1)
+    for m in (m3, m1):
+        m.assemble()
+    x = np.random.default_rng(2).standard_normal(m3.ndof)
+    y3, y1 = m3.spmv(x), m1.spmv(x)
+    assert np.abs(y3 - y1).max() <= 1e-13 * np.abs(y1).max()
+    u3, i3 = m3.solve(P["f"])
+    uref, _, _ = OG.evaluate(P)
+    assert i3["status"] == 0
+    assert np.linalg.norm(u3 - uref) <= TOL_U * np.linalg.norm(uref)
+    C3, _, _ = m3.grad()
+    assert abs(C3 - OG.compliance(P["f"], uref)) <= TOL_C * abs(OG.compliance(P["f"], uref))
