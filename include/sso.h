@@ -140,12 +140,13 @@ typedef struct {
    * upper node blocks (n, m >= n) of the symmetric K_bc (44 % fewer value bytes on
    * shell grids); pass 1 of the SpMV forms the upper row sums, the transpose
    * contributions (sender-ordered slots) and p^T K p, the x / r update adds each
-   * node's incoming slots in ascending source order.  3 = upper node blocks, each
-   * node's run stored column-major (every 6x6 block one contiguous 288-byte chunk),
-   * and a ONE-pass "pull" SpMV: the warp owning row node m streams its upper run and
-   * the stored blocks (n, m) of its lower neighbours n < m (an L2 hit: nodes are
-   * dealt round-robin, so the owner streams them in the same window) and forms
-   * y_m = sum_{j>=m} K_mj x_j + sum_{n<m} K_nm^T x_n; no transpose buffer.  Storage
+   * node's incoming slots in ascending source order.  3 = upper node blocks, each one
+   * contiguous 38-double record (36 values column-major + 2 zero pads), and a ONE-pass
+   * "pull" SpMV: the CTA that owns a chunk of row nodes streams their upper runs (one
+   * bulk copy) and the stored blocks (n, m) of their lower neighbours n < m (one TMA
+   * gather4 per node; an L2 hit: chunks are dealt round-robin, so the owner streams them
+   * in the same window) and forms y_m = sum_{j>=m} K_mj x_j + sum_{n<m} K_nm^T x_n; no
+   * transpose buffer.  Storage
    * 3 also applies to strips (owned nodes precede halo nodes locally, so lower
    * neighbours are owned); storage 2 is single-strip only (else full storage).
    * Exports return the full CSR.  Other values -> SSO_E_INVALID. */
@@ -185,11 +186,14 @@ int sso_set_design(sso_handle h, const double* x, const double* y, const double*
 int sso_set_stream(sso_handle h, void* cuda_stream, sso_mem mem);
 
 /* A1 + A2: element stiffness for all elements, segmented-sum assembly into the fixed
- * CSR values, supports by elimination, Jacobi diagonal.  Errors: SSO_E_DEGENERATE
- * (element id in the message), SSO_E_SINGULAR (free DOF with diagonal <= 0). */
+ * CSR values (layout per sso_options.storage), supports by elimination, Jacobi diagonal
+ * (and, with precond = 1, the inverse 6x6 node blocks).  Errors: SSO_E_DEGENERATE
+ * (element id in the message), SSO_E_SINGULAR (free DOF with diagonal <= 0 or a node
+ * block that is not positive definite). */
 int sso_assemble(sso_handle h);
 
-/* A3: Jacobi-PCG on K_bc u = f_bc.  f [6 n_nodes] (entries at constrained DOFs ignored),
+/* A3: Jacobi-PCG (point or node-block, sso_options.precond) on K_bc u = f_bc to
+ * |r| <= rtol |f_bc|.  f [6 n_nodes] (entries at constrained DOFs ignored),
  * u [6 n_nodes] output (zeros at constrained DOFs); read as x0 when warm_start.
  * info may be NULL ([batch] entries otherwise).  Errors: SSO_E_STATE (not assembled),
  * SSO_E_NOT_SPD, SSO_E_NOT_CONVERGED (u = last iterate). */
@@ -289,7 +293,8 @@ int sso_export_dinv(sso_handle h, double* dinv);
 
 /* Device storage of the assembled matrix: stored values / node blocks (owned rows) and
  * the layout in use: *symmetric = 0 full storage, 2 upper blocks with the two-pass
- * transpose SpMV, 3 upper blocks (column-major runs) with the one-pass pull SpMV. */
+ * transpose SpMV, 3 upper blocks (38-double column-major records) with the one-pass pull
+ * SpMV.  stored_values counts the 36 values per block (not the record pads). */
 int sso_storage_info(sso_handle h, int64_t* stored_values, int64_t* stored_blocks, int32_t* symmetric);
 
 /* Partition of this handle: number of strips held, first owned global node, owned
