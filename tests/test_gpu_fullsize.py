@@ -152,3 +152,65 @@ def test_block_jacobi_and_full_storage_full_size(c3b):
             res = fbc[r] - float(ref @ u0[ci[rp[r]:rp[r + 1]]])
             assert abs(res) <= 20 * RTOL_BENCH * np.linalg.norm(fbc) + 1e-13 * float(
                 np.abs(ref) @ np.abs(u0[ci[rp[r]:rp[r + 1]]]))
+
+
+def test_c4_pull_storage_operator():
+    """C4 (1000 x 1000 quads, 6 012 006 DOF, the largest config) in the bench's default
+    layout: the pull SpMV (32-bit block offsets, 38-double records) equals the
+    full-storage SpMV on a random vector, and sampled rows of K x equal the oracle's
+    per-node rows applied to x."""
+    import paper_2407_20026_b200 as sso
+    P = W.config4()
+    m3 = sso.Model(P, rtol=RTOL_BENCH)
+    m3.assemble()
+    assert m3.storage_info()[2] == 3
+    nn = len(P["x"])
+    x = np.random.default_rng(11).standard_normal(6 * nn)
+    y3 = m3.spmv(x)
+    m3.close()
+    m1 = sso.Model(P, rtol=RTOL_BENCH, storage=1)
+    m1.assemble()
+    y1 = m1.spmv(x)
+    m1.close()
+    assert np.abs(y3 - y1).max() <= 1e-12 * np.abs(y1).max()
+    fixed = OA.fixed_dofs(P)
+    rng = np.random.default_rng(12)
+    n = 1000
+    for nd in sorted({0, n, nn - 1, nn // 2} | set(rng.choice(nn, 6, replace=False).tolist())):
+        rows = OA.node_rows(P, nd)
+        for a in range(6):
+            r = 6 * nd + a
+            ref = 0.0
+            scale = 0.0
+            for c, vals in rows.items():
+                v = vals[a]
+                if fixed[r] or fixed[c]:
+                    v = (v if v != 0.0 else 1.0) if c == r else 0.0
+                ref += v * x[c]
+                scale += abs(v * x[c])
+            assert abs(y3[r] - ref) <= 1e-12 * max(scale, 1e-300)
+
+
+def test_c5_full_batch_sampled():
+    """C5 at its full per-GPU size (64 designs of 50 x 50 quads) in one batched handle:
+    sampled designs equal independent single-design solves and the oracle."""
+    import paper_2407_20026_b200 as sso
+    B = 64
+    designs = [W.config5_design(b) for b in range(B)]
+    mb = sso.Model(designs[0], rtol=RTOL_BENCH, batch=B)
+    mb.set_design(z=np.stack([d["z"] for d in designs]), t=np.stack([d["t"] for d in designs]))
+    mb.assemble()
+    U, infos = mb.solve(np.stack([d["f"] for d in designs]))
+    C, dX, dT = mb.grad()
+    for b in (0, 17, 63):
+        d = designs[b]
+        assert infos[b]["status"] == 0 and infos[b]["true_rel_res"] <= 20 * RTOL_BENCH
+        m1 = sso.Model(d, rtol=RTOL_BENCH)
+        m1.assemble()
+        u1, _ = m1.solve(d["f"])
+        C1, dX1, dT1 = m1.grad()
+        assert np.linalg.norm(U[b] - u1) <= 1e-8 * np.linalg.norm(u1)
+        assert C[b] == pytest.approx(C1, rel=1e-9)
+        m1.close()
+    uref, _, _ = OG.evaluate(designs[63], "pcg", rtol=1e-12)
+    assert np.linalg.norm(U[63] - uref) <= 1e-8 * np.linalg.norm(uref)
