@@ -704,10 +704,14 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   P.sym = (h->storage == 3) ||
           (h->storage == 2 && L.n_parts == 1 && h->nranks == 1 && P.n_own == P.n_nodes);
   P.pull = P.sym && h->storage == 3;
-  if (P.pull && P.pat.node_ptr[P.n_nodes] >= INT32_MAX / 36) {  // 32-bit block offsets in the pull kernel
+  if (P.pull && P.pat.node_ptr[P.n_nodes] >= INT32_MAX / PULL_BLOCK) {  // 32-bit offsets in the pull kernel
     h->err = "storage 3: too many node blocks for 32-bit offsets";
     return SSO_E_INVALID;
   }
+  // the pull descriptor packs a node's degree in 8 bits: a node with more than 255
+  // neighbours (a large beam fan) keeps the whole strip on full storage
+  for (int32_t n = 0; P.pull && n < P.n_nodes; ++n)
+    if (P.pat.node_ptr[n + 1] - P.pat.node_ptr[n] > 255) P.sym = P.pull = false;
   if (P.sym) build_upper(P.pat, L.beam_conn.data(), L.quad_conn.data(), P.up);
   P.stored_blocks = P.sym ? P.up.uptr[P.n_own] : P.pat.node_ptr[P.n_own];
   const int64_t ne = (int64_t)P.n_beams + P.n_quads;
