@@ -702,7 +702,8 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, i
 // them in ascending j.  Chunks holding a node that does not fit (udeg > 5 or
 // ldeg > 4) take a general path reading the values from global memory.
 // ---------------------------------------------------------------------------
-// Consumer lane -> compute unit u = 3 j + h (31 = idle).  Searched offline for the record
+// Consumer lane -> compute unit u = 3 j + h (31 = idle).  Searched (tools/pull_lane_perm.py,
+// checked by tests/test_pull_layout.py) for the record
 // layout (19-word stride, own region after the 80-word pulled slots): every 16-byte shared
 // load of an interior node and the row-pair store hit 8 distinct bank groups per quarter
 // warp (4 wavefronts per instruction; the identity mapping needs 5.6), and the three lanes
