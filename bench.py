@@ -435,7 +435,8 @@ def run_batch(args):
     B = args.batch
     designs = [W.config5_design(rank * B + b) for b in range(B)]
     stream = torch.cuda.current_stream()
-    m = sso.Model(designs[0], rtol=RTOL, batch=B, stream=stream.cuda_stream, device=dev.index)
+    m = sso.Model(designs[0], rtol=RTOL, batch=B, stream=stream.cuda_stream, device=dev.index,
+                  precond=args.precond)
     Z = torch.from_numpy(np.stack([d["z"] for d in designs])).to(dev)
     T = torch.from_numpy(np.stack([d["t"] for d in designs])).to(dev)
     F = torch.from_numpy(np.stack([d["f"] for d in designs])).to(dev)
@@ -485,6 +486,7 @@ def run_batch(args):
                           "data": "synthetic (workloads.config5_design, seeded)",
                           "config": {"workload": f"C5: {B} designs/GPU x 50x50 MITC-4 quads (15 606 DOF each)",
                                      "rtol": RTOL, "cg_iters_max": max(its), "cg_iters_min": min(its),
+                                     "precond": {0: "point Jacobi", 1: "node-block Jacobi"}[args.precond],
                                      "parallelism": f"{world} GPU(s) x {B} designs, no collective"},
                           "gpu_launches": m.launch_count() - l0, "clocks": clk.summary()}))
     if world > 1:
