@@ -1580,9 +1580,11 @@ void launch_cg_update_sym(cudaStream_t s, int ndof, const double* dinv, double* 
 }
 
 // pull SpMV (storage 3).  SSO_PULL_VARIANT selects (chunk nodes, buffers, CTAs per SM,
-// consumer warps): 0 (default) (8, 2, 4, 4), 1 (16, 2, 2, 8), 2 (8, 3, 3, 4), 3 (4, 2, 8, 2).
-// Measured at C3b: 68.4, 72.4, 72.4, 75.9 us (finer chunks pay the producer per chunk, larger
-// ones limit the CTAs per SM).
+// consumer warps): 0 (default) (12, 2, 3, 4), 1 (8, 2, 4, 4), 2 (16, 2, 2, 8), 3 (8, 3, 3, 4).
+// Measured at C3b: 67.0, 68.4, 69.9, 71.6 us; also tried (live us): (4, 2, 8, 2) 75.9,
+// (16, 2, 2, 4) 72.3, (12, 2, 3, 6) 93 (spills), (10, 2, 3, 5) 71.7, (12, 3, 2, 4) 76.0,
+// (12, 2, 3, 3) 70.5.  Finer chunks pay the producer per chunk, larger ones limit the
+// CTAs per SM (shared memory) or spill.
 struct PullVariant {
   int smem;
   int minb;
@@ -1598,8 +1600,8 @@ struct PullVariant {
     (NB * PullChunkSmem<C, W>::BUF + W * PullChunkSmem<C, W>::RED) * 8, M, 32 * (W + 1), C,           \
         spmv_pull_cta_kernel<true, C, NB, M, W>, spmv_pull_cta_kernel<false, C, NB, M, W>             \
   }
-static const PullVariant kPullVariants[] = {PULL_CTA_VARIANT(8, 2, 4, 4), PULL_CTA_VARIANT(16, 2, 2, 8),
-                                            PULL_CTA_VARIANT(8, 3, 3, 4), PULL_CTA_VARIANT(4, 2, 8, 2)};
+static const PullVariant kPullVariants[] = {PULL_CTA_VARIANT(12, 2, 3, 4), PULL_CTA_VARIANT(8, 2, 4, 4),
+                                            PULL_CTA_VARIANT(16, 2, 2, 8), PULL_CTA_VARIANT(8, 3, 3, 4)};
 static int g_pull_v = -1;
 
 static const PullVariant& pull_variant(int* smem) {

@@ -21,7 +21,7 @@ import sys
 from pathlib import Path
 
 UNITS = [(j, h) for j in range(9) for h in range(3)]
-C = 8  # nodes per chunk (default variant)
+C = 12  # nodes per chunk (default variant)
 
 
 def words(j, h, t, i, bi):
