@@ -1579,8 +1579,8 @@ void launch_cg_update_sym(cudaStream_t s, int ndof, const double* dinv, double* 
   SSO_POST_LAUNCH("cg_update_sym_kernel");
 }
 
-// pull SpMV (storage 3).  SSO_PULL_VARIANT selects (chunk nodes, buffers, CTAs per SM,
-// consumer warps): 0 (default) (12, 2, 3, 4), 1 (8, 2, 4, 4), 2 (16, 2, 2, 8), 3 (8, 3, 3, 4).
+// pull SpMV (storage 3).  Variants (chunk nodes, buffers, CTAs per SM, consumer warps):
+// 0 (12, 2, 3, 4) single designs, 1 (8, 2, 4, 4) batches, 2 (16, 2, 2, 8), 3 (8, 3, 3, 4).
 // Measured at C3b: 67.0, 68.4, 69.9, 71.6 us; also tried (live us): (4, 2, 8, 2) 75.9,
 // (16, 2, 2, 4) 72.3, (12, 2, 3, 6) 93 (spills), (10, 2, 3, 5) 71.7, (12, 3, 2, 4) 76.0,
 // (12, 2, 3, 3) 70.5.  Finer chunks pay the producer per chunk, larger ones limit the
@@ -1602,20 +1602,26 @@ struct PullVariant {
   }
 static const PullVariant kPullVariants[] = {PULL_CTA_VARIANT(12, 2, 3, 4), PULL_CTA_VARIANT(8, 2, 4, 4),
                                             PULL_CTA_VARIANT(16, 2, 2, 8), PULL_CTA_VARIANT(8, 3, 3, 4)};
-static int g_pull_v = -1;
-
-static const PullVariant& pull_variant(int* smem) {
-  if (g_pull_v < 0) {
+// Variant per launch: SSO_PULL_VARIANT if set, else 0 for single designs and 1 (8-node
+// chunks, more CTAs per design) for batches (C5: 220 vs 206 designs/s).
+static const PullVariant& pull_variant(int B, int* smem) {
+  static int env_v = -2;
+  static bool attr_set[sizeof(kPullVariants) / sizeof(kPullVariants[0])] = {};
+  const int nv = (int)(sizeof(kPullVariants) / sizeof(kPullVariants[0]));
+  if (env_v == -2) {
     const char* e = getenv("SSO_PULL_VARIANT");
-    int v = e ? atoi(e) : 0;
-    if (v < 0 || v >= (int)(sizeof(kPullVariants) / sizeof(kPullVariants[0]))) v = 0;
+    env_v = e ? atoi(e) : -1;
+    if (env_v >= nv) env_v = -1;
+  }
+  const int v = env_v >= 0 ? env_v : (B > 1 ? 1 : 0);
+  if (!attr_set[v]) {
     cudaFuncSetAttribute(kPullVariants[v].dot, cudaFuncAttributeMaxDynamicSharedMemorySize, kPullVariants[v].smem);
     cudaFuncSetAttribute(kPullVariants[v].plain, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kPullVariants[v].smem);
-    g_pull_v = v;
+    attr_set[v] = true;
   }
-  *smem = kPullVariants[g_pull_v].smem;
-  return kPullVariants[g_pull_v];
+  *smem = kPullVariants[v].smem;
+  return kPullVariants[v];
 }
 
 void build_pull_desc(const UpperPattern& U, std::vector<int32_t>& d) {
@@ -1666,7 +1672,7 @@ void launch_spmv_pull(cudaStream_t s, const CUtensorMap* tmap, int n_nodes, int 
                       const double* x, double* y, double* partial, CgState* st, const BatchStrides& bs) {
   if (n_nodes <= 0) return;
   int smem;
-  const PullVariant& V = pull_variant(&smem);
+  const PullVariant& V = pull_variant(bs.B, &smem);
   const int ctas = std::max(1, V.minb * (cg_grid() / 4) / bs.B);  // persistent: minb CTAs per SM in total
   const int chunk = V.chunk;
   const int units = (n_nodes + chunk - 1) / chunk;
