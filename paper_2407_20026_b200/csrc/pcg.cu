@@ -1583,7 +1583,8 @@ void launch_cg_update_sym(cudaStream_t s, int ndof, const double* dinv, double* 
 // 0 (12, 2, 3, 4) single designs, 1 (8, 2, 4, 4) batches, 2 (16, 2, 2, 8), 3 (8, 3, 3, 4).
 // Measured at C3b: 67.0, 68.4, 69.9, 71.6 us; also tried (live us): (4, 2, 8, 2) 75.9,
 // (16, 2, 2, 4) 72.3, (12, 2, 3, 6) 93 (spills), (10, 2, 3, 5) 71.7, (12, 3, 2, 4) 76.0,
-// (12, 2, 3, 3) 70.5.  Finer chunks pay the producer per chunk, larger ones limit the
+// (12, 2, 3, 3) 70.5, (9, 2, 4, 3) 67.5, (6, 2, 5, 3) 69.1, (15, 2, 2, 5) 69.6.  Finer chunks
+// pay the producer per chunk, larger ones limit the
 // CTAs per SM (shared memory) or spill.
 struct PullVariant {
   int smem;
