@@ -485,3 +485,20 @@ def test_pull_storage_general_nodes(sso):
     assert np.linalg.norm(u3 - uref) <= TOL_U * np.linalg.norm(uref)
     C3, _, _ = m3.grad()
     assert abs(C3 - OG.compliance(P["f"], uref)) <= TOL_C * abs(OG.compliance(P["f"], uref))
+
+
+def test_pull_storage_many_designs(sso):
+    """A batch larger than the persistent grid (one CTA per design, many chunks per CTA)
+    with the pull SpMV: every design equals its own single-design solve."""
+    B = 200
+    designs = [W.config5_design(b, n=6) for b in range(B)]
+    mb = sso.Model(designs[0], rtol=1e-12, batch=B)
+    mb.set_design(z=np.stack([d["z"] for d in designs]), t=np.stack([d["t"] for d in designs]))
+    mb.assemble()
+    U, infos = mb.solve(np.stack([d["f"] for d in designs]))
+    for b in (0, 99, 199):
+        m1 = sso.Model(designs[b], rtol=1e-12)
+        m1.assemble()
+        u1, _ = m1.solve(designs[b]["f"])
+        assert infos[b]["status"] == 0
+        assert np.linalg.norm(U[b] - u1) <= 1e-9 * np.linalg.norm(u1)
