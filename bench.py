@@ -226,10 +226,18 @@ def run_gpu(args):
     import paper_2407_20026_b200 as sso
     import workloads as W
 
-    P = W.config3b()
+    # N > 1: by default every GPU evaluates its own C3b design (independent evaluations, as
+    # in an optimisation loop over designs; weak scaling, no collective).  --strips splits one
+    # C3b into N node strips with NCCL halos and allreduces instead (strong scaling).
+    replicas = world > 1 and not args.strips
+    P = W.shell_config3(408, cfg=3, design=rank) if replicas else W.config3b()
     t0 = time.perf_counter()
     stream = torch.cuda.current_stream()
-    if world > 1:
+    if replicas:
+        m = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index, storage=args.storage,
+                      precond=args.precond)
+        parallelism = f"{world} GPUs x one C3b design each (independent evaluations, no collective)"
+    elif world > 1:
         # strong scaling: C3b split into `world` node strips, one per GPU; halos of p
         # and the CG scalars travel through NCCL
         import torch.distributed as dist
@@ -299,7 +307,8 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = args.steps / (ms_total / 1000.0)  # one (partitioned) C3b evaluation per step
+    # one C3b evaluation per step on every GPU (replicas) or one partitioned evaluation per step
+    value = (world if replicas else 1) * args.steps / (ms_total / 1000.0)
     cg_iters = int(np.median(iters))
 
     # ---- e2e: host buffers through the C ABI, copies inside the timed region --
@@ -327,7 +336,7 @@ def run_gpu(args):
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = e2e_steps / e2e_s
+    e2e_value = (world if replicas else 1) * e2e_steps / e2e_s
 
     # ---- roofline of the dominant kernel (SpMV inside PCG) --------------------
     peak, peak_src = measured_peaks()
@@ -384,7 +393,7 @@ def run_gpu(args):
         cpu = cpu_baseline_obj(P, cg_iters) if (world == 1 and not args.no_cpu) else None
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "scaling": "weak" if replicas else "strong", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (workloads.config3b, seeded)",
                "config": {"workload": "C3b: 408x408 MITC-4 shell quads, 1 003 686 DOF (reading c15)",
                           "n_nodes": n_nodes, "n_quads": nq, "ndof": ndof, "nnz": nnz,
@@ -511,6 +520,8 @@ def main():
     ap.add_argument("--storage", type=int, default=0,
                     help="sso_options.storage for single-GPU C3b (0 = library default)")
     ap.add_argument("--workload", default="C3b", choices=["C3b", "C5"])
+    ap.add_argument("--strips", action="store_true",
+                    help="N > 1: split one C3b into N node strips (NCCL) instead of one design per GPU")
     ap.add_argument("--batch", type=int, default=64, help="C5 designs per GPU")
     ap.add_argument("--virtual-parts", type=int, default=1,
                     help="run the partitioned (strip) algorithm with P strips on one GPU")

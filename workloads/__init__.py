@@ -181,14 +181,15 @@ def config2():
                     sup_node=bnd, sup_mask=np.full(len(bnd), PINNED), f=f)
 
 
-def shell_config3(n: int, cfg: int = 3, supports: str = "clamped_edges", L: float = 10.0):
+def shell_config3(n: int, cfg: int = 3, supports: str = "clamped_edges", L: float = 10.0, design: int = 0):
     """C3 / C3b / C4 shell family, SURVEY.md §8(d) C3, C3b, C4.
 
     z = 1.5 sin sin + dz, dz = s * sum of 8 Fourier modes scaled to max|dz| = 0.2 m;
     t ~ log-uniform [0.05, 0.2]; E = 30 GPa, nu = 0.2; self-weight rho = 2400 kg/m^3
     plus 2 kN/m^2.  supports: 'clamped_edges' (C3) or 'c4' (edge y=0 clamped, corners
-    (0, L), (L, L) pinned)."""
-    rng = _rng(cfg)
+    (0, L), (L, L) pinned).  design > 0 draws another seeded instance of the recipe
+    (design 0 is the configuration itself)."""
+    rng = _rng(cfg, design)
     x, y = grid_nodes(n, L)
     dz = _fourier_field(x, y, L, rng, 8)
     amax = np.max(np.abs(dz))
