@@ -214,3 +214,23 @@ def test_c5_full_batch_sampled():
         m1.close()
     uref, _, _ = OG.evaluate(designs[63], "pcg", rtol=1e-12)
     assert np.linalg.norm(U[63] - uref) <= 1e-8 * np.linalg.norm(uref)
+
+
+def test_c3b_eight_strips(c3b):
+    """The partitioned algorithm at the bench size: C3b in 8 node strips
+    (in-process transport, pull storage on every strip) reaches the bench tolerance with the
+    single-strip iteration count (±2 %) and the same solution within the CG error."""
+    import paper_2407_20026_b200 as sso
+    _, P, m = c3b
+    u1, i1 = m.solve(P["f"])
+    m8 = sso.Model(P, rtol=RTOL_BENCH, n_parts=8)
+    assert m8.n_parts_here == 8 and m8.storage_info()[2] == 3
+    m8.assemble()
+    u8, i8 = m8.solve(P["f"])
+    assert i8["status"] == 0 and i8["true_rel_res"] <= 20 * RTOL_BENCH
+    assert abs(i8["iters"] - i1["iters"]) <= 0.02 * i1["iters"]
+    assert np.linalg.norm(u8 - u1) <= 1e-6 * np.linalg.norm(u1)
+    C8, _, _ = m8.grad()
+    C1, _, _ = m.grad()
+    assert C8 == pytest.approx(C1, rel=1e-9)
+    m8.close()
