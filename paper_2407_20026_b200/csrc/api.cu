@@ -21,6 +21,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -133,6 +134,9 @@ struct Part {
   int32_t* pdesc = nullptr;           // pull: 16-int per-node descriptors (build_pull_desc)
   double* binv = nullptr;             // precond 1: [B][21][n_own] packed (K_nn)^-1
   double* zb = nullptr;               // precond 1: z = M^-1 r [B][ndof]
+  bool cgf = false;                   // fused x / r / p update (cg_update_fused): one design, one
+                                      // part, point Jacobi, full or pull storage
+  double* p2 = nullptr;               // cgf: the second p buffer (ping-pong)
   CUtensorMap pull_tmap;              // pull: [B n_ublocks][36] view of vals for the gather4 TMA
   UpperPattern up;
   int64_t* lptr = nullptr;            // sym: incoming transpose slots per node
@@ -479,10 +483,19 @@ constexpr int PROF_EVERY = 16;
 // Partitioned: p update, halo of p, SpMV + local p^T q, allreduce, alpha; update +
 // local r^T z / r^T r, allreduce, beta and the convergence test.  `rec` brackets part 0's SpMV with
 // the event pair ev[0], ev[1].
-int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev) {
+int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev, int it) {
   int rc;
   if (!h->distributed()) {
     Part& P = h->P0();
+    if (P.cgf) {  // SpMV of the current p, then x / r / p_next in one kernel (ping-pong p)
+      double* pc = (it & 1) ? P.p2 : P.p;
+      double* pn = (it & 1) ? P.p : P.p2;
+      if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
+      spmv_apply(s, P, pc, P.q, P.st);
+      if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
+      launch_cg_update_fused(s, (int)P.ndof_own, P.dinv, P.xs, P.r, pc, P.q, pn, P.partial, P.st);
+      return SSO_OK;
+    }
     if (P.binv)
       launch_cg_pupdate_z(s, (int)P.ndof_own, P.zb, P.p, P.st, P.bs);
     else
@@ -548,7 +561,7 @@ int build_chunk_graph(sso_ctx* h, int prof_slot, cudaGraphExec_t* out) {
   int rc = SSO_OK;
   for (int i = 0; i < K && rc == SSO_OK; ++i) {
     const bool rec = prof_slot >= 0 && (i % PROF_EVERY) == 0;
-    rc = cg_iteration(h, h->cap_stream, rec ? &h->chunk_ev[prof_slot][2 * i] : nullptr);
+    rc = cg_iteration(h, h->cap_stream, rec ? &h->chunk_ev[prof_slot][2 * i] : nullptr, i);
   }
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
@@ -580,7 +593,7 @@ void free_part(Part& P) {
                   P.inc_slot, P.stage, P.vals, P.dinv, P.f, P.fbc, P.xs, P.r, P.p, P.q, P.tmp, P.gu,
                   P.gf, P.partial, P.st, P.flags, P.tickets, P.scal, P.slot_partial, P.dxyz, P.dt,
                   P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
-                  P.lptr, P.lslot, P.lpull, P.pdesc, P.binv, P.zb, P.tbuf, P.dE,
+                  P.lptr, P.lslot, P.lpull, P.pdesc, P.binv, P.zb, P.p2, P.tbuf, P.dE,
                   P.ub, P.fb, P.lam, P.dxyz2, P.dt2, P.dE2, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -828,6 +841,15 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   AL(xs, B * P.ndof);
   AL(r, B * P.ndof);
   AL(p, B * P.ndof);
+  {
+    const char* env = getenv("SSO_CG_FUSED");
+    P.cgf = B == 1 && L.n_parts == 1 && h->nranks == 1 && h->precond != 1 && (P.pull || !P.sym) &&
+            h->check_every % 2 == 0 && cg_fused_grid() > 0 && !(env && env[0] == '0');
+  }
+  if (P.cgf) {
+    AL(p2, P.ndof);
+    CK(h, cudaMemset(P.p2, 0, P.ndof * sizeof(double)));
+  }
   AL(q, B * P.ndof);
   AL(tmp, B * P.ndof);
   AL(gu, B * P.ndof);
@@ -1194,6 +1216,8 @@ static int replace_step(sso_ctx* h, int mode) {
       launch_cg_replace_block(h->stream, P.n_own, P.fbc, P.tmp, P.binv, P.r, P.zb, P.partial, P.st, mode, P.bs);
     else
       launch_cg_replace(h->stream, (int)P.ndof_own, P.fbc, P.tmp, P.dinv, P.r, P.p, P.partial, P.st, mode, P.bs);
+    // fused form: a chunk (even length) ends with the current p in P.p, the previous in P.p2
+    if (P.cgf) launch_cg_pfix(h->stream, (int)P.ndof_own, P.dinv, P.r, P.p2, P.p, P.st);
   }
   if (h->distributed()) {
     if ((rc = allreduce(h, 2))) return rc;

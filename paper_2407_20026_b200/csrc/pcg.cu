@@ -1087,10 +1087,146 @@ __global__ void __launch_bounds__(256) cg_pupdate_kernel(int ndof, const double*
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
     const double2 ri = r2[i], di = d2[i];
     double2 pi = p2[i];
-    pi.x = di.x * ri.x + beta * pi.x;
-    pi.y = di.y * ri.y + beta * pi.y;
+    // z = dinv r rounded, then one fma: the rounding of cg_update_fused_kernel
+    pi.x = __fma_rn(beta, pi.x, __dmul_rn(di.x, ri.x));
+    pi.y = __fma_rn(beta, pi.y, __dmul_rn(di.y, ri.y));
     p2[i] = pi;
   }
+}
+
+// Fused form of cg_update + cg_pupdate for one design on one part (point Jacobi).
+// Phase 1 as cg_update_kernel (x += alpha p, r -= alpha q, z = dinv r; r^T z, r^T r
+// over the grid, the last CTA forms beta and the convergence test); then a grid-wide
+// barrier (every CTA co-resident: the grid is bounded by the occupancy, launched on an
+// otherwise idle stream after the SpMV) and phase 2: p_next = z + beta p, from
+// registers for the first FUSED_ITEMS double2 of each thread.  p_next goes to the
+// OTHER p buffer (ping-pong), so a residual replacement can re-form it (cg_pfix).
+// The barrier wait is bounded: a grid that is not co-resident fails with
+// SSO_E_CUDA instead of hanging the device.
+constexpr int FUSED_ITEMS = 4;
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(256, 3) cg_update_fused_kernel(int ndof, const double* __restrict__ dinv,
+                                                                 double* __restrict__ x,
+                                                                 double* __restrict__ r,
+                                                                 const double* __restrict__ p,
+                                                                 const double* __restrict__ q,
+                                                                 double* __restrict__ pn,
+                                                                 double* __restrict__ partial,
+                                                                 CgState* st) {
+  __shared__ double sm[64];
+  __shared__ int s_go;
+  if (st->done) return;  // set only by earlier kernels: the same for every CTA
+  const unsigned gen0 = st->gen;  // advanced only after every CTA has arrived below
+  const double alpha = st->alpha;
+  double v[2] = {0.0, 0.0};  // r^T z, r^T r
+  const int64_t n2 = ndof / 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const double2* __restrict__ p2 = reinterpret_cast<const double2*>(p);
+  const double2* __restrict__ q2 = reinterpret_cast<const double2*>(q);
+  const double2* __restrict__ d2 = reinterpret_cast<const double2*>(dinv);
+  double2* __restrict__ x2 = reinterpret_cast<double2*>(x);
+  double2* __restrict__ r2 = reinterpret_cast<double2*>(r);
+  double2* __restrict__ pn2 = reinterpret_cast<double2*>(pn);
+  double2 zk[FUSED_ITEMS], pk[FUSED_ITEMS];
+#pragma unroll
+  for (int k = 0; k < FUSED_ITEMS; ++k) {
+    const int64_t i = i0 + k * stride;
+    zk[k] = pk[k] = make_double2(0.0, 0.0);
+    if (i < n2) {
+      const double2 pi = p2[i], qi = q2[i], di = d2[i];
+      double2 xi = x2[i], ri = r2[i];
+      xi.x += alpha * pi.x;
+      xi.y += alpha * pi.y;
+      ri.x -= alpha * qi.x;
+      ri.y -= alpha * qi.y;
+      x2[i] = xi;
+      r2[i] = ri;
+      v[0] += ri.x * (di.x * ri.x) + ri.y * (di.y * ri.y);
+      v[1] += ri.x * ri.x + ri.y * ri.y;
+      zk[k] = make_double2(__dmul_rn(di.x, ri.x), __dmul_rn(di.y, ri.y));
+      pk[k] = pi;
+    }
+  }
+  for (int64_t i = i0 + FUSED_ITEMS * stride; i < n2; i += stride) {
+    const double2 pi = p2[i], qi = q2[i], di = d2[i];
+    double2 xi = x2[i], ri = r2[i];
+    xi.x += alpha * pi.x;
+    xi.y += alpha * pi.y;
+    ri.x -= alpha * qi.x;
+    ri.y -= alpha * qi.y;
+    x2[i] = xi;
+    r2[i] = ri;
+    v[0] += ri.x * (di.x * ri.x) + ri.y * (di.y * ri.y);
+    v[1] += ri.x * ri.x + ri.y * ri.y;
+  }
+  const bool last = grid_sum<2>(v, partial, &st->ticket[1], sm);
+  if (threadIdx.x == 0) {
+    if (last) {
+      const double rz_new = v[0];
+      st->beta = rz_new / st->rz;
+      st->rz_prev = st->rz;
+      st->rz = rz_new;
+      st->rr = v[1];
+      st->iter += 1;
+      st->pfix = 0;
+      if (v[1] <= st->tol2) {
+        st->done = 1;
+        st->status = SSO_OK;
+      } else if (st->iter >= st->max_iter) {
+        st->done = 1;
+        st->status = SSO_E_NOT_CONVERGED;
+      }
+      __threadfence();
+      atomicAdd(&st->gen, 1u);  // release the grid
+      s_go = 1;
+    } else {
+      // bounded wait (~2^22 polls): a non-co-resident grid reports instead of hanging
+      int go = 0;
+      for (int spin = 0; spin < (1 << 22); ++spin) {
+        if (ld_acquire_u32(&st->gen) != gen0) {
+          go = 1;
+          break;
+        }
+        __nanosleep(64);
+      }
+      if (!go) {
+        st->status = SSO_E_CUDA;
+        st->done = 1;
+      }
+      s_go = go;
+    }
+  }
+  __syncthreads();
+  if (!s_go || __ldcg(&st->done)) return;
+  const double beta = __ldcg(&st->beta);
+#pragma unroll
+  for (int k = 0; k < FUSED_ITEMS; ++k) {
+    const int64_t i = i0 + k * stride;
+    if (i < n2) pn2[i] = make_double2(__fma_rn(beta, pk[k].x, zk[k].x), __fma_rn(beta, pk[k].y, zk[k].y));
+  }
+  for (int64_t i = i0 + FUSED_ITEMS * stride; i < n2; i += stride) {
+    const double2 ri = r2[i], di = d2[i], pi = p2[i];
+    pn2[i] = make_double2(__fma_rn(beta, pi.x, __dmul_rn(di.x, ri.x)), __fma_rn(beta, pi.y, __dmul_rn(di.y, ri.y)));
+  }
+}
+
+// p_out = dinv r + beta p_in after a residual replacement of the fused form
+__global__ void __launch_bounds__(256) cg_pfix_kernel(int ndof, const double* __restrict__ dinv,
+                                                      const double* __restrict__ r,
+                                                      const double* __restrict__ pin,
+                                                      double* __restrict__ pout, const CgState* st) {
+  if (st->done || !st->pfix) return;
+  const double beta = st->beta;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndof; i += stride)
+    pout[i] = __fma_rn(beta, pin[i], __dmul_rn(dinv[i], r[i]));
 }
 
 // f_bc = f with fixed DOFs zeroed; x = x0 (fixed zeroed) or 0; r = f_bc - K x0; p = z = dinv r.
@@ -1330,6 +1466,7 @@ __global__ void __launch_bounds__(256) cg_replace_kernel(int ndof, const double*
       // the next p update forms p = z + beta p: restart (final) -> beta = 0
       st->beta = (mode == REPL_FINAL) ? 0.0 : v[0] / st->rz_prev;
       st->act = 0;
+      st->pfix = 1;
     }
   }
 }
@@ -1704,6 +1841,31 @@ void launch_cg_update(cudaStream_t s, int ndof, const double* dinv, double* x, d
                       const BatchStrides& bs) {
   cg_update_kernel<<<dim3(vec_grid(ndof, bs.B), bs.B), 256, 0, s>>>(ndof, dinv, x, r, p, q, partial, st, bs);
   SSO_POST_LAUNCH("cg_update_kernel");
+}
+
+int cg_fused_grid() {
+  static int g = -1;
+  if (g < 0) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cg_update_fused_kernel, 256, 0) != cudaSuccess) occ = 0;
+    cg_grid();
+    g = std::min(occ, 3) * g_sms;
+  }
+  return g;
+}
+
+void launch_cg_update_fused(cudaStream_t s, int ndof, const double* dinv, double* x, double* r,
+                            const double* p, const double* q, double* pn, double* partial, CgState* st) {
+  const int64_t need = ((int64_t)ndof / 2 + 255) / 256;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cg_fused_grid()));
+  cg_update_fused_kernel<<<grid, 256, 0, s>>>(ndof, dinv, x, r, p, q, pn, partial, st);
+  SSO_POST_LAUNCH("cg_update_fused_kernel");
+}
+
+void launch_cg_pfix(cudaStream_t s, int ndof, const double* dinv, const double* r, const double* pin,
+                    double* pout, const CgState* st) {
+  cg_pfix_kernel<<<vec_grid(ndof), 256, 0, s>>>(ndof, dinv, r, pin, pout, st);
+  SSO_POST_LAUNCH("cg_pfix_kernel");
 }
 
 void launch_cg_pupdate(cudaStream_t s, int ndof, const double* dinv, const double* r, double* p,

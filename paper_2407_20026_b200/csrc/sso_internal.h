@@ -82,6 +82,8 @@ struct CgState {
   int restarts;     // final true-residual restarts used
   int floor;        // 1 = the true residual sits far above the recurrence (fp64 floor):
                     //     no further replacements / restarts
+  int pfix;         // 1 = r was replaced after the fused update formed p: re-form p
+  unsigned int gen; // grid-barrier generation of the fused update kernel
 };
 
 // error flags written by device kernels (atomicMin on the offending index)
@@ -160,6 +162,16 @@ void launch_cg_update(cudaStream_t s, int ndof, const double* dinv, double* x, d
 void launch_cg_pupdate(cudaStream_t s, int ndof, const double* dinv, const double* r,
                        double* p, CgState* st,
     const BatchStrides& bs = BatchStrides());
+// Fused x / r update + p update (single design, single part, point Jacobi): one
+// kernel with a grid-wide barrier between the r^T z reduction and p_next = z + beta p
+// (ping-pong p buffers, so a residual replacement can re-form p from the previous one).
+void launch_cg_update_fused(cudaStream_t s, int ndof, const double* dinv, double* x, double* r,
+                            const double* p, const double* q, double* pn, double* partial, CgState* st);
+// p_out = dinv r + beta p_in after a residual replacement (st->pfix), else nothing.
+void launch_cg_pfix(cudaStream_t s, int ndof, const double* dinv, const double* r, const double* pin,
+                    double* pout, const CgState* st);
+// largest co-resident grid of the fused update kernel (0 = unavailable)
+int cg_fused_grid();
 // Symmetric (upper-block) storage SpMV: pass 1 streams the upper runs (TMA ring),
 // writes the upper row sums to y and the transpose contributions K_nm^T x_n to
 // tbuf; pass 2 adds each node's incoming slots (ascending source node) and, with
