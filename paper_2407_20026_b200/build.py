@@ -37,7 +37,7 @@ def nvcc():
 
 def build(verbose=False, force=False):
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    hdrs = [os.path.join(CSRC, "sso_internal.h"), os.path.join(CSRC, "shell_math.cuh"),
+    hdrs = [os.path.join(CSRC, "sso_internal.h"), os.path.join(CSRC, "shell_math.cuh"), os.path.join(CSRC, "cg_fused.cuh"),
             os.path.join(ROOT, "include", "sso.h")]
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)

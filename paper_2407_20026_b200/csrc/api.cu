@@ -134,8 +134,8 @@ struct Part {
   int32_t* pdesc = nullptr;           // pull: 16-int per-node descriptors (build_pull_desc)
   double* binv = nullptr;             // precond 1: [B][21][n_own] packed (K_nn)^-1
   double* zb = nullptr;               // precond 1: z = M^-1 r [B][ndof]
-  bool cgf = false;                   // fused x / r / p update (cg_update_fused): one design, one
-                                      // part, point Jacobi, full or pull storage
+  bool cgf = false;                   // fused x / r / p update (cg_update_fused / _block_fused): one
+                                      // part, full or pull storage, B <= the co-resident grid
   double* p2 = nullptr;               // cgf: the second p buffer (ping-pong)
   CUtensorMap pull_tmap;              // pull: [B n_ublocks][36] view of vals for the gather4 TMA
   UpperPattern up;
@@ -493,7 +493,10 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev, int it) {
       if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
       spmv_apply(s, P, pc, P.q, P.st);
       if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
-      launch_cg_update_fused(s, (int)P.ndof_own, P.dinv, P.xs, P.r, pc, P.q, pn, P.partial, P.st);
+      if (P.binv)
+        launch_cg_update_block_fused(s, P.n_own, P.binv, P.xs, P.r, pc, P.q, pn, P.partial, P.st, P.bs);
+      else
+        launch_cg_update_fused(s, (int)P.ndof_own, P.dinv, P.xs, P.r, pc, P.q, pn, P.partial, P.st, P.bs);
       return SSO_OK;
     }
     if (P.binv)
@@ -843,12 +846,13 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   AL(p, B * P.ndof);
   {
     const char* env = getenv("SSO_CG_FUSED");
-    P.cgf = B == 1 && L.n_parts == 1 && h->nranks == 1 && h->precond != 1 && (P.pull || !P.sym) &&
-            h->check_every % 2 == 0 && cg_fused_grid() > 0 && !(env && env[0] == '0');
+    const int fg = h->precond == 1 ? cg_block_fused_grid() : cg_fused_grid();
+    P.cgf = B <= fg && L.n_parts == 1 && h->nranks == 1 && (P.pull || !P.sym) && h->check_every % 2 == 0 &&
+            !(env && env[0] == '0');
   }
   if (P.cgf) {
-    AL(p2, P.ndof);
-    CK(h, cudaMemset(P.p2, 0, P.ndof * sizeof(double)));
+    AL(p2, B * P.ndof);
+    CK(h, cudaMemset(P.p2, 0, B * P.ndof * sizeof(double)));
   }
   AL(q, B * P.ndof);
   AL(tmp, B * P.ndof);
@@ -1212,12 +1216,16 @@ static int replace_step(sso_ctx* h, int mode) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     launch_cg_check(h->stream, P.st, mode, P.B);
-    if (P.binv)
+    // fused form: a chunk (even length) ends with the current p in P.p, the previous in
+    // P.p2; a replaced r re-forms p from the previous one (the classic form forms p in
+    // the next iteration's p update)
+    if (P.binv) {
       launch_cg_replace_block(h->stream, P.n_own, P.fbc, P.tmp, P.binv, P.r, P.zb, P.partial, P.st, mode, P.bs);
-    else
+      if (P.cgf) launch_cg_pfix_z(h->stream, (int)P.ndof_own, P.zb, P.p2, P.p, P.st, P.bs);
+    } else {
       launch_cg_replace(h->stream, (int)P.ndof_own, P.fbc, P.tmp, P.dinv, P.r, P.p, P.partial, P.st, mode, P.bs);
-    // fused form: a chunk (even length) ends with the current p in P.p, the previous in P.p2
-    if (P.cgf) launch_cg_pfix(h->stream, (int)P.ndof_own, P.dinv, P.r, P.p2, P.p, P.st);
+      if (P.cgf) launch_cg_pfix(h->stream, (int)P.ndof_own, P.dinv, P.r, P.p2, P.p, P.st, P.bs);
+    }
   }
   if (h->distributed()) {
     if ((rc = allreduce(h, 2))) return rc;

@@ -13,6 +13,7 @@
 // z [B][6 n_own] is stored by the update so that the p update reads one vector.
 // Kernels are node-granular (a thread per node, its 6-vectors as 3 double2) and
 // keep the atomic-free fixed-order reductions of pcg.cu (same epilogues).
+#include "cg_fused.cuh"
 #include "sso_internal.h"
 
 namespace sso {
@@ -338,10 +339,113 @@ __global__ void __launch_bounds__(256) cg_pupdate_z_kernel(int ndof, const doubl
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
     const double2 zi = z2[i];
     double2 pi = p2[i];
-    pi.x = zi.x + beta * pi.x;
-    pi.y = zi.y + beta * pi.y;
+    pi.x = __fma_rn(beta, pi.x, zi.x);  // the rounding of the fused form
+    pi.y = __fma_rn(beta, pi.y, zi.y);
     p2[i] = pi;
   }
+}
+
+// Fused form of cg_update_block + cg_pupdate_z (one part, B <= cg_fused_grid()):
+// x += alpha p, r -= alpha q, z = M^-1 r with r^T z, r^T r over the grid, the grid
+// barrier of cg_fused.cuh, then p_next = z + beta p into the other p buffer, z kept
+// in registers for the first FB_ITEMS nodes of each thread (no z round trip).
+constexpr int FB_ITEMS = 3;
+
+__global__ void __launch_bounds__(256, 2) cg_update_block_fused_kernel(
+    int n_nodes, const double* __restrict__ binv, double* __restrict__ x, double* __restrict__ r,
+    const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ pn,
+    double* __restrict__ partial, CgState* st, BatchStrides bs) {
+  __shared__ double sm[64];
+  __shared__ int s_go;
+  {
+    const int bd = blockIdx.y;
+    binv += (int64_t)bd * 21 * n_nodes;
+    x += bd * bs.dof;
+    r += bd * bs.dof;
+    p += bd * bs.dof;
+    q += bd * bs.dof;
+    pn += bd * bs.dof;
+    partial += bd * bs.partial;
+    st += bd;
+  }
+  if (st->done) return;
+  const unsigned gen0 = st->gen;
+  const double alpha = st->alpha;
+  double v[2] = {0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double zk[FB_ITEMS][6], pk[FB_ITEMS][6];
+  auto step = [&](int64_t n, double (&zi)[6], double (&pi)[6]) {
+    double xi[6], ri[6], qi[6];
+    ld6(x, n, xi);
+    ld6(r, n, ri);
+    ld6(p, n, pi);
+    ld6(q, n, qi);
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+      xi[a] += alpha * pi[a];
+      ri[a] -= alpha * qi[a];
+    }
+    st6(x, n, xi);
+    st6(r, n, ri);
+    block_apply(binv, n_nodes, n, ri, zi);
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+      v[0] += ri[a] * zi[a];
+      v[1] += ri[a] * ri[a];
+    }
+  };
+#pragma unroll
+  for (int k = 0; k < FB_ITEMS; ++k)
+    if (n0 + k * stride < n_nodes) step(n0 + k * stride, zk[k], pk[k]);
+  for (int64_t n = n0 + FB_ITEMS * stride; n < n_nodes; n += stride) {
+    double zi[6], pi[6];
+    step(n, zi, pi);
+  }
+  const bool last = grid_sum<2>(v, partial, &st->ticket[1], sm);
+  if (threadIdx.x == 0) s_go = cg_fused_epilogue(last, v, st, gen0);
+  __syncthreads();
+  if (!s_go || __ldcg(&st->done)) return;
+  const double beta = __ldcg(&st->beta);
+#pragma unroll
+  for (int k = 0; k < FB_ITEMS; ++k) {
+    const int64_t n = n0 + k * stride;
+    if (n < n_nodes) {
+      double o[6];
+#pragma unroll
+      for (int a = 0; a < 6; ++a) o[a] = __fma_rn(beta, pk[k][a], zk[k][a]);
+      st6(pn, n, o);
+    }
+  }
+  for (int64_t n = n0 + FB_ITEMS * stride; n < n_nodes; n += stride) {
+    double ri[6], pi[6], zi[6], o[6];
+    ld6(r, n, ri);
+    ld6(p, n, pi);
+    block_apply(binv, n_nodes, n, ri, zi);
+#pragma unroll
+    for (int a = 0; a < 6; ++a) o[a] = __fma_rn(beta, pi[a], zi[a]);
+    st6(pn, n, o);
+  }
+}
+
+// p_out = z + beta p_in after a residual replacement of the fused form (z from
+// cg_replace_block_kernel)
+__global__ void __launch_bounds__(256) cg_pfix_z_kernel(int ndof, const double* __restrict__ z,
+                                                        const double* __restrict__ pin,
+                                                        double* __restrict__ pout, const CgState* st,
+                                                        BatchStrides bs) {
+  {
+    const int bd = blockIdx.y;
+    z += bd * bs.dof;
+    pin += bd * bs.dof;
+    pout += bd * bs.dof;
+    st += bd;
+  }
+  if (st->done || !st->pfix) return;
+  const double beta = st->beta;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ndof; i += stride)
+    pout[i] = __fma_rn(beta, pin[i], z[i]);
 }
 
 // Residual replacement (designs selected by cg_check): r = f_bc - K x, z = M^-1 r (replace epilogue)
@@ -387,8 +491,9 @@ __global__ void __launch_bounds__(256) cg_replace_block_kernel(int n_nodes, cons
       st->rz = v[0];
       st->rr = v[1];
       st->rr_ref = v[1];
-      st->beta = (mode == REPL_FINAL) ? 0.0 : v[0] / st->rz_prev;
+      st->beta = (mode == REPL_FINAL || st->act == 2) ? 0.0 : v[0] / st->rz_prev;
       st->act = 0;
+      st->pfix = 1;
     }
   }
 }
@@ -430,6 +535,33 @@ void launch_cg_pupdate_z(cudaStream_t s, int ndof, const double* z, double* p, C
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)cg_grid() / bs.B));
   cg_pupdate_z_kernel<<<dim3(grid, bs.B), 256, 0, s>>>(ndof, z, p, st, bs);
   SSO_POST_LAUNCH("cg_pupdate_z_kernel");
+}
+
+int cg_block_fused_grid() {
+  static int g = -1;
+  if (g < 0) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cg_update_block_fused_kernel, 256, 0) != cudaSuccess)
+      occ = 0;
+    g = std::min(occ, 2) * (cg_grid() / 4);
+  }
+  return g;
+}
+
+void launch_cg_update_block_fused(cudaStream_t s, int n_nodes, const double* binv, double* x, double* r,
+                                  const double* p, const double* q, double* pn, double* partial, CgState* st,
+                                  const BatchStrides& bs) {
+  const int64_t need = ((int64_t)n_nodes + 255) / 256;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cg_block_fused_grid() / bs.B));
+  cg_update_block_fused_kernel<<<dim3(grid, bs.B), 256, 0, s>>>(n_nodes, binv, x, r, p, q, pn, partial, st, bs);
+  SSO_POST_LAUNCH("cg_update_block_fused_kernel");
+}
+
+void launch_cg_pfix_z(cudaStream_t s, int ndof, const double* z, const double* pin, double* pout,
+                      const CgState* st, const BatchStrides& bs) {
+  const int grid = node_grid(ndof / 6, bs.B);
+  cg_pfix_z_kernel<<<dim3(grid, bs.B), 256, 0, s>>>(ndof, z, pin, pout, st, bs);
+  SSO_POST_LAUNCH("cg_pfix_z_kernel");
 }
 
 void launch_cg_replace_block(cudaStream_t s, int n_nodes, const double* fbc, const double* Kx, const double* binv,

@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "cg_fused.cuh"
 #include "sso_internal.h"
 
 namespace sso {
@@ -1094,33 +1095,35 @@ __global__ void __launch_bounds__(256) cg_pupdate_kernel(int ndof, const double*
   }
 }
 
-// Fused form of cg_update + cg_pupdate for one design on one part (point Jacobi).
+// Fused form of cg_update + cg_pupdate for the designs of one part (point Jacobi).
 // Phase 1 as cg_update_kernel (x += alpha p, r -= alpha q, z = dinv r; r^T z, r^T r
 // over the grid, the last CTA forms beta and the convergence test); then a grid-wide
-// barrier (every CTA co-resident: the grid is bounded by the occupancy, launched on an
-// otherwise idle stream after the SpMV) and phase 2: p_next = z + beta p, from
-// registers for the first FUSED_ITEMS double2 of each thread.  p_next goes to the
-// OTHER p buffer (ping-pong), so a residual replacement can re-form it (cg_pfix).
-// The barrier wait is bounded: a grid that is not co-resident fails with
-// SSO_E_CUDA instead of hanging the device.
-constexpr int FUSED_ITEMS = 4;
+// barrier (cg_fused.cuh) and phase 2: p_next = z + beta p, from registers for the
+// first FUSED_ITEMS double2 of each thread.  p_next goes to the OTHER p buffer
+// (ping-pong), so a residual replacement can re-form it (cg_pfix).
+constexpr int FUSED_ITEMS = 7;
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__global__ void __launch_bounds__(256, 3) cg_update_fused_kernel(int ndof, const double* __restrict__ dinv,
+__global__ void __launch_bounds__(256, 2) cg_update_fused_kernel(int ndof, const double* __restrict__ dinv,
                                                                  double* __restrict__ x,
                                                                  double* __restrict__ r,
                                                                  const double* __restrict__ p,
                                                                  const double* __restrict__ q,
                                                                  double* __restrict__ pn,
                                                                  double* __restrict__ partial,
-                                                                 CgState* st) {
+                                                                 CgState* st, BatchStrides bs) {
   __shared__ double sm[64];
   __shared__ int s_go;
+  {  // design of a batch (blockIdx.y): its own CTAs, reduction and barrier
+    const int bd = blockIdx.y;
+    dinv += bd * bs.dof;
+    x += bd * bs.dof;
+    r += bd * bs.dof;
+    p += bd * bs.dof;
+    q += bd * bs.dof;
+    pn += bd * bs.dof;
+    partial += bd * bs.partial;
+    st += bd;
+  }
   if (st->done) return;  // set only by earlier kernels: the same for every CTA
   const unsigned gen0 = st->gen;  // advanced only after every CTA has arrived below
   const double alpha = st->alpha;
@@ -1167,42 +1170,7 @@ __global__ void __launch_bounds__(256, 3) cg_update_fused_kernel(int ndof, const
     v[1] += ri.x * ri.x + ri.y * ri.y;
   }
   const bool last = grid_sum<2>(v, partial, &st->ticket[1], sm);
-  if (threadIdx.x == 0) {
-    if (last) {
-      const double rz_new = v[0];
-      st->beta = rz_new / st->rz;
-      st->rz_prev = st->rz;
-      st->rz = rz_new;
-      st->rr = v[1];
-      st->iter += 1;
-      st->pfix = 0;
-      if (v[1] <= st->tol2) {
-        st->done = 1;
-        st->status = SSO_OK;
-      } else if (st->iter >= st->max_iter) {
-        st->done = 1;
-        st->status = SSO_E_NOT_CONVERGED;
-      }
-      __threadfence();
-      atomicAdd(&st->gen, 1u);  // release the grid
-      s_go = 1;
-    } else {
-      // bounded wait (~2^22 polls): a non-co-resident grid reports instead of hanging
-      int go = 0;
-      for (int spin = 0; spin < (1 << 22); ++spin) {
-        if (ld_acquire_u32(&st->gen) != gen0) {
-          go = 1;
-          break;
-        }
-        __nanosleep(64);
-      }
-      if (!go) {
-        st->status = SSO_E_CUDA;
-        st->done = 1;
-      }
-      s_go = go;
-    }
-  }
+  if (threadIdx.x == 0) s_go = cg_fused_epilogue(last, v, st, gen0);
   __syncthreads();
   if (!s_go || __ldcg(&st->done)) return;
   const double beta = __ldcg(&st->beta);
@@ -1221,7 +1189,16 @@ __global__ void __launch_bounds__(256, 3) cg_update_fused_kernel(int ndof, const
 __global__ void __launch_bounds__(256) cg_pfix_kernel(int ndof, const double* __restrict__ dinv,
                                                       const double* __restrict__ r,
                                                       const double* __restrict__ pin,
-                                                      double* __restrict__ pout, const CgState* st) {
+                                                      double* __restrict__ pout, const CgState* st,
+                                                      BatchStrides bs) {
+  {
+    const int bd = blockIdx.y;
+    dinv += bd * bs.dof;
+    r += bd * bs.dof;
+    pin += bd * bs.dof;
+    pout += bd * bs.dof;
+    st += bd;
+  }
   if (st->done || !st->pfix) return;
   const double beta = st->beta;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -1343,7 +1320,7 @@ __global__ void cg_scalar_kernel(CgState* st, int phase) {
       st->rr = st->red[1];
       st->rr_ref = st->red[1];
       // restart (final): p = z; periodic: beta from the replaced r^T z
-      st->beta = (phase == PH_REPLACED + 1) ? 0.0 : st->red[0] / st->rz_prev;
+      st->beta = (phase == PH_REPLACED + 1 || st->act == 2) ? 0.0 : st->red[0] / st->rz_prev;
       st->act = 0;
     }
     return;
@@ -1409,7 +1386,7 @@ __global__ void cg_check_kernel(CgState* st, int mode, int B) {
     S->act = 0;
     if (!S->done && !S->floor && S->rr < REPL_FACTOR * S->rr_ref) {
       if (drifted) S->floor = 1;
-      else S->act = 1;
+      else S->act = (tt > REPL_CONT * REPL_CONT * S->rr) ? 2 : 1;
     }
   } else {
     S->act = 0;
@@ -1464,7 +1441,7 @@ __global__ void __launch_bounds__(256) cg_replace_kernel(int ndof, const double*
       st->rr = v[1];
       st->rr_ref = v[1];
       // the next p update forms p = z + beta p: restart (final) -> beta = 0
-      st->beta = (mode == REPL_FINAL) ? 0.0 : v[0] / st->rz_prev;
+      st->beta = (mode == REPL_FINAL || st->act == 2) ? 0.0 : v[0] / st->rz_prev;
       st->act = 0;
       st->pfix = 1;
     }
@@ -1849,22 +1826,24 @@ int cg_fused_grid() {
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cg_update_fused_kernel, 256, 0) != cudaSuccess) occ = 0;
     cg_grid();
-    g = std::min(occ, 3) * g_sms;
+    g = std::min(occ, 2) * g_sms;
   }
   return g;
 }
 
 void launch_cg_update_fused(cudaStream_t s, int ndof, const double* dinv, double* x, double* r,
-                            const double* p, const double* q, double* pn, double* partial, CgState* st) {
+                            const double* p, const double* q, double* pn, double* partial, CgState* st,
+                            const BatchStrides& bs) {
+  // every CTA of every design co-resident (bs.B <= cg_fused_grid(), checked at create)
   const int64_t need = ((int64_t)ndof / 2 + 255) / 256;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cg_fused_grid()));
-  cg_update_fused_kernel<<<grid, 256, 0, s>>>(ndof, dinv, x, r, p, q, pn, partial, st);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cg_fused_grid() / bs.B));
+  cg_update_fused_kernel<<<dim3(grid, bs.B), 256, 0, s>>>(ndof, dinv, x, r, p, q, pn, partial, st, bs);
   SSO_POST_LAUNCH("cg_update_fused_kernel");
 }
 
 void launch_cg_pfix(cudaStream_t s, int ndof, const double* dinv, const double* r, const double* pin,
-                    double* pout, const CgState* st) {
-  cg_pfix_kernel<<<vec_grid(ndof), 256, 0, s>>>(ndof, dinv, r, pin, pout, st);
+                    double* pout, const CgState* st, const BatchStrides& bs) {
+  cg_pfix_kernel<<<dim3(vec_grid(ndof, bs.B), bs.B), 256, 0, s>>>(ndof, dinv, r, pin, pout, st, bs);
   SSO_POST_LAUNCH("cg_pfix_kernel");
 }
 

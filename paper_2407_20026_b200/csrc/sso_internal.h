@@ -162,16 +162,25 @@ void launch_cg_update(cudaStream_t s, int ndof, const double* dinv, double* x, d
 void launch_cg_pupdate(cudaStream_t s, int ndof, const double* dinv, const double* r,
                        double* p, CgState* st,
     const BatchStrides& bs = BatchStrides());
-// Fused x / r update + p update (single design, single part, point Jacobi): one
+// Fused x / r update + p update (one part, point Jacobi, B <= cg_fused_grid()): one
 // kernel with a grid-wide barrier between the r^T z reduction and p_next = z + beta p
 // (ping-pong p buffers, so a residual replacement can re-form p from the previous one).
 void launch_cg_update_fused(cudaStream_t s, int ndof, const double* dinv, double* x, double* r,
-                            const double* p, const double* q, double* pn, double* partial, CgState* st);
+                            const double* p, const double* q, double* pn, double* partial, CgState* st,
+                            const BatchStrides& bs);
 // p_out = dinv r + beta p_in after a residual replacement (st->pfix), else nothing.
 void launch_cg_pfix(cudaStream_t s, int ndof, const double* dinv, const double* r, const double* pin,
-                    double* pout, const CgState* st);
+                    double* pout, const CgState* st, const BatchStrides& bs);
 // largest co-resident grid of the fused update kernel (0 = unavailable)
 int cg_fused_grid();
+// node-block Jacobi forms (block_jacobi.cu): the fused update and the p re-form
+// from z after a residual replacement
+void launch_cg_update_block_fused(cudaStream_t s, int n_nodes, const double* binv, double* x, double* r,
+                                  const double* p, const double* q, double* pn, double* partial, CgState* st,
+                                  const BatchStrides& bs);
+void launch_cg_pfix_z(cudaStream_t s, int ndof, const double* z, const double* pin, double* pout,
+                      const CgState* st, const BatchStrides& bs);
+int cg_block_fused_grid();
 // Symmetric (upper-block) storage SpMV: pass 1 streams the upper runs (TMA ring),
 // writes the upper row sums to y and the transpose contributions K_nm^T x_n to
 // tbuf; pass 2 adds each node's incoming slots (ascending source node) and, with
@@ -242,6 +251,8 @@ enum ReplMode { REPL_PERIODIC = 0, REPL_FINAL = 1 };
 constexpr double REPL_FACTOR = 1e-4;
 constexpr int MAX_RESTARTS = 2;
 constexpr double REPL_DRIFT = 10.0;
+constexpr double REPL_CONT = 2.0;   // periodic replacement continues CG (beta from the replaced
+                                    // r) while |f - K x| <= REPL_CONT |r|, else restarts (beta = 0)
 void launch_cg_true_res(cudaStream_t s, int ndof, const double* fbc, const double* Kx, double* partial,
                         CgState* st, const BatchStrides& bs = BatchStrides());
 void launch_cg_check(cudaStream_t s, CgState* st, int mode, int B);

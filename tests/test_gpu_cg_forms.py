@@ -2,6 +2,8 @@
 
   * the fused x / r / p update (cg_update_fused_kernel, ping-pong p buffers, one grid
     barrier) against the classic update + p-update kernels (SSO_CG_FUSED=0);
+  * the same for the node-block Jacobi preconditioner (precond = 1,
+    cg_update_block_fused_kernel / cg_pfix_z_kernel);
   * the reliable-update modes 0 (recurrence only), 1 (final true-residual check and
     restart, the default) and 2 (also periodic residual replacement, which re-forms p
     from the previous p buffer in the fused form: cg_pfix_kernel).
@@ -41,13 +43,14 @@ def _model(sso, P, fused, **kw):
             os.environ["SSO_CG_FUSED"] = old
 
 
+@pytest.mark.parametrize("precond", [0, 1])
 @pytest.mark.parametrize("storage", [1, 3])
 @pytest.mark.parametrize("reliable", [0, 1, 2])
 @pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("make", [W.config1, W.config2])
-def test_cg_forms_against_oracle(sso, make, fused, reliable, storage):
+def test_cg_forms_against_oracle(sso, make, fused, reliable, storage, precond):
     P = make()
-    m = _model(sso, P, fused, rtol=1e-12, reliable=reliable, storage=storage, check_every=8)
+    m = _model(sso, P, fused, rtol=1e-12, reliable=reliable, storage=storage, precond=precond, check_every=8)
     m.assemble()
     u, info = m.solve(P["f"])
     assert info["status"] == 0
@@ -55,14 +58,15 @@ def test_cg_forms_against_oracle(sso, make, fused, reliable, storage):
     assert np.linalg.norm(u - uref) <= 1e-9 * np.linalg.norm(uref)
 
 
+@pytest.mark.parametrize("precond", [0, 1])
 @pytest.mark.parametrize("reliable", [1, 2])
-def test_fused_matches_classic_midsize(sso, reliable):
+def test_fused_matches_classic_midsize(sso, reliable, precond):
     """80 x 80 shell (39 366 DOF, hundreds of iterations over many chunks, periodic
     replacements with reliable = 2): fused and classic forms reach the same solution."""
     P = W.shell_config3(80, cfg=3)
     out = {}
     for fused in (False, True):
-        m = _model(sso, P, fused, rtol=1e-11, reliable=reliable)
+        m = _model(sso, P, fused, rtol=1e-11, reliable=reliable, precond=precond)
         m.assemble()
         u, info = m.solve(P["f"])
         assert info["status"] == 0 and info["true_rel_res"] < 1e-10
@@ -70,3 +74,28 @@ def test_fused_matches_classic_midsize(sso, reliable):
     (u0, i0), (u1, i1) = out[False], out[True]
     assert np.linalg.norm(u1 - u0) <= 1e-9 * np.linalg.norm(u0)
     assert abs(i1 - i0) <= max(3, i0 // 100)
+
+
+@pytest.mark.parametrize("precond", [0, 1])
+@pytest.mark.parametrize("reliable", [1, 2])
+def test_fused_batched_designs(sso, reliable, precond):
+    """A batch of designs (one CTA set, reduction and grid barrier per design) in the
+    fused form equals the classic form design by design."""
+    B = 6
+    designs = [W.config5_design(b, n=12) for b in range(B)]
+    Z = np.stack([d["z"] for d in designs])
+    T = np.stack([d["t"] for d in designs])
+    F = np.stack([d["f"] for d in designs])
+    out = {}
+    for fused in (False, True):
+        m = _model(sso, designs[0], fused, rtol=1e-12, batch=B, reliable=reliable, precond=precond,
+                   check_every=8)
+        m.set_design(z=Z, t=T)
+        m.assemble()
+        U, infos = m.solve(F)
+        assert all(i["status"] == 0 for i in infos)
+        out[fused] = U
+    for b in range(B):
+        assert np.linalg.norm(out[True][b] - out[False][b]) <= 1e-9 * np.linalg.norm(out[False][b])
+    uref, _, _ = OG.evaluate(designs[2])
+    assert np.linalg.norm(out[True][2] - uref) <= 1e-9 * np.linalg.norm(uref)

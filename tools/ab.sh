@@ -4,7 +4,7 @@
 CMD=$1; R=$2; shift 2
 i=0
 for L in "$@"; do
-  d=/tmp/ab$i; rm -rf $d && mkdir -p $d && cp -r paper_2407_20026_b200 workloads tools $d/
+  d=/tmp/ab$i; rm -rf $d && mkdir -p $d && cp -r paper_2407_20026_b200 workloads tools oracle bench.py __graft_entry__.py profiles $d/
   cp $L $d/paper_2407_20026_b200/libsso.so; i=$((i+1))
 done
 for r in $(seq $R); do
