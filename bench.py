@@ -393,7 +393,10 @@ def run_gpu(args):
         cpu = cpu_baseline_obj(P, cg_iters) if (world == 1 and not args.no_cpu) else None
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-               "scaling": "weak" if replicas else "strong", "vs_baseline": None, "dtype": "f64",
+               # the default series (N = 1, 2, 4, ...: one design per GPU) is weak scaling; the
+               # strip modes split one C3b (strong)
+               "scaling": "strong" if (args.strips or args.virtual_parts > 1) else "weak",
+               "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (workloads.config3b, seeded)",
                "config": {"workload": "C3b: 408x408 MITC-4 shell quads, 1 003 686 DOF (reading c15)",
                           "n_nodes": n_nodes, "n_quads": nq, "ndof": ndof, "nnz": nnz,
