@@ -129,7 +129,7 @@ struct Part {
   // partition maps
   int32_t* block_rank = nullptr;      // quads [n_quads][16] (fused assembly; upper ranks when sym)
   bool sym = false;                   // upper-block (symmetric) storage, single-strip handles
-  bool pull = false;                  // sym with the one-pass pull SpMV (storage 3, column-major runs)
+  bool pull = false;                  // sym with the one-pass pull SpMV (storage 3, 2x2 sub-block records)
   int32_t* lpull = nullptr;           // pull: (source node, upper block) per incoming block
   int32_t* pdesc = nullptr;           // pull: 16-int per-node descriptors (build_pull_desc)
   double* binv = nullptr;             // precond 1: [B][21][n_own] packed (K_nn)^-1
@@ -1989,9 +1989,9 @@ int sso_export_csr(sso_handle h, int64_t* row_ptr, int32_t* col_idx, double* val
       const int32_t m = T.node_col[b0 + k];
       const UpperPattern& U = P.up;
       // run position of (row a, column 6 ku + b): row-major (storage 2) or column-major (3)
-      // (storage 2) row-major runs; (storage 3) PULL_BLOCK records, column-major values
+      // (storage 2) row-major runs; (storage 3) PULL_BLOCK records (rec_off)
       auto at = [&](int64_t u0, int64_t ud, int64_t ku, int ra, int cb) {
-        return P.pull ? PULL_BLOCK * (u0 + ku) + 6 * cb + ra : 36 * u0 + 6 * ra * ud + 6 * ku + cb;
+        return P.pull ? PULL_BLOCK * (u0 + ku) + rec_off(ra, cb) : 36 * u0 + 6 * ra * ud + 6 * ku + cb;
       };
       if (m >= n) {
         const int64_t ud = U.uptr[n + 1] - U.uptr[n];

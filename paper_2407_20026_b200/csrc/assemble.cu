@@ -42,14 +42,14 @@ __global__ void __launch_bounds__(256) assemble_kernel(
     const int rowlen = 6 * deg;
     const int total = 36 * deg;
     const uint8_t mrow = fixed_mask[n];
-    // run layout: row-major (a, rem) runs, or (cm) one PULL_BLOCK record per block, column-major
+    // run layout: row-major (a, rem) runs, or (cm) one PULL_BLOCK record per block (rec_off)
     double* out = vals + (cm ? PULL_BLOCK : 36) * b0;
     for (int v = lane; v < total; v += 32) {
       const int a = cm ? v % 6 : v / rowlen;
       const int rem = cm ? v / 6 : v - a * rowlen;
       const int k = rem / 6;
       const int b = rem - 6 * k;
-      const int dst = cm ? PULL_BLOCK * k + 6 * b + a : v;
+      const int dst = cm ? PULL_BLOCK * k + rec_off(a, b) : v;
       const int64_t blk = b0 + k;
       const int m = node_col[blk];
       double s = 0.0;

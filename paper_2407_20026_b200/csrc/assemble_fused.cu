@@ -321,14 +321,14 @@ __global__ void __launch_bounds__(128, 4) quad_assemble_fused_kernel(
   if (node_ok) {
     const uint8_t mrow = fixed_mask[n];
     // run layout: row-major (a, rem) runs of 36 deg values, or (cm) one PULL_BLOCK record per
-    // block with the values column-major; v walks the values in storage order
+    // block (2x2 sub-blocks, rec_off); v walks the values block by block
     double* out = vals + (cm ? PULL_BLOCK : 36) * b0;
     for (int v = t16; v < 36 * deg; v += 16) {
       const int a = cm ? v % 6 : v / rowlen;
       const int rem = cm ? v / 6 : v - a * rowlen;
       const int kb = rem / 6;
       const int b = rem - 6 * kb;
-      const int dst = cm ? PULL_BLOCK * kb + 6 * b + a : v;
+      const int dst = cm ? PULL_BLOCK * kb + rec_off(a, b) : v;
       const int m = node_col[b0 + kb];
       double s = nbuf[a * rowlen + rem];
       const bool diag = (m == n) && (a == b);

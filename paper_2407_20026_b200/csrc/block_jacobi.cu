@@ -100,7 +100,7 @@ __device__ __forceinline__ bool grid_sum(double (&v)[NV], double* partial, unsig
 
 // (K_nn)^-1 of every owned node from the assembled values.  Run layout: 0 full storage
 // (row-major runs, diagonal block at its rank in the node's column list), 2 upper blocks
-// row-major (diagonal block first), 3 upper-block records (PULL_BLOCK, column-major; diagonal first).
+// row-major (diagonal block first), 3 upper-block records (PULL_BLOCK, rec_off; diagonal first).
 __global__ void __launch_bounds__(128) block_inverse_kernel(int n_nodes, const int64_t* __restrict__ node_ptr,
                                                             const int32_t* __restrict__ node_col,
                                                             const double* __restrict__ vals, int layout,
@@ -128,15 +128,14 @@ __global__ void __launch_bounds__(128) block_inverse_kernel(int n_nodes, const i
     cs = 1;
   } else {
     off = PULL_BLOCK * b0;
-    rs = 1;
-    cs = 6;
+    rs = cs = 0;  // record layout (rec_off)
   }
   // Cholesky K_nn = L L^T (lower, in place), then (K_nn)^-1 = L^-T L^-1
   double L[6][6];
 #pragma unroll
   for (int a = 0; a < 6; ++a)
 #pragma unroll
-    for (int b = 0; b < 6; ++b) L[a][b] = vals[off + a * rs + b * cs];
+    for (int b = 0; b < 6; ++b) L[a][b] = vals[off + (layout == 3 ? rec_off(a, b) : a * rs + b * cs)];
   bool ok = true;
 #pragma unroll
   for (int j = 0; j < 6; ++j) {

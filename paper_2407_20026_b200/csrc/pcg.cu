@@ -652,11 +652,13 @@ __global__ void __launch_bounds__(SPMV_WARPS * 32, MINB) spmv_tma_kernel(
 
 // ---------------------------------------------------------------------------
 // Symmetric "pull" SpMV (storage 3).  Only the upper node blocks (n, m >= n) are
-// stored.  Each block is one contiguous record of PULL_BLOCK = 38 doubles: the 6x6
-// values COLUMN-major (K[a][b] at 6b + a) followed by 2 zero pad doubles.  The pad
-// makes the record stride 19 16-byte words (odd), which spreads the 16-byte
-// shared-memory reads of the consumers over all bank groups (an 18-word stride
-// keeps them on even groups: 2-way conflicts).  A node's upper run is its records
+// stored.  Each block is one contiguous record of PULL_BLOCK = 38 doubles: nine 2x2
+// sub-blocks of 4 doubles (column-major inside; rec_off in sso_internal.h) followed by
+// 2 zero pad doubles.  The pad makes the record stride 19 16-byte words (odd), which
+// spreads the 16-byte shared-memory reads of the consumers over all bank groups (an
+// 18-word stride keeps them on even groups: 2-way conflicts).  The 2x2 sub-blocks let one
+// instruction sequence serve both uses of a block (K_mj x_j for its row node, K_nm^T x_n
+// for its column node) with no divergent branch.  A node's upper run is its records
 // for k = 0 .. udeg-1 (block k at PULL_BLOCK (uptr[n] + k)).  The row node m needs
 //   y_m = sum_{j >= m} K_mj x_j + sum_{n < m} K_nm^T x_n:
 // its own run (contiguous) and the records (n, m) of its lower neighbours n < m,
@@ -703,12 +705,13 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, i
 // them in ascending j.  Chunks holding a node that does not fit (udeg > 5 or
 // ldeg > 4) take a general path reading the values from global memory.
 // ---------------------------------------------------------------------------
-// Consumer lane -> compute unit u = 3 j + h (31 = idle).  Searched (tools/pull_lane_perm.py,
-// checked by tests/test_pull_layout.py) for the record
-// layout (19-word stride, own region after the 80-word pulled slots): every 16-byte shared
-// load of an interior node and the row-pair store hit 8 distinct bank groups per quarter
-// warp (4 wavefronts per instruction; the identity mapping needs 5.6), and the three lanes
-// of a block (same 48-byte x gather) share a quarter warp for all blocks but one.
+// Consumer lane -> compute unit u = 3 j + h (31 = idle).  Checked by tests/test_pull_layout.py
+// against the shared-memory bank model of tools/pull_lane_perm.py for the 2x2 sub-block
+// records (19-word record stride, own region after the 80-word pulled slots): 34/7 = 4.86
+// wavefronts per 16-byte load of an interior node (the identity needs 6.5), the optimum of
+// an annealing search over lane and sub-block slot permutations (tools/pull_perm_anneal.c),
+// and the three lanes of a block (same 48-byte x gather) share a quarter warp for all
+// blocks but one.
 __constant__ int8_t kPullUnitOfLane[32] = {17, 31, 16, 19, 15, 31, 18, 20, 11, 13, 9,  14, 7,  12, 10, 8,
                                            0,  6,  31, 5,  2,  4,  3,  1,  31, 24, 23, 21, 31, 26, 25, 22};
 
@@ -850,7 +853,7 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
         const int b_first = D[0];
         const double* blk[NPW];
         double2 xv[NPW][3];
-        bool act[NPW];
+        bool act[NPW], ownb[NPW];
 #pragma unroll
         for (int e = 0; e < NPW; ++e) {  // node i = warp + 8 e of the chunk: operands first
           const int i = warp + W * e;
@@ -859,13 +862,14 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
           const int udeg = fl & 255, nb = udeg + ((fl >> 8) & 255);
           act[e] = i < nc && jl < nb;
           blk[e] = own;
+          ownb[e] = jl < udeg;
           if (act[e]) {
             int xn;
             if (jl < udeg) {
-              blk[e] = own + PULL_BLOCK * (Di[0] - b_first + jl) + 2 * hl;
+              blk[e] = own + PULL_BLOCK * (Di[0] - b_first + jl);
               xn = Di[2 + jl];
             } else {
-              blk[e] = buf + S::PSLOT * i + PULL_BLOCK * (jl - udeg) + 12 * hl;
+              blk[e] = buf + S::PSLOT * i + PULL_BLOCK * (jl - udeg);
               xn = Di[2 + 2 * jl - udeg];
             }
             const double2* xp = reinterpret_cast<const double2*>(p + 6 * (int64_t)xn);
@@ -882,51 +886,40 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
           // nine entries in a fixed tree
           double t0 = 0.0, t1 = 0.0;
           if (act[e]) {
-            const int i = warp + W * e;
-            const int udeg = D[PULL_DESC * i + 1] & 255;
-            const double* r = blk[e];
-            const double2 x0 = xv[e][0], x1 = xv[e][1], x2 = xv[e][2];
-            // two partial chains per output (b even / b odd) halve the dependent FMA latency
-            double u0, u1;
-            if (jl < udeg) {  // own K_mj, column-major: pairs (K[2h][b], K[2h+1][b]) at 6b + 2h
-              const double2 v0 = *reinterpret_cast<const double2*>(r);
-              const double2 v1 = *reinterpret_cast<const double2*>(r + 6);
-              const double2 v2 = *reinterpret_cast<const double2*>(r + 12);
-              const double2 v3 = *reinterpret_cast<const double2*>(r + 18);
-              const double2 v4 = *reinterpret_cast<const double2*>(r + 24);
-              const double2 v5 = *reinterpret_cast<const double2*>(r + 30);
-              t0 = v0.x * x0.x;
-              t1 = v0.y * x0.x;
-              u0 = v1.x * x0.y;
-              u1 = v1.y * x0.y;
-              t0 = fma(v2.x, x1.x, t0);
-              t1 = fma(v2.y, x1.x, t1);
-              u0 = fma(v3.x, x1.y, u0);
-              u1 = fma(v3.y, x1.y, u1);
-              t0 = fma(v4.x, x2.x, t0);
-              t1 = fma(v4.y, x2.x, t1);
-              u0 = fma(v5.x, x2.y, u0);
-              u1 = fma(v5.y, x2.y, u1);
-            } else {  // pulled K_nm: columns 2h, 2h+1 (12 contiguous) against x_n
-              const double2 a01 = *reinterpret_cast<const double2*>(r);
-              const double2 a23 = *reinterpret_cast<const double2*>(r + 2);
-              const double2 a45 = *reinterpret_cast<const double2*>(r + 4);
-              const double2 b01 = *reinterpret_cast<const double2*>(r + 6);
-              const double2 b23 = *reinterpret_cast<const double2*>(r + 8);
-              const double2 b45 = *reinterpret_cast<const double2*>(r + 10);
-              t0 = a01.x * x0.x;
-              t1 = b01.x * x0.x;
-              u0 = a01.y * x0.y;
-              u1 = b01.y * x0.y;
-              t0 = fma(a23.x, x1.x, t0);
-              t1 = fma(b23.x, x1.x, t1);
-              u0 = fma(a23.y, x1.y, u0);
-              u1 = fma(b23.y, x1.y, u1);
-              t0 = fma(a45.x, x2.x, t0);
-              t1 = fma(b45.x, x2.x, t1);
-              u0 = fma(a45.y, x2.y, u0);
-              u1 = fma(b45.y, x2.y, u1);
+            // Branch-free over own and pulled units.  Sub-block k = (k00, k10 | k01, k11) of the
+            // unit's strip: own K_mj uses sub-blocks (h, sb) -- outputs 2h, 2h+1 = rows, x_j
+            // components 2 sb, 2 sb + 1 = columns; pulled K_nm^T uses (sb, h) -- outputs =
+            // columns of K, x_n components = rows.  Both are t0 += k00 X0 + m X1,
+            // t1 += n X0 + k11 X1 with (m, n) = (k01, k10) own, (k10, k01) pulled; even and odd
+            // components in separate chains (the summation order of the oracle-checked form).
+            const bool ow = ownb[e];
+            double2 P[3], Q[3];
+#pragma unroll
+            for (int sb = 0; sb < 3; ++sb) {
+              const double* sp = blk[e] + 4 * pull_sub_slot(ow ? 3 * sb + hl : 3 * hl + sb);
+              P[sb] = *reinterpret_cast<const double2*>(sp);
+              Q[sb] = *reinterpret_cast<const double2*>(sp + 2);
             }
+            double m[3], n[3];
+#pragma unroll
+            for (int sb = 0; sb < 3; ++sb) {
+              m[sb] = ow ? Q[sb].x : P[sb].y;
+              n[sb] = ow ? P[sb].y : Q[sb].x;
+            }
+            const double2 x0 = xv[e][0], x1 = xv[e][1], x2 = xv[e][2];
+            double u0, u1;
+            t0 = P[0].x * x0.x;
+            t1 = n[0] * x0.x;
+            u0 = m[0] * x0.y;
+            u1 = Q[0].y * x0.y;
+            t0 = fma(P[1].x, x1.x, t0);
+            t1 = fma(n[1], x1.x, t1);
+            u0 = fma(m[1], x1.y, u0);
+            u1 = fma(Q[1].y, x1.y, u1);
+            t0 = fma(P[2].x, x2.x, t0);
+            t1 = fma(n[2], x2.x, t1);
+            u0 = fma(m[2], x2.y, u0);
+            u1 = fma(Q[2].y, x2.y, u1);
             t0 += u0;
             t1 += u1;
           }
@@ -966,7 +959,7 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
             const double* bk = vals + PULL_BLOCK * ((int64_t)b0 + kb);
             double t = 0.0;
 #pragma unroll
-            for (int c = 0; c < 6; ++c) t = fma(bk[6 * c + a], p[6 * (int64_t)m + c], t);
+            for (int c = 0; c < 6; ++c) t = fma(bk[rec_off(a, c)], p[6 * (int64_t)m + c], t);
             y += t;
           }
           for (int jp = 0; jp < ldeg; ++jp) {
@@ -974,7 +967,7 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
             const double* bk = vals + PULL_BLOCK * (int64_t)e2.y;
             double t = 0.0;
 #pragma unroll
-            for (int c = 0; c < 6; ++c) t = fma(bk[6 * a + c], p[6 * (int64_t)e2.x + c], t);
+            for (int c = 0; c < 6; ++c) t = fma(bk[rec_off(c, a)], p[6 * (int64_t)e2.x + c], t);
             y += t;
           }
           const int64_t row = 6 * ((int64_t)first + i) + a;

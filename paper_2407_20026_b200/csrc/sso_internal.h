@@ -206,9 +206,19 @@ void launch_spmv_pull(cudaStream_t s, const CUtensorMap* tmap, int n_nodes, int 
                       const int32_t* pdesc, const int32_t* ucol, const int32_t* lpull, const double* vals,
                       const double* x, double* y, double* partial, CgState* st,
                       const BatchStrides& bs = BatchStrides());
-// Storage 3 stores each upper 6x6 block as a record of PULL_BLOCK doubles: column-major
-// values (K[a][b] at 6b + a) then 2 zero pads (an odd 16-byte-word stride, see pcg.cu).
+// Storage 3 stores each upper 6x6 block as a record of PULL_BLOCK doubles: the nine 2x2
+// sub-blocks (A, B) = K[2A..2A+1][2B..2B+1], 4 doubles each (column-major inside), sub-block
+// 3B + A in slot PULL_SUB_POS nibble, then 2 zero pads (an odd 16-byte-word stride, see
+// pcg.cu).  A 16-byte half of a sub-block is a (row pair, one column) of K -- a row-pair
+// product for the block's own row node and, with its neighbour half, a column-pair product of
+// K^T for its column node: the same loads and FMA chains serve both (branch-free consumers).
 constexpr int PULL_BLOCK = 38;
+constexpr unsigned long long PULL_SUB_POS = 0x876543210ull;
+__host__ __device__ constexpr int pull_sub_slot(int s) { return (int)((PULL_SUB_POS >> (4 * s)) & 15); }
+// offset of K[a][b] inside a record
+__host__ __device__ constexpr int rec_off(int a, int b) {
+  return 4 * pull_sub_slot(3 * (b >> 1) + (a >> 1)) + 2 * (b & 1) + (a & 1);
+}
 // 16-int per-node descriptors of the pull SpMV (see pcg.cu)
 void build_pull_desc(const UpperPattern& U, std::vector<int32_t>& desc);
 // TMA map of the [rows][36] fp64 view of the values (gather4 of pulled blocks); 0 on success

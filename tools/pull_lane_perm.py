@@ -4,9 +4,11 @@ kPullUnitOfLane).
 Model (sm_100a shared memory): a warp's 16-byte load is served in quarter-warp phases
 of 8 lanes; a phase costs as many wavefronts as the largest number of its lanes that
 hit the same 16-byte bank group (word index mod 8).  Consumer lane L computes unit
-u = 3 j + h (block j of the node's slot, row pair h); per instruction t = 0..5 it reads
-  own block j (< 5):    word OWN + 19 (b_i + j) + 3 t + h     (column-major pairs)
-  pulled block j (>= 5): word 80 i + 19 (j - 5) + 6 h + t     (columns 2h, 2h+1)
+u = 3 j + h (block j of the node's slot, output pair h).  A record holds the 6x6 block as
+nine 2x2 sub-blocks (A, B) of 4 doubles at 4 (3 B + A) (column-major inside); per
+instruction t = 0..5 (sub-block sb = t / 2, 16-byte half t % 2) the unit reads
+  own block j (< 5):    word OWN + 19 (b_i + j) + 6 sb + 2 h + t % 2   (sub-blocks (h, sb))
+  pulled block j (>= 5): word 80 i + 19 (j - 5) + 6 h + 2 sb + t % 2    (sub-blocks (sb, h))
 with the 38-double record stride (19 words), the 80-word pulled slot per node and the
 own region after the pulled slots (OWN = 80 C), i = node index in the chunk, b_i = 5 i
 (interior nodes).  The row-pair store red[27 e + u] is modelled too.  A second term
@@ -25,9 +27,10 @@ C = 12  # nodes per chunk (default variant)
 
 
 def words(j, h, t, i, bi):
-    if j < 5:
-        return 80 * C + 19 * (bi + j) + 3 * t + h
-    return 80 * i + 19 * (j - 5) + 6 * h + t
+    sb, half = t // 2, t % 2  # 2x2 sub-block index along the unit's strip, which 16-byte half
+    if j < 5:   # own K_mj: sub-blocks (h, sb) at 4 (3 sb + h) doubles
+        return 80 * C + 19 * (bi + j) + 6 * sb + 2 * h + half
+    return 80 * i + 19 * (j - 5) + 6 * h + 2 * sb + half  # pulled: sub-blocks (sb, h)
 
 
 def phases(ws):
@@ -92,3 +95,4 @@ if __name__ == "__main__":
         p = table_from_source()
         print("identity:", wavefronts(list(range(27)) + [None] * 5))
         print("table:   ", wavefronts(p), "wavefronts per instruction,", split_blocks(p), "split block(s)")
+
