@@ -878,6 +878,13 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
             xv[e][2] = xp[2];
           }
         }
+        // p of this lane's output row (p^T q), loaded with the x gathers
+        double prow = 0.0;
+        if (DOT && lane < 6 * NPW) {
+          const int e = lane / 6, a = lane - 6 * e;
+          const int i = warp + W * e;
+          if (i < nc) prow = p[6 * ((int64_t)first + i) + a];
+        }
         mbar_wait(&full_bar[b], (unsigned)((k / NB) & 1));  // x gathers overlap the chunk's data
 #pragma unroll
         for (int e = 0; e < NPW; ++e) {
@@ -938,7 +945,7 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
             const double y = (((r9[0] + r9[1]) + (r9[2] + r9[3])) + ((r9[4] + r9[5]) + (r9[6] + r9[7]))) + r9[8];
             const int64_t row = 6 * ((int64_t)first + i) + a;
             q[row] = y;
-            if (DOT) pq[0] += p[row] * y;
+            if (DOT) pq[0] += prow * y;
           }
         }
       } else if (lane < 6 * NPW) {
