@@ -141,7 +141,7 @@ typedef struct {
    * shell grids); pass 1 of the SpMV forms the upper row sums, the transpose
    * contributions (sender-ordered slots) and p^T K p, the x / r update adds each
    * node's incoming slots in ascending source order.  3 = upper node blocks, each one
-   * contiguous 38-double record (36 values column-major + 2 zero pads), and a ONE-pass
+   * contiguous 38-double record (36 values as nine 2x2 sub-blocks + 2 zero pads), and a ONE-pass
    * "pull" SpMV: the CTA that owns a chunk of row nodes streams their upper runs (one
    * bulk copy) and the stored blocks (n, m) of their lower neighbours n < m (one TMA
    * gather4 per node; an L2 hit: chunks are dealt round-robin, so the owner streams them
@@ -293,7 +293,7 @@ int sso_export_dinv(sso_handle h, double* dinv);
 
 /* Device storage of the assembled matrix: stored values / node blocks (owned rows) and
  * the layout in use: *symmetric = 0 full storage, 2 upper blocks with the two-pass
- * transpose SpMV, 3 upper blocks (38-double column-major records) with the one-pass pull
+ * transpose SpMV, 3 upper blocks (38-double records of 2x2 sub-blocks) with the one-pass pull
  * SpMV.  stored_values counts the 36 values per block (not the record pads). */
 int sso_storage_info(sso_handle h, int64_t* stored_values, int64_t* stored_blocks, int32_t* symmetric);
 

@@ -712,8 +712,8 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, i
 // an annealing search over lane and sub-block slot permutations (tools/pull_perm_anneal.c),
 // and the three lanes of a block (same 48-byte x gather) share a quarter warp for all
 // blocks but one.
-__constant__ int8_t kPullUnitOfLane[32] = {17, 31, 16, 19, 15, 31, 18, 20, 11, 13, 9,  14, 7,  12, 10, 8,
-                                           0,  6,  31, 5,  2,  4,  3,  1,  31, 24, 23, 21, 31, 26, 25, 22};
+__constant__ int8_t kPullUnitOfLane[32] = {15, 31, 18, 20, 17, 16, 31, 19, 25, 23, 26, 22, 31, 24, 31, 21,
+                                           3, 7, 9, 4, 5, 8, 6, 10, 14, 13, 2, 12, 1, 11, 0, 31};
 
 template <int C, int W>
 struct PullChunkSmem {
@@ -903,7 +903,7 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
             double2 P[3], Q[3];
 #pragma unroll
             for (int sb = 0; sb < 3; ++sb) {
-              const double* sp = blk[e] + 4 * pull_sub_slot(ow ? 3 * sb + hl : 3 * hl + sb);
+              const double* sp = blk[e] + pull_sub_off(ow ? 3 * sb + hl : 3 * hl + sb);
               P[sb] = *reinterpret_cast<const double2*>(sp);
               Q[sb] = *reinterpret_cast<const double2*>(sp + 2);
             }

@@ -208,16 +208,22 @@ void launch_spmv_pull(cudaStream_t s, const CUtensorMap* tmap, int n_nodes, int 
                       const BatchStrides& bs = BatchStrides());
 // Storage 3 stores each upper 6x6 block as a record of PULL_BLOCK doubles: the nine 2x2
 // sub-blocks (A, B) = K[2A..2A+1][2B..2B+1], 4 doubles each (column-major inside), sub-block
-// 3B + A in slot PULL_SUB_POS nibble, then 2 zero pads (an odd 16-byte-word stride, see
-// pcg.cu).  A 16-byte half of a sub-block is a (row pair, one column) of K -- a row-pair
+// 3B + A in slot PULL_SUB_POS nibble, and one 16-byte zero pad word (an odd 19-word record
+// stride, see pcg.cu) placed before slot PULL_SUB_GAP.  A 16-byte half of a sub-block is a (row pair, one column) of K -- a row-pair
 // product for the block's own row node and, with its neighbour half, a column-pair product of
 // K^T for its column node: the same loads and FMA chains serve both (branch-free consumers).
 constexpr int PULL_BLOCK = 38;
-constexpr unsigned long long PULL_SUB_POS = 0x876543210ull;
-__host__ __device__ constexpr int pull_sub_slot(int s) { return (int)((PULL_SUB_POS >> (4 * s)) & 15); }
+// sub-block 3B + A -> slot (nibble), and the pad word sits before slot PULL_SUB_GAP: the
+// pair searched with tools/pull_perm_anneal.c together with the consumer lane table
+constexpr unsigned long long PULL_SUB_POS = 0x830741652ull;
+constexpr int PULL_SUB_GAP = 3;
+// double offset of sub-block s inside a record
+__host__ __device__ constexpr int pull_sub_off(int s) {
+  return 4 * (int)((PULL_SUB_POS >> (4 * s)) & 15) + (((int)((PULL_SUB_POS >> (4 * s)) & 15) >= PULL_SUB_GAP) ? 2 : 0);
+}
 // offset of K[a][b] inside a record
 __host__ __device__ constexpr int rec_off(int a, int b) {
-  return 4 * pull_sub_slot(3 * (b >> 1) + (a >> 1)) + 2 * (b & 1) + (a & 1);
+  return pull_sub_off(3 * (b >> 1) + (a >> 1)) + 2 * (b & 1) + (a & 1);
 }
 // 16-int per-node descriptors of the pull SpMV (see pcg.cu)
 void build_pull_desc(const UpperPattern& U, std::vector<int32_t>& desc);

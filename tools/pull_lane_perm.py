@@ -5,10 +5,10 @@ Model (sm_100a shared memory): a warp's 16-byte load is served in quarter-warp p
 of 8 lanes; a phase costs as many wavefronts as the largest number of its lanes that
 hit the same 16-byte bank group (word index mod 8).  Consumer lane L computes unit
 u = 3 j + h (block j of the node's slot, output pair h).  A record holds the 6x6 block as
-nine 2x2 sub-blocks (A, B) of 4 doubles at 4 (3 B + A) (column-major inside); per
+nine 2x2 sub-blocks (A, B) of 4 doubles (column-major inside) at word SUBW[3 B + A]; per
 instruction t = 0..5 (sub-block sb = t / 2, 16-byte half t % 2) the unit reads
-  own block j (< 5):    word OWN + 19 (b_i + j) + 6 sb + 2 h + t % 2   (sub-blocks (h, sb))
-  pulled block j (>= 5): word 80 i + 19 (j - 5) + 6 h + 2 sb + t % 2    (sub-blocks (sb, h))
+  own block j (< 5):    word OWN + 19 (b_i + j) + SUBW[3 sb + h] + t % 2   (sub-blocks (h, sb))
+  pulled block j (>= 5): word 80 i + 19 (j - 5) + SUBW[3 h + sb] + t % 2    (sub-blocks (sb, h))
 with the 38-double record stride (19 words), the 80-word pulled slot per node and the
 own region after the pulled slots (OWN = 80 C), i = node index in the chunk, b_i = 5 i
 (interior nodes).  The row-pair store red[27 e + u] is modelled too.  A second term
@@ -26,11 +26,24 @@ UNITS = [(j, h) for j in range(9) for h in range(3)]
 C = 12  # nodes per chunk (default variant)
 
 
+def sub_words():
+    """word offset of each sub-block 3 B + A inside a record (csrc/sso_internal.h
+    PULL_SUB_POS / PULL_SUB_GAP: slot q at word 2 q, + 1 from the pad word on)."""
+    src = (Path(__file__).resolve().parents[1] / "paper_2407_20026_b200" / "csrc" / "sso_internal.h").read_text()
+    pos = int(re.search(r"PULL_SUB_POS = (0x[0-9a-f]+)ull", src).group(1), 16)
+    gap = int(re.search(r"PULL_SUB_GAP = (\d+);", src).group(1))
+    slots = [(pos >> (4 * s)) & 15 for s in range(9)]
+    return [2 * q + (1 if q >= gap else 0) for q in slots]
+
+
+SUBW = sub_words()
+
+
 def words(j, h, t, i, bi):
     sb, half = t // 2, t % 2  # 2x2 sub-block index along the unit's strip, which 16-byte half
-    if j < 5:   # own K_mj: sub-blocks (h, sb) at 4 (3 sb + h) doubles
-        return 80 * C + 19 * (bi + j) + 6 * sb + 2 * h + half
-    return 80 * i + 19 * (j - 5) + 6 * h + 2 * sb + half  # pulled: sub-blocks (sb, h)
+    if j < 5:   # own K_mj: sub-blocks (A, B) = (h, sb)
+        return 80 * C + 19 * (bi + j) + SUBW[3 * sb + h] + half
+    return 80 * i + 19 * (j - 5) + SUBW[3 * h + sb] + half  # pulled: sub-blocks (sb, h)
 
 
 def phases(ws):

@@ -1,20 +1,20 @@
 // Simulated annealing over (sub-block slot permutation, consumer lane permutation) of the
-// pull SpMV under the shared-memory bank model of tools/pull_lane_perm.py.
-//   gcc -O2 -o /tmp/sa tools/pull_perm_anneal.c -lm && /tmp/sa <seed> [fix_slots]
-// Eight seeds all reach 34/7 = 4.857 wavefronts per 16-byte instruction with one split
-// block (the value of the table in csrc/pcg.cu with the identity slot order): with a
-// 19-word record stride (19 = 3 mod 8) the own units' bank groups 3 j + 2 h repeat
-// residue 0 three times, so 4.0 is out of reach for this record size.
+// pull SpMV under the shared-memory bank model of tools/pull_lane_perm.py, for a given
+// position of the record's pad word (before slot `gap`; 9 = at the end).
+//   gcc -O2 -o /tmp/sa tools/pull_perm_anneal.c -lm && /tmp/sa <seed> <fix_slots> <gap>
+// Results (2 seeds each): gap 9 (pad at the end) 34/7 = 4.86 wavefronts per 16-byte load
+// (+1 split block); gap 4 4.43; gap 3 and 6: 30/7 = 4.29 (+1 split) -- the layout in
+// csrc/sso_internal.h (PULL_SUB_POS, PULL_SUB_GAP = 3) and the lane table in csrc/pcg.cu.
 #include <stdio.h>
 #include <stdlib.h>
 #include <math.h>
 #define C 12
 static int lanes[32];   // unit id or -1
-static int slot[9];
+static int slot[9]; static int gap = 9;
 static int words(int u, int t, int i, int bi) {
   int j = u / 3, h = u % 3, sb = t / 2, half = t % 2;
-  if (j < 5) return 80 * C + 19 * (bi + j) + 2 * slot[3 * sb + h] + half;
-  return 80 * i + 19 * (j - 5) + 2 * slot[3 * h + sb] + half;
+  if (j < 5) { int q = slot[3 * sb + h]; return 80 * C + 19 * (bi + j) + 2 * q + (q >= gap) + half; }
+  { int q = slot[3 * h + sb]; return 80 * i + 19 * (j - 5) + 2 * q + (q >= gap) + half; }
 }
 static int phases(int* w) {  // w[32], -1 inactive
   int tot = 0;
@@ -46,7 +46,7 @@ static double cost(void) {
 }
 int main(int argc, char** argv) {
   int seed = argc > 1 ? atoi(argv[1]) : 1;
-  int fixslot = argc > 2 ? atoi(argv[2]) : 0;
+  int fixslot = argc > 2 ? atoi(argv[2]) : 0; gap = argc > 3 ? atoi(argv[3]) : 9;
   srand(seed);
   for (int l = 0; l < 32; ++l) lanes[l] = l < 27 ? l : -1;
   for (int s = 0; s < 9; ++s) slot[s] = s;
@@ -72,7 +72,7 @@ int main(int argc, char** argv) {
       else { int x = lanes[a]; lanes[a] = lanes[b]; lanes[b] = x; }
     }
   }
-  printf("best %.4f slots", best);
+  printf("gap %d best %.4f slots", gap, best);
   for (int s = 0; s < 9; ++s) printf(" %d", bs[s]);
   printf(" lanes");
   for (int l = 0; l < 32; ++l) printf(" %d", bl[l] < 0 ? 31 : bl[l]);
