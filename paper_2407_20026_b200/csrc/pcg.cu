@@ -841,6 +841,13 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
     double2* red = reinterpret_cast<double2*>(red_base) + (size_t)warp * 27 * NPW;
     const int ul = kPullUnitOfLane[lane];
     const int jl = ul < 27 ? ul / 3 : 9, hl = ul < 27 ? ul - 3 * (ul / 3) : 0;
+    // this lane's sub-block offsets inside a record: own units (h, sb), pulled units (sb, h)
+    int offO[3], offP[3];
+#pragma unroll
+    for (int sb = 0; sb < 3; ++sb) {
+      offO[sb] = pull_sub_off(3 * sb + hl);
+      offP[sb] = pull_sub_off(3 * hl + sb);
+    }
     for (int k = 0; k < cnt; ++k) {
       const int b = k % NB;
       const double* buf = sbase + (size_t)b * S::BUF;
@@ -903,7 +910,7 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
             double2 P[3], Q[3];
 #pragma unroll
             for (int sb = 0; sb < 3; ++sb) {
-              const double* sp = blk[e] + pull_sub_off(ow ? 3 * sb + hl : 3 * hl + sb);
+              const double* sp = blk[e] + (ow ? offO[sb] : offP[sb]);
               P[sb] = *reinterpret_cast<const double2*>(sp);
               Q[sb] = *reinterpret_cast<const double2*>(sp + 2);
             }
