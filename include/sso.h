@@ -227,6 +227,18 @@ int sso_grad_adjoint(sso_handle h, const double* lambda, double* dg_dxyz, double
  * handles.  Errors: SSO_E_STATE (no solve yet). */
 int sso_grad_E(sso_handle h, sso_objective obj, double* dC_dE);
 
+/* SIMP density design variable (Eq. 12:
+ * E_j = p_T,j^P E_*,j).  rho, E0 [n_beams + n_quads] (beams first, shared by a batch;
+ * pointer kind per mem): the element moduli become E_e = rho_e^P E0_e on the device, and
+ * G_e = rho_e^P G0_e when G0 [n_beams + n_quads] is given, else E_e / (2 (1 + nu_e)).
+ * sso_grad_density then returns dC_drho [batch][n_beams + n_quads] =
+ * dC/dE_e * P rho_e^(P-1) E0_e at the last solve (the chain rule of Eq. 12 applied on the
+ * device to sso_grad_E's dC/dE).  Invalidates the assembly; sso_set_material ends the
+ * density mode.  Single-strip handles.  Errors: SSO_E_INVALID (rho outside (0, 1],
+ * P < 1, E0 / G0 <= 0 or non-finite), SSO_E_STATE (grad without a density or a solve). */
+int sso_set_density(sso_handle h, const double* rho, double penal, const double* E0, const double* G0);
+int sso_grad_density(sso_handle h, sso_objective obj, double* dC_drho);
+
 /* Replace the element moduli E [n_beams + n_quads] (shared by a batch; pointer kind per
  * mem); G follows (derived G recomputed, given G scaled).  Invalidates the assembly.
  * Single-strip handles.  Errors: SSO_E_INVALID (E <= 0). */

@@ -91,6 +91,8 @@ _sig = {
     "sso_adjoint_solve": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.POINTER(sso_solve_info)]),
     "sso_grad_adjoint": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sso_set_material": (C.c_int, [_H, C.c_void_p]),
+    "sso_set_density": (C.c_int, [_H, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]),
+    "sso_grad_density": (C.c_int, [_H, C.c_int, C.c_void_p]),
     "sso_set_prescribed": (C.c_int, [_H, C.c_void_p]),
     "sso_set_area_load": (C.c_int, [_H, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sso_hat_filter": (C.c_int, [_H, C.c_int32, C.c_double, C.c_int32, C.c_void_p, C.c_void_p]),
@@ -342,6 +344,25 @@ class Model:
         self._check(_lib.sso_grad_adjoint(self.h, lam.ctypes.data, dX.ctypes.data, dT.ctypes.data,
                                           dE.ctypes.data))
         return dX.reshape(3, self.n_nodes), dT[: self.n_quads], dE
+
+    def set_density(self, rho, penal, E0, G0=None):
+        """SIMP densities (Eq. 12): E = rho^P E0 (G = rho^P G0, or derived from nu),
+        per element, beams first.  Requires a new assemble()."""
+        dev = self._mode(rho)
+        if not dev:
+            rho, E0 = _np(rho, np.float64), _np(E0, np.float64)
+            G0 = None if G0 is None else _np(G0, np.float64)
+        self._check(_lib.sso_set_density(self.h, _ptr(rho, np.float64), float(penal), _ptr(E0, np.float64),
+                                         None if G0 is None else _ptr(G0, np.float64)))
+
+    def grad_density(self, objective=OBJ_COMPLIANCE):
+        """dC/drho per element (beams first, then quads) after set_density, [batch, n_elems]
+        or [n_elems]."""
+        ne = self.n_beams + self.g_quads
+        out = np.zeros(self.batch * ne)
+        self._mode()
+        self._check(_lib.sso_grad_density(self.h, objective, out.ctypes.data))
+        return out.reshape(self.batch, ne) if self.batch > 1 else out
 
     def set_material(self, E):
         dev = self._mode(E)

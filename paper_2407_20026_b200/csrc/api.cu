@@ -117,6 +117,8 @@ struct Part {
   // general-objective adjoint (sso_adjoint_solve / sso_grad_adjoint): primal backups,
   // lambda and the second polarization pass (allocated on first use)
   double *ub = nullptr, *fb = nullptr, *lam = nullptr, *dxyz2 = nullptr, *dt2 = nullptr, *dE2 = nullptr;
+  // SIMP density (sso_set_density): rho, reference moduli E0 and (optional) G0 per element
+  double *rho = nullptr, *E0 = nullptr, *G0 = nullptr;
   // design-dependent area loads (sso_set_area_load): local per-quad q, w and the
   // per-quad lumped value a = (q + w t) A / 4 [B][n_quads]
   double *ld_q = nullptr, *ld_w = nullptr, *ld_a = nullptr;
@@ -164,6 +166,9 @@ struct sso_ctx {
   double drill_alpha = 1e-3;
   int warm_start = 0;
   int check_every = 64;
+  bool simp = false;        // sso_set_density active (E = rho^P E0)
+  bool simp_chain = false;  // sso_grad_density in progress: dC/dE -> dC/drho before the copy-out
+  double penal = 1.0;
   int batch = 1;  // designs per handle
   int reliable = 1;  // 0 plain CG, 1 final true-residual restart, 2 + periodic replacement
   int assembly = 0;  // 0 auto (fused when the mesh allows), 1 staged
@@ -597,7 +602,8 @@ void free_part(Part& P) {
                   P.gf, P.partial, P.st, P.flags, P.tickets, P.scal, P.slot_partial, P.dxyz, P.dt,
                   P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
                   P.lptr, P.lslot, P.lpull, P.pdesc, P.binv, P.zb, P.p2, P.tbuf, P.dE,
-                  P.ub, P.fb, P.lam, P.dxyz2, P.dt2, P.dE2, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask};
+                  P.ub, P.fb, P.lam, P.dxyz2, P.dt2, P.dE2, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask,
+                  P.rho, P.E0, P.G0};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -1482,6 +1488,7 @@ static int grad_impl(sso_ctx* h, sso_objective obj, double* Part::*fv, int uvec,
   }
   if (dC_dE) {
     Part& P = h->P0();
+    if (h->simp_chain) launch_simp_chain(h->stream, P.n_beams + P.n_quads, h->batch, P.rho, h->penal, P.E0, P.dE);
     CK(h, cudaMemcpyAsync(dC_dE, P.dE, (size_t)h->batch * (P.n_beams + P.n_quads) * sizeof(double), kind_out(h),
                           h->stream));
   }
@@ -1670,7 +1677,10 @@ static int grad_prescribed(sso_ctx* h, sso_objective obj, double* C, double* dC_
     CK(h, cudaMemcpyAsync(dC_dxyz, P.dxyz, 3 * (size_t)P.n_nodes * sizeof(double), kind_out(h), h->stream));
   if (dC_dt && P.n_quads)
     CK(h, cudaMemcpyAsync(dC_dt, P.dt, (size_t)P.n_quads * sizeof(double), kind_out(h), h->stream));
-  if (dC_dE) CK(h, cudaMemcpyAsync(dC_dE, P.dE, (size_t)ne * sizeof(double), kind_out(h), h->stream));
+  if (dC_dE) {
+    if (h->simp_chain) launch_simp_chain(h->stream, (int)ne, 1, P.rho, h->penal, P.E0, P.dE);
+    CK(h, cudaMemcpyAsync(dC_dE, P.dE, (size_t)ne * sizeof(double), kind_out(h), h->stream));
+  }
   if ((r = sync(h))) return r;
   if (C) {
     const double v = s * h->h_scal[2];
@@ -1764,9 +1774,57 @@ int sso_set_area_load(sso_handle h, const double* q, const double* w, const doub
   return SSO_OK;
 }
 
+int sso_set_density(sso_handle h, const double* rho, double penal, const double* E0, const double* G0) {
+  if (!h || !rho || !E0) return SSO_E_INVALID;
+  if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_set_density is defined for single-strip handles");
+  if (!(penal >= 1.0) || !std::isfinite(penal)) FAIL(h, SSO_E_INVALID, "sso_set_density: penalty P must be >= 1");
+  Part& P = h->P0();
+  const int64_t ne = (int64_t)P.n_beams + P.n_quads;
+  if (ne == 0) FAIL(h, SSO_E_INVALID, "sso_set_density: no elements");
+  const cudaMemcpyKind kin = h->mem == SSO_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost;
+  std::vector<double> r((size_t)ne), e0((size_t)ne), g0(G0 ? (size_t)ne : 0);
+  CK(h, cudaMemcpy(r.data(), rho, ne * sizeof(double), kin));
+  CK(h, cudaMemcpy(e0.data(), E0, ne * sizeof(double), kin));
+  if (G0) CK(h, cudaMemcpy(g0.data(), G0, ne * sizeof(double), kin));
+  for (int64_t k = 0; k < ne; ++k) {
+    if (!(r[k] > 0.0 && r[k] <= 1.0) || !(e0[k] > 0.0) || !std::isfinite(e0[k]) ||
+        (G0 && (!(g0[k] > 0.0) || !std::isfinite(g0[k])))) {
+      char buf[112];
+      snprintf(buf, sizeof buf, "element %lld: rho outside (0, 1] or E0 / G0 <= 0 or non-finite", (long long)k);
+      FAIL(h, SSO_E_INVALID, buf);
+    }
+  }
+  int rc;
+  if (!P.rho && (rc = dalloc(h, &P.rho, ne))) return rc;
+  if (!P.E0 && (rc = dalloc(h, &P.E0, ne))) return rc;
+  if (G0 && !P.G0 && (rc = dalloc(h, &P.G0, ne))) return rc;
+  CK(h, cudaMemcpy(P.rho, r.data(), ne * sizeof(double), cudaMemcpyHostToDevice));
+  CK(h, cudaMemcpy(P.E0, e0.data(), ne * sizeof(double), cudaMemcpyHostToDevice));
+  if (G0) CK(h, cudaMemcpy(P.G0, g0.data(), ne * sizeof(double), cudaMemcpyHostToDevice));
+  launch_simp_material(h->stream, (int)ne, P.rho, penal, P.E0, G0 ? P.G0 : nullptr, P.nu, P.E, P.G);
+  CKL(h);
+  // later sso_set_material calls scale G from these moduli
+  std::fill(P.g_derived.begin(), P.g_derived.end(), G0 ? 0 : 1);
+  h->simp = true;
+  h->penal = penal;
+  h->assembled = false;
+  h->solved = false;
+  return sync(h);
+}
+
+int sso_grad_density(sso_handle h, sso_objective obj, double* dC_drho) {
+  if (!h || !dC_drho) return SSO_E_INVALID;
+  if (!h->simp) FAIL(h, SSO_E_STATE, "sso_grad_density without sso_set_density");
+  h->simp_chain = true;
+  const int rc = sso_grad_E(h, obj, dC_drho);
+  h->simp_chain = false;
+  return rc;
+}
+
 int sso_set_material(sso_handle h, const double* E) {
   if (!h || !E) return SSO_E_INVALID;
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_set_material is defined for single-strip handles");
+  h->simp = false;
   Part& P = h->P0();
   const int64_t ne = (int64_t)P.n_beams + P.n_quads;
   std::vector<double> e((size_t)ne), g((size_t)ne);

@@ -383,4 +383,42 @@ void launch_node_reduce(cudaStream_t s, int n_nodes, const int64_t* inc_ptr, con
   SSO_POST_LAUNCH("node_reduce_kernel");
 }
 
+// SIMP density design variable (Eq. 12):
+// E_e = rho_e^P E0_e; G_e = rho_e^P G0_e when given, else E_e / (2 (1 + nu_e)).
+__global__ void simp_material_kernel(int ne, const double* __restrict__ rho, double penal,
+                                     const double* __restrict__ E0, const double* __restrict__ G0,
+                                     const double* __restrict__ nu, double* __restrict__ E,
+                                     double* __restrict__ G) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
+    const double f = pow(rho[e], penal);
+    E[e] = f * E0[e];
+    G[e] = G0 ? f * G0[e] : E[e] / (2.0 * (1.0 + nu[e]));
+  }
+}
+
+// dC/drho_e = dC/dE_e * P rho_e^(P-1) E0_e (chain rule of Eq. 12), in place, every design
+__global__ void simp_chain_kernel(int ne, int B, const double* __restrict__ rho, double penal,
+                                  const double* __restrict__ E0, double* __restrict__ dE) {
+  const int64_t n = (int64_t)ne * B;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(k % ne);
+    dE[k] *= penal * pow(rho[e], penal - 1.0) * E0[e];
+  }
+}
+
+void launch_simp_material(cudaStream_t s, int ne, const double* rho, double penal, const double* E0,
+                          const double* G0, const double* nu, double* E, double* G) {
+  if (ne <= 0) return;
+  simp_material_kernel<<<(ne + 255) / 256, 256, 0, s>>>(ne, rho, penal, E0, G0, nu, E, G);
+  SSO_POST_LAUNCH("simp_material_kernel");
+}
+
+void launch_simp_chain(cudaStream_t s, int ne, int B, const double* rho, double penal, const double* E0,
+                       double* dE) {
+  if (ne <= 0) return;
+  const int64_t n = (int64_t)ne * B;
+  simp_chain_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(ne, B, rho, penal, E0, dE);
+  SSO_POST_LAUNCH("simp_chain_kernel");
+}
+
 }  // namespace sso

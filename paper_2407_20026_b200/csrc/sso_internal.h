@@ -305,6 +305,11 @@ void launch_area_load_grad(cudaStream_t s, int n_beams, int n_quads, const doubl
                            double* slot_partial, double* dt, const BatchStrides& bs);
 
 // Gradient kernels
+// SIMP density (grad.cu): E, G from rho^P and the reference moduli; dC/drho from dC/dE in place
+void launch_simp_material(cudaStream_t s, int ne, const double* rho, double penal, const double* E0,
+                          const double* G0, const double* nu, double* E, double* G);
+void launch_simp_chain(cudaStream_t s, int ne, int B, const double* rho, double penal, const double* E0,
+                       double* dE);
 void launch_beam_grad(cudaStream_t s, int n_beams, const double* x, const double* y,
                       const double* z, const int32_t* conn, const double* A,
                       const double* Iy, const double* Iz, const double* J, const double* E,
