@@ -326,23 +326,32 @@ class Model:
         return out.reshape(self.batch, ne) if self.batch > 1 else out
 
     def adjoint_solve(self, dg_du):
-        """lambda with K lambda = dg/du (primal state kept).  Returns (lambda, info)."""
+        """lambda with K lambda = dg/du (primal state kept).  Returns (lambda, info); with
+        batch > 1, dg_du and lambda are [B, ndof] and info a list of B dicts."""
         self._mode()
+        B = self.batch
         g = _np(dg_du, np.float64)
-        lam = np.zeros(self.ndof)
-        info = sso_solve_info()
-        self._check(_lib.sso_adjoint_solve(self.h, g.ctypes.data, lam.ctypes.data, C.byref(info)))
-        return lam, info.as_dict()
+        lam = np.zeros(B * self.ndof)
+        infos = (sso_solve_info * B)()
+        self._check(_lib.sso_adjoint_solve(self.h, g.ctypes.data, lam.ctypes.data, infos))
+        if B > 1:
+            return lam.reshape(B, self.ndof), [i.as_dict() for i in infos]
+        return lam, infos[0].as_dict()
 
     def grad_adjoint(self, lam):
-        """(-lambda^T dK/dX u [3, n], -lambda^T dK/dt u [n_quads], -lambda^T dK/dE u [n_elems])."""
+        """(-lambda^T dK/dX u [3, n], -lambda^T dK/dt u [n_quads], -lambda^T dK/dE u [n_elems]);
+        with batch > 1 each gets a leading design axis."""
         self._mode()
+        B = self.batch
         lam = _np(lam, np.float64)
-        dX = np.zeros(3 * self.n_nodes)
-        dT = np.zeros(max(self.n_quads, 1))
-        dE = np.zeros(self.n_beams + self.g_quads)
+        ne = self.n_beams + self.g_quads
+        dX = np.zeros(B * 3 * self.n_nodes)
+        dT = np.zeros(B * max(self.n_quads, 1))
+        dE = np.zeros(B * ne)
         self._check(_lib.sso_grad_adjoint(self.h, lam.ctypes.data, dX.ctypes.data, dT.ctypes.data,
                                           dE.ctypes.data))
+        if B > 1:
+            return dX.reshape(B, 3, self.n_nodes), dT.reshape(B, -1)[:, : self.n_quads], dE.reshape(B, ne)
         return dX.reshape(3, self.n_nodes), dT[: self.n_quads], dE
 
     def set_density(self, rho, penal, E0, G0=None):

@@ -119,6 +119,7 @@ struct Part {
   double *ub = nullptr, *fb = nullptr, *lam = nullptr, *dxyz2 = nullptr, *dt2 = nullptr, *dE2 = nullptr;
   // SIMP density (sso_set_density): rho, reference moduli E0 and (optional) G0 per element
   double *rho = nullptr, *E0 = nullptr, *G0 = nullptr;
+  double* coef = nullptr;  // adjoint polarization: per-design coefficients [5][B]
   // design-dependent area loads (sso_set_area_load): local per-quad q, w and the
   // per-quad lumped value a = (q + w t) A / 4 [B][n_quads]
   double *ld_q = nullptr, *ld_w = nullptr, *ld_a = nullptr;
@@ -603,7 +604,7 @@ void free_part(Part& P) {
                   P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
                   P.lptr, P.lslot, P.lpull, P.pdesc, P.binv, P.zb, P.p2, P.tbuf, P.dE,
                   P.ub, P.fb, P.lam, P.dxyz2, P.dt2, P.dE2, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask,
-                  P.rho, P.E0, P.G0};
+                  P.rho, P.E0, P.G0, P.coef};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -1566,21 +1567,22 @@ static int grad_pass(sso_ctx* h, Part& P, const double* U, double s, double u_lo
 
 int sso_adjoint_solve(sso_handle h, const double* dg_du, double* lambda, sso_solve_info* info) {
   if (!h || !dg_du || !lambda) return SSO_E_INVALID;
-  if (h->distributed() || h->batch > 1) FAIL(h, SSO_E_INVALID, "sso_adjoint_solve is defined for single-strip, single-design handles");
+  if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_adjoint_solve is defined for single-strip handles");
   if (!h->assembled) FAIL(h, SSO_E_STATE, "sso_adjoint_solve before sso_assemble");
   Part& P = h->P0();
+  const int64_t nv = (int64_t)P.B * P.ndof;  // every design of a batch
   int r;
-  if (!P.ub && (r = dalloc(h, &P.ub, P.ndof))) return r;
-  if (!P.fb && (r = dalloc(h, &P.fb, P.ndof))) return r;
+  if (!P.ub && (r = dalloc(h, &P.ub, nv))) return r;
+  if (!P.fb && (r = dalloc(h, &P.fb, nv))) return r;
   const bool was_solved = h->solved;
   // keep the primal (u, f): the adjoint reuses the CG buffers
-  CK(h, cudaMemcpyAsync(P.ub, P.xs, P.ndof * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(P.fb, P.f, P.ndof * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(P.ub, P.xs, nv * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(P.fb, P.f, nv * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   h->skip_load = true;
   const int rc = sso_solve(h, dg_du, lambda, info);  // K symmetric: K^T lambda = K lambda
   h->skip_load = false;
-  CK(h, cudaMemcpyAsync(P.xs, P.ub, P.ndof * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-  CK(h, cudaMemcpyAsync(P.f, P.fb, P.ndof * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(P.xs, P.ub, nv * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(P.f, P.fb, nv * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   int rs = sync(h);
   if (rs) return rs;
   h->solved = was_solved;
@@ -1588,40 +1590,61 @@ int sso_adjoint_solve(sso_handle h, const double* dg_du, double* lambda, sso_sol
 }
 
 // -lambda^T (dK/dp u - df/dp) [+ s u^T df/dp when u_load_s != 0] at the primal state, lambda in
-// P.lam, into P.dxyz / P.dt / P.dE (single strip, batch 1).
+// P.lam, into P.dxyz / P.dt / P.dE (single strip; every design of a batch, u_load_s only for
+// batch 1).
 static int adjoint_grad_dev(sso_ctx* h, double u_load_s) {
   Part& P = h->P0();
+  const int B = P.B;
   const int64_t ne = (int64_t)P.n_beams + P.n_quads;
+  const int64_t nq1 = std::max<int32_t>(P.n_quads, 1), ne1 = std::max<int64_t>(ne, 1);
   int r;
-  if (!P.dxyz2 && (r = dalloc(h, &P.dxyz2, 3 * (int64_t)P.n_nodes))) return r;
-  if (!P.dt2 && (r = dalloc(h, &P.dt2, std::max<int32_t>(P.n_quads, 1)))) return r;
-  if (!P.dE2 && (r = dalloc(h, &P.dE2, std::max<int64_t>(ne, 1)))) return r;
+  if (!P.dxyz2 && (r = dalloc(h, &P.dxyz2, 3 * (int64_t)B * P.n_nodes))) return r;
+  if (!P.dt2 && (r = dalloc(h, &P.dt2, B * nq1))) return r;
+  if (!P.dE2 && (r = dalloc(h, &P.dE2, B * ne1))) return r;
+  if (!P.coef && (r = dalloc(h, &P.coef, 5 * (int64_t)B))) return r;
   // polarization: lambda^T K u = [(u + c l)^T K (u + c l) - (u - c l)^T K (u - c l)] / (4 c),
-  // c = |u| / |lambda| balances the two states (bilinear result, quadratic kernels)
+  // c = |u| / |lambda| per design balances the two states (bilinear result, quadratic kernels)
+  std::vector<double> uu(B), ll(B);
   {
     Scope sc(h, F_REDUCE);
     launch_dot_local(h->stream, (int)P.ndof, P.xs, P.xs, P.partial, P.st, P.bs);
-    CK(h, cudaMemcpyAsync(&h->h_scal[0], &P.st->red[0], sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaMemcpyAsync(h->h_chunk, P.st, B * sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
+    if ((r = sync(h))) return r;
+    for (int d = 0; d < B; ++d) uu[d] = h->h_chunk[d].red[0];
     launch_dot_local(h->stream, (int)P.ndof, P.lam, P.lam, P.partial, P.st, P.bs);
-    CK(h, cudaMemcpyAsync(&h->h_scal[1], &P.st->red[0], sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaMemcpyAsync(h->h_chunk, P.st, B * sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
+    if ((r = sync(h))) return r;
+    for (int d = 0; d < B; ++d) ll[d] = h->h_chunk[d].red[0];
   }
-  if ((r = sync(h))) return r;
-  const double uu = h->h_scal[0], ll = h->h_scal[1];
-  const double c = (uu > 0.0 && ll > 0.0) ? std::sqrt(uu / ll) : 1.0;
+  // coefficient rows: ones, -c, +c, 1/c, -1/c
+  std::vector<double> cf(5 * (size_t)B);
+  for (int d = 0; d < B; ++d) {
+    const double c = (uu[d] > 0.0 && ll[d] > 0.0) ? std::sqrt(uu[d] / ll[d]) : 1.0;
+    cf[d] = 1.0;
+    cf[B + d] = -c;
+    cf[2 * B + d] = c;
+    cf[3 * B + d] = 1.0 / c;
+    cf[4 * B + d] = -1.0 / c;
+  }
+  CK(h, cudaMemcpy(P.coef, cf.data(), cf.size() * sizeof(double), cudaMemcpyHostToDevice));
+  const double* one = P.coef;
+  const double *mc = P.coef + B, *pc = P.coef + 2 * B, *ic = P.coef + 3 * B, *mic = P.coef + 4 * B;
   {
     Scope sc(h, F_GRAD);
-    launch_lincomb(h->stream, P.ndof, 1.0, P.xs, -c, P.lam, P.gu);  // u - c lambda
+    launch_lincomb_rows(h->stream, P.ndof, B, one, P.xs, mc, P.lam, P.gu);  // u - c lambda
     if ((r = grad_pass(h, P, P.gu, 0.25))) return r;
-    CK(h, cudaMemcpyAsync(P.dxyz2, P.dxyz, 3 * (size_t)P.n_nodes * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-    CK(h, cudaMemcpyAsync(P.dt2, P.dt, std::max<int32_t>(P.n_quads, 1) * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-    CK(h, cudaMemcpyAsync(P.dE2, P.dE, std::max<int64_t>(ne, 1) * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-    launch_lincomb(h->stream, P.ndof, 1.0, P.xs, c, P.lam, P.gu);   // u + c lambda
+    CK(h, cudaMemcpyAsync(P.dxyz2, P.dxyz, 3 * (size_t)B * P.n_nodes * sizeof(double), cudaMemcpyDeviceToDevice,
+                          h->stream));
+    CK(h, cudaMemcpyAsync(P.dt2, P.dt, B * nq1 * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(P.dE2, P.dE, B * ne1 * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    launch_lincomb_rows(h->stream, P.ndof, B, one, P.xs, pc, P.lam, P.gu);  // u + c lambda
     // the "+" pass also carries c * s u^T df/dp, which the 1/c below turns into s u^T df/dp
-    if ((r = grad_pass(h, P, P.gu, 0.25, c * u_load_s))) return r;
+    // (batch 1: u_load_s comes from the prescribed-support path only)
+    if ((r = grad_pass(h, P, P.gu, 0.25, B == 1 ? cf[2] * u_load_s : 0.0))) return r;
     // -(1/4)[dE(w+) - dE(w-)] / c  ==  -lambda^T (dK/dp) u
-    launch_lincomb(h->stream, 3 * (int64_t)P.n_nodes, 1.0 / c, P.dxyz, -1.0 / c, P.dxyz2, P.dxyz);
-    launch_lincomb(h->stream, P.n_quads, 1.0 / c, P.dt, -1.0 / c, P.dt2, P.dt);
-    launch_lincomb(h->stream, ne, 1.0 / c, P.dE, -1.0 / c, P.dE2, P.dE);
+    launch_lincomb_rows(h->stream, 3 * (int64_t)P.n_nodes, B, ic, P.dxyz, mic, P.dxyz2, P.dxyz);
+    if (P.n_quads) launch_lincomb_rows(h->stream, P.n_quads, B, ic, P.dt, mic, P.dt2, P.dt);
+    launch_lincomb_rows(h->stream, ne, B, ic, P.dE, mic, P.dE2, P.dE);
   }
   CKL(h);
   return SSO_OK;
@@ -1629,19 +1652,20 @@ static int adjoint_grad_dev(sso_ctx* h, double u_load_s) {
 
 int sso_grad_adjoint(sso_handle h, const double* lambda, double* dg_dxyz, double* dg_dt, double* dg_dE) {
   if (!h || !lambda) return SSO_E_INVALID;
-  if (h->distributed() || h->batch > 1) FAIL(h, SSO_E_INVALID, "sso_grad_adjoint is defined for single-strip, single-design handles");
+  if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_grad_adjoint is defined for single-strip handles");
   if (!h->solved) FAIL(h, SSO_E_STATE, "sso_grad_adjoint before a successful sso_solve");
   Part& P = h->P0();
   const int64_t ne = (int64_t)P.n_beams + P.n_quads;
+  const size_t B = (size_t)P.B;
   int r;
-  if (!P.lam && (r = dalloc(h, &P.lam, P.ndof))) return r;
+  if (!P.lam && (r = dalloc(h, &P.lam, (int64_t)B * P.ndof))) return r;
   if ((r = vec_in(h, lambda, &Part::lam))) return r;
   if ((r = adjoint_grad_dev(h, 0.0))) return r;
   if (dg_dxyz)
-    CK(h, cudaMemcpyAsync(dg_dxyz, P.dxyz, 3 * (size_t)P.n_nodes * sizeof(double), kind_out(h), h->stream));
+    CK(h, cudaMemcpyAsync(dg_dxyz, P.dxyz, 3 * B * P.n_nodes * sizeof(double), kind_out(h), h->stream));
   if (dg_dt && P.n_quads)
-    CK(h, cudaMemcpyAsync(dg_dt, P.dt, (size_t)P.n_quads * sizeof(double), kind_out(h), h->stream));
-  if (dg_dE) CK(h, cudaMemcpyAsync(dg_dE, P.dE, (size_t)ne * sizeof(double), kind_out(h), h->stream));
+    CK(h, cudaMemcpyAsync(dg_dt, P.dt, B * P.n_quads * sizeof(double), kind_out(h), h->stream));
+  if (dg_dE) CK(h, cudaMemcpyAsync(dg_dE, P.dE, B * ne * sizeof(double), kind_out(h), h->stream));
   return sync(h);
 }
 

@@ -279,6 +279,9 @@ void launch_cg_scalar(cudaStream_t s, CgState* st, int phase);
 void launch_pack(cudaStream_t s, int count, const int32_t* idx, const double* vec, double* buf);
 void launch_allreduce_parts(cudaStream_t s, CgState* const* sts, int n_parts, int nvals);
 // out = a x + b y (elementwise, n doubles)
+// out[d] = a[d] x[d] + b[d] y[d] over B contiguous rows of n (coefficients on the device)
+void launch_lincomb_rows(cudaStream_t s, int64_t n, int B, const double* a, const double* x, const double* b,
+                         const double* y, double* out);
 void launch_lincomb(cudaStream_t s, int64_t n, double a, const double* x, double b, const double* y, double* out);
 void launch_gather(cudaStream_t s, int n, const int32_t* idx, const double* src, double* dst);
 void launch_scatter(cudaStream_t s, int n, const int32_t* idx, const double* src, double* dst);

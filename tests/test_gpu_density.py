@@ -3,7 +3,8 @@ Eq. 12: E_j = p_T,j^P E_*,j) against the oracle: sso_set_density forms E = rho^P
 G = rho^P G0 or the derived G) on the device, sso_grad_density returns
 dC/drho = dC/dE * P rho^(P-1) E0.  The oracle side is oracle/grad.py simp_gradient on
 material_gradient, pinned to a complex step through rho in tests/test_oracle_grad.py.
-Tolerances as tests/test_gpu_parity.py (u 1e-9, gradients 1e-7 with a 1e-3 max floor)."""
+Tolerances as tests/test_gpu_parity.py (u 1e-9, gradients 1e-7 with a 1e-3 max floor).
+Also the batched general-objective adjoint."""
 import numpy as np
 import pytest
 
@@ -65,3 +66,45 @@ def test_simp_density_errors_and_material_reset(sso):
     assert np.linalg.norm(u - uref) <= 1e-9 * np.linalg.norm(uref)
     with pytest.raises(sso.SSOError):
         m.grad_density()
+
+
+@pytest.mark.parametrize("precond", [0, 1])
+def test_batched_general_adjoint(sso, precond):
+    """SURVEY.md §8(f) row 2 "a second (batched) PCG with rhs dg/du": a batch of designs
+    solves its adjoints together and each design's lambda and -lambda^T (dK/dp) u equal the
+    single-design ones (and, for one design, the oracle's)."""
+    from oracle import assembly as OA
+    B = 4
+    designs = [W.config5_design(b, n=10) for b in range(B)]
+    Z = np.stack([d["z"] for d in designs])
+    T = np.stack([d["t"] for d in designs])
+    F = np.stack([d["f"] for d in designs])
+    fixed = OA.fixed_dofs(designs[0])
+    rng = np.random.default_rng(21)
+    Cg = rng.standard_normal((B, 6 * len(designs[0]["x"])))
+    Cg[:, fixed] = 0.0
+    mb = sso.Model(designs[0], rtol=1e-12, batch=B, precond=precond)
+    mb.set_design(z=Z, t=T)
+    mb.assemble()
+    U, _ = mb.solve(F)
+    Lam, infos = mb.adjoint_solve(Cg)
+    assert all(i["status"] == 0 for i in infos)
+    dX, dT, dE = mb.grad_adjoint(Lam)
+    for b in (0, 3):
+        m1 = sso.Model(designs[b], rtol=1e-12, precond=precond)
+        m1.assemble()
+        u1, _ = m1.solve(designs[b]["f"])
+        l1, _ = m1.adjoint_solve(Cg[b])
+        assert np.linalg.norm(U[b] - u1) <= 1e-9 * np.linalg.norm(u1)
+        assert np.linalg.norm(Lam[b] - l1) <= 1e-9 * np.linalg.norm(l1)
+        x1, t1, e1 = m1.grad_adjoint(l1)
+        for got, ref in ((dX[b], x1), (dT[b], t1), (dE[b], e1)):
+            fl = 1e-3 * np.abs(ref).max()
+            assert np.all(np.abs(got - ref) <= 1e-7 * np.maximum(np.abs(ref), fl))
+    # design 2 against the oracle
+    P2 = designs[2]
+    uref, _, _ = OG.evaluate(P2)
+    rX, rT, rE = OG.adjoint_general(P2, uref, Lam[2])
+    for got, ref in ((dX[2], rX), (dT[2], rT), (dE[2], rE)):
+        fl = 1e-3 * np.abs(ref).max()
+        assert np.all(np.abs(got - ref) <= 1e-6 * np.maximum(np.abs(ref), fl))
