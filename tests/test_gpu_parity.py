@@ -502,3 +502,23 @@ def test_pull_storage_many_designs(sso):
         u1, _ = m1.solve(designs[b]["f"])
         assert infos[b]["status"] == 0
         assert np.linalg.norm(U[b] - u1) <= 1e-9 * np.linalg.norm(u1)
+
+
+@pytest.mark.parametrize("storage", [1, 3])
+@pytest.mark.parametrize("sup", ["corners", "edge"])
+def test_single_element(sso, sup, storage):
+    """Smallest mesh: one MITC-4 quad (one ragged chunk, one node per CTA slot in use)
+    against the oracle -- u, C and the adjoint gradient."""
+    P = W.tiny_shell(1, supports=sup)
+    m = sso.Model(P, rtol=1e-12, storage=storage)
+    m.assemble()
+    u, info = m.solve(P["f"])
+    assert info["status"] == 0
+    uref, _, _ = OG.evaluate(P)
+    assert np.linalg.norm(u - uref) <= TOL_U * np.linalg.norm(uref)
+    Cv, dX, dT = m.grad(sso.OBJ_COMPLIANCE)
+    assert abs(Cv - OG.compliance(P["f"], uref)) <= TOL_C * abs(Cv)
+    gX, gT = OG.adjoint_gradient(P, uref, 1.0)
+    fl = 1e-3 * np.abs(gX).max()
+    assert np.all(np.abs(dX - gX) <= 1e-6 * np.maximum(np.abs(gX), fl))
+    assert np.all(np.abs(dT - gT) <= 1e-6 * np.maximum(np.abs(gT), 1e-3 * np.abs(gT).max()))
