@@ -196,7 +196,8 @@ def run_reference(args):
     value = float(np.median(vals))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": 1000.0 / value, "higher_is_better": True,
+            "scaling": "strong" if args.strips else "weak",  # the label of the arm it is compared with
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C3b: 408x408 MITC-4 shell quads, 1 003 686 DOF (reading c15)",
                        "rtol": RTOL, "cg_iters": cg_iters},
