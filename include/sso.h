@@ -281,9 +281,10 @@ int sso_set_area_load(sso_handle h, const double* q, const double* w, const doub
  * centroids, beams then quads, each the mean of its nodes (on_elements != 0;
  * n = n_beams + n_quads).  in, out: [ncomp][n] fp64, ncomp in 1..3 (e.g. the three rows of
  * dC/dxyz), pointer kind per mem; out may not alias in.  The neighbour cell grid is
- * cached per (kind, radius) and rebuilt after sso_set_design changes coordinates.
- * Single-strip, batch-1 handles.  Errors: SSO_E_INVALID (radius <= 0 or non-finite,
- * ncomp out of range, NULL pointers, partitioned / batched handle). */
+ * cached per (kind, radius) and rebuilt after sso_set_design changes coordinates.  A batch
+ * filters every design over its own coordinates (in, out [batch][ncomp][n]; the designs'
+ * grids are built per call).  Single-strip handles.  Errors: SSO_E_INVALID (radius <= 0 or
+ * non-finite, ncomp out of range, NULL pointers, partitioned handle). */
 int sso_hat_filter(sso_handle h, int32_t on_elements, double radius, int32_t ncomp, const double* in,
                    double* out);
 

@@ -400,7 +400,9 @@ class Model:
 
     def hat_filter(self, values, radius, on_elements=False):
         """Hat filter of sensitivities (include/sso.h sso_hat_filter): values [n] or
-        [ncomp<=3, n] over nodes (n_nodes) or element centroids (n_beams + n_quads)."""
+        [ncomp<=3, n] over nodes (n_nodes) or element centroids (n_beams + n_quads); with
+        batch > 1 a leading design axis ([B, n] or [B, ncomp, n]), each design filtered over
+        its own coordinates."""
         dev = self._mode(values)
         if dev:
             import torch
@@ -409,7 +411,8 @@ class Model:
         else:
             v = _np(values, np.float64)
             out = np.empty_like(v)
-        ncomp = 1 if v.ndim == 1 else int(v.shape[0])
+        lead = 1 if self.batch > 1 else 0
+        ncomp = 1 if v.ndim == 1 + lead else int(v.shape[lead])
         self._check(_lib.sso_hat_filter(self.h, 1 if on_elements else 0, float(radius), ncomp,
                                         _ptr(v, np.float64), _ptr(out, np.float64)))
         return out

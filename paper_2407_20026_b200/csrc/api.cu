@@ -1880,16 +1880,18 @@ namespace {
 // Hat filter (filter.cu).  The cell grid is built here on the host from the current
 // design-0 coordinates: cubic cells of edge >= radius, so every point within the
 // radius lies in the 27 cells around a point's own cell.
-int build_filter_grid(sso_ctx* h, int on_elements, double radius) {
-  sso_ctx::FilterGrid& g = h->fgrid[on_elements ? 1 : 0];
+// design bd's coordinates into grid g (the cached grid of design 0, or a per-call grid of a
+// batch design)
+int build_filter_grid(sso_ctx* h, int on_elements, double radius, int bd, sso_ctx::FilterGrid& g) {
   if (g.valid && g.radius == radius) return SSO_OK;
   free_filter_grid(g);
   Part& P = h->P0();
   const int64_t nn = P.n_nodes;
+  const int64_t off = (int64_t)bd * P.bs.node;
   std::vector<double> X(nn), Y(nn), Z(nn);
-  CK(h, cudaMemcpyAsync(X.data(), P.x, nn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  CK(h, cudaMemcpyAsync(Y.data(), P.y, nn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  CK(h, cudaMemcpyAsync(Z.data(), P.z, nn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaMemcpyAsync(X.data(), P.x + off, nn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaMemcpyAsync(Y.data(), P.y + off, nn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaMemcpyAsync(Z.data(), P.z + off, nn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   std::vector<double> px, py, pz;
   if (!on_elements) {
@@ -1966,29 +1968,39 @@ int sso_hat_filter(sso_handle h, int32_t on_elements, double radius, int32_t nco
                    double* out) {
   if (!h || !in || !out) return SSO_E_INVALID;
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_hat_filter is defined for single-strip handles");
-  if (h->batch != 1) FAIL(h, SSO_E_INVALID, "sso_hat_filter is defined for batch 1 handles");
   if (!(radius > 0.0) || !std::isfinite(radius)) FAIL(h, SSO_E_INVALID, "radius must be positive and finite");
   if (ncomp < 1 || ncomp > 3) FAIL(h, SSO_E_INVALID, "ncomp must be 1, 2 or 3");
-  int rc = build_filter_grid(h, on_elements != 0, radius);
-  if (rc) return rc;
-  sso_ctx::FilterGrid& g = h->fgrid[on_elements ? 1 : 0];
-  const int64_t n = g.n;
-  if (n == 0) return SSO_OK;
-  const double* din = in;
-  double* dout = out;
-  if (h->mem == SSO_MEM_HOST) {
-    CK(h, cudaMemcpyAsync(g.io, in, ncomp * n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-    din = g.io;
-    dout = g.io + 3 * n;
+  // batch 1: the grid is cached per (kind, radius); a batch builds each design's grid from its
+  // own coordinates for this call (in / out [batch][ncomp][n])
+  for (int bd = 0; bd < h->batch; ++bd) {
+    sso_ctx::FilterGrid tmp;
+    sso_ctx::FilterGrid& g = h->batch == 1 ? h->fgrid[on_elements ? 1 : 0] : tmp;
+    int rc = build_filter_grid(h, on_elements != 0, radius, bd, g);
+    if (rc) return rc;
+    const int64_t n = g.n;
+    if (n == 0) {
+      if (&g == &tmp) free_filter_grid(tmp);
+      return SSO_OK;
+    }
+    const double* din = in + (int64_t)bd * ncomp * n;
+    double* dout = out + (int64_t)bd * ncomp * n;
+    if (h->mem == SSO_MEM_HOST) {
+      CK(h, cudaMemcpyAsync(g.io, din, ncomp * n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+      din = g.io;
+      dout = g.io + 3 * n;
+    }
+    const long long g0 = g_launches;
+    launch_hat_filter(h->stream, (int)n, ncomp, g.px, g.py, g.pz, g.cell_of, g.perm, g.cell_start, g.gx, g.gy,
+                      g.gz, radius, din, dout);
+    CKL(h);
+    h->launches += g_launches - g0;
+    if (h->mem == SSO_MEM_HOST)
+      CK(h, cudaMemcpyAsync(out + (int64_t)bd * ncomp * n, dout, ncomp * n * sizeof(double), cudaMemcpyDeviceToHost,
+                            h->stream));
+    if ((rc = sync(h))) return rc;
+    if (&g == &tmp) free_filter_grid(tmp);
   }
-  const long long g0 = g_launches;
-  launch_hat_filter(h->stream, (int)n, ncomp, g.px, g.py, g.pz, g.cell_of, g.perm, g.cell_start, g.gx, g.gy,
-                    g.gz, radius, din, dout);
-  CKL(h);
-  h->launches += g_launches - g0;
-  if (h->mem == SSO_MEM_HOST)
-    CK(h, cudaMemcpyAsync(out, dout, ncomp * n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  return sync(h);
+  return SSO_OK;
 }
 
 int sso_spmv(sso_handle h, const double* xin, double* yout) {

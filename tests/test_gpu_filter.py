@@ -93,3 +93,25 @@ def test_hat_filter_large_sampled(sso, n, radius, on_elements):
     rows = np.unique(np.concatenate([[0, npts - 1, npts // 2], rng.integers(0, npts, 40)]))
     ref = OF.hat_filter_rows(P, radius, v, rows, on_elements)
     _close(out[:, rows], ref, 1e-12)
+
+
+@pytest.mark.parametrize("on_elements", [False, True])
+def test_hat_filter_batched_designs(sso, on_elements):
+    """A batch filters every design over its own (design-dependent) coordinates: each design
+    equals the oracle on that design's problem; 1- and 3-component layouts."""
+    B = 3
+    designs = [W.config5_design(b, n=8) for b in range(B)]
+    m = sso.Model(designs[0], batch=B)
+    m.set_design(z=np.stack([d["z"] for d in designs]), t=np.stack([d["t"] for d in designs]))
+    n = len(OF.points(designs[0], on_elements))
+    rng = np.random.default_rng(5)
+    radius = 2.5
+    v1 = rng.standard_normal((B, n))
+    v3 = rng.standard_normal((B, 3, n))
+    g1 = m.hat_filter(v1, radius, on_elements)
+    g3 = m.hat_filter(v3, radius, on_elements)
+    for b in range(B):
+        _close(g1[b], OF.hat_filter(designs[b], radius, v1[b], on_elements), 1e-13)
+        _close(g3[b], OF.hat_filter(designs[b], radius, v3[b], on_elements), 1e-13)
+    # the designs differ in z, so their filters differ
+    assert np.abs(g1[0] - g1[1]).max() > 0 or np.array_equal(v1[0], v1[1])
