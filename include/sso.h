@@ -254,8 +254,8 @@ int sso_set_material(sso_handle h, const double* E);
  * While active, sso_grad / sso_grad_E return the compliance gradient C = s f^T u,
  * dC/dp = -lambda^T dK/dp u + (lambda + s u)^T df/dp with lambda = s u_hom (the same loads
  * with b = 0: one more PCG solve inside sso_grad); sso_grad_at is refused.
- * Single-strip, batch-1 handles.  Errors: SSO_E_INVALID (non-finite b, partitioned or
- * batched handle). */
+ * Single-strip handles; a batch takes one b per design ([batch][6 n_nodes]; not combined
+ * with area loads).  Errors: SSO_E_INVALID (non-finite b, partitioned handle). */
 int sso_set_prescribed(sso_handle h, const double* b);
 
 /* Design-dependent area loads (Eq. 6 with

@@ -380,8 +380,8 @@ class Model:
         self._check(_lib.sso_set_material(self.h, _ptr(E, np.float64)))
 
     def set_prescribed(self, b):
-        """Prescribed support displacements b [6 n_nodes] (constrained entries used);
-        None switches them off.  Requires a new assemble()."""
+        """Prescribed support displacements b [6 n_nodes] ([B, 6 n_nodes] for a batch;
+        constrained entries used); None switches them off.  Requires a new assemble()."""
         dev = self._mode(b)
         if b is not None and not dev:
             b = _np(b, np.float64)

@@ -1368,7 +1368,7 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
   if (lift) {  // K_ff u_f = f_f - K_fc b (reading c18)
     Part& P = h->P0();
     Scope sc(h, F_UPDATE);
-    launch_lincomb(h->stream, P.ndof, 1.0, P.f, -1.0, P.kb, P.feff);
+    launch_lincomb(h->stream, (int64_t)P.B * P.ndof, 1.0, P.f, -1.0, P.kb, P.feff);
   }
   CK(h, cudaEventRecord(h->ev_a, h->stream));
   for (auto& pp : h->parts) {
@@ -1405,7 +1405,7 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
   if (lift) {  // u = u_f + b
     Part& P = h->P0();
     Scope sc(h, F_UPDATE);
-    launch_lincomb(h->stream, P.ndof, 1.0, P.xs, 1.0, P.pb, P.xs);
+    launch_lincomb(h->stream, (int64_t)P.B * P.ndof, 1.0, P.xs, 1.0, P.pb, P.xs);
   }
   if ((rc = vec_out(h, u, &Part::xs))) return rc;
   if ((rc = sync(h))) return rc;
@@ -1677,10 +1677,14 @@ static int grad_prescribed(sso_ctx* h, sso_objective obj, double* C, double* dC_
   const double s = (obj == SSO_OBJ_STRAIN_ENERGY) ? 0.5 : 1.0;
   Part& P = h->P0();
   const int64_t ne = (int64_t)P.n_beams + P.n_quads;
+  const int B = P.B;
+  const int64_t nv = (int64_t)B * P.ndof;
+  if (B > 1 && h->area_load)
+    FAIL(h, SSO_E_INVALID, "prescribed displacements with area loads are defined for batch-1 handles");
   int r;
-  if (!P.lam && (r = dalloc(h, &P.lam, P.ndof))) return r;
-  if (!P.gf && (r = dalloc(h, &P.gf, P.ndof))) return r;
-  CK(h, cudaMemcpyAsync(P.gf, P.f, P.ndof * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  if (!P.lam && (r = dalloc(h, &P.lam, nv))) return r;
+  if (!P.gf && (r = dalloc(h, &P.gf, nv))) return r;
+  CK(h, cudaMemcpyAsync(P.gf, P.f, nv * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   // the adjoint solve through the public entry, with device pointers for the call
   const sso_mem mem = h->mem;
   h->mem = SSO_MEM_DEVICE;
@@ -1689,27 +1693,28 @@ static int grad_prescribed(sso_ctx* h, sso_objective obj, double* C, double* dC_
   if (r) return r;
   {
     Scope sc(h, F_UPDATE);
-    launch_lincomb(h->stream, P.ndof, s, P.lam, 0.0, P.lam, P.lam);
+    launch_lincomb(h->stream, nv, s, P.lam, 0.0, P.lam, P.lam);
   }
   if ((r = adjoint_grad_dev(h, s))) return r;
   {
     Scope sc(h, F_REDUCE);
     launch_dot_local(h->stream, (int)P.ndof, P.f, P.xs, P.partial, P.st, P.bs);
-    CK(h, cudaMemcpyAsync(&h->h_scal[2], &P.st->red[0], sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaMemcpyAsync(h->h_chunk, P.st, B * sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
   }
   if (dC_dxyz)
-    CK(h, cudaMemcpyAsync(dC_dxyz, P.dxyz, 3 * (size_t)P.n_nodes * sizeof(double), kind_out(h), h->stream));
+    CK(h, cudaMemcpyAsync(dC_dxyz, P.dxyz, 3 * (size_t)B * P.n_nodes * sizeof(double), kind_out(h), h->stream));
   if (dC_dt && P.n_quads)
-    CK(h, cudaMemcpyAsync(dC_dt, P.dt, (size_t)P.n_quads * sizeof(double), kind_out(h), h->stream));
+    CK(h, cudaMemcpyAsync(dC_dt, P.dt, (size_t)B * P.n_quads * sizeof(double), kind_out(h), h->stream));
   if (dC_dE) {
-    if (h->simp_chain) launch_simp_chain(h->stream, (int)ne, 1, P.rho, h->penal, P.E0, P.dE);
-    CK(h, cudaMemcpyAsync(dC_dE, P.dE, (size_t)ne * sizeof(double), kind_out(h), h->stream));
+    if (h->simp_chain) launch_simp_chain(h->stream, (int)ne, B, P.rho, h->penal, P.E0, P.dE);
+    CK(h, cudaMemcpyAsync(dC_dE, P.dE, (size_t)B * ne * sizeof(double), kind_out(h), h->stream));
   }
   if ((r = sync(h))) return r;
   if (C) {
-    const double v = s * h->h_scal[2];
-    if (h->mem == SSO_MEM_HOST) *C = v;
-    else CK(h, cudaMemcpy(C, &v, sizeof(double), cudaMemcpyHostToDevice));
+    std::vector<double> v(B);
+    for (int d = 0; d < B; ++d) v[d] = s * h->h_chunk[d].red[0];
+    if (h->mem == SSO_MEM_HOST) std::memcpy(C, v.data(), B * sizeof(double));
+    else CK(h, cudaMemcpy(C, v.data(), B * sizeof(double), cudaMemcpyHostToDevice));
   }
   return SSO_OK;
 }
@@ -1731,27 +1736,28 @@ int sso_set_prescribed(sso_handle h, const double* b) {
     h->solved = false;
     return SSO_OK;
   }
-  if (h->distributed() || h->batch > 1)
-    FAIL(h, SSO_E_INVALID, "sso_set_prescribed is defined for single-strip, single-design handles");
+  if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_set_prescribed is defined for single-strip handles");
   Part& P = h->P0();
+  const int64_t nv = (int64_t)P.B * P.ndof;  // one b per design of a batch
   int r;
-  if (!P.pb && (r = dalloc(h, &P.pb, P.ndof))) return r;
-  if (!P.kb && (r = dalloc(h, &P.kb, P.ndof))) return r;
-  if (!P.feff && (r = dalloc(h, &P.feff, P.ndof))) return r;
+  if (!P.pb && (r = dalloc(h, &P.pb, nv))) return r;
+  if (!P.kb && (r = dalloc(h, &P.kb, nv))) return r;
+  if (!P.feff && (r = dalloc(h, &P.feff, nv))) return r;
   if (!P.free_mask) {  // per-node support bitmasks, all clear
     if ((r = dalloc(h, &P.free_mask, P.n_nodes))) return r;
     CK(h, cudaMemsetAsync(P.free_mask, 0, P.n_nodes, h->stream));
   }
-  std::vector<double> hb(P.ndof);
-  CK(h, cudaMemcpy(hb.data(), b, P.ndof * sizeof(double),
+  std::vector<double> hb(nv);
+  CK(h, cudaMemcpy(hb.data(), b, nv * sizeof(double),
                    h->mem == SSO_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost));
   std::vector<uint8_t> mask(P.n_nodes);
   CK(h, cudaMemcpy(mask.data(), P.fixed_mask, P.n_nodes, cudaMemcpyDeviceToHost));
-  for (int64_t i = 0; i < P.ndof; ++i) {
-    if (!std::isfinite(hb[i])) FAIL(h, SSO_E_INVALID, "sso_set_prescribed: non-finite value");
-    if (!((mask[i / 6] >> (i % 6)) & 1)) hb[i] = 0.0;  // only the constrained DOFs carry b
+  for (int64_t k = 0; k < nv; ++k) {
+    const int64_t i = k % P.ndof;
+    if (!std::isfinite(hb[k])) FAIL(h, SSO_E_INVALID, "sso_set_prescribed: non-finite value");
+    if (!((mask[i / 6] >> (i % 6)) & 1)) hb[k] = 0.0;  // only the constrained DOFs carry b
   }
-  CK(h, cudaMemcpy(P.pb, hb.data(), P.ndof * sizeof(double), cudaMemcpyHostToDevice));
+  CK(h, cudaMemcpy(P.pb, hb.data(), nv * sizeof(double), cudaMemcpyHostToDevice));
   h->prescribed = true;
   h->assembled = false;  // K_full b is formed by the next sso_assemble
   h->solved = false;

@@ -6,8 +6,9 @@ system solved by dense LU), through the C-ABI (sso_set_prescribed):
   * C = s f^T u within 1e-10 and dC/dX, dC/dt, dC/dE within 1e-7 (the gradient runs a
     second PCG solve for lambda = s u_hom inside sso_grad);
   * with design-dependent area loads on top;
-  * switching b off restores the plain path bit-exactly; refusals on batch handles and
-    sso_grad_at.
+  * switching b off restores the plain path bit-exactly; refusals (sso_grad_at, area loads
+    on a batch);
+  * one b per design of a batch, equal to the single-design solves.
 """
 import numpy as np
 import pytest
@@ -122,5 +123,48 @@ def test_prescribed_refusals(sso):
         m.grad_at(P["f"], np.zeros(6 * len(P["x"])))
     designs = [W.config5_design(k, n=6) for k in range(2)]
     mb = sso.Model(designs[0], batch=2)
+    with pytest.raises(sso.SSOError):  # a batch takes one b per design
+        mb.set_prescribed(np.full(6 * len(designs[0]["x"]), np.nan))
+    # prescribed + area loads on a batch is refused at the gradient
+    mb.set_prescribed(np.stack([b_vec(d, 2) for d in designs]))
+    mb.set_area_load(np.full(len(designs[0]["quad_conn"]), 1e3), None)
+    mb.assemble()
+    mb.solve(np.stack([d["f"] for d in designs]))
     with pytest.raises(sso.SSOError):
-        mb.set_prescribed(b_vec(designs[0], 2))
+        mb.grad(0)
+
+
+@pytest.mark.parametrize("s_obj", [0, 1])
+def test_prescribed_batched_designs(sso, s_obj):
+    """One b per design of a batch: every design equals its single-design prescribed
+    solve and gradient, and design 1 the oracle's Lagrange system."""
+    B = 3
+    s = 1.0 if s_obj == 0 else 0.5
+    designs = [W.config5_design(k, n=8) for k in range(B)]
+    bs = np.stack([b_vec(d, 10 + k) for k, d in enumerate(designs)])
+    mb = sso.Model(designs[0], rtol=1e-12, batch=B)
+    mb.set_design(z=np.stack([d["z"] for d in designs]), t=np.stack([d["t"] for d in designs]))
+    mb.set_prescribed(bs)
+    mb.assemble()
+    U, infos = mb.solve(np.stack([d["f"] for d in designs]))
+    assert all(i["status"] == 0 for i in infos)
+    C, dX, dT = mb.grad(s_obj)
+    dE = mb.grad_E(s_obj)
+    fixed = OA.fixed_dofs(designs[0])
+    for k in range(B):
+        assert np.array_equal(U[k][fixed], bs[k][fixed])
+        m1 = sso.Model(designs[k], rtol=1e-12)
+        m1.set_prescribed(bs[k])
+        m1.assemble()
+        u1, _ = m1.solve(designs[k]["f"])
+        assert np.linalg.norm(U[k] - u1) <= 1e-9 * np.linalg.norm(u1)
+        c1, x1, t1 = m1.grad(s_obj)
+        assert C[k] == pytest.approx(c1, rel=1e-10)
+        assert _rel(dX[k], x1) <= 1e-7 and _rel(dT[k], t1) <= 1e-7
+        assert _rel(dE[k], m1.grad_E(s_obj)) <= 1e-7
+    P1 = designs[1]
+    uref = OP.solve(P1, np.where(fixed, bs[1], 0.0))
+    assert np.linalg.norm(U[1] - uref) <= 1e-9 * np.linalg.norm(uref)
+    rX, rT, rE = OP.gradient(P1, uref, s)
+    assert C[1] == pytest.approx(OP.compliance(P1, uref, s), rel=1e-10)
+    assert _rel(dX[1], rX) <= 1e-7 and _rel(dT[1], rT) <= 1e-7 and _rel(dE[1], rE) <= 1e-7
