@@ -355,7 +355,6 @@ __global__ void __launch_bounds__(256, 2) cg_update_block_fused_kernel(
     const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ pn,
     double* __restrict__ partial, CgState* st, BatchStrides bs) {
   __shared__ double sm[64];
-  __shared__ int s_go;
   {
     const int bd = blockIdx.y;
     binv += (int64_t)bd * 21 * n_nodes;
@@ -368,8 +367,8 @@ __global__ void __launch_bounds__(256, 2) cg_update_block_fused_kernel(
     st += bd;
   }
   if (st->done) return;
-  const unsigned gen0 = st->gen;
-  const double alpha = st->alpha;
+  const double alpha = st->alpha, rz_old = st->rz;  // before CTA 0 rewrites them
+  const long long iter_old = st->iter;
   double v[2] = {0.0, 0.0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t n0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -401,11 +400,15 @@ __global__ void __launch_bounds__(256, 2) cg_update_block_fused_kernel(
     double zi[6], pi[6];
     step(n, zi, pi);
   }
-  const bool last = grid_sum<2>(v, partial, &st->ticket[1], sm);
-  if (threadIdx.x == 0) s_go = cg_fused_epilogue(last, v, st, gen0);
-  __syncthreads();
-  if (!s_go || __ldcg(&st->done)) return;
-  const double beta = __ldcg(&st->beta);
+  if (!cg_fused_allreduce(v, partial, &st->arrive, sm)) {
+    if (threadIdx.x == 0) {
+      st->status = SSO_E_CUDA;
+      st->done = 1;
+    }
+    return;
+  }
+  double beta;
+  if (!cg_fused_step(v, st, rz_old, iter_old, beta)) return;
 #pragma unroll
   for (int k = 0; k < FB_ITEMS; ++k) {
     const int64_t n = n0 + k * stride;

@@ -1,12 +1,13 @@
-// Grid barrier and beta epilogue shared by the fused CG update kernels
-// (cg_update_fused_kernel in pcg.cu, cg_update_block_fused_kernel in block_jacobi.cu).
+// Grid all-reduce shared by the fused CG update kernels (cg_update_fused_kernel in pcg.cu,
+// cg_update_block_fused_kernel in block_jacobi.cu).
 //
-// A fused update forms r^T z and r^T r over the grid (last-CTA reduction), the last
-// CTA writes beta / the convergence test into the state and advances st->gen; every
-// other CTA waits for the generation to move, then all form p_next = z + beta p.
-// All CTAs are co-resident by construction (grid bounded by the occupancy, launched
-// on an otherwise idle stream after the SpMV); the wait is still bounded so that a
-// broken launch reports SSO_E_CUDA instead of hanging the device.
+// A fused update forms r^T z and r^T r over the grid: every CTA publishes its two partials,
+// counts itself in (one atomic), waits until all CTAs of its design have arrived, then sums
+// ALL partials itself in one fixed order -- every CTA obtains bit-identical totals, forms beta
+// and the convergence test locally and goes on to p_next = z + beta p with no second
+// release step; CTA 0 records the state.  All CTAs are co-resident by construction (grid
+// bounded by the occupancy, launched on an otherwise idle stream after the SpMV); the wait
+// is still bounded so that a broken launch reports SSO_E_CUDA instead of hanging the device.
 #pragma once
 
 #include "sso_internal.h"
@@ -19,35 +20,94 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
-// Thread 0 of each CTA.  last: this CTA did the final reduction (v = r^T z, r^T r).
-// Returns 1 when the CTA may proceed to the p update.
-__device__ __forceinline__ int cg_fused_epilogue(bool last, const double (&v)[2], CgState* st, unsigned gen0) {
-  if (last) {
-    const double rz_new = v[0];
-    st->beta = rz_new / st->rz;
-    st->rz_prev = st->rz;
+__device__ __forceinline__ double fused_warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// v: this thread's (r^T z, r^T r) partials in, the grid totals out (every thread).  part:
+// 2 doubles per CTA; arrive: the design's monotonic arrival counter (+gridDim.x per launch).
+// sm: 64 doubles of shared memory.  Returns 0 if the arrival wait timed out.
+__device__ __forceinline__ int cg_fused_allreduce(double (&v)[2], double* part, unsigned* arrive, double* sm) {
+  __shared__ int s_ok;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned G = gridDim.x;
+  double a0 = fused_warp_sum(v[0]), a1 = fused_warp_sum(v[1]);
+  if (lane == 0) {
+    sm[2 * w] = a0;
+    sm[2 * w + 1] = a1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double c0 = 0.0, c1 = 0.0;
+    for (int i = 0; i < nw; ++i) {
+      c0 += sm[2 * i];
+      c1 += sm[2 * i + 1];
+    }
+    part[2 * blockIdx.x] = c0;
+    part[2 * blockIdx.x + 1] = c1;
+    __threadfence();
+    const unsigned old = atomicAdd(arrive, 1u);
+    const unsigned target = (old / G + 1) * G;
+    int ok = 0;
+    for (int spin = 0; spin < (1 << 23); ++spin) {  // ~0.3 s at most
+      if ((int)(ld_acquire_u32(arrive) - target) >= 0) {
+        ok = 1;
+        break;
+      }
+      __nanosleep(20);
+    }
+    s_ok = ok;
+  }
+  __syncthreads();
+  if (!s_ok) return 0;
+  a0 = a1 = 0.0;
+  for (unsigned b = threadIdx.x; b < G; b += blockDim.x) {
+    a0 += __ldcg(part + 2 * b);
+    a1 += __ldcg(part + 2 * b + 1);
+  }
+  a0 = fused_warp_sum(a0);
+  a1 = fused_warp_sum(a1);
+  if (lane == 0) {
+    sm[2 * w + 32] = a0;  // second half: the first half may still be read above
+    sm[2 * w + 33] = a1;
+  }
+  __syncthreads();
+  double t0 = 0.0, t1 = 0.0;
+  for (int i = 0; i < nw; ++i) {  // every thread, the same order
+    t0 += sm[2 * i + 32];
+    t1 += sm[2 * i + 33];
+  }
+  v[0] = t0;
+  v[1] = t1;
+  return 1;
+}
+
+// beta and the convergence test from the grid totals; CTA 0 records the state.  Returns 1
+// when the caller goes on to the p update (not converged / not stopped).
+__device__ __forceinline__ int cg_fused_step(const double (&v)[2], CgState* st, double rz_old, long long iter_old,
+                                            double& beta) {
+  const double rz_new = v[0], rr = v[1];
+  beta = rz_new / rz_old;
+  const bool conv = rr <= st->tol2;
+  const bool maxed = iter_old + 1 >= st->max_iter;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->beta = beta;
+    st->rz_prev = rz_old;
     st->rz = rz_new;
-    st->rr = v[1];
-    st->iter += 1;
+    st->rr = rr;
+    st->iter = iter_old + 1;
     st->pfix = 0;
-    if (v[1] <= st->tol2) {
+    if (conv) {
       st->done = 1;
       st->status = SSO_OK;
-    } else if (st->iter >= st->max_iter) {
+    } else if (maxed) {
       st->done = 1;
       st->status = SSO_E_NOT_CONVERGED;
     }
-    __threadfence();
-    atomicAdd(&st->gen, 1u);  // release the grid
-    return 1;
   }
-  for (int spin = 0; spin < (1 << 22); ++spin) {  // ~0.3 s at most
-    if (ld_acquire_u32(&st->gen) != gen0) return 1;
-    __nanosleep(64);
-  }
-  st->status = SSO_E_CUDA;
-  st->done = 1;
-  return 0;
+  return !(conv || maxed);
 }
 
 }  // namespace sso

@@ -1119,7 +1119,6 @@ __global__ void __launch_bounds__(256, 2) cg_update_fused_kernel(int ndof, const
                                                                  double* __restrict__ partial,
                                                                  CgState* st, BatchStrides bs) {
   __shared__ double sm[64];
-  __shared__ int s_go;
   {  // design of a batch (blockIdx.y): its own CTAs, reduction and barrier
     const int bd = blockIdx.y;
     dinv += bd * bs.dof;
@@ -1132,8 +1131,9 @@ __global__ void __launch_bounds__(256, 2) cg_update_fused_kernel(int ndof, const
     st += bd;
   }
   if (st->done) return;  // set only by earlier kernels: the same for every CTA
-  const unsigned gen0 = st->gen;  // advanced only after every CTA has arrived below
-  const double alpha = st->alpha;
+  // read before the all-reduce (CTA 0 rewrites them after every CTA has arrived)
+  const double alpha = st->alpha, rz_old = st->rz;
+  const long long iter_old = st->iter;
   double v[2] = {0.0, 0.0};  // r^T z, r^T r
   const int64_t n2 = ndof / 2;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -1176,11 +1176,15 @@ __global__ void __launch_bounds__(256, 2) cg_update_fused_kernel(int ndof, const
     v[0] += ri.x * (di.x * ri.x) + ri.y * (di.y * ri.y);
     v[1] += ri.x * ri.x + ri.y * ri.y;
   }
-  const bool last = grid_sum<2>(v, partial, &st->ticket[1], sm);
-  if (threadIdx.x == 0) s_go = cg_fused_epilogue(last, v, st, gen0);
-  __syncthreads();
-  if (!s_go || __ldcg(&st->done)) return;
-  const double beta = __ldcg(&st->beta);
+  if (!cg_fused_allreduce(v, partial, &st->arrive, sm)) {
+    if (threadIdx.x == 0) {
+      st->status = SSO_E_CUDA;
+      st->done = 1;
+    }
+    return;
+  }
+  double beta;
+  if (!cg_fused_step(v, st, rz_old, iter_old, beta)) return;
 #pragma unroll
   for (int k = 0; k < FUSED_ITEMS; ++k) {
     const int64_t i = i0 + k * stride;

@@ -83,7 +83,7 @@ struct CgState {
   int floor;        // 1 = the true residual sits far above the recurrence (fp64 floor):
                     //     no further replacements / restarts
   int pfix;         // 1 = r was replaced after the fused update formed p: re-form p
-  unsigned int gen; // grid-barrier generation of the fused update kernel
+  unsigned int arrive;  // fused update: CTAs arrived (monotonic, +grid per launch)
 };
 
 // error flags written by device kernels (atomicMin on the offending index)
