@@ -1359,6 +1359,7 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
     h->h_st[bd].tol2 = h->rtol * h->rtol;
     h->h_st[bd].max_iter = h->max_iter;
     h->h_st[bd].dist = dist ? 1 : 0;
+    h->h_st[bd].defer_alpha = (!dist && h->P0().cgf) ? 1 : 0;  // the fused update forms alpha
   }
   for (auto& pp : h->parts)
     CK(h, cudaMemcpyAsync(pp->st, h->h_st, pp->B * sizeof(CgState), cudaMemcpyHostToDevice, h->stream));

@@ -367,8 +367,10 @@ __global__ void __launch_bounds__(256, 2) cg_update_block_fused_kernel(
     st += bd;
   }
   if (st->done) return;
-  const double alpha = st->alpha, rz_old = st->rz;  // before CTA 0 rewrites them
+  const double rz_old = st->rz;  // before CTA 0 rewrites it
   const long long iter_old = st->iter;
+  double alpha, pqv;
+  if (!cg_fused_alpha(partial + PQ_OFF, st, sm, rz_old, alpha, pqv)) return;
   double v[2] = {0.0, 0.0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t n0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(256, 2) cg_update_block_fused_kernel(
     return;
   }
   double beta;
-  if (!cg_fused_step(v, st, rz_old, iter_old, beta)) return;
+  if (!cg_fused_step(v, st, rz_old, iter_old, alpha, pqv, beta)) return;
 #pragma unroll
   for (int k = 0; k < FB_ITEMS; ++k) {
     const int64_t n = n0 + k * stride;

@@ -84,15 +84,51 @@ __device__ __forceinline__ int cg_fused_allreduce(double (&v)[2], double* part, 
   return 1;
 }
 
+// alpha = r^T z / p^T q at the start of a fused update.  With st->defer_alpha the SpMV left
+// st->npq partials of p^T q at pq_part: every CTA sums them in one fixed order (bit-identical
+// in all CTAs); otherwise the SpMV's last CTA already stored alpha.  Returns 0 (all CTAs) when
+// p^T q <= 0: CTA 0 records SSO_E_NOT_SPD.
+__device__ __forceinline__ int cg_fused_alpha(const double* pq_part, CgState* st, double* sm, double rz_old,
+                                             double& alpha, double& pqv) {
+  if (!st->defer_alpha) {
+    alpha = st->alpha;
+    pqv = st->pq;
+    return 1;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int np = st->npq;
+  double a = 0.0;
+  for (int b = threadIdx.x; b < np; b += blockDim.x) a += __ldcg(pq_part + b);
+  a = fused_warp_sum(a);
+  if (lane == 0) sm[w] = a;
+  __syncthreads();
+  double t = 0.0;
+  for (int i = 0; i < nw; ++i) t += sm[i];  // every thread, the same order
+  __syncthreads();                          // sm is reused by the all-reduce
+  pqv = t;
+  if (!(t > 0.0)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->pq = t;
+      st->status = SSO_E_NOT_SPD;
+      st->done = 1;
+    }
+    return 0;
+  }
+  alpha = rz_old / t;
+  return 1;
+}
+
 // beta and the convergence test from the grid totals; CTA 0 records the state.  Returns 1
 // when the caller goes on to the p update (not converged / not stopped).
 __device__ __forceinline__ int cg_fused_step(const double (&v)[2], CgState* st, double rz_old, long long iter_old,
-                                            double& beta) {
+                                            double alpha, double pqv, double& beta) {
   const double rz_new = v[0], rr = v[1];
   beta = rz_new / rz_old;
   const bool conv = rr <= st->tol2;
   const bool maxed = iter_old + 1 >= st->max_iter;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->alpha = alpha;
+    st->pq = pqv;
     st->beta = beta;
     st->rz_prev = rz_old;
     st->rz = rz_new;

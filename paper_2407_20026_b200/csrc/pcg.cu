@@ -634,7 +634,13 @@ __global__ void __launch_bounds__(SPMV_WARPS * 32, MINB) spmv_tma_kernel(
     __syncwarp();
   }
   if (DOT) {
-    if (grid_sum<1>(pq, partial, &st->ticket[0], sm) && threadIdx.x == 0) {
+    if (st->defer_alpha) {  // the fused update sums the partials (fixed order) in every CTA
+      block_sum<1>(pq, sm);
+      if (threadIdx.x == 0) {
+        partial[PQ_OFF + blockIdx.x] = pq[0];
+        if (blockIdx.x == 0) st->npq = (int)gridDim.x;
+      }
+    } else if (grid_sum<1>(pq, partial, &st->ticket[0], sm) && threadIdx.x == 0) {
       if (st->dist) {
         st->red[0] = pq[0];
         return;
@@ -994,7 +1000,13 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
     }
   }
   if (DOT) {
-    if (grid_sum<1>(pq, partial, &st->ticket[0], sm) && threadIdx.x == 0) {
+    if (st->defer_alpha) {  // the fused update sums the partials (fixed order) in every CTA
+      block_sum<1>(pq, sm);
+      if (threadIdx.x == 0) {
+        partial[PQ_OFF + blockIdx.x] = pq[0];
+        if (blockIdx.x == 0) st->npq = (int)gridDim.x;
+      }
+    } else if (grid_sum<1>(pq, partial, &st->ticket[0], sm) && threadIdx.x == 0) {
       if (st->dist) {
         st->red[0] = pq[0];
         return;
@@ -1132,8 +1144,10 @@ __global__ void __launch_bounds__(256, 2) cg_update_fused_kernel(int ndof, const
   }
   if (st->done) return;  // set only by earlier kernels: the same for every CTA
   // read before the all-reduce (CTA 0 rewrites them after every CTA has arrived)
-  const double alpha = st->alpha, rz_old = st->rz;
+  const double rz_old = st->rz;
   const long long iter_old = st->iter;
+  double alpha, pqv;
+  if (!cg_fused_alpha(partial + PQ_OFF, st, sm, rz_old, alpha, pqv)) return;
   double v[2] = {0.0, 0.0};  // r^T z, r^T r
   const int64_t n2 = ndof / 2;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -1184,7 +1198,7 @@ __global__ void __launch_bounds__(256, 2) cg_update_fused_kernel(int ndof, const
     return;
   }
   double beta;
-  if (!cg_fused_step(v, st, rz_old, iter_old, beta)) return;
+  if (!cg_fused_step(v, st, rz_old, iter_old, alpha, pqv, beta)) return;
 #pragma unroll
   for (int k = 0; k < FUSED_ITEMS; ++k) {
     const int64_t i = i0 + k * stride;

@@ -84,6 +84,9 @@ struct CgState {
                     //     no further replacements / restarts
   int pfix;         // 1 = r was replaced after the fused update formed p: re-form p
   unsigned int arrive;  // fused update: CTAs arrived (monotonic, +grid per launch)
+  int defer_alpha;  // 1 = the SpMV leaves its p^T q partials (partial + PQ_OFF) and the fused
+                    //     update forms p^T q and alpha in every CTA (no last-CTA tail)
+  int npq;          // number of those partials (the SpMV grid)
 };
 
 // error flags written by device kernels (atomicMin on the offending index)
@@ -213,6 +216,9 @@ void launch_spmv_pull(cudaStream_t s, const CUtensorMap* tmap, int n_nodes, int 
 // product for the block's own row node and, with its neighbour half, a column-pair product of
 // K^T for its column node: the same loads and FMA chains serve both (branch-free consumers).
 constexpr int PULL_BLOCK = 38;
+// offset of the SpMV's p^T q partials inside a design's partial buffer (16 cg_grid() doubles)
+// when the fused update forms alpha (CgState::defer_alpha); SpMV grids stay below it
+constexpr int PQ_OFF = 4096;
 // sub-block 3B + A -> slot (nibble), and the pad word sits before slot PULL_SUB_GAP: the
 // pair searched with tools/pull_perm_anneal.c together with the consumer lane table
 constexpr unsigned long long PULL_SUB_POS = 0x830741652ull;
