@@ -99,3 +99,21 @@ def test_fused_batched_designs(sso, reliable, precond):
         assert np.linalg.norm(out[True][b] - out[False][b]) <= 1e-9 * np.linalg.norm(out[False][b])
     uref, _, _ = OG.evaluate(designs[2])
     assert np.linalg.norm(out[True][2] - uref) <= 1e-9 * np.linalg.norm(uref)
+
+
+@pytest.mark.parametrize("precond", [0, 1])
+def test_fused_reductions_deterministic(sso, precond):
+    """The fused update's all-CTA all-reduce and the SpMV partials summed in every CTA give
+    bit-identical iterates: a 200 x 200 shell (242 406 DOF, the full co-resident grid) solved
+    twice on one handle and once on a fresh handle returns the same u and iteration count."""
+    P = W.shell_config3(200, cfg=3)
+    m = sso.Model(P, rtol=1e-8, precond=precond)
+    m.assemble()
+    u1, i1 = m.solve(P["f"])
+    u2, i2 = m.solve(P["f"])
+    m3 = sso.Model(P, rtol=1e-8, precond=precond)
+    m3.assemble()
+    u3, i3 = m3.solve(P["f"])
+    assert i1["status"] == 0 and i1["iters"] == i2["iters"] == i3["iters"]
+    assert np.array_equal(u1, u2) and np.array_equal(u1, u3)
+    assert i1["true_rel_res"] < 1e-7
