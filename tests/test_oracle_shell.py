@@ -7,7 +7,8 @@ What fixes the element without any implementation to compare against:
   * invariance under cyclic relabelling and reversal of the nodes (SPEC.md:174);
   * K(2E) = 2 K(E) bit-exact (SPEC.md:175);
   * membrane and bending patch tests on a distorted patch;
-  * Navier series for a simply supported square plate (Kirchhoff and Mindlin);
+  * Navier series for a simply supported square plate (Kirchhoff and Mindlin),
+    thin (t/a = 0.01) and thick (t/a = 0.1, 0.2: pins the transverse shear);
   * complex-step t dK/dt equals the closed form K_m + 3 K_b + K_s + K_d.
 """
 import math
@@ -154,9 +155,9 @@ def _navier_series(q, a, D, ks_G_t=None, terms=101):
     return s * a ** 4
 
 
-@pytest.mark.slow
-def test_navier_plate():
-    n, a, t, Ep, nu, q = 32, 1.0, 0.01, 1e9, 0.3, 1.0
+def _navier_center(n, a, t, Ep, nu, q):
+    """Centre deflection of the oracle's hard simply supported square plate
+    (w = 0 on every edge, tangential rotation fixed, u = v = 0)."""
     x, y = W.grid_nodes(n, a)
     conn = W.grid_quads(n)
     nq = len(conn)
@@ -174,10 +175,39 @@ def test_navier_plate():
     P = W._problem("navier", x, y, np.zeros_like(x), quad_conn=conn, t=np.full(nq, t),
                    E=np.full(nq, Ep), nu=np.full(nq, nu), sup_node=sn, sup_mask=sm, f=f)
     u, _, _ = Gd.evaluate(P)
+    return -u[6 * ((n // 2) * (n + 1) + n // 2) + 2]
+
+
+@pytest.mark.slow
+def test_navier_plate():
+    n, a, t, Ep, nu, q = 32, 1.0, 0.01, 1e9, 0.3, 1.0
+    wc = _navier_center(n, a, t, Ep, nu, q)
     D = Ep * t ** 3 / (12 * (1 - nu ** 2))
-    wc = -u[6 * ((n // 2) * (n + 1) + n // 2) + 2]
     wk = _navier_series(q, a, D)
     assert wk / (q * a ** 4 / D) == pytest.approx(0.0040624, rel=1e-4)
     wm = _navier_series(q, a, D, ks_G_t=5 / 6 * Ep / (2 * (1 + nu)) * t)
     assert abs(wc / wk - 1) < 0.01
     assert abs(wc / wm - 1) < 0.005
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("t", [0.1, 0.2])
+def test_navier_thick_plate_shear(t):
+    """Thick-plate pin of the MITC-4 transverse shear (§2.2.1, SURVEY
+    §8(c) C2(f), C10): at t/a = 0.1 and 0.2 the Mindlin shear term is 2-8 % of the
+    centre deflection (at t/a = 0.01 it is 5e-4), so k_s, G = E/(2(1+nu)) and the
+    J^-1 mapping of the tied covariant strains are all visible.  The hard simply
+    supported Mindlin plate has the closed-form Navier series with modal factor
+    (1 + D k^2 / (k_s G t)), k^2 = (m pi/a)^2 + (n pi/a)^2; the 32x32 oracle mesh must
+    be within 0.3 % of it, while the same series with k_s = 1 (a plausible wrong
+    shear factor) must be further than 0.5 % away (the pin discriminates)."""
+    n, a, Ep, nu, q = 32, 1.0, 1e9, 0.3, 1.0
+    wc = _navier_center(n, a, t, Ep, nu, q)
+    D = Ep * t ** 3 / (12 * (1 - nu ** 2))
+    G = Ep / (2 * (1 + nu))
+    wm = _navier_series(q, a, D, ks_G_t=5 / 6 * G * t)
+    wk = _navier_series(q, a, D)
+    w_ks1 = _navier_series(q, a, D, ks_G_t=1.0 * G * t)
+    assert wm / wk - 1 > 0.02                   # the shear term is large here
+    assert abs(wc / wm - 1) < 0.003, wc / wm
+    assert abs(wm / w_ks1 - 1) > 0.005          # k_s = 1 would fail the 0.3 % bar
