@@ -211,3 +211,36 @@ def test_navier_thick_plate_shear(t):
     assert wm / wk - 1 > 0.02                   # the shear term is large here
     assert abs(wc / wm - 1) < 0.003, wc / wm
     assert abs(wm / w_ks1 - 1) > 0.005          # k_s = 1 would fail the 0.3 % bar
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_constant_transverse_shear_energy(seed):
+    """Closed-form energy of a constant transverse-shear state on a distorted flat
+    quad: with w = c1 x + c2 y and constant rotations
+    (th_x, th_y) = (a, b) there is no membrane strain, no curvature and no drilling
+    strain, and MITC-4's tied covariant strains reproduce the constant Cartesian
+    shear (gamma_xz, gamma_yz) = (c1 + b, c2 - a) exactly on any bilinear quad
+    (gamma_xi = gamma . x_xi is linear in eta along xi-lines, and J^-1 J = I).
+    So 1/2 u^T K u = 1/2 k_s G t A (gamma_xz^2 + gamma_yz^2) to rounding.  This
+    fixes k_s, G, the shear sign convention beta = (th_y, -th_x) and the J^-1
+    mapping on non-rectangular elements (a transposed J^-1 fails it)."""
+    rng = np.random.default_rng(100 + seed)
+    base = np.array([[0, 0], [1, 0], [1, 1], [0, 1]], float)
+    P2 = base + rng.uniform(-0.25, 0.25, size=(4, 2))
+    th = rng.uniform(0, 2 * math.pi)
+    Rz = np.array([[math.cos(th), -math.sin(th)], [math.sin(th), math.cos(th)]])
+    P2 = P2 @ Rz.T * rng.uniform(0.01, 3.0) + rng.normal(size=2)
+    X = np.column_stack([P2, np.zeros(4)])
+    t = rng.uniform(0.05, 0.3)
+    c1, c2, a, b = rng.normal(size=4)
+    u = np.zeros(24)
+    for i in range(4):
+        u[6 * i + 2] = c1 * X[i, 0] + c2 * X[i, 1]
+        u[6 * i + 3] = a
+        u[6 * i + 4] = b
+    K = shell.shell_K(X, t, E, NU)
+    x, y = X[:, 0], X[:, 1]
+    area = 0.5 * abs((x[2] - x[0]) * (y[3] - y[1]) - (x[3] - x[1]) * (y[2] - y[0]))
+    G = E / (2 * (1 + NU))
+    ref = 0.5 * (5 / 6) * G * t * area * ((c1 + b) ** 2 + (c2 - a) ** 2)
+    assert 0.5 * u @ K @ u == pytest.approx(ref, rel=1e-11)
