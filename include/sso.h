@@ -136,25 +136,21 @@ typedef struct {
    * matrices) when the mesh is quad-only with node degree <= 10; 1 = always the staged
    * path (element kernel, then the segmented-sum gather). */
   int32_t assembly;
-  /* 0 (default) = storage 3.  1 = full CSR storage.  2 = single-strip handles keep only the
-   * upper node blocks (n, m >= n) of the symmetric K_bc (44 % fewer value bytes on
-   * shell grids); pass 1 of the SpMV forms the upper row sums, the transpose
-   * contributions (sender-ordered slots) and p^T K p, the x / r update adds each
-   * node's incoming slots in ascending source order.  3 = upper node blocks, each one
-   * contiguous 38-double record (36 values as nine 2x2 sub-blocks + 2 zero pads), and a ONE-pass
-   * "pull" SpMV: the CTA that owns a chunk of row nodes streams their upper runs (one
-   * bulk copy) and the stored blocks (n, m) of their lower neighbours n < m (one TMA
-   * gather4 per node; an L2 hit: chunks are dealt round-robin, so the owner streams them
-   * in the same window) and forms y_m = sum_{j>=m} K_mj x_j + sum_{n<m} K_nm^T x_n; no
-   * transpose buffer.  Storage
-   * 3 also applies to strips (owned nodes precede halo nodes locally, so lower
-   * neighbours are owned); storage 2 is single-strip only (else full storage).
-   * Exports return the full CSR.  Other values -> SSO_E_INVALID. */
+  /* 0 (default) = storage 3.  1 = full CSR storage (row-major runs of 36 deg values per node).
+   * 3 = upper node blocks (n, m >= n) of the symmetric K_bc only (44 % fewer value bytes on
+   * shell grids), each one contiguous 38-double record (36 values as nine 2x2 sub-blocks + 2
+   * zero pads), and a ONE-pass "pull" SpMV: the CTA that owns a chunk of row nodes streams
+   * their upper runs (one bulk copy) and the stored blocks (n, m) of their lower neighbours
+   * n < m (one TMA gather4 per node; an L2 hit: chunks are dealt round-robin, so the owner
+   * streams them in the same window) and forms
+   * y_m = sum_{j>=m} K_mj x_j + sum_{n<m} K_nm^T x_n.  Storage 3 also applies to strips
+   * (owned nodes precede halo nodes locally, so lower neighbours are owned).  Exports return
+   * the full CSR.  Other values (including the retired 2) -> SSO_E_INVALID. */
   int32_t storage;
   /* Preconditioner of the CG (reading c10 / c19): 0 (default) = point Jacobi, M =
    * diag(K_bc) (the north star's); 1 = node-block Jacobi, M = blockdiag(K_nn) of the 6x6
    * diagonal block of every node (inverted once per sso_assemble; about 30 % fewer
-   * iterations on shells).  precond 1 with storage 2 -> SSO_E_INVALID. */
+   * iterations on shells). */
   int32_t precond;
 } sso_options;
 
@@ -164,6 +160,22 @@ typedef struct {
   double true_rel_res;    /* |f_bc - K_bc u| / |f_bc| recomputed at exit               */
   double ms;              /* device time of the solve (CUDA events)                    */
   int32_t status;         /* sso_status of this solve                                  */
+  /* Certification (Eq. 1 solved by CG).  CG from
+   * x0 = 0 is the Lanczos process on M^-1 K: its coefficients form the tridiagonal
+   * T[k][k] = 1/alpha_k + beta_{k-1}/alpha_{k-1}, T[k][k+1] = sqrt(beta_k)/alpha_k, whose
+   * extreme eigenvalues (Ritz values; formed on the device by Sturm multisection) lie
+   * inside the spectrum of M^-1 K.  lanczos_iters = coefficients used (the first CG
+   * segment, at most 2^18; a restart starts a new sequence).  With r = f_bc - K u the
+   * TRUE residual, rz = r^T M^-1 r, C = f_bc^T u = |u|_K^2 and m_min <= lambda_min(M)
+   * (min 1/dinv, or min over nodes of 1/|(K_nn)^-1|_F for precond 1):
+   *   err_energy_est = sqrt(rz / (lanczos_lmin C))                    >= |e|_K / |u|_K
+   *   err2_est       = sqrt(rz) / (lanczos_lmin sqrt(m_min)) / |u|_2   >= |e|_2 / |u|_2
+   * where ">=" holds with the exact lambda_min(M^-1 K) in place of lanczos_lmin (which is
+   * an upper estimate of it: the figures are estimates, exact once CG has resolved the
+   * smallest eigenvalue).  NaN when undefined (no iterations, C <= 0). */
+  int32_t lanczos_iters;
+  double lanczos_lmin, lanczos_lmax;
+  double err_energy_est, err2_est;
 } sso_solve_info;
 
 /* Fill *o with the defaults listed above.  Always SSO_OK. */
@@ -307,9 +319,8 @@ int sso_export_ke(sso_handle h, int64_t first, int64_t count, double* ke);
 int sso_export_dinv(sso_handle h, double* dinv);
 
 /* Device storage of the assembled matrix: stored values / node blocks (owned rows) and
- * the layout in use: *symmetric = 0 full storage, 2 upper blocks with the two-pass
- * transpose SpMV, 3 upper blocks (38-double records of 2x2 sub-blocks) with the one-pass pull
- * SpMV.  stored_values counts the 36 values per block (not the record pads). */
+ * the layout in use: *symmetric = 0 full storage, 3 upper blocks (38-double records of 2x2
+ * sub-blocks) with the one-pass pull SpMV.  stored_values counts the 36 values per block (not the record pads). */
 int sso_storage_info(sso_handle h, int64_t* stored_values, int64_t* stored_blocks, int32_t* symmetric);
 
 /* Partition of this handle: number of strips held, first owned global node, owned

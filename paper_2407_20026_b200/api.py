@@ -68,11 +68,15 @@ class sso_options(C.Structure):
 
 class sso_solve_info(C.Structure):
     _fields_ = [("iters", C.c_int64), ("rel_res", C.c_double), ("true_rel_res", C.c_double),
-                ("ms", C.c_double), ("status", C.c_int32)]
+                ("ms", C.c_double), ("status", C.c_int32), ("lanczos_iters", C.c_int32),
+                ("lanczos_lmin", C.c_double), ("lanczos_lmax", C.c_double),
+                ("err_energy_est", C.c_double), ("err2_est", C.c_double)]
 
     def as_dict(self):
         return dict(iters=self.iters, rel_res=self.rel_res, true_rel_res=self.true_rel_res,
-                    ms=self.ms, status=self.status)
+                    ms=self.ms, status=self.status, lanczos_iters=self.lanczos_iters,
+                    lanczos_lmin=self.lanczos_lmin, lanczos_lmax=self.lanczos_lmax,
+                    err_energy_est=self.err_energy_est, err2_est=self.err2_est)
 
 
 _H = C.c_void_p
@@ -127,13 +131,37 @@ class SSOError(RuntimeError):
         self.code = code
 
 
-def _ptr(a, dtype):
+_TORCH_DT = {np.dtype(np.float64): "torch.float64", np.dtype(np.int32): "torch.int32",
+             np.dtype(np.uint8): "torch.uint8"}
+
+
+def _ptr(a, dtype, n=None, device=None):
+    """Pointer of a numpy array or torch tensor after checking what the C ABI relies on:
+    dtype, C-contiguity, at least n elements and (tensors) the handle's device.  Raises
+    ValueError instead of letting the library read or write out of bounds."""
     if a is None:
         return None
+    dtype = np.dtype(dtype)
     if isinstance(a, np.ndarray):
-        assert a.dtype == dtype and a.flags["C_CONTIGUOUS"], (a.dtype, dtype)
+        if a.dtype != dtype or not a.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"expected a C-contiguous {dtype} array, got {a.dtype} "
+                             f"(contiguous={a.flags['C_CONTIGUOUS']})")
+        if n is not None and a.size < n:
+            raise ValueError(f"array has {a.size} elements, the call needs {n}")
         return a.ctypes.data
-    # torch tensor
+    if not hasattr(a, "data_ptr"):
+        raise ValueError(f"expected a numpy array or torch tensor, got {type(a).__name__}")
+    if str(a.dtype) != _TORCH_DT[dtype]:
+        raise ValueError(f"expected a {_TORCH_DT[dtype]} tensor, got {a.dtype}")
+    if not a.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    if n is not None and a.numel() < n:
+        raise ValueError(f"tensor has {a.numel()} elements, the call needs {n}")
+    if a.is_cuda and device is not None and a.device.index != device:
+        raise ValueError(f"tensor on cuda:{a.device.index}, the handle lives on cuda:{device}")
+    if not a.is_cuda:
+        # a CPU tensor is host memory: only valid in host mode (checked by _mode)
+        pass
     return a.data_ptr()
 
 
@@ -210,6 +238,8 @@ class Model:
         self.batch = batch
         self._mem = MEM_HOST
         self._stream = stream
+        self._dev_opt = device
+        self._device_idx = None
 
     # -- plumbing ----------------------------------------------------------
     def _check(self, rc):
@@ -218,16 +248,35 @@ class Model:
         return rc
 
     def _mode(self, *arrays):
-        dev = any(_is_device(a) for a in arrays if a is not None)
+        """Pointer kind of this call's buffers: all device (torch CUDA tensors) or all host.
+        Device mode orders the library after torch's current stream: a side stream is handed
+        over as the handle's stream; torch's default (legacy) stream is passed as NULL, which
+        makes every entry point wait for the work queued on it and it for the library's
+        (include/sso.h sso_set_stream)."""
+        given = [a for a in arrays if a is not None]
+        devs = [_is_device(a) for a in given]
+        if any(devs) and not all(devs):
+            raise ValueError("mixed host and device buffers in one call")
+        dev = bool(devs) and all(devs)
         mem = MEM_DEVICE if dev else MEM_HOST
         stream = None
         if dev:
             import torch
-            stream = torch.cuda.current_stream().cuda_stream
-        if mem != self._mem or (dev and stream != self._stream):
+            want = self._device_index()
+            for a in given:
+                if a.device.index != want:
+                    raise ValueError(f"tensor on cuda:{a.device.index}, the handle lives on cuda:{want}")
+            stream = torch.cuda.current_stream(want).cuda_stream or None
+        if mem != self._mem or (dev and stream != self._stream) or (dev and stream is None):
             self._check(_lib.sso_set_stream(self.h, stream, mem))
             self._mem, self._stream = mem, (stream if dev else self._stream)
         return dev
+
+    def _device_index(self):
+        if self._device_idx is None:
+            import torch
+            self._device_idx = self._dev_opt if self._dev_opt >= 0 else torch.cuda.current_device()
+        return self._device_idx
 
     def close(self):
         if getattr(self, "h", None):
@@ -255,7 +304,8 @@ class Model:
         dev = self._mode(x, y, z, t)
         conv = (lambda a: a) if dev else (lambda a: _np(a, np.float64))
         arrs = [None if a is None else conv(a) for a in (x, y, z, t)]
-        self._check(_lib.sso_set_design(self.h, *[_ptr(a, np.float64) for a in arrs]))
+        ns = [self.batch * self.g_nodes] * 3 + [self.batch * self.g_quads]
+        self._check(_lib.sso_set_design(self.h, *[_ptr(a, np.float64, n) for a, n in zip(arrs, ns)]))
 
     def assemble(self):
         self._check(_lib.sso_assemble(self.h))
@@ -273,7 +323,8 @@ class Model:
             import torch
             u = torch.zeros(shape, dtype=torch.float64, device=f.device)
         infos = (sso_solve_info * self.batch)()
-        rc = _lib.sso_solve(self.h, _ptr(f, np.float64), _ptr(u, np.float64), infos)
+        nv = self.batch * self.ndof
+        rc = _lib.sso_solve(self.h, _ptr(f, np.float64, nv), _ptr(u, np.float64, nv), infos)
         if raise_on_error:
             self._check(rc)
         if self.batch > 1:
@@ -301,14 +352,16 @@ class Model:
                 Cv, dX, dT = np.zeros(B), np.zeros(B * 3 * self.n_nodes), np.zeros(B * max(self.n_quads, 1))
         else:
             Cv, dX, dT = out
+        nX, nT = B * 3 * self.n_nodes, B * self.n_quads
         if f is None:
-            rc = _lib.sso_grad(self.h, objective, _ptr(Cv, np.float64), _ptr(dX, np.float64),
-                               _ptr(dT, np.float64))
+            rc = _lib.sso_grad(self.h, objective, _ptr(Cv, np.float64, B), _ptr(dX, np.float64, nX),
+                               _ptr(dT, np.float64, nT))
         else:
             if not dev:
                 f, u = _np(f, np.float64), _np(u, np.float64)
-            rc = _lib.sso_grad_at(self.h, objective, _ptr(f, np.float64), _ptr(u, np.float64),
-                                  _ptr(Cv, np.float64), _ptr(dX, np.float64), _ptr(dT, np.float64))
+            nv = B * self.ndof
+            rc = _lib.sso_grad_at(self.h, objective, _ptr(f, np.float64, nv), _ptr(u, np.float64, nv),
+                                  _ptr(Cv, np.float64, B), _ptr(dX, np.float64, nX), _ptr(dT, np.float64, nT))
         self._check(rc)
         if out is not None:
             return out
@@ -425,7 +478,8 @@ class Model:
         else:
             x = _np(x, np.float64)
             y = np.empty_like(x)
-        self._check(_lib.sso_spmv(self.h, _ptr(x, np.float64), _ptr(y, np.float64)))
+        nv = self.batch * self.ndof
+        self._check(_lib.sso_spmv(self.h, _ptr(x, np.float64, nv), _ptr(y, np.float64, nv)))
         return y
 
     def export_csr(self, values=True):

@@ -8,7 +8,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsso.so")
 SOURCES = ["api.cu", "elements.cu", "assemble.cu", "assemble_fused.cu", "pcg.cu", "grad.cu",
-           "filter.cu", "loads.cu", "block_jacobi.cu", "pattern.cpp"]
+           "filter.cu", "loads.cu", "block_jacobi.cu", "lanczos.cu", "pattern.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -37,27 +37,33 @@ def nvcc():
 
 def build(verbose=False, force=False):
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    hdrs = [os.path.join(CSRC, "sso_internal.h"), os.path.join(CSRC, "shell_math.cuh"), os.path.join(CSRC, "cg_fused.cuh"),
-            os.path.join(ROOT, "include", "sso.h")]
+    import glob
+    hdrs = sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))) + [
+        os.path.join(ROOT, "include", "sso.h")]
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(p) < t for p in srcs + hdrs):
             return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    log = []
-    for s in srcs:
-        o = os.path.join(objdir, os.path.basename(s) + ".o")
+    def compile_one(src):
+        o = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [nvcc(), *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-               "-I", nccl_include(), "-c", s, "-o", o]
-        if s.endswith(".cpp"):
+               "-I", nccl_include(), "-c", src, "-o", o]
+        if src.endswith(".cpp"):
             cmd[1:1] = ["-x", "cu"]
         r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, o, r
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, srcs))
+    objs, log = [], []
+    for src, o, r in results:
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed on {s}")
+            raise RuntimeError(f"nvcc failed on {src}")
         objs.append(o)
     cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)

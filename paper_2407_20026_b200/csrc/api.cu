@@ -131,8 +131,8 @@ struct Part {
   std::vector<char> g_derived;          // G = E / (2 (1 + nu)) when G was not given
   // partition maps
   int32_t* block_rank = nullptr;      // quads [n_quads][16] (fused assembly; upper ranks when sym)
-  bool sym = false;                   // upper-block (symmetric) storage, single-strip handles
-  bool pull = false;                  // sym with the one-pass pull SpMV (storage 3, 2x2 sub-block records)
+  bool sym = false;                   // upper-block (symmetric) storage = pull (kept as one name)
+  bool pull = false;                  // upper blocks with the one-pass pull SpMV (storage 3, 2x2 sub-block records)
   int32_t* lpull = nullptr;           // pull: (source node, upper block) per incoming block
   int32_t* pdesc = nullptr;           // pull: 16-int per-node descriptors (build_pull_desc)
   double* binv = nullptr;             // precond 1: [B][21][n_own] packed (K_nn)^-1
@@ -140,11 +140,15 @@ struct Part {
   bool cgf = false;                   // fused x / r / p update (cg_update_fused / _block_fused): one
                                       // part, full or pull storage, B <= the co-resident grid
   double* p2 = nullptr;               // cgf: the second p buffer (ping-pong)
+  // Lanczos certification (lanczos.cu): CG coefficient history [B][lz_cap][2], the
+  // tridiagonal scratch of the same size, the M scale per design (device bits, host value)
+  double *lz_hist = nullptr, *lz_T = nullptr;
+  int lz_cap = 0;
+  unsigned long long* mscale_d = nullptr;
+  std::vector<double> mscale_h;
   CUtensorMap pull_tmap;              // pull: [B n_ublocks][36] view of vals for the gather4 TMA
   UpperPattern up;
-  int64_t* lptr = nullptr;            // sym: incoming transpose slots per node
-  int32_t* lslot = nullptr;
-  double* tbuf = nullptr;             // sym: transpose contributions [B][6 n_tslots]
+  int64_t* lptr = nullptr;            // pull: incoming blocks per node
   int64_t stored_blocks = 0;          // node blocks kept on the device for the owned rows
   int max_inc = 0, max_deg = 0;       // over owned nodes
   bool fused = false;                 // element + assembly in one pass (quad-only meshes)
@@ -161,6 +165,10 @@ struct sso_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaStream_t cap_stream = nullptr;
+  // the caller works on the legacy default stream (sso_set_stream(h, NULL, SSO_MEM_DEVICE)):
+  // every entry point orders the handle's stream after it and it after the handle's work
+  bool order_legacy = false;
+  cudaEvent_t ev_order[2] = {nullptr, nullptr};
   sso_mem mem = SSO_MEM_HOST;
   double rtol = 1e-10;
   int64_t max_iter = 200000;
@@ -173,7 +181,7 @@ struct sso_ctx {
   int batch = 1;  // designs per handle
   int reliable = 1;  // 0 plain CG, 1 final true-residual restart, 2 + periodic replacement
   int assembly = 0;  // 0 auto (fused when the mesh allows), 1 staged
-  int storage = 0;   // 0 / 1 full CSR storage, 2 symmetric upper blocks (single-strip handles)
+  int storage = 0;   // 1 full CSR storage, 3 upper blocks + pull SpMV (0 = 3)
   int precond = 0;   // 0 point Jacobi, 1 node-block Jacobi (block_jacobi.cu)
   bool area_load = false;  // design-dependent area loads active (sso_set_area_load)
   bool skip_load = false;  // adjoint solves: the right-hand side is dg/du only, b = 0
@@ -344,6 +352,33 @@ int sync(sso_ctx* h) {
   return SSO_OK;
 }
 
+// Every ABI entry point taking a handle: make the handle's device current (restored on
+// return) and, when the caller's device buffers are ordered by the legacy default stream,
+// order the handle's stream after the work already queued there and that stream after
+// the handle's work.
+struct Entry {
+  sso_ctx* h;
+  int prev = -1;
+  explicit Entry(sso_ctx* h_) : h(h_) {
+    if (!h) return;
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != h->device && cudaSetDevice(h->device) == cudaSuccess) prev = cur;
+    if (h->order_legacy && h->mem == SSO_MEM_DEVICE && h->ev_order[0]) {
+      cudaEventRecord(h->ev_order[0], cudaStreamLegacy);
+      cudaStreamWaitEvent(h->stream, h->ev_order[0], 0);
+    }
+  }
+  ~Entry() {
+    if (!h) return;
+    if (h->order_legacy && h->mem == SSO_MEM_DEVICE && h->ev_order[1]) {
+      cudaEventRecord(h->ev_order[1], h->stream);
+      cudaStreamWaitEvent(cudaStreamLegacy, h->ev_order[1], 0);
+    }
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+#define ENTER(h) Entry entry_guard_(h)
+
 // ---------------------------------------------------------------------------
 // Transports: halo exchange of a per-part vector and allreduce of CgState::red.
 // ---------------------------------------------------------------------------
@@ -358,18 +393,13 @@ double* vec_of(Part& P, int v) {
   }
 }
 
-// y = K x for the part's owned rows (full or symmetric storage); with st also
-// p^T q and alpha (CG) -- for symmetric storage the CG form leaves y = the upper
-// row sums and the receiver sums to cg_update (launch_cg_update_sym).  x must have
-// its halo filled (partitioned handles).
+// y = K x for the part's owned rows (full or upper-block storage); with st also
+// p^T q (and alpha, unless the fused update forms it).  x must have its halo filled
+// (partitioned handles).
 void spmv_apply(cudaStream_t s, Part& P, const double* x, double* y, CgState* st) {
   if (P.pull)
     launch_spmv_pull(s, &P.pull_tmap, P.n_own, (int)(P.bs.nnz / PULL_BLOCK), P.pdesc, P.node_col, P.lpull, P.vals, x, y,
                      st ? P.partial : nullptr, st, P.bs);
-  else if (P.sym && st)
-    launch_spmv_sym_cg(s, P.n_own, P.node_ptr, P.node_col, P.vals, x, y, P.tbuf, P.partial, st, P.bs);
-  else if (P.sym)
-    launch_spmv_sym(s, P.n_own, P.node_ptr, P.node_col, P.vals, x, y, P.tbuf, P.lptr, P.lslot, P.bs);
   else if (st)
     launch_spmv_dot(s, P.n_own, P.node_ptr, P.node_col, P.vals, x, y, P.partial, st, P.bs);
   else
@@ -514,9 +544,6 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev, int it) {
     if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
     if (P.binv)
       launch_cg_update_block(s, P.n_own, P.binv, P.xs, P.r, P.p, P.q, P.zb, P.partial, P.st, P.bs);
-    else if (P.sym && !P.pull)
-      launch_cg_update_sym(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.tbuf, P.lptr, P.lslot, P.partial,
-                           P.st, P.bs);
     else
       launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st, P.bs);
     return SSO_OK;
@@ -602,9 +629,9 @@ void free_part(Part& P) {
                   P.inc_slot, P.stage, P.vals, P.dinv, P.f, P.fbc, P.xs, P.r, P.p, P.q, P.tmp, P.gu,
                   P.gf, P.partial, P.st, P.flags, P.tickets, P.scal, P.slot_partial, P.dxyz, P.dt,
                   P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
-                  P.lptr, P.lslot, P.lpull, P.pdesc, P.binv, P.zb, P.p2, P.tbuf, P.dE,
+                  P.lptr, P.lpull, P.pdesc, P.binv, P.zb, P.p2, P.dE,
                   P.ub, P.fb, P.lam, P.dxyz2, P.dt2, P.dE2, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask,
-                  P.rho, P.E0, P.G0, P.coef};
+                  P.rho, P.E0, P.G0, P.coef, P.lz_hist, P.lz_T, P.mscale_d};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -636,6 +663,8 @@ void free_all(sso_ctx* h) {
   if (h->ev_a) cudaEventDestroy(h->ev_a);
   if (h->ev_b) cudaEventDestroy(h->ev_b);
   for (auto e : h->ev_done)
+    if (e) cudaEventDestroy(e);
+  for (auto e : h->ev_order)
     if (e) cudaEventDestroy(e);
   if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
@@ -723,10 +752,8 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   P.fused = h->assembly == 0 && P.n_beams == 0 && P.n_quads > 0 && P.max_deg <= fused_max_degree();
   // Storage 3 works on strips too: owned nodes come first in the local numbering, so every
   // lower neighbour (n < m) of an owned row m is owned and stores the block (n, m) itself, and
-  // halo neighbours are always upper.  Storage 2 (receiver slots) stays single-strip.
-  P.sym = (h->storage == 3) ||
-          (h->storage == 2 && L.n_parts == 1 && h->nranks == 1 && P.n_own == P.n_nodes);
-  P.pull = P.sym && h->storage == 3;
+  // halo neighbours are always upper.
+  P.sym = P.pull = (h->storage == 3);
   if (P.pull && P.pat.node_ptr[P.n_nodes] >= INT32_MAX / PULL_BLOCK) {  // 32-bit offsets in the pull kernel
     h->err = "storage 3: too many node blocks for 32-bit offsets";
     return SSO_E_INVALID;
@@ -744,7 +771,6 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   P.bs.quad = P.n_quads;
   P.bs.stage = 36 * P.n_staged;
   P.bs.nnz = P.pull ? PULL_BLOCK * P.up.n_ublocks() : 36 * (P.sym ? P.up.n_ublocks() : P.n_blocks);
-  P.bs.tbuf = 6 * std::max<int64_t>(P.sym && !P.pull ? P.up.n_tslots : 0, 1);
   P.bs.dof = P.ndof;
   P.bs.partial = 16 * (int64_t)cg_grid();
   P.bs.slot = 3 * std::max<int64_t>(P.n_slots, 1);
@@ -812,15 +838,10 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
     UP(contrib_ptr, P.up.ucontrib_ptr.data(), P.up.n_ublocks() + 1);
     UP(contrib, P.up.ucontrib.data(), (int64_t)P.up.ucontrib.size());
     UP(lptr, P.up.lptr.data(), P.n_nodes + 1);
-    if (P.pull) {
-      UP(lpull, P.up.lpull.data(), (int64_t)P.up.lpull.size());
-      std::vector<int32_t> desc;
-      build_pull_desc(P.up, desc);
-      UP(pdesc, desc.data(), (int64_t)desc.size());
-    } else {
-      UP(lslot, P.up.lslot.data(), (int64_t)P.up.lslot.size());
-      AL(tbuf, B * P.bs.tbuf);
-    }
+    UP(lpull, P.up.lpull.data(), (int64_t)P.up.lpull.size());
+    std::vector<int32_t> desc;
+    build_pull_desc(P.up, desc);
+    UP(pdesc, desc.data(), (int64_t)desc.size());
   } else {
     UP(node_ptr, P.pat.node_ptr.data(), P.n_nodes + 1);
     UP(node_col, P.pat.node_col.data(), P.n_blocks);
@@ -854,7 +875,7 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   {
     const char* env = getenv("SSO_CG_FUSED");
     const int fg = h->precond == 1 ? cg_block_fused_grid() : cg_fused_grid();
-    P.cgf = B <= fg && L.n_parts == 1 && h->nranks == 1 && (P.pull || !P.sym) && h->check_every % 2 == 0 &&
+    P.cgf = B <= fg && L.n_parts == 1 && h->nranks == 1 && h->check_every % 2 == 0 &&
             !(env && env[0] == '0');
   }
   if (P.cgf) {
@@ -875,6 +896,13 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   AL(dt, (int64_t)B * std::max<int32_t>(P.n_quads, 1));
   AL(dt_own, std::max<int32_t>(P.n_own_quads, 1));
   AL(dE, (int64_t)B * std::max<int64_t>(ne, 1));
+  // Lanczos history: the first CG segment of up to 2^18 iterations per design (2^22 / B for
+  // batches); longer solves keep the leading 2^18 coefficients (still interlacing Ritz values)
+  P.lz_cap = (int)std::min<int64_t>(h->max_iter, B == 1 ? (1 << 18) : std::max(1024, (1 << 22) / B));
+  AL(lz_hist, 2 * (int64_t)B * P.lz_cap);
+  AL(lz_T, 2 * (int64_t)B * P.lz_cap);
+  AL(mscale_d, B);
+  P.mscale_h.assign((size_t)B, 0.0);
   P.h_nu = nu;
   P.g_derived.assign((size_t)ne, mat->G ? 0 : 1);
 #undef UP
@@ -890,8 +918,6 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   P.pat.contrib.shrink_to_fit();
   P.up.ucontrib.clear();
   P.up.ucontrib.shrink_to_fit();
-  P.up.lslot.clear();
-  P.up.lslot.shrink_to_fit();
   P.up.lpull.clear();
   P.up.lpull.shrink_to_fit();
   P.pat.inc_slot.clear();
@@ -940,6 +966,57 @@ int design_in(sso_ctx* h, const double* src, int64_t n_global, double* Part::*ds
     CK(h, cudaMemcpy(P.*dst, loc.data(), loc.size() * sizeof(double), cudaMemcpyHostToDevice));
   }
   return SSO_OK;
+}
+
+// Per-design scale of the preconditioner for the 2-norm error estimate (lanczos.cu
+// mscale_kernel): min over parts / ranks, kept on the host after every assembly.
+int mscale_update(sso_ctx* h) {
+  const int B = h->batch;
+  std::vector<double> m((size_t)B, 0.0);
+  bool first = true;
+  for (auto& pp : h->parts) {
+    Part& P = *pp;
+    CK(h, cudaMemsetAsync(P.mscale_d, 0xff, B * sizeof(unsigned long long), h->stream));
+    {
+      long long g0 = g_launches;
+      launch_mscale(h->stream, P.n_own, P.dinv, P.binv, P.mscale_d, P.bs);
+      h->launches += g_launches - g0;
+    }
+    if (h->nranks > 1)  // positive doubles order like their bit patterns: min of the bits
+      CKN(h, nccl().AllReduce(P.mscale_d, P.mscale_d, B, ncclUint64, ncclMin, h->comm, h->stream));
+    std::vector<unsigned long long> bits((size_t)B);
+    CK(h, cudaMemcpyAsync(bits.data(), P.mscale_d, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          h->stream));
+    int rc = sync(h);
+    if (rc) return rc;
+    for (int bd = 0; bd < B; ++bd) {
+      double v;
+      std::memcpy(&v, &bits[bd], sizeof v);
+      if (bits[bd] == ~0ull) v = 0.0;
+      m[bd] = first ? v : std::min(m[bd], v);
+    }
+    first = false;
+  }
+  for (auto& pp : h->parts) pp->mscale_h = m;
+  return SSO_OK;
+}
+
+// Error estimates of a finished solve (include/sso.h sso_solve_info): with lambda_min the
+// smallest Ritz value of M^-1 K (an upper estimate of the true one), r the true residual,
+// rz = r^T M^-1 r, and C = f_bc^T x = |x|_K^2 (CG from x0 = 0):
+//   |e|_K / |x|_K <= sqrt(rz / (lambda_min C))                    (energy norm)
+//   |e|_2 / |x|_2 <= sqrt(rz) / (lambda_min sqrt(m_min)) / |x|_2   (m_min <= lambda_min(M))
+void fill_cert(sso_ctx* h, int bd, const CgState& S, sso_solve_info& info) {
+  const double nanv = std::nan("");
+  info.lanczos_lmin = S.lz_min;
+  info.lanczos_lmax = S.lz_max;
+  info.lanczos_iters = S.lz_n;
+  const double lmin = S.lz_min, rz = S.red[1], fx = S.red[2], xx = S.red[3];
+  const double mmin = h->P0().mscale_h[bd];
+  info.err_energy_est = (lmin > 0.0 && fx > 0.0 && rz >= 0.0) ? std::sqrt(rz / (lmin * fx)) : nanv;
+  info.err2_est = (lmin > 0.0 && mmin > 0.0 && xx > 0.0 && rz >= 0.0)
+                      ? std::sqrt(rz) / (lmin * std::sqrt(mmin)) / std::sqrt(xx)
+                      : nanv;
 }
 
 }  // namespace
@@ -1018,12 +1095,12 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
     g_create_err = "options: batch >= 1, and batch > 1 needs n_parts == nranks == 1";
     return SSO_E_INVALID;
   }
-  if (o.precond < 0 || o.precond > 1 || (o.precond == 1 && o.storage == 2)) {
-    g_create_err = "options: precond must be 0 or 1 (1 needs storage 0, 1 or 3)";
+  if (o.precond < 0 || o.precond > 1) {
+    g_create_err = "options: precond must be 0 or 1";
     return SSO_E_INVALID;
   }
-  if (o.storage < 0 || o.storage > 3) {
-    g_create_err = "options: storage must be 0, 1, 2 or 3";
+  if (o.storage < 0 || o.storage > 3 || o.storage == 2) {
+    g_create_err = "options: storage must be 0, 1 or 3";
     return SSO_E_INVALID;
   }
   if (o.nranks > 1 && !o.nccl_unique_id) {
@@ -1118,22 +1195,32 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
   cudaEventCreate(&h->ev_b);
   cudaEventCreateWithFlags(&h->ev_done[0], cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->ev_done[1], cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&h->ev_order[0], cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&h->ev_order[1], cudaEventDisableTiming);
   *out = h;
   return SSO_OK;
 }
 
 int sso_set_stream(sso_handle h, void* cuda_stream, sso_mem mem) {
   if (!h) return SSO_E_INVALID;
+  ENTER(h);
   if (cuda_stream) {
-    if (h->own_stream) cudaStreamDestroy(h->stream);
+    if (h->own_stream) {
+      cudaStreamSynchronize(h->stream);
+      cudaStreamDestroy(h->stream);
+    }
     h->own_stream = false;
     h->stream = (cudaStream_t)cuda_stream;
+    h->order_legacy = false;
+  } else {
+    h->order_legacy = (mem == SSO_MEM_DEVICE);
   }
   h->mem = mem;
   return SSO_OK;
 }
 
 int sso_set_design(sso_handle h, const double* x, const double* y, const double* z, const double* t) {
+  ENTER(h);
   if (!h) return SSO_E_INVALID;
   int rc;
   if (x && (rc = design_in(h, x, h->g_nodes, &Part::x, false))) return rc;
@@ -1178,6 +1265,7 @@ static int assemble_pass(sso_ctx* h, bool unconstrained) {
 }
 
 int sso_assemble(sso_handle h) {
+  ENTER(h);
   if (!h) return SSO_E_INVALID;
   int rc = reset_flags(h);
   if (rc) return rc;
@@ -1196,13 +1284,14 @@ int sso_assemble(sso_handle h) {
     for (auto& pp : h->parts) {
       Part& P = *pp;
       Scope sc(h, F_ASSEMBLE);
-      launch_block_inverse(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.pull ? 3 : (P.sym ? 2 : 0), P.binv,
+      launch_block_inverse(h->stream, P.n_own, P.node_ptr, P.node_col, P.vals, P.pull ? 3 : 0, P.binv,
                            P.flags, P.bs);
     }
     CKL(h);
   }
   rc = check_flags(h);
   if (rc) return rc;
+  if ((rc = mscale_update(h))) return rc;
   h->assembled = true;
   h->solved = false;
   return SSO_OK;
@@ -1317,6 +1406,7 @@ static int solve_chunks(sso_ctx* h) {
 }
 
 int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
+  ENTER(h);
   const bool add_load = h && h->area_load && !h->skip_load;
   if (!h || (!f && !add_load) || !u) {
     if (h) h->err = "null argument";
@@ -1361,10 +1451,15 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
     h->h_st[bd].dist = dist ? 1 : 0;
     h->h_st[bd].defer_alpha = (!dist && h->P0().cgf) ? 1 : 0;  // the fused update forms alpha
   }
-  for (auto& pp : h->parts)
+  for (auto& pp : h->parts) {
+    for (int bd = 0; bd < h->batch; ++bd) {  // this part's Lanczos history
+      h->h_st[bd].lz = pp->lz_hist + 2 * (int64_t)bd * pp->lz_cap;
+      h->h_st[bd].lz_cap = pp->lz_cap;
+    }
     CK(h, cudaMemcpyAsync(pp->st, h->h_st, pp->B * sizeof(CgState), cudaMemcpyHostToDevice, h->stream));
-  // the pinned staging struct is reused below: make the uploads complete first
-  if ((rc = sync(h))) return rc;
+    // the pinned staging struct is reused: make the upload complete first
+    if ((rc = sync(h))) return rc;
+  }
   const bool lift = h->prescribed && !h->skip_load;
   if (lift) {  // K_ff u_f = f_f - K_fc b (reading c18)
     Part& P = h->P0();
@@ -1397,10 +1492,16 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
     Part& P = *pp;
     long long g1 = g_launches;
     spmv_apply(h->stream, P, P.xs, P.tmp, nullptr);
-    launch_residual_norm(h->stream, (int)P.ndof_own, P.fbc, P.tmp, P.partial, P.st, P.bs);
+    launch_cert_sums(h->stream, P.n_own, P.fbc, P.tmp, P.xs, P.dinv, P.binv, P.partial, P.st, P.bs);
     h->launches += g_launches - g1;
   }
-  if ((rc = allreduce(h, 1))) return rc;
+  if ((rc = allreduce(h, 4))) return rc;
+  {  // extreme Ritz values of M^-1 K from part 0's coefficient history (the same in every part)
+    Part& P = h->P0();
+    long long g1 = g_launches;
+    launch_lanczos_ritz(h->stream, P.st, P.lz_T, P.lz_cap, P.B);
+    h->launches += g_launches - g1;
+  }
   CK(h, cudaMemcpyAsync(h->h_st, h->P0().st, h->batch * sizeof(CgState), cudaMemcpyDeviceToHost,
                         h->stream));
   if (lift) {  // u = u_f + b
@@ -1421,6 +1522,7 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
       info[bd].iters = Sb.iter;
       info[bd].rel_res = Sb.ff > 0 ? std::sqrt(Sb.rr / Sb.ff) : 0.0;
       info[bd].true_rel_res = Sb.ff > 0 ? std::sqrt(Sb.red[0] / Sb.ff) : 0.0;
+      fill_cert(h, bd, Sb, info[bd]);
       info[bd].ms = ms;
       info[bd].status = st_b;
     }
@@ -1530,6 +1632,7 @@ static int grad_prescribed(sso_ctx* h, sso_objective obj, double* C, double* dC_
                            double* dC_dE);
 
 int sso_grad(sso_handle h, sso_objective obj, double* C, double* dC_dxyz, double* dC_dt) {
+  ENTER(h);
   if (!h) return SSO_E_INVALID;
   if (obj != SSO_OBJ_COMPLIANCE && obj != SSO_OBJ_STRAIN_ENERGY) FAIL(h, SSO_E_INVALID, "unknown objective");
   if (!h->solved) FAIL(h, SSO_E_STATE, "sso_grad before a successful sso_solve");
@@ -1539,6 +1642,7 @@ int sso_grad(sso_handle h, sso_objective obj, double* C, double* dC_dxyz, double
 
 int sso_grad_at(sso_handle h, sso_objective obj, const double* f, const double* u, double* C,
                 double* dC_dxyz, double* dC_dt) {
+  ENTER(h);
   if (!h || !f || !u) return SSO_E_INVALID;
   if (obj != SSO_OBJ_COMPLIANCE && obj != SSO_OBJ_STRAIN_ENERGY) FAIL(h, SSO_E_INVALID, "unknown objective");
   if (h->prescribed) FAIL(h, SSO_E_INVALID, "sso_grad_at is not defined with prescribed displacements (use sso_grad)");
@@ -1567,6 +1671,7 @@ static int grad_pass(sso_ctx* h, Part& P, const double* U, double s, double u_lo
 }
 
 int sso_adjoint_solve(sso_handle h, const double* dg_du, double* lambda, sso_solve_info* info) {
+  ENTER(h);
   if (!h || !dg_du || !lambda) return SSO_E_INVALID;
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_adjoint_solve is defined for single-strip handles");
   if (!h->assembled) FAIL(h, SSO_E_STATE, "sso_adjoint_solve before sso_assemble");
@@ -1652,6 +1757,7 @@ static int adjoint_grad_dev(sso_ctx* h, double u_load_s) {
 }
 
 int sso_grad_adjoint(sso_handle h, const double* lambda, double* dg_dxyz, double* dg_dt, double* dg_dE) {
+  ENTER(h);
   if (!h || !lambda) return SSO_E_INVALID;
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_grad_adjoint is defined for single-strip handles");
   if (!h->solved) FAIL(h, SSO_E_STATE, "sso_grad_adjoint before a successful sso_solve");
@@ -1721,6 +1827,7 @@ static int grad_prescribed(sso_ctx* h, sso_objective obj, double* C, double* dC_
 }
 
 int sso_grad_E(sso_handle h, sso_objective obj, double* dC_dE) {
+  ENTER(h);
   if (!h || !dC_dE) return SSO_E_INVALID;
   if (obj != SSO_OBJ_COMPLIANCE && obj != SSO_OBJ_STRAIN_ENERGY) FAIL(h, SSO_E_INVALID, "unknown objective");
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_grad_E is defined for single-strip handles");
@@ -1730,6 +1837,7 @@ int sso_grad_E(sso_handle h, sso_objective obj, double* dC_dE) {
 }
 
 int sso_set_prescribed(sso_handle h, const double* b) {
+  ENTER(h);
   if (!h) return SSO_E_INVALID;
   if (!b) {
     if (h->prescribed) h->assembled = false;
@@ -1766,6 +1874,7 @@ int sso_set_prescribed(sso_handle h, const double* b) {
 }
 
 int sso_set_area_load(sso_handle h, const double* q, const double* w, const double* dir) {
+  ENTER(h);
   if (!h) return SSO_E_INVALID;
   if (!q && !w) {
     h->area_load = false;
@@ -1806,6 +1915,7 @@ int sso_set_area_load(sso_handle h, const double* q, const double* w, const doub
 }
 
 int sso_set_density(sso_handle h, const double* rho, double penal, const double* E0, const double* G0) {
+  ENTER(h);
   if (!h || !rho || !E0) return SSO_E_INVALID;
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_set_density is defined for single-strip handles");
   if (!(penal >= 1.0) || !std::isfinite(penal)) FAIL(h, SSO_E_INVALID, "sso_set_density: penalty P must be >= 1");
@@ -1844,6 +1954,7 @@ int sso_set_density(sso_handle h, const double* rho, double penal, const double*
 }
 
 int sso_grad_density(sso_handle h, sso_objective obj, double* dC_drho) {
+  ENTER(h);
   if (!h || !dC_drho) return SSO_E_INVALID;
   if (!h->simp) FAIL(h, SSO_E_STATE, "sso_grad_density without sso_set_density");
   h->simp_chain = true;
@@ -1853,6 +1964,7 @@ int sso_grad_density(sso_handle h, sso_objective obj, double* dC_drho) {
 }
 
 int sso_set_material(sso_handle h, const double* E) {
+  ENTER(h);
   if (!h || !E) return SSO_E_INVALID;
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_set_material is defined for single-strip handles");
   h->simp = false;
@@ -1973,6 +2085,7 @@ extern "C" {
 
 int sso_hat_filter(sso_handle h, int32_t on_elements, double radius, int32_t ncomp, const double* in,
                    double* out) {
+  ENTER(h);
   if (!h || !in || !out) return SSO_E_INVALID;
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_hat_filter is defined for single-strip handles");
   if (!(radius > 0.0) || !std::isfinite(radius)) FAIL(h, SSO_E_INVALID, "radius must be positive and finite");
@@ -2011,6 +2124,7 @@ int sso_hat_filter(sso_handle h, int32_t on_elements, double radius, int32_t nco
 }
 
 int sso_spmv(sso_handle h, const double* xin, double* yout) {
+  ENTER(h);
   if (!h || !xin || !yout) return SSO_E_INVALID;
   if (!h->assembled) FAIL(h, SSO_E_STATE, "sso_spmv before sso_assemble");
   int rc;
@@ -2041,6 +2155,7 @@ int sso_sizes(sso_handle h, int64_t* ndof, int64_t* nnz, int64_t* n_blocks) {
 }
 
 int sso_storage_info(sso_handle h, int64_t* stored_values, int64_t* stored_blocks, int32_t* symmetric) {
+  ENTER(h);
   if (!h) return SSO_E_INVALID;
   int64_t v = 0, b = 0;
   bool sym = true, pull = true;
@@ -2052,12 +2167,13 @@ int sso_storage_info(sso_handle h, int64_t* stored_values, int64_t* stored_block
   }
   if (stored_values) *stored_values = v;
   if (stored_blocks) *stored_blocks = b;
-  if (symmetric) *symmetric = sym ? (pull ? 3 : 2) : 0;
+  if (symmetric) *symmetric = (sym && pull) ? 3 : 0;
   return SSO_OK;
 }
 
 int sso_part_info(sso_handle h, int32_t* n_parts_here, int32_t* own_node_begin, int32_t* own_nodes,
                   int32_t* own_quads) {
+  ENTER(h);
   if (!h) return SSO_E_INVALID;
   if (n_parts_here) *n_parts_here = (int32_t)h->parts.size();
   if (own_node_begin) *own_node_begin = h->user_node_begin;
@@ -2067,6 +2183,7 @@ int sso_part_info(sso_handle h, int32_t* n_parts_here, int32_t* own_node_begin, 
 }
 
 int sso_export_csr(sso_handle h, int64_t* row_ptr, int32_t* col_idx, double* vals) {
+  ENTER(h);
   if (!h) return SSO_E_INVALID;
   if (vals && !h->assembled) FAIL(h, SSO_E_STATE, "export of values before sso_assemble");
   // rows of the owned nodes of every part, in global node order, columns in
@@ -2089,10 +2206,10 @@ int sso_export_csr(sso_handle h, int64_t* row_ptr, int32_t* col_idx, double* val
       if (!P.sym) return pv[36 * b0 + 6 * a * deg + 6 * k + b];
       const int32_t m = T.node_col[b0 + k];
       const UpperPattern& U = P.up;
-      // run position of (row a, column 6 ku + b): row-major (storage 2) or column-major (3)
-      // (storage 2) row-major runs; (storage 3) PULL_BLOCK records (rec_off)
+      // position of (row a, column b) of upper block ku: one PULL_BLOCK record per block (rec_off)
       auto at = [&](int64_t u0, int64_t ud, int64_t ku, int ra, int cb) {
-        return P.pull ? PULL_BLOCK * (u0 + ku) + rec_off(ra, cb) : 36 * u0 + 6 * ra * ud + 6 * ku + cb;
+        (void)ud;
+        return PULL_BLOCK * (u0 + ku) + rec_off(ra, cb);
       };
       if (m >= n) {
         const int64_t ud = U.uptr[n + 1] - U.uptr[n];
@@ -2130,6 +2247,7 @@ int sso_export_csr(sso_handle h, int64_t* row_ptr, int32_t* col_idx, double* val
 }
 
 int sso_export_scatter(sso_handle h, int32_t* block_rank) {
+  ENTER(h);
   if (!h || !block_rank) return SSO_E_INVALID;
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_export_scatter is defined for single-part handles");
   std::memcpy(block_rank, h->P0().pat.block_rank.data(), h->P0().pat.block_rank.size() * sizeof(int32_t));
@@ -2137,6 +2255,7 @@ int sso_export_scatter(sso_handle h, int32_t* block_rank) {
 }
 
 int sso_export_ke(sso_handle h, int64_t first, int64_t count, double* ke) {
+  ENTER(h);
   if (!h || !ke) return SSO_E_INVALID;
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_export_ke is defined for single-part handles");
   Part& P = h->P0();
@@ -2170,6 +2289,7 @@ int sso_export_ke(sso_handle h, int64_t first, int64_t count, double* ke) {
 }
 
 int sso_export_dinv(sso_handle h, double* dinv) {
+  ENTER(h);
   if (!h || !dinv) return SSO_E_INVALID;
   if (!h->assembled) FAIL(h, SSO_E_STATE, "export of dinv before sso_assemble");
   for (auto& pp : h->parts) {
@@ -2181,12 +2301,14 @@ int sso_export_dinv(sso_handle h, double* dinv) {
 }
 
 int sso_profile_enable(sso_handle h, int32_t on) {
+  ENTER(h);
   if (!h) return SSO_E_INVALID;
   h->tm.on = on != 0;
   return SSO_OK;
 }
 
 int sso_profile_read(sso_handle h, const char* name, double* total_ms, int64_t* launches) {
+  ENTER(h);
   if (!h || !name) return SSO_E_INVALID;
   static const char* names[F_COUNT] = {"element", "assemble", "spmv", "update", "grad", "reduce"};
   for (int k = 0; k < F_COUNT; ++k)
@@ -2199,6 +2321,7 @@ int sso_profile_read(sso_handle h, const char* name, double* total_ms, int64_t* 
 }
 
 int sso_profile_reset(sso_handle h) {
+  ENTER(h);
   if (!h) return SSO_E_INVALID;
   for (int k = 0; k < F_COUNT; ++k) {
     h->tm.total_ms[k] = 0;
@@ -2211,9 +2334,12 @@ int64_t sso_launch_count(sso_handle h) { return h ? h->launches : 0; }
 
 void sso_destroy(sso_handle h) {
   if (!h) return;
+  int cur = -1;
+  const bool sw = cudaGetDevice(&cur) == cudaSuccess && cur != h->device && cudaSetDevice(h->device) == cudaSuccess;
   cudaStreamSynchronize(h->stream);
   free_all(h);
   delete h;
+  if (sw) cudaSetDevice(cur);
 }
 
 // ---------------------------------------------------------------------------

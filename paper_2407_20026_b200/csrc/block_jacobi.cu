@@ -13,6 +13,7 @@
 // z [B][6 n_own] is stored by the update so that the p update reads one vector.
 // Kernels are node-granular (a thread per node, its 6-vectors as 3 double2) and
 // keep the atomic-free fixed-order reductions of pcg.cu (same epilogues).
+#include "cg_common.cuh"
 #include "cg_fused.cuh"
 #include "sso_internal.h"
 
@@ -20,87 +21,10 @@ namespace sso {
 
 namespace {
 
-__device__ __forceinline__ int tri6(int a, int b) { return a * 6 - (a * (a - 1)) / 2 + (b - a); }
-
-// 6-vector loads / stores at 6 n (48-byte aligned)
-__device__ __forceinline__ void ld6(const double* __restrict__ v, int64_t n, double (&o)[6]) {
-  const double2* p = reinterpret_cast<const double2*>(v + 6 * n);
-  const double2 a = p[0], b = p[1], c = p[2];
-  o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y; o[4] = c.x; o[5] = c.y;
-}
-__device__ __forceinline__ void st6(double* __restrict__ v, int64_t n, const double (&o)[6]) {
-  double2* p = reinterpret_cast<double2*>(v + 6 * n);
-  p[0] = make_double2(o[0], o[1]);
-  p[1] = make_double2(o[2], o[3]);
-  p[2] = make_double2(o[4], o[5]);
-}
-
-// z = Binv_n r (packed symmetric), fixed-order sums
-__device__ __forceinline__ void block_apply(const double* __restrict__ binv, int64_t nn, int64_t n,
-                                            const double (&r)[6], double (&z)[6]) {
-  double m[21];
-#pragma unroll
-  for (int e = 0; e < 21; ++e) m[e] = binv[e * nn + n];
-#pragma unroll
-  for (int a = 0; a < 6; ++a) {
-    double s = 0.0;
-#pragma unroll
-    for (int b = 0; b < 6; ++b) s = fma(m[a <= b ? tri6(a, b) : tri6(b, a)], r[b], s);
-    z[a] = s;
-  }
-}
-
-// Block sums / last-CTA reduction: the same scheme as pcg.cu (fixed order).
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-template <int NV>
-__device__ __forceinline__ void block_sum(double (&v)[NV], double* sm) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < NV; ++k) sm[w * NV + k] = v[k];
-  __syncthreads();
-  if (w == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] = warp_sum((lane < nw) ? sm[lane * NV + k] : 0.0);
-  }
-  __syncthreads();
-}
-template <int NV>
-__device__ __forceinline__ bool grid_sum(double (&v)[NV], double* partial, unsigned int* ticket, double* sm) {
-  __shared__ bool last;
-  block_sum<NV>(v, sm);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) partial[(int64_t)blockIdx.x * NV + k] = v[k];
-    __threadfence();
-    const unsigned t = atomicAdd(ticket, 1u);
-    last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!last) return false;
-  __threadfence();
-  double acc[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
-#pragma unroll
-    for (int k = 0; k < NV; ++k) acc[k] += __ldcg(partial + (int64_t)b * NV + k);
-  block_sum<NV>(acc, sm);
-#pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = acc[k];
-  if (threadIdx.x == 0) *ticket = 0u;
-  return true;
-}
 
 // (K_nn)^-1 of every owned node from the assembled values.  Run layout: 0 full storage
-// (row-major runs, diagonal block at its rank in the node's column list), 2 upper blocks
-// row-major (diagonal block first), 3 upper-block records (PULL_BLOCK, rec_off; diagonal first).
+// (row-major runs, diagonal block at its rank in the node's column list), 3 upper-block
+// records (PULL_BLOCK, rec_off; diagonal first).
 __global__ void __launch_bounds__(128) block_inverse_kernel(int n_nodes, const int64_t* __restrict__ node_ptr,
                                                             const int32_t* __restrict__ node_col,
                                                             const double* __restrict__ vals, int layout,
@@ -120,10 +44,6 @@ __global__ void __launch_bounds__(128) block_inverse_kernel(int n_nodes, const i
     int k = 0;
     while (k < deg && node_col[b0 + k] != n) ++k;
     off = 36 * b0 + 6 * k;
-    rs = 6 * deg;
-    cs = 1;
-  } else if (layout == 2) {
-    off = 36 * b0;
     rs = 6 * deg;
     cs = 1;
   } else {
@@ -309,6 +229,7 @@ __global__ void __launch_bounds__(256) cg_update_block_kernel(int n_nodes, const
     st->rz = rz_new;
     st->rr = v[1];
     st->iter += 1;
+    lz_record(st, st->alpha, st->beta);
     if (v[1] <= st->tol2) {
       st->done = 1;
       st->status = SSO_OK;
@@ -557,8 +478,9 @@ void launch_cg_update_block_fused(cudaStream_t s, int n_nodes, const double* bin
                                   const BatchStrides& bs) {
   const int64_t need = ((int64_t)n_nodes + 255) / 256;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cg_block_fused_grid() / bs.B));
-  cg_update_block_fused_kernel<<<dim3(grid, bs.B), 256, 0, s>>>(n_nodes, binv, x, r, p, q, pn, partial, st, bs);
-  SSO_POST_LAUNCH("cg_update_block_fused_kernel");
+  const cudaError_t e = launch_cooperative(cg_update_block_fused_kernel, dim3(grid, bs.B), dim3(256), s, n_nodes,
+                                           binv, x, r, p, q, pn, partial, st, bs);
+  SSO_POST_LAUNCH_RC("cg_update_block_fused_kernel", e);
 }
 
 void launch_cg_pfix_z(cudaStream_t s, int ndof, const double* z, const double* pin, double* pout,

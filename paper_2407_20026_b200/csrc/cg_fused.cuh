@@ -5,9 +5,11 @@
 // counts itself in (one atomic), waits until all CTAs of its design have arrived, then sums
 // ALL partials itself in one fixed order -- every CTA obtains bit-identical totals, forms beta
 // and the convergence test locally and goes on to p_next = z + beta p with no second
-// release step; CTA 0 records the state.  All CTAs are co-resident by construction (grid
-// bounded by the occupancy, launched on an otherwise idle stream after the SpMV); the wait
-// is still bounded so that a broken launch reports SSO_E_CUDA instead of hanging the device.
+// release step; CTA 0 records the state.  All CTAs are co-resident: the grid is bounded by
+// the occupancy and the kernels are launched cooperatively (launch_cooperative in
+// sso_internal.h: the driver co-schedules the whole grid or rejects the launch).  The wait is
+// still bounded (2^23 polls with a 20 ns back-off: a few seconds at most) so that a broken
+// launch reports SSO_E_CUDA instead of hanging the device.
 #pragma once
 
 #include "sso_internal.h"
@@ -51,7 +53,7 @@ __device__ __forceinline__ int cg_fused_allreduce(double (&v)[2], double* part, 
     const unsigned old = atomicAdd(arrive, 1u);
     const unsigned target = (old / G + 1) * G;
     int ok = 0;
-    for (int spin = 0; spin < (1 << 23); ++spin) {  // ~0.3 s at most
+    for (int spin = 0; spin < (1 << 23); ++spin) {  // a few seconds at most
       if ((int)(ld_acquire_u32(arrive) - target) >= 0) {
         ok = 1;
         break;
@@ -135,6 +137,7 @@ __device__ __forceinline__ int cg_fused_step(const double (&v)[2], CgState* st, 
     st->rr = rr;
     st->iter = iter_old + 1;
     st->pfix = 0;
+    lz_record(st, alpha, beta);
     if (conv) {
       st->done = 1;
       st->status = SSO_OK;

@@ -155,7 +155,6 @@ void build_upper(const HostPattern& P, const int32_t* beam_conn, const int32_t* 
     const int64_t src = P.node_ptr[n] + first_upper[n];
     std::copy(P.node_col.begin() + src, P.node_col.begin() + P.node_ptr[n + 1], U.ucol.begin() + U.uptr[n]);
   }
-  U.n_tslots = U.uptr[nn] - nn;
   // element block ranks in the upper lists, and the upper contributor lists
   U.urank.resize(P.block_rank.size());
   U.ucontrib_ptr.assign((size_t)U.uptr[nn] + 1, 0);
@@ -192,18 +191,11 @@ void build_upper(const HostPattern& P, const int32_t* beam_conn, const int32_t* 
         }
     }
   }
-  // incoming sender slots per node, ascending source node
+  // incoming blocks per node (lptr), ascending source node
   U.lptr.assign((size_t)nn + 1, 0);
   for (int32_t n = 0; n < nn; ++n)
     for (int64_t k = U.uptr[n] + 1; k < U.uptr[n + 1]; ++k) U.lptr[U.ucol[k] + 1]++;
   for (int32_t n = 0; n < nn; ++n) U.lptr[n + 1] += U.lptr[n];
-  U.lslot.resize((size_t)U.lptr[nn]);
-  {
-    std::vector<int64_t> fill(U.lptr.begin(), U.lptr.end() - 1);
-    for (int32_t n = 0; n < nn; ++n)
-      for (int64_t k = U.uptr[n] + 1; k < U.uptr[n + 1]; ++k)
-        U.lslot[fill[U.ucol[k]]++] = (int32_t)(U.uptr[n] - n + (k - U.uptr[n]) - 1);
-  }
   // pull lists (storage 3): the same incoming blocks as (source node, upper block index)
   U.lpull.resize(2 * (size_t)U.lptr[nn]);
   {

@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "cg_common.cuh"
 #include "cg_fused.cuh"
 #include "sso_internal.h"
 
@@ -44,62 +45,6 @@ const char* last_launch_error() { return g_launch_err; }
 namespace {
 
 int g_sms = 0;
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Block-wide sum of NV values (fixed order); result valid in thread 0.
-template <int NV>
-__device__ __forceinline__ void block_sum(double (&v)[NV], double* sm /*[32*NV]*/) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < NV; ++k) sm[w * NV + k] = v[k];
-  __syncthreads();
-  if (w == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      double s = (lane < nw) ? sm[lane * NV + k] : 0.0;
-      v[k] = warp_sum(s);
-    }
-  }
-  __syncthreads();
-}
-
-// Write this CTA's partials; returns true in the last CTA to arrive, which then
-// owns the fixed-order final reduction (result in thread 0 of that CTA).
-template <int NV>
-__device__ __forceinline__ bool grid_sum(double (&v)[NV], double* partial, unsigned int* ticket,
-                                         double* sm) {
-  __shared__ bool last;
-  block_sum<NV>(v, sm);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) partial[(int64_t)blockIdx.x * NV + k] = v[k];
-    __threadfence();
-    unsigned int t = atomicAdd(ticket, 1u);
-    last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!last) return false;
-  __threadfence();
-  double acc[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
-#pragma unroll
-    for (int k = 0; k < NV; ++k) acc[k] += __ldcg(partial + (int64_t)b * NV + k);
-  block_sum<NV>(acc, sm);
-#pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = acc[k];
-  if (threadIdx.x == 0) *ticket = 0u;  // re-arm for the next launch
-  return true;
-}
 
 // Transposed butterfly: reduce 6 (padded to 8) per-lane values across the warp
 // in 9 shuffles.  On return, lane L holds the total of value index
@@ -230,322 +175,6 @@ __device__ __forceinline__ double node_rows(const double* base, int64_t b0, int 
 // term is sum over the lanes holding block 0 of t_b p_n[b], so alpha is formed
 // at the end of pass 1 and the receiver sums move into the x / r update.
 // ---------------------------------------------------------------------------
-
-// v[i] for a lane-dependent i without forcing v into local memory
-__device__ __forceinline__ double pick6(const double (&v)[6], int i) {
-  double r = v[0];
-  r = (i == 1) ? v[1] : r;
-  r = (i == 2) ? v[2] : r;
-  r = (i == 3) ? v[3] : r;
-  r = (i == 4) ? v[4] : r;
-  r = (i == 5) ? v[5] : r;
-  return r;
-}
-
-// One node (general degree): row sums + transpose slots; returns y[vi(lane)] and adds
-// the lane's share of -p_n^T K_nn p_n to *dq (DOT).
-__device__ __forceinline__ double node_rows_sym(const double* base, int deg, int ncol,
-                                                const double* __restrict__ x, const double (&xn)[6],
-                                                double* __restrict__ tn, double* dq, int lane) {
-  const int rowlen = 6 * deg;
-  double acc[8];
-#pragma unroll
-  for (int a = 0; a < 8; ++a) acc[a] = 0.0;
-  for (int r0 = 0; r0 < rowlen; r0 += 32) {
-    const int rem = r0 + lane;
-    const bool act = rem < rowlen;
-    const int k = act ? rem / 6 : 0;
-    const int m = __shfl_sync(0xffffffffu, ncol, k);
-    if (act) {
-      const int b = rem - 6 * k;
-      const double xv = x[6 * (int64_t)m + b];
-      double t = 0.0;
-#pragma unroll
-      for (int a = 0; a < 6; ++a) {
-        const double v = base[a * rowlen + rem];
-        acc[a] += v * xv;
-        t += v * xn[a];
-      }
-      if (k > 0) tn[rem - 6] = t;
-      else *dq -= t * pick6(xn, b);
-    }
-  }
-  return reduce6(acc, lane);
-}
-
-template <bool DOT, int SPMV_STAGES, int SLOT_DEG, int MINB>
-__global__ void __launch_bounds__(SPMV_WARPS * 32, MINB) spmv_sym_pass1_kernel(
-    int n_nodes, int nodes_per_warp, const int64_t* __restrict__ uptr,
-    const int32_t* __restrict__ ucol, const double* __restrict__ vals,
-    const double* __restrict__ p, double* __restrict__ q, double* __restrict__ tbuf,
-    double* __restrict__ partial, CgState* st, BatchStrides bs) {
-  constexpr int SLOT_DOUBLES = 36 * SLOT_DEG;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t bar[SPMV_WARPS][SPMV_STAGES];
-  __shared__ double sm[32];
-  {
-    const int bd = blockIdx.y;
-    vals += bd * bs.nnz;
-    p += bd * bs.dof;
-    q += bd * bs.dof;
-    tbuf += bd * bs.tbuf;
-    if (DOT) {
-      partial += bd * bs.partial;
-      st += bd;
-    }
-  }
-  if (DOT && st->done) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * SPMV_WARPS + warp;
-  const int64_t nb = gw * nodes_per_warp;
-  const int64_t left = (int64_t)n_nodes - nb;
-  const int cnt = left <= 0 ? 0 : (int)(left < nodes_per_warp ? left : nodes_per_warp);
-  double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * SPMV_STAGES * SLOT_DOUBLES;
-  uint64_t* wbar = bar[warp];
-  uint64_t pol = 0;
-  if (lane == 0) {
-#pragma unroll
-    for (int s = 0; s < SPMV_STAGES; ++s) mbar_init(&wbar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    pol = evict_first_policy();
-  }
-  __syncwarp();
-  auto issue = [&](int k) {  // lane 0 only
-    const int64_t n = nb + k;
-    const int s = k % SPMV_STAGES;
-    const int64_t b0 = uptr[n], b1 = uptr[n + 1];
-    if (b1 - b0 <= SLOT_DEG) {
-      const unsigned bytes = (unsigned)(288 * (b1 - b0));
-      mbar_arrive_expect_tx(&wbar[s], bytes);
-      bulk_g2s(ring + (size_t)s * SLOT_DOUBLES, vals + 36 * b0, bytes, &wbar[s], pol);
-    } else {
-      mbar_arrive(&wbar[s]);
-    }
-  };
-  // pairs of nodes per step: nodes k, k+1 are consumed while k+2 .. k+S-1 stream in
-  if (lane == 0)
-    for (int k = 0; k < min(SPMV_STAGES - 2, cnt); ++k) issue(k);
-  const int vi = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-  const bool writer = ((lane & 3) == 0) && vi < 6;
-  double dq = 0.0;  // this lane's share of p^T K p
-  int64_t b0n = 0;
-  int degn = 0, ncoln = 0;
-  if (cnt > 0) {
-    b0n = uptr[nb];
-    degn = (int)(uptr[nb + 1] - b0n);
-    ncoln = (lane < degn) ? __ldg(ucol + b0n + lane) : 0;
-  }
-  for (int k = 0; k < cnt; k += 2) {
-    const bool twoB = k + 1 < cnt;
-    if (lane == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (k + SPMV_STAGES - 2 < cnt) issue(k + SPMV_STAGES - 2);
-      if (k + SPMV_STAGES - 1 < cnt) issue(k + SPMV_STAGES - 1);
-    }
-    const int64_t nA = nb + k, nB = nA + 1;
-    const int64_t bA = b0n;
-    const int degA = degn, ncolA = ncoln;
-    int64_t bB = 0;
-    int degB = 0, ncolB = 0;
-    if (twoB) {
-      bB = uptr[nB];
-      degB = (int)(uptr[nB + 1] - bB);
-      ncolB = (lane < degB) ? __ldg(ucol + bB + lane) : 0;
-    }
-    if (k + 2 < cnt) {
-      b0n = uptr[nA + 2];
-      degn = (int)(uptr[nA + 3] - b0n);
-      ncoln = (lane < degn) ? __ldg(ucol + b0n + lane) : 0;
-    }
-    double* tA = tbuf + 6 * (bA - nA);  // sender-ordered slots of node A
-    double* tB = tbuf + 6 * (bB - nB);
-    double xA[6], xB[6];
-#pragma unroll
-    for (int a = 0; a < 6; ++a) {
-      xA[a] = p[6 * nA + a];
-      xB[a] = twoB ? p[6 * nB + a] : 0.0;
-    }
-    const int sA = k % SPMV_STAGES, sB = (k + 1) % SPMV_STAGES;
-    double yA = 0.0, yB = 0.0;
-    if (degA <= 5 && degB <= 5) {
-      // common case (at most 5 upper blocks: <= 30 row positions, one per lane)
-      const int rlA = 6 * degA, rlB = 6 * degB;
-      const bool aA = lane < rlA, aB = lane < rlB;
-      const int kA = aA ? lane / 6 : 0, kB = aB ? lane / 6 : 0;
-      const int mA = __shfl_sync(0xffffffffu, ncolA, kA);
-      const int mB = __shfl_sync(0xffffffffu, ncolB, kB);
-      const int cA = lane - 6 * kA, cB = lane - 6 * kB;
-      const double xgA = aA ? p[6 * (int64_t)mA + cA] : 0.0;
-      const double xgB = aB ? p[6 * (int64_t)mB + cB] : 0.0;
-      mbar_wait(&wbar[sA], (unsigned)((k / SPMV_STAGES) & 1));
-      if (twoB) mbar_wait(&wbar[sB], (unsigned)(((k + 1) / SPMV_STAGES) & 1));
-      const double* baseA = ring + (size_t)sA * SLOT_DOUBLES;
-      const double* baseB = ring + (size_t)sB * SLOT_DOUBLES;
-      double accA[8], accB[8];
-#pragma unroll
-      for (int a = 0; a < 8; ++a) accA[a] = accB[a] = 0.0;
-      if (aA) {
-        double t = 0.0;
-#pragma unroll
-        for (int a = 0; a < 6; ++a) {
-          const double v = baseA[a * rlA + lane];
-          accA[a] = v * xgA;
-          t += v * xA[a];
-        }
-        if (kA > 0) tA[lane - 6] = t;
-        else dq -= t * p[6 * nA + cA];
-      }
-      if (aB) {
-        double t = 0.0;
-#pragma unroll
-        for (int a = 0; a < 6; ++a) {
-          const double v = baseB[a * rlB + lane];
-          accB[a] = v * xgB;
-          t += v * xB[a];
-        }
-        if (kB > 0) tB[lane - 6] = t;
-        else dq -= t * p[6 * nB + cB];
-      }
-      yA = reduce6(accA, lane);
-      yB = reduce6(accB, lane);
-    } else {
-      // general degree: one node at a time
-      for (int h2 = 0; h2 < (twoB ? 2 : 1); ++h2) {
-        const int64_t b0 = h2 ? bB : bA;
-        const int deg = h2 ? degB : degA;
-        const int s = h2 ? sB : sA;
-        mbar_wait(&wbar[s], (unsigned)(((k + h2) / SPMV_STAGES) & 1));
-        const double* base = (deg <= SLOT_DEG) ? ring + (size_t)s * SLOT_DOUBLES : vals + 36 * b0;
-        double y;
-        if (deg <= 32) {
-          y = node_rows_sym(base, deg, h2 ? ncolB : ncolA, p, h2 ? xB : xA, h2 ? tB : tA, &dq, lane);
-        } else {
-          const int rowlen = 6 * deg;
-          double acc[8];
-#pragma unroll
-          for (int a = 0; a < 8; ++a) acc[a] = 0.0;
-          for (int rem = lane; rem < rowlen; rem += 32) {
-            const int kk = rem / 6, b = rem - 6 * (rem / 6);
-            const int m = __ldg(ucol + b0 + kk);
-            const double xv = p[6 * (int64_t)m + b];
-            double t = 0.0;
-#pragma unroll
-            for (int a = 0; a < 6; ++a) {
-              const double v = base[a * rowlen + rem];
-              acc[a] += v * xv;
-              t += v * (h2 ? xB[a] : xA[a]);
-            }
-            if (kk > 0) (h2 ? tB : tA)[rem - 6] = t;
-            else dq -= t * pick6(h2 ? xB : xA, b);
-          }
-          y = reduce6(acc, lane);
-        }
-        if (h2) yB = y; else yA = y;
-      }
-    }
-    if (writer) {
-      q[6 * nA + vi] = yA;
-      if (DOT) dq += 2.0 * p[6 * nA + vi] * yA;
-      if (twoB) {
-        q[6 * nB + vi] = yB;
-        if (DOT) dq += 2.0 * p[6 * nB + vi] * yB;
-      }
-    }
-    __syncwarp();
-  }
-  if (DOT) {
-    double v[1] = {dq};
-    if (grid_sum<1>(v, partial, &st->ticket[0], sm) && threadIdx.x == 0) {
-      if (st->dist) {
-        st->red[0] = v[0];
-        return;
-      }
-      st->pq = v[0];
-      if (!(v[0] > 0.0)) {
-        st->status = SSO_E_NOT_SPD;
-        st->done = 1;
-      } else {
-        st->alpha = st->rz / v[0];
-      }
-    }
-  }
-}
-
-// Symmetric storage, pass 2 (plain SpMV): y[d] += node d/6's incoming slots (contiguous).
-__global__ void __launch_bounds__(256) spmv_sym_pass2_kernel(int ndof, const int64_t* __restrict__ lptr,
-                                                             const int32_t* __restrict__ lslot,
-                                                             const double* __restrict__ tbuf,
-                                                             double* __restrict__ y, BatchStrides bs) {
-  tbuf += blockIdx.y * bs.tbuf;
-  y += blockIdx.y * bs.dof;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < ndof; d += stride) {
-    const int64_t m = d / 6;
-    const int b = (int)(d - 6 * m);
-    double v = y[d];
-    for (int64_t l = lptr[m]; l < lptr[m + 1]; ++l) v += tbuf[6 * (int64_t)lslot[l] + b];
-    y[d] = v;
-  }
-}
-
-// CG x / r update with the symmetric receiver sums folded in: q = y_up + incoming slots.
-__global__ void __launch_bounds__(256) cg_update_sym_kernel(int ndof, const double* __restrict__ dinv,
-                                                            double* __restrict__ x, double* __restrict__ r,
-                                                            const double* __restrict__ p,
-                                                            const double* __restrict__ yup,
-                                                            const double* __restrict__ tbuf,
-                                                            const int64_t* __restrict__ lptr,
-                                                            const int32_t* __restrict__ lslot,
-                                                            double* __restrict__ partial, CgState* st,
-                                                            BatchStrides bs) {
-  __shared__ double sm[64];
-  {
-    const int bd = blockIdx.y;
-    dinv += bd * bs.dof;
-    x += bd * bs.dof;
-    r += bd * bs.dof;
-    p += bd * bs.dof;
-    yup += bd * bs.dof;
-    tbuf += bd * bs.tbuf;
-    partial += bd * bs.partial;
-    st += bd;
-  }
-  if (st->done) return;
-  const double alpha = st->alpha;
-  double v[2] = {0.0, 0.0};
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < ndof; d += stride) {
-    const int64_t m = d / 6;
-    const int b = (int)(d - 6 * m);
-    double q = yup[d];
-    for (int64_t l = lptr[m]; l < lptr[m + 1]; ++l) q += tbuf[6 * (int64_t)lslot[l] + b];
-    x[d] += alpha * p[d];
-    const double ri = r[d] - alpha * q;
-    r[d] = ri;
-    v[0] += ri * (dinv[d] * ri);
-    v[1] += ri * ri;
-  }
-  if (grid_sum<2>(v, partial, &st->ticket[1], sm) && threadIdx.x == 0) {
-    if (st->dist) {
-      st->red[0] = v[0];
-      st->red[1] = v[1];
-      return;
-    }
-    const double rz_new = v[0];
-    st->beta = rz_new / st->rz;
-    st->rz_prev = st->rz;
-    st->rz = rz_new;
-    st->rr = v[1];
-    st->iter += 1;
-    if (v[1] <= st->tol2) {
-      st->done = 1;
-      st->status = SSO_OK;
-    } else if (st->iter >= st->max_iter) {
-      st->done = 1;
-      st->status = SSO_E_NOT_CONVERGED;
-    }
-  }
-}
 
 // q = K p; with DOT also p^T q -> alpha (CG) and an early exit once `done`.
 // STAGES ring slots of SLOT_DEG 6x6 blocks per warp; MINB CTAs per SM.
@@ -1076,6 +705,7 @@ __global__ void __launch_bounds__(256) cg_update_kernel(int ndof, const double* 
     st->rz = rz_new;
     st->rr = v[1];
     st->iter += 1;
+    lz_record(st, st->alpha, st->beta);
     if (v[1] <= st->tol2) {
       st->done = 1;
       st->status = SSO_OK;
@@ -1367,6 +997,7 @@ __global__ void cg_scalar_kernel(CgState* st, int phase) {
     st->rz = rz_new;
     st->rr = st->red[1];
     st->iter += 1;
+    lz_record(st, st->alpha, st->beta);
     if (st->rr <= st->tol2) {
       st->done = 1;
       st->status = SSO_OK;
@@ -1412,6 +1043,7 @@ __global__ void cg_check_kernel(CgState* st, int mode, int B) {
     if (!S->done && !S->floor && S->rr < REPL_FACTOR * S->rr_ref) {
       if (drifted) S->floor = 1;
       else S->act = (tt > REPL_CONT * REPL_CONT * S->rr) ? 2 : 1;
+      if (S->act == 2) S->lz_frozen = 1;  // restart (beta = 0)
     }
   } else {
     S->act = 0;
@@ -1423,6 +1055,7 @@ __global__ void cg_check_kernel(CgState* st, int mode, int B) {
         S->act = 1;
         S->done = 0;
         S->restarts += 1;
+        S->lz_frozen = 1;  // a restarted CG is a new Lanczos sequence: keep the first one
       }
     }
   }
@@ -1646,33 +1279,39 @@ struct SpmvVariant {
   void (*plain)(int, int, const int64_t*, const int32_t*, const double*, const double*, double*,
                 double*, CgState*, BatchStrides);
 };
-// symmetric pass 1: 4-slot ring (two nodes consumed per step), <= 5 upper blocks per slot
-constexpr int SYM_STAGES = 4, SYM_SLOT_DEG = 5, SYM_MINB = 2;
 #define SPMV_VARIANT(S, D, M) \
   { S, D, M, spmv_tma_kernel<true, S, D, M>, spmv_tma_kernel<false, S, D, M> }
 static const SpmvVariant kSpmvVariants[] = {
     SPMV_VARIANT(4, 10, 2), SPMV_VARIANT(3, 10, 3), SPMV_VARIANT(2, 9, 4), SPMV_VARIANT(3, 9, 3),
     SPMV_VARIANT(2, 10, 4)};
 
+// true the first time it is called for the current device with this mask (kernel attributes
+// are per device: a process may hold handles on several GPUs)
+static bool first_on_device(uint64_t& mask) {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) d = 0;
+  const uint64_t bit = 1ull << d;
+  if (mask & bit) return false;
+  mask |= bit;
+  return true;
+}
+
 static const SpmvVariant& spmv_variant() {
   static int v = -1;
+  static uint64_t attr_mask = 0;
   if (v < 0) {
     const char* e = getenv("SSO_SPMV_VARIANT");
     v = e ? atoi(e) : 2;  // default: 2-slot ring, 4 CTAs per SM (measured best at C3b)
     const int nv = (int)(sizeof(kSpmvVariants) / sizeof(kSpmvVariants[0]));
     if (v < 0 || v >= nv) v = 0;
-    const SpmvVariant& V = kSpmvVariants[v];
+  }
+  const SpmvVariant& V = kSpmvVariants[v];
+  if (first_on_device(attr_mask)) {
     const int smem = SPMV_WARPS * V.stages * 36 * V.slot_deg * 8;
     cudaFuncSetAttribute(V.dot, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(V.plain, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(spmv_sym_pass1_kernel<true, SYM_STAGES, SYM_SLOT_DEG, SYM_MINB>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SPMV_WARPS * SYM_STAGES * 36 * SYM_SLOT_DEG * 8);
-    cudaFuncSetAttribute(spmv_sym_pass1_kernel<false, SYM_STAGES, SYM_SLOT_DEG, SYM_MINB>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SPMV_WARPS * SYM_STAGES * 36 * SYM_SLOT_DEG * 8);
   }
-  return kSpmvVariants[v];
+  return V;
 }
 
 static void spmv_config(int n_nodes, int B, int* grid, int* npw, int* smem) {
@@ -1694,48 +1333,6 @@ void launch_spmv_dot(cudaStream_t s, int n_nodes, const int64_t* node_ptr, const
   spmv_variant().dot<<<dim3(grid, bs.B), SPMV_WARPS * 32, smem, s>>>(n_nodes, npw, node_ptr, node_col, vals,
                                                                      p, q, partial, st, bs);
   SSO_POST_LAUNCH("spmv_dot_kernel");
-}
-
-static void sym_config(int n_nodes, int B, int* grid, int* npw, int* smem) {
-  spmv_variant();  // kernel attributes
-  const int ctas = std::max(1, SYM_MINB * (cg_grid() / 4) / B);
-  const int64_t warps = (int64_t)ctas * SPMV_WARPS;
-  int per = (int)((n_nodes + warps - 1) / warps);
-  if (per < 1) per = 1;
-  *npw = per;
-  *grid = (int)std::max<int64_t>(1, (((int64_t)n_nodes + per - 1) / per + SPMV_WARPS - 1) / SPMV_WARPS);
-  *smem = SPMV_WARPS * SYM_STAGES * 36 * SYM_SLOT_DEG * 8;
-}
-
-void launch_spmv_sym(cudaStream_t s, int n_nodes, const int64_t* uptr, const int32_t* ucol,
-                     const double* vals, const double* x, double* y, double* tbuf,
-                     const int64_t* lptr, const int32_t* lslot, const BatchStrides& bs) {
-  int grid, npw, smem;
-  sym_config(n_nodes, bs.B, &grid, &npw, &smem);
-  spmv_sym_pass1_kernel<false, SYM_STAGES, SYM_SLOT_DEG, SYM_MINB><<<dim3(grid, bs.B), SPMV_WARPS * 32, smem, s>>>(
-      n_nodes, npw, uptr, ucol, vals, x, y, tbuf, nullptr, nullptr, bs);
-  SSO_POST_LAUNCH("spmv_sym_pass1_kernel");
-  const int ndof = 6 * n_nodes;
-  spmv_sym_pass2_kernel<<<dim3(vec_grid(ndof, bs.B), bs.B), 256, 0, s>>>(ndof, lptr, lslot, tbuf, y, bs);
-  SSO_POST_LAUNCH("spmv_sym_pass2_kernel");
-}
-
-void launch_spmv_sym_cg(cudaStream_t s, int n_nodes, const int64_t* uptr, const int32_t* ucol,
-                        const double* vals, const double* p, double* y, double* tbuf,
-                        double* partial, CgState* st, const BatchStrides& bs) {
-  int grid, npw, smem;
-  sym_config(n_nodes, bs.B, &grid, &npw, &smem);
-  spmv_sym_pass1_kernel<true, SYM_STAGES, SYM_SLOT_DEG, SYM_MINB><<<dim3(grid, bs.B), SPMV_WARPS * 32, smem, s>>>(
-      n_nodes, npw, uptr, ucol, vals, p, y, tbuf, partial, st, bs);
-  SSO_POST_LAUNCH("spmv_sym_pass1_kernel");
-}
-
-void launch_cg_update_sym(cudaStream_t s, int ndof, const double* dinv, double* x, double* r,
-                          const double* p, const double* yup, const double* tbuf, const int64_t* lptr,
-                          const int32_t* lslot, double* partial, CgState* st, const BatchStrides& bs) {
-  cg_update_sym_kernel<<<dim3(vec_grid(ndof, bs.B), bs.B), 256, 0, s>>>(ndof, dinv, x, r, p, yup, tbuf, lptr,
-                                                                        lslot, partial, st, bs);
-  SSO_POST_LAUNCH("cg_update_sym_kernel");
 }
 
 // pull SpMV (storage 3).  Variants (chunk nodes, buffers, CTAs per SM, consumer warps):
@@ -1766,7 +1363,7 @@ static const PullVariant kPullVariants[] = {PULL_CTA_VARIANT(12, 2, 3, 4), PULL_
 // chunks, more CTAs per design) for batches (C5: 220 vs 206 designs/s).
 static const PullVariant& pull_variant(int B, int* smem) {
   static int env_v = -2;
-  static bool attr_set[sizeof(kPullVariants) / sizeof(kPullVariants[0])] = {};
+  static uint64_t attr_mask[sizeof(kPullVariants) / sizeof(kPullVariants[0])] = {};
   const int nv = (int)(sizeof(kPullVariants) / sizeof(kPullVariants[0]));
   if (env_v == -2) {
     const char* e = getenv("SSO_PULL_VARIANT");
@@ -1774,11 +1371,10 @@ static const PullVariant& pull_variant(int B, int* smem) {
     if (env_v >= nv) env_v = -1;
   }
   const int v = env_v >= 0 ? env_v : (B > 1 ? 1 : 0);
-  if (!attr_set[v]) {
+  if (first_on_device(attr_mask[v])) {
     cudaFuncSetAttribute(kPullVariants[v].dot, cudaFuncAttributeMaxDynamicSharedMemorySize, kPullVariants[v].smem);
     cudaFuncSetAttribute(kPullVariants[v].plain, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kPullVariants[v].smem);
-    attr_set[v] = true;
   }
   *smem = kPullVariants[v].smem;
   return kPullVariants[v];
@@ -1882,8 +1478,9 @@ void launch_cg_update_fused(cudaStream_t s, int ndof, const double* dinv, double
   // every CTA of every design co-resident (bs.B <= cg_fused_grid(), checked at create)
   const int64_t need = ((int64_t)ndof / 2 + 255) / 256;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, cg_fused_grid() / bs.B));
-  cg_update_fused_kernel<<<dim3(grid, bs.B), 256, 0, s>>>(ndof, dinv, x, r, p, q, pn, partial, st, bs);
-  SSO_POST_LAUNCH("cg_update_fused_kernel");
+  const cudaError_t e = launch_cooperative(cg_update_fused_kernel, dim3(grid, bs.B), dim3(256), s, ndof, dinv, x, r,
+                                           p, q, pn, partial, st, bs);
+  SSO_POST_LAUNCH_RC("cg_update_fused_kernel", e);
 }
 
 void launch_cg_pfix(cudaStream_t s, int ndof, const double* dinv, const double* r, const double* pin,

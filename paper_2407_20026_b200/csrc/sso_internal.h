@@ -1,5 +1,6 @@
 // Internal declarations of the B200 JAX-SSO hot-path library (not part of the ABI).
 #pragma once
+#include <utility>
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -35,21 +36,17 @@ struct HostPattern {
 };
 
 // Upper-triangular (symmetric) node-block storage: node n keeps only the blocks
-// (n, m) with m >= n (the diagonal block first).  The transpose contribution
-// K_nm^T x_n of the k-th (k >= 1) upper block of node n is written to the
-// sender-ordered slot uptr[n] - n + k - 1 (contiguous per sender); node m sums
-// its incoming slots lslot[lptr[m] ..] in ascending source node.
+// (n, m) with m >= n (the diagonal block first).  Node m's incoming blocks (n, m),
+// n < m, are lpull[lptr[m] ..] in ascending source node n (the pull SpMV).
 struct UpperPattern {
   std::vector<int64_t> uptr;          // [n_nodes+1]
   std::vector<int32_t> ucol;          // [n_ublocks]
   std::vector<int32_t> urank;         // beams [Eb][4], quads [Eq][16]: rank in ucol(node_i) or -1
   std::vector<int64_t> ucontrib_ptr;  // [n_ublocks+1]
   std::vector<int32_t> ucontrib;      // staged block ids of upper blocks, ascending (e, i, j)
-  std::vector<int64_t> lptr;          // [n_nodes+1]
-  std::vector<int32_t> lslot;         // incoming sender slots, ascending source node
+  std::vector<int64_t> lptr;          // [n_nodes+1] incoming blocks per node
   std::vector<int32_t> lpull;         // [2 * incoming]: (source node n, upper block index of (n, m))
   int64_t n_ublocks() const { return (int64_t)ucol.size(); }
-  int64_t n_tslots = 0;
 };
 void build_upper(const HostPattern& P, const int32_t* beam_conn, const int32_t* quad_conn,
                  UpperPattern& U);
@@ -87,7 +84,26 @@ struct CgState {
   int defer_alpha;  // 1 = the SpMV leaves its p^T q partials (partial + PQ_OFF) and the fused
                     //     update forms p^T q and alpha in every CTA (no last-CTA tail)
   int npq;          // number of those partials (the SpMV grid)
+  // Lanczos history of the CG coefficients (Eq. 1 solved by CG; SURVEY
+  // §8(c) C5 "extract Lanczos extreme Ritz values from (alpha, beta)"): (alpha_k, beta_k) of
+  // every iteration of the first CG segment (recording stops at a restart), [lz_cap][2];
+  // lanczos.cu forms the extreme Ritz values of M^-1 K from it.
+  double* lz;
+  int lz_cap, lz_n, lz_frozen;
+  double lz_min, lz_max;
 };
+
+#ifdef __CUDACC__
+// Record iteration k's (alpha_k, beta_k); called by the one thread that completes an
+// iteration (fused update CTA 0, the last CTA of the classic update, cg_scalar_kernel).
+__device__ __forceinline__ void lz_record(CgState* st, double alpha, double beta) {
+  if (st->lz && !st->lz_frozen && st->lz_n < st->lz_cap) {
+    st->lz[2 * st->lz_n] = alpha;
+    st->lz[2 * st->lz_n + 1] = beta;
+    st->lz_n += 1;
+  }
+}
+#endif
 
 // error flags written by device kernels (atomicMin on the offending index)
 struct DevFlags {
@@ -119,7 +135,6 @@ struct BatchStrides {
   int64_t dof = 0;      // vectors [B][6 n]
   int64_t partial = 0;  // per-CTA partials [B][..]
   int64_t slot = 0;     // gradient slot partials [B][3 n_slots]
-  int64_t tbuf = 0;     // symmetric-storage transpose slots [B][6 n_tslots]
 };
 
 // Launch wrappers (implemented in the .cu files).  All are stream-ordered.
@@ -184,23 +199,6 @@ void launch_cg_update_block_fused(cudaStream_t s, int n_nodes, const double* bin
 void launch_cg_pfix_z(cudaStream_t s, int ndof, const double* z, const double* pin, double* pout,
                       const CgState* st, const BatchStrides& bs);
 int cg_block_fused_grid();
-// Symmetric (upper-block) storage SpMV: pass 1 streams the upper runs (TMA ring),
-// writes the upper row sums to y and the transpose contributions K_nm^T x_n to
-// tbuf; pass 2 adds each node's incoming slots (ascending source node) and, with
-// st != nullptr, forms p^T q and alpha like launch_spmv_dot.
-void launch_spmv_sym(cudaStream_t s, int n_nodes, const int64_t* uptr, const int32_t* ucol,
-                     const double* vals, const double* x, double* y, double* tbuf,
-                     const int64_t* lptr, const int32_t* lslot, const BatchStrides& bs = BatchStrides());
-// CG with symmetric storage: pass 1 only (upper row sums -> y, transpose slots,
-// p^T K p and alpha); the receiver sums are folded into launch_cg_update_sym.
-void launch_spmv_sym_cg(cudaStream_t s, int n_nodes, const int64_t* uptr, const int32_t* ucol,
-                        const double* vals, const double* p, double* y,
-                        double* tbuf, double* partial, CgState* st,
-                        const BatchStrides& bs = BatchStrides());
-void launch_cg_update_sym(cudaStream_t s, int ndof, const double* dinv, double* x, double* r,
-                          const double* p, const double* yup, const double* tbuf, const int64_t* lptr,
-                          const int32_t* lslot, double* partial, CgState* st,
-                          const BatchStrides& bs = BatchStrides());
 // Symmetric pull SpMV (storage 3): upper node blocks stored column-major per run;
 // the row-owner warp streams its upper run and the upper blocks (n, m) of its lower
 // neighbours (pull list lpull = [(n, upper block index)] per node, via lptr) and
@@ -239,8 +237,7 @@ void launch_spmv(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
                  const int32_t* node_col, const double* vals, const double* x, double* y,
     const BatchStrides& bs = BatchStrides());
 // Node-block Jacobi preconditioner (sso_options.precond = 1, block_jacobi.cu).  binv
-// [B][21][n] packed upper triangles of (K_nn)^-1; layout 0 full runs, 2 upper row-major
-// runs, 3 upper column-major runs.
+// [B][21][n] packed upper triangles of (K_nn)^-1; layout 0 full runs, 3 upper-block records.
 void launch_block_inverse(cudaStream_t s, int n_nodes, const int64_t* node_ptr, const int32_t* node_col,
                           const double* vals, int layout, double* binv, DevFlags* flags,
                           const BatchStrides& bs = BatchStrides());
@@ -256,6 +253,16 @@ void launch_cg_pupdate_z(cudaStream_t s, int ndof, const double* z, double* p, C
 void launch_cg_replace_block(cudaStream_t s, int n_nodes, const double* fbc, const double* Kx, const double* binv,
                              double* r, double* z, double* partial, CgState* st, int mode,
                              const BatchStrides& bs = BatchStrides());
+// Lanczos certification (lanczos.cu): extreme Ritz values of M^-1 K from the recorded CG
+// coefficients of every design (st->lz_min / lz_max; Tbuf scratch [B][cap][2]); the
+// end-of-solve sums red[0..3] = |r|^2, r^T M^-1 r, f_bc^T x, x^T x of the true residual
+// (binv != nullptr: node-block M); the per-design M scale (min 1/dinv or 1/|Binv_n|_F)
+// as the bit pattern of a positive double, atomicMin-reduced into out[B] (pre-set to ~0).
+void launch_lanczos_ritz(cudaStream_t s, CgState* st, double* Tbuf, int cap, int B);
+void launch_cert_sums(cudaStream_t s, int n_nodes, const double* fbc, const double* Kx, const double* x,
+                      const double* dinv, const double* binv, double* partial, CgState* st, const BatchStrides& bs);
+void launch_mscale(cudaStream_t s, int n_nodes, const double* dinv, const double* binv, unsigned long long* out,
+                   const BatchStrides& bs);
 void launch_residual_norm(cudaStream_t s, int ndof, const double* f, const double* Kx,
                           double* partial, CgState* st,
     const BatchStrides& bs = BatchStrides());
@@ -346,6 +353,30 @@ extern long long g_launches;  // launch counter (per process; handles add their 
   } while (0)
 void note_launch_error(const char* name, cudaError_t e);
 const char* last_launch_error();
+
+// Cooperative launch (cudaLaunchAttributeCooperative) for the kernels with a grid-wide
+// barrier: the driver guarantees that every CTA is co-resident or rejects the launch
+// (cudaErrorCooperativeLaunchTooLarge) instead of leaving CTAs spinning on CTAs that
+// cannot be scheduled (a shared GPU, MPS, concurrent streams).  Captures into graphs.
+template <typename... K, typename... A>
+inline cudaError_t launch_cooperative(void (*kern)(K...), dim3 grid, dim3 block, cudaStream_t s, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+}
+#define SSO_POST_LAUNCH_RC(name, rc)                           \
+  do {                                                         \
+    ++::sso::g_launches;                                       \
+    if ((rc) != cudaSuccess) ::sso::note_launch_error(name, rc); \
+  } while (0)
 
 }  // namespace sso
 

@@ -271,12 +271,11 @@ def test_fused_assembly_matches_staged(sso, make):
     assert np.allclose(mf.export_dinv(), ms.export_dinv(), rtol=1e-14, atol=0)
 
 
-@pytest.mark.parametrize("storage", [2, 3])
+@pytest.mark.parametrize("storage", [3])
 @pytest.mark.parametrize("make", [W.config2, mixed, W.config1, lambda: W.shell_config3(40, cfg=3)])
 def test_symmetric_storage_matches_full(sso, make, storage):
-    """Upper-block (symmetric) storage -- two-pass transpose SpMV (2) or one-pass pull
-    SpMV over column-major runs (3) -- reproduces the full-storage operator, solve and
-    gradient."""
+    """Upper-block (symmetric) storage with the one-pass pull SpMV (3) reproduces the
+    full-storage operator, solve and gradient."""
     P = make()
     ms = sso.Model(P, rtol=1e-12, storage=storage)
     mf = sso.Model(P, rtol=1e-12, storage=1)
@@ -453,7 +452,7 @@ def test_block_jacobi_batched_and_partitioned(sso):
     _, i0 = m0.solve(P["f"])
     assert i1["iters"] < i0["iters"]
     with pytest.raises(Exception):
-        sso.Model(P, precond=1, storage=2)
+        sso.Model(P, storage=2)   # the two-pass transpose layout is retired
     with pytest.raises(Exception):
         sso.Model(P, precond=2)
 
