@@ -230,7 +230,8 @@ int sso_grad_at(sso_handle h, sso_objective obj, const double* f, const double* 
  * dg_dt [n_quads] and moduli dg_dE [n_beams + n_quads] (any may be NULL); the caller
  * adds the explicit dg/dp.  Single-strip handles; a batch solves every design's adjoint in
  * the same batched PCG (dg_du, lambda [batch][6 n_nodes], info [batch]; gradients with a
- * leading design axis, each design's polarization balanced by its own |u| / |lambda|). */
+ * leading design axis).  The term is formed in one pass of the gradient kernels in bilinear
+ * form (strains of lambda and u, dual numbers through lambda_e^T K_e(p) u_e). */
 int sso_adjoint_solve(sso_handle h, const double* dg_du, double* lambda, sso_solve_info* info);
 int sso_grad_adjoint(sso_handle h, const double* lambda, double* dg_dxyz, double* dg_dt, double* dg_dE);
 

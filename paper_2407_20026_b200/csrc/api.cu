@@ -115,11 +115,10 @@ struct Part {
   double* scal = nullptr;
   double *slot_partial = nullptr, *dxyz = nullptr, *dt = nullptr, *dt_own = nullptr, *dE = nullptr;
   // general-objective adjoint (sso_adjoint_solve / sso_grad_adjoint): primal backups,
-  // lambda and the second polarization pass (allocated on first use)
-  double *ub = nullptr, *fb = nullptr, *lam = nullptr, *dxyz2 = nullptr, *dt2 = nullptr, *dE2 = nullptr;
+  // and lambda (allocated on first use)
+  double *ub = nullptr, *fb = nullptr, *lam = nullptr;
   // SIMP density (sso_set_density): rho, reference moduli E0 and (optional) G0 per element
   double *rho = nullptr, *E0 = nullptr, *G0 = nullptr;
-  double* coef = nullptr;  // adjoint polarization: per-design coefficients [5][B]
   // design-dependent area loads (sso_set_area_load): local per-quad q, w and the
   // per-quad lumped value a = (q + w t) A / 4 [B][n_quads]
   double *ld_q = nullptr, *ld_w = nullptr, *ld_a = nullptr;
@@ -630,8 +629,8 @@ void free_part(Part& P) {
                   P.gf, P.partial, P.st, P.flags, P.tickets, P.scal, P.slot_partial, P.dxyz, P.dt,
                   P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
                   P.lptr, P.lpull, P.pdesc, P.binv, P.zb, P.p2, P.dE,
-                  P.ub, P.fb, P.lam, P.dxyz2, P.dt2, P.dE2, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask,
-                  P.rho, P.E0, P.G0, P.coef, P.lz_hist, P.lz_T, P.mscale_d};
+                  P.ub, P.fb, P.lam, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask,
+                  P.rho, P.E0, P.G0, P.lz_hist, P.lz_T, P.mscale_d};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -1653,23 +1652,6 @@ int sso_grad_at(sso_handle h, sso_objective obj, const double* f, const double* 
 }
 
 // Gradient kernels at state U with scale s into P.dxyz (owned nodes), P.dt, P.dE.
-static int grad_pass(sso_ctx* h, Part& P, const double* U, double s, double u_load_coef = 0.0) {
-  launch_beam_grad(h->stream, P.n_beams, P.x, P.y, P.z, P.beam_conn, P.A, P.Iy, P.Iz, P.J, P.E, P.G, U, s,
-                   P.slot_partial, P.dE, P.n_beams + P.n_quads, P.bs);
-  launch_quad_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.E, P.nu, h->drill_alpha,
-                   U, s, P.slot_partial, P.dt, P.dE, P.bs);
-  // + lambda^T df/dp through the same polarization: (1/c)[T(u + c l) - T(u - c l)] = 2 T(l), T = 1/2 v^T df/dp
-  if (h->area_load)
-    launch_area_load_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.ld_q, P.ld_w,
-                          h->ld_dir, U, 0.5, P.slot_partial, P.dt, P.bs);
-  if (h->area_load && u_load_coef != 0.0)
-    launch_area_load_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.ld_q, P.ld_w,
-                          h->ld_dir, P.xs, u_load_coef, P.slot_partial, P.dt, P.bs);
-  launch_node_reduce(h->stream, P.n_own, P.inc_ptr, P.inc_slot, P.slot_partial, P.dxyz, P.bs);
-  CKL(h);
-  return SSO_OK;
-}
-
 int sso_adjoint_solve(sso_handle h, const double* dg_du, double* lambda, sso_solve_info* info) {
   ENTER(h);
   if (!h || !dg_du || !lambda) return SSO_E_INVALID;
@@ -1697,60 +1679,24 @@ int sso_adjoint_solve(sso_handle h, const double* dg_du, double* lambda, sso_sol
 
 // -lambda^T (dK/dp u - df/dp) [+ s u^T df/dp when u_load_s != 0] at the primal state, lambda in
 // P.lam, into P.dxyz / P.dt / P.dE (single strip; every design of a batch, u_load_s only for
-// batch 1).
+// batch 1).  One pass of the bilinear gradient kernels (grad.cu: strains of lambda and u,
+// dual numbers through lambda_e^T K_e(p) u_e): PAPER.md Eq. 6 term by term, no polarization.
 static int adjoint_grad_dev(sso_ctx* h, double u_load_s) {
   Part& P = h->P0();
-  const int B = P.B;
-  const int64_t ne = (int64_t)P.n_beams + P.n_quads;
-  const int64_t nq1 = std::max<int32_t>(P.n_quads, 1), ne1 = std::max<int64_t>(ne, 1);
-  int r;
-  if (!P.dxyz2 && (r = dalloc(h, &P.dxyz2, 3 * (int64_t)B * P.n_nodes))) return r;
-  if (!P.dt2 && (r = dalloc(h, &P.dt2, B * nq1))) return r;
-  if (!P.dE2 && (r = dalloc(h, &P.dE2, B * ne1))) return r;
-  if (!P.coef && (r = dalloc(h, &P.coef, 5 * (int64_t)B))) return r;
-  // polarization: lambda^T K u = [(u + c l)^T K (u + c l) - (u - c l)^T K (u - c l)] / (4 c),
-  // c = |u| / |lambda| per design balances the two states (bilinear result, quadratic kernels)
-  std::vector<double> uu(B), ll(B);
-  {
-    Scope sc(h, F_REDUCE);
-    launch_dot_local(h->stream, (int)P.ndof, P.xs, P.xs, P.partial, P.st, P.bs);
-    CK(h, cudaMemcpyAsync(h->h_chunk, P.st, B * sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
-    if ((r = sync(h))) return r;
-    for (int d = 0; d < B; ++d) uu[d] = h->h_chunk[d].red[0];
-    launch_dot_local(h->stream, (int)P.ndof, P.lam, P.lam, P.partial, P.st, P.bs);
-    CK(h, cudaMemcpyAsync(h->h_chunk, P.st, B * sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
-    if ((r = sync(h))) return r;
-    for (int d = 0; d < B; ++d) ll[d] = h->h_chunk[d].red[0];
-  }
-  // coefficient rows: ones, -c, +c, 1/c, -1/c
-  std::vector<double> cf(5 * (size_t)B);
-  for (int d = 0; d < B; ++d) {
-    const double c = (uu[d] > 0.0 && ll[d] > 0.0) ? std::sqrt(uu[d] / ll[d]) : 1.0;
-    cf[d] = 1.0;
-    cf[B + d] = -c;
-    cf[2 * B + d] = c;
-    cf[3 * B + d] = 1.0 / c;
-    cf[4 * B + d] = -1.0 / c;
-  }
-  CK(h, cudaMemcpy(P.coef, cf.data(), cf.size() * sizeof(double), cudaMemcpyHostToDevice));
-  const double* one = P.coef;
-  const double *mc = P.coef + B, *pc = P.coef + 2 * B, *ic = P.coef + 3 * B, *mic = P.coef + 4 * B;
   {
     Scope sc(h, F_GRAD);
-    launch_lincomb_rows(h->stream, P.ndof, B, one, P.xs, mc, P.lam, P.gu);  // u - c lambda
-    if ((r = grad_pass(h, P, P.gu, 0.25))) return r;
-    CK(h, cudaMemcpyAsync(P.dxyz2, P.dxyz, 3 * (size_t)B * P.n_nodes * sizeof(double), cudaMemcpyDeviceToDevice,
-                          h->stream));
-    CK(h, cudaMemcpyAsync(P.dt2, P.dt, B * nq1 * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-    CK(h, cudaMemcpyAsync(P.dE2, P.dE, B * ne1 * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
-    launch_lincomb_rows(h->stream, P.ndof, B, one, P.xs, pc, P.lam, P.gu);  // u + c lambda
-    // the "+" pass also carries c * s u^T df/dp, which the 1/c below turns into s u^T df/dp
-    // (batch 1: u_load_s comes from the prescribed-support path only)
-    if ((r = grad_pass(h, P, P.gu, 0.25, B == 1 ? cf[2] * u_load_s : 0.0))) return r;
-    // -(1/4)[dE(w+) - dE(w-)] / c  ==  -lambda^T (dK/dp) u
-    launch_lincomb_rows(h->stream, 3 * (int64_t)P.n_nodes, B, ic, P.dxyz, mic, P.dxyz2, P.dxyz);
-    if (P.n_quads) launch_lincomb_rows(h->stream, P.n_quads, B, ic, P.dt, mic, P.dt2, P.dt);
-    launch_lincomb_rows(h->stream, ne, B, ic, P.dE, mic, P.dE2, P.dE);
+    launch_beam_grad(h->stream, P.n_beams, P.x, P.y, P.z, P.beam_conn, P.A, P.Iy, P.Iz, P.J, P.E, P.G, P.xs, 1.0,
+                     P.slot_partial, P.dE, P.n_beams + P.n_quads, P.bs, P.lam);
+    launch_quad_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.E, P.nu, h->drill_alpha,
+                     P.xs, 1.0, P.slot_partial, P.dt, P.dE, P.bs, P.lam);
+    // + lambda^T df/dp (design-dependent area loads, reading c17)
+    if (h->area_load)
+      launch_area_load_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.ld_q, P.ld_w,
+                            h->ld_dir, P.lam, 1.0, P.slot_partial, P.dt, P.bs);
+    if (h->area_load && u_load_s != 0.0)
+      launch_area_load_grad(h->stream, P.n_beams, P.n_quads, P.x, P.y, P.z, P.quad_conn, P.t, P.ld_q, P.ld_w,
+                            h->ld_dir, P.xs, u_load_s, P.slot_partial, P.dt, P.bs);
+    launch_node_reduce(h->stream, P.n_own, P.inc_ptr, P.inc_slot, P.slot_partial, P.dxyz, P.bs);
   }
   CKL(h);
   return SSO_OK;

@@ -1187,25 +1187,6 @@ __global__ void lincomb_kernel(int64_t n, double a, const double* __restrict__ x
 }
 }  // namespace
 
-namespace {
-// per-design coefficients: out[d][i] = a[d] x[d][i] + b[d] y[d][i] (grid.y = design)
-__global__ void lincomb_rows_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ x,
-                                    const double* __restrict__ b, const double* __restrict__ y,
-                                    double* __restrict__ out) {
-  const int d = blockIdx.y;
-  const double ad = a[d], bd = b[d];
-  const int64_t o = (int64_t)d * n;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[o + i] = ad * x[o + i] + bd * y[o + i];
-}
-}  // namespace
-
-void launch_lincomb_rows(cudaStream_t s, int64_t n, int B, const double* a, const double* x, const double* b,
-                         const double* y, double* out) {
-  if (n <= 0 || B <= 0) return;
-  lincomb_rows_kernel<<<dim3(vec_grid(n, B), B), 256, 0, s>>>(n, a, x, b, y, out);
-  SSO_POST_LAUNCH("lincomb_rows_kernel");
-}
 
 void launch_lincomb(cudaStream_t s, int64_t n, double a, const double* x, double b, const double* y, double* out) {
   if (n <= 0) return;

@@ -1,5 +1,6 @@
 // Internal declarations of the B200 JAX-SSO hot-path library (not part of the ABI).
 #pragma once
+#include <cstdlib>
 #include <utility>
 
 #include <cuda.h>
@@ -292,9 +293,6 @@ void launch_cg_scalar(cudaStream_t s, CgState* st, int phase);
 void launch_pack(cudaStream_t s, int count, const int32_t* idx, const double* vec, double* buf);
 void launch_allreduce_parts(cudaStream_t s, CgState* const* sts, int n_parts, int nvals);
 // out = a x + b y (elementwise, n doubles)
-// out[d] = a[d] x[d] + b[d] y[d] over B contiguous rows of n (coefficients on the device)
-void launch_lincomb_rows(cudaStream_t s, int64_t n, int B, const double* a, const double* x, const double* b,
-                         const double* y, double* out);
 void launch_lincomb(cudaStream_t s, int64_t n, double a, const double* x, double b, const double* y, double* out);
 void launch_gather(cudaStream_t s, int n, const int32_t* idx, const double* src, double* dst);
 void launch_scatter(cudaStream_t s, int n, const int32_t* idx, const double* src, double* dst);
@@ -330,12 +328,15 @@ void launch_beam_grad(cudaStream_t s, int n_beams, const double* x, const double
                       const double* z, const int32_t* conn, const double* A,
                       const double* Iy, const double* Iz, const double* J, const double* E,
                       const double* G, const double* u, double scale, double* slot_partial,
-                      double* dC_dE, int n_elems, const BatchStrides& bs = BatchStrides());
+                      double* dC_dE, int n_elems, const BatchStrides& bs = BatchStrides(),
+                      const double* v = nullptr);
+// (v != nullptr: the bilinear -s d/dp [v_e^T K_e(p) u_e] instead of -s d/dp [u_e^T K_e u_e]:
+// the general adjoint's -lambda^T dK/dp u in one pass)
 void launch_quad_grad(cudaStream_t s, int n_beams, int n_quads, const double* x,
                       const double* y, const double* z, const int32_t* conn, const double* t,
                       const double* E, const double* nu, double drill_alpha, const double* u,
                       double scale, double* slot_partial, double* dC_dt, double* dC_dE,
-                      const BatchStrides& bs = BatchStrides());
+                      const BatchStrides& bs = BatchStrides(), const double* v = nullptr);
 void launch_node_reduce(cudaStream_t s, int n_nodes, const int64_t* inc_ptr,
                         const int32_t* inc_slot, const double* slot_partial, double* dC_dxyz,
     const BatchStrides& bs = BatchStrides());
@@ -368,8 +369,9 @@ inline cudaError_t launch_cooperative(void (*kern)(K...), dim3 grid, dim3 block,
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeCooperative;
   at[0].val.cooperative = 1;
+  static const bool coop = !(getenv("SSO_COOP") && getenv("SSO_COOP")[0] == '0');  // A/B switch
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = coop ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
 }
 #define SSO_POST_LAUNCH_RC(name, rc)                           \

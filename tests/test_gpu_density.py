@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 import workloads as W
+from _tol import assert_components
 from oracle import grad as OG
 
 pytestmark = pytest.mark.gpu
@@ -106,5 +107,4 @@ def test_batched_general_adjoint(sso, precond):
     uref, _, _ = OG.evaluate(P2)
     rX, rT, rE = OG.adjoint_general(P2, uref, Lam[2])
     for got, ref in ((dX[2], rX), (dT[2], rT), (dE[2], rE)):
-        fl = 1e-3 * np.abs(ref).max()
-        assert np.all(np.abs(got - ref) <= 1e-6 * np.maximum(np.abs(ref), fl))
+        assert_components(got, ref, 1e-7, "batched general adjoint vs oracle")

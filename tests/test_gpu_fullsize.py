@@ -209,11 +209,14 @@ def test_c5_full_batch_sampled():
         m1.assemble()
         u1, _ = m1.solve(d["f"])
         C1, dX1, dT1 = m1.grad()
-        assert np.linalg.norm(U[b] - u1) <= 1e-8 * np.linalg.norm(u1)
-        assert C[b] == pytest.approx(C1, rel=1e-9)
+        assert np.linalg.norm(U[b] - u1) <= 1e-9 * np.linalg.norm(u1)
+        assert C[b] == pytest.approx(C1, rel=1e-10)
         m1.close()
-    uref, _, _ = OG.evaluate(designs[63], "pcg", rtol=1e-12)
-    assert np.linalg.norm(U[63] - uref) <= 1e-8 * np.linalg.norm(uref)
+    uref, _, _ = OG.evaluate(designs[63], "pcg", rtol=1e-13)
+    err = np.linalg.norm(U[63] - uref) / np.linalg.norm(uref)
+    print(f"C5 design 63: |u - u_oracle| / |u_oracle| = {err:.3e}, estimate {infos[63]['err2_est']:.3e}")
+    assert err <= 1e-9
+    assert err <= 1.01 * infos[63]["err2_est"] + 1e-13
 
 
 def test_c3b_eight_strips(c3b):
@@ -229,7 +232,11 @@ def test_c3b_eight_strips(c3b):
     u8, i8 = m8.solve(P["f"])
     assert i8["status"] == 0 and i8["true_rel_res"] <= 20 * RTOL_BENCH
     assert abs(i8["iters"] - i1["iters"]) <= 0.02 * i1["iters"]
-    assert np.linalg.norm(u8 - u1) <= 1e-6 * np.linalg.norm(u1)
+    d = np.linalg.norm(u8 - u1) / np.linalg.norm(u1)
+    print(f"C3b 8 strips vs 1: |u8 - u1| / |u1| = {d:.3e}; estimates {i8['err2_est']:.3e}, {i1['err2_est']:.3e}")
+    # two CG solutions to rtol 1e-10: they differ by at most the sum of their errors
+    assert d <= 1.01 * (i8["err2_est"] + i1["err2_est"]) + 1e-13
+    assert d <= 1e-6
     C8, _, _ = m8.grad()
     C1, _, _ = m.grad()
     assert C8 == pytest.approx(C1, rel=1e-9)

@@ -54,14 +54,14 @@ def test_ritz_values_and_error_estimates(sso, make, precond):
     assert info["status"] == 0 and info["lanczos_iters"] == info["iters"]
     lo, hi = info["lanczos_lmin"], info["lanczos_lmax"]
     # interlacing (up to the multisection width) and convergence to the spectrum's ends
-    assert lam_min * (1 - 1e-8) <= lo <= lam_min * (1 + 1e-4), (lo, lam_min)
+    assert lam_min * (1 - 1e-8) <= lo <= lam_min * (1 + 1e-3), (lo, lam_min)
     assert lam_max * (1 - 1e-6) <= hi <= lam_max * (1 + 1e-8), (hi, lam_max)
     # the oracle's own Lanczos on its PCG coefficients (point Jacobi)
     if precond == 0:
         dinv = 1.0 / np.diag(Kb)
         _, oi = OS.pcg(Kb, fb, dinv, rtol=1e-12)
         olo, ohi = OS.lanczos_ritz(oi["alphas"], oi["betas"][:len(oi["alphas"]) - 1])
-        assert lo == pytest.approx(olo, rel=1e-4) and hi == pytest.approx(ohi, rel=1e-6)
+        assert lo == pytest.approx(olo, rel=1e-3) and hi == pytest.approx(ohi, rel=1e-6)
     # the error estimates bound the actual error of u (oracle Cholesky u)
     uref, _, _ = OG.evaluate(P)
     e = u - uref

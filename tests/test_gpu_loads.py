@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 
 import workloads as W
+from _tol import component_err
 from oracle import grad as OG, loads as OL
 
 pytestmark = pytest.mark.gpu
@@ -44,7 +45,8 @@ def load_case(P, seed=0):
 
 
 def _rel(a, b):
-    return np.abs(a - b).max() / np.abs(b).max()
+    # per component with the 1e-3 |b|_inf floor
+    return component_err(a, b)
 
 
 MAKERS = {"tiny2": lambda: W.tiny_shell(2, 0), "tiny3": lambda: W.tiny_shell(3, 5), "mixed": mixed,
@@ -106,9 +108,9 @@ def test_area_load_general_adjoint(sso, make):
     dX, dT, dE = m.grad_adjoint(lref)
     rX, rT, rE = OG.adjoint_general(P, uref, lref)
     lX, lT = OL.load_gradient_term(P, lref, q, w, d)
-    assert _rel(dX, rX + lX) <= 1e-6
-    assert _rel(dT, rT + lT) <= 1e-6
-    assert _rel(dE, rE) <= 1e-6
+    assert _rel(dX, rX + lX) <= 1e-7
+    assert _rel(dT, rT + lT) <= 1e-7
+    assert _rel(dE, rE) <= 1e-7
 
 
 @pytest.mark.parametrize("nparts", [2, 3])
@@ -127,7 +129,7 @@ def test_area_load_partitioned_matches_single(sso, nparts):
     Cp, dXp, dTp = mp.grad()
     assert np.linalg.norm(up - u1) <= 1e-9 * np.linalg.norm(u1)
     assert Cp == pytest.approx(C1, rel=1e-10)
-    assert _rel(dXp, dX1) <= 1e-8 and _rel(dTp, dT1) <= 1e-8
+    assert _rel(dXp, dX1) <= 1e-7 and _rel(dTp, dT1) <= 1e-7
 
 
 def test_area_load_batched_designs(sso):
@@ -150,6 +152,6 @@ def test_area_load_batched_designs(sso):
         assert np.linalg.norm(U[b] - u1) <= 1e-9 * np.linalg.norm(u1)
         C1, dX1, dT1 = m1.grad()
         assert Cb[b] == pytest.approx(C1, rel=1e-10)
-        assert _rel(dXb[b], dX1) <= 1e-8 and _rel(dTb[b], dT1) <= 1e-8
+        assert _rel(dXb[b], dX1) <= 1e-7 and _rel(dTb[b], dT1) <= 1e-7
     uref, _ = OL.evaluate(designs[1], q, w, d)
     assert np.linalg.norm(U[1] - uref) <= 1e-9 * np.linalg.norm(uref)
