@@ -4,13 +4,19 @@ reading c15), one step = one full pass of the hot path: A1+A2 element
 stiffness + assembly (sso_assemble), A3 Jacobi-PCG to rtol (sso_solve), A4
 compliance + adjoint gradient (sso_grad).  A0 (pattern) runs once at create.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3b|C4|C5]
+                  [--replicas] [--virtual-parts P] [--impl reference]
 
-N > 1 runs under torchrun (one rank per GPU): the same C3b evaluation split
-into N contiguous node strips, one per GPU, with the halo of p and the CG
-scalars exchanged through NCCL every iteration (strong scaling; DESIGN.md
-"Multi-GPU").  --virtual-parts P runs that partitioned algorithm with P strips
-on one GPU (in-process transport).
+N > 1 runs under torchrun (one rank per GPU).  By default the workload is split
+into N contiguous node strips, one per GPU: every CG iteration exchanges the halo
+of u over NCCL (overlapped with the interior rows' SpMV) and performs ONE
+allreduce of the CG scalars (single-reduction CG, csrc/cg_sr.cu) -- strong
+scaling (north_star "rows and elements partitioned across
+2/4/8 GPUs").  --replicas instead evaluates one seeded design per GPU
+(independent evaluations, no collective; weak scaling).  --virtual-parts P runs
+the partitioned algorithm with P strips on one GPU (in-process transport).
+--workload C4 is the north star's 6 M DOF partitioned configuration; C5 the
+batched design evaluation (64 designs per GPU).
 `--impl reference` times the CPU oracle (oracle/) on a bounded sample of the
 same workload on the host cores, extrapolated to the same metric.
 """
@@ -40,6 +46,21 @@ def measured_peaks():
             d = json.load(fh)
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+FLOP_ASM = 12495.0   # fp64 flop per quad, fused assembly (ncu exact DFMA/DMUL/DADD counts, profiles/r01)
+FLOP_GRAD = 37426.0  # fp64 flop per quad, forward-mode dual-number gradient (same source)
+
+
+def fp64_peak_tflops():
+    """DFMA peak measured on the box by tools/dfma_peak.cu (profiles/fp64_peak.json), else the
+    value derived from the guide's unit counts (64 FMA/clk/SM x 148 SMs x 1.965 GHz x 2)."""
+    p = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["tflops"]), "measured (profiles/fp64_peak.json, tools/dfma_peak.cu)"
+    return 37.2, "derived (64 DFMA/clk/SM x 148 SMs x 1.965 GHz)"
 
 
 def ncu_traffic(storage_kind):
@@ -113,35 +134,71 @@ def dist_env():
 # CPU oracle baseline (bounded sample, extrapolated to the C3b workload)
 # ----------------------------------------------------------------------------
 
-def oracle_sample(P, n_elem=2000, n_grad=1000, pcg_grid=60, pcg_iters=200):
-    """Times the oracle as it stands on a bounded sample of workload P:
-    element stiffness + DOK insertion per element, adjoint-gradient work per
-    element (complex step), and one Jacobi-PCG iteration per stored non-zero on
-    a same-family grid the oracle can assemble.  Returns per-unit seconds."""
-    from oracle import assembly as OA, grad as OG, solve as OS
-    import scipy.sparse as sp
+_WP = None
+
+
+def _worker_init(workload):
+    global _WP
     import workloads as W
-    nq = len(P["quad_conn"])
-    rng = np.random.default_rng(0)
-    X = OA.coords(P)
-    # A1 + A2: element matrices + DOK scatter for a sample of elements
-    elems = rng.choice(nq, n_elem, replace=False)
-    t0 = time.perf_counter()
+    _WP = {"C3b": W.config3b, "C4": W.config4}[workload]()
+
+
+def _worker_elems(elems):
+    """A1 + A2 on a chunk of elements (K_e + dict-of-keys insertion) and nothing else."""
+    from oracle import assembly as OA
+    X = OA.coords(_WP)
     dok = {}
     for e in elems:
-        Ke = OA.element_K(P, int(e), X)
-        dofs = OA.element_dofs(OA.element_nodes(P, int(e)))
+        Ke = OA.element_K(_WP, int(e), X)
+        dofs = OA.element_dofs(OA.element_nodes(_WP, int(e)))
         for a, ra in enumerate(dofs):
             for b, cb in enumerate(dofs):
                 dok[(ra, cb)] = dok.get((ra, cb), 0.0) + Ke[a, b]
-    t_elem = (time.perf_counter() - t0) / n_elem
-    # A4: adjoint gradient per element (13 complex-step element derivatives)
-    u = W.random_state(len(P["x"]), 1)
-    t0 = time.perf_counter()
-    for e in elems[:n_grad]:
-        OG.element_grad(P, int(e), u, 1.0, X)
-    t_grad = (time.perf_counter() - t0) / n_grad
-    # A3: PCG iteration cost per non-zero on a same-recipe grid
+    return len(elems)
+
+
+def _worker_grads(elems):
+    """A4 on a chunk of elements (13 complex-step element derivatives each)."""
+    import workloads as W
+    from oracle import assembly as OA, grad as OG
+    X = OA.coords(_WP)
+    u = W.random_state(len(_WP["x"]), 1)
+    for e in elems:
+        OG.element_grad(_WP, int(e), u, 1.0, X)
+    return len(elems)
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def oracle_sample(workload, n_quads, cores, n_elem_per_core=250, n_grad_per_core=40, pcg_grid=60,
+                  pcg_iters=200):
+    """Times the oracle as it stands on a bounded sample of the workload, on `cores` host
+    cores (SURVEY.md §8(d) "Oracle timing"): element stiffness + DOK insertion and the
+    complex-step adjoint gradient over a multiprocessing.Pool of `cores` workers (chunks of
+    seeded elements), and Jacobi-PCG iterations (scipy CSR SpMV, one thread) on a
+    same-recipe grid the oracle can assemble.  Returns per-unit seconds (elements per
+    second of the whole pool, PCG seconds per iteration per stored non-zero)."""
+    import multiprocessing as mp
+    from oracle import assembly as OA, solve as OS
+    import scipy.sparse as sp
+    import workloads as W
+    rng = np.random.default_rng(0)
+    n_elem, n_grad = n_elem_per_core * cores, n_grad_per_core * cores
+    elems = rng.choice(n_quads, max(n_elem, n_grad), replace=False)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores, initializer=_worker_init, initargs=(workload,)) as pool:
+        pool.map(_worker_elems, [elems[:1]] * cores)  # workers built their inputs
+        t0 = time.perf_counter()
+        pool.map(_worker_elems, np.array_split(elems[:n_elem], cores))
+        t_elem = (time.perf_counter() - t0) / n_elem
+        t0 = time.perf_counter()
+        pool.map(_worker_grads, np.array_split(elems[:n_grad], cores))
+        t_grad = (time.perf_counter() - t0) / n_grad
     Q = W.shell_config3(pcg_grid, cfg=3)
     nd = 6 * len(Q["x"])
     rp, ci, v = OA.csr_from_dok(OA.assemble_dok(Q), nd)
@@ -160,20 +217,28 @@ def oracle_rate(n_quads, nnz, cg_iters, t_elem, t_grad, t_it_nnz):
     return 1.0 / t_eval, t_eval
 
 
-C3B_NQ = N_GRID * N_GRID
-C3B_NNZ = 36 * ((N_GRID + 1) ** 2 + 4 * N_GRID * (N_GRID + 1) + 4 * N_GRID * N_GRID)
+def grid_nnz(n):
+    return 36 * ((n + 1) ** 2 + 4 * n * (n + 1) + 4 * n * n)
 
 
-def cpu_baseline_obj(P, cg_iters):
+WORKLOADS = {"C3b": (408, "C3b: 408x408 MITC-4 shell quads, 1 003 686 DOF (reading c15)"),
+             "C4": (1000, "C4: 1000x1000 MITC-4 shell quads, 6 012 006 DOF, edge y=0 clamped + 2 pinned corners")}
+
+
+def cpu_baseline_obj(workload, cg_iters, cores=None):
+    n = WORKLOADS[workload][0]
+    cores = cores or host_cores()
     t0 = time.perf_counter()
-    te, tg, ti = oracle_sample(P)
+    te, tg, ti = oracle_sample(workload, n * n, cores)
     wall = time.perf_counter() - t0
-    rate, t_eval = oracle_rate(C3B_NQ, C3B_NNZ, cg_iters, te, tg, ti)
-    return {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": (f"oracle timed on 2000 C3b elements (K_e + DOK), 1000 element gradients "
-                       f"(complex step) and 200 PCG iterations on a 60x60 same-recipe grid "
-                       f"({wall:.1f} s of CPU); extrapolated to C3b: {C3B_NQ} elements, "
-                       f"{C3B_NNZ} nnz, {cg_iters} CG iterations -> {t_eval:.1f} s per eval"),
+    rate, t_eval = oracle_rate(n * n, grid_nnz(n), cg_iters, te, tg, ti)
+    return {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": (f"oracle as it stands on {workload} (extrapolated, not a full run): {250 * cores} "
+                       f"elements (K_e + DOK) and {40 * cores} element gradients (complex step) over a "
+                       f"{cores}-process pool, 200 PCG iterations (scipy CSR, 1 thread) on a 60x60 "
+                       f"same-recipe grid; {wall:.1f} s wall; scaled to {n * n} elements, "
+                       f"{grid_nnz(n)} nnz, {cg_iters} CG iterations -> {t_eval:.1f} s per eval"),
+            "extrapolated": True,
             "per_unit_s": {"element": te, "grad_element": tg, "cg_iter_per_nnz": ti}}
 
 
@@ -181,31 +246,34 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    import workloads as W
-    P = W.config3b()
+    n, wname = WORKLOADS[args.workload if args.workload in WORKLOADS else "C3b"]
     cg_iters = args.cg_iters
+    cores = host_cores()
     times = []
     vals = []
     for k in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        te, tg, ti = oracle_sample(P, n_elem=200, n_grad=100, pcg_grid=32, pcg_iters=60)
+        te, tg, ti = oracle_sample(args.workload if args.workload in WORKLOADS else "C3b", n * n, cores,
+                                   n_elem_per_core=40, n_grad_per_core=6, pcg_grid=32, pcg_iters=60)
         dt = time.perf_counter() - t0
         if k >= args.warmup:
             times.append(dt)
-            vals.append(oracle_rate(C3B_NQ, C3B_NNZ, cg_iters, te, tg, ti)[0])
+            vals.append(oracle_rate(n * n, grid_nnz(n), cg_iters, te, tg, ti)[0])
     value = float(np.median(vals))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 / value, "higher_is_better": True,
-            "scaling": "strong" if args.strips else "weak",  # the label of the arm it is compared with
+            # the label of the GPU arm it is compared with
+            "scaling": "weak" if (world > 1 and args.replicas) else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C3b: 408x408 MITC-4 shell quads, 1 003 686 DOF (reading c15)",
-                       "rtol": RTOL, "cg_iters": cg_iters},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": ("per step: oracle on 200 C3b elements (K_e + DOK), 100 element "
-                                        "gradients, 60 PCG iterations on a 32x32 same-recipe grid; "
-                                        f"extrapolated to C3b with {cg_iters} CG iterations; "
-                                        f"median sample wall {np.median(times):.2f} s")},
+            "config": {"workload": wname, "rtol": RTOL, "cg_iters": cg_iters},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "extrapolated": True,
+                             "sample": (f"per step (extrapolated, not a full run): oracle on {40 * cores} "
+                                        f"elements (K_e + DOK) and {6 * cores} element gradients over a "
+                                        f"{cores}-process pool, 60 PCG iterations (scipy CSR, 1 thread) on "
+                                        f"a 32x32 same-recipe grid; scaled to {args.workload} with "
+                                        f"{cg_iters} CG iterations; median sample wall {np.median(times):.2f} s")},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -227,29 +295,31 @@ def run_gpu(args):
     import paper_2407_20026_b200 as sso
     import workloads as W
 
-    # N > 1: by default every GPU evaluates its own C3b design (independent evaluations, as
-    # in an optimisation loop over designs; weak scaling, no collective).  --strips splits one
-    # C3b into N node strips with NCCL halos and allreduces instead (strong scaling).
-    replicas = world > 1 and not args.strips
-    P = W.shell_config3(408, cfg=3, design=rank) if replicas else W.config3b()
+    # N > 1: the workload split into N node strips over NCCL (strong scaling, the default);
+    # --replicas: every GPU evaluates its own seeded design of the workload (weak scaling).
+    replicas = world > 1 and args.replicas
+    n_grid, wname = WORKLOADS[args.workload]
+    cfg, sup = (4, "c4") if args.workload == "C4" else (3, "clamped_edges")
+    P = W.shell_config3(n_grid, cfg=cfg, supports=sup, design=rank if replicas else 0)
     t0 = time.perf_counter()
     stream = torch.cuda.current_stream()
     if replicas:
         m = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index, storage=args.storage,
                       precond=args.precond)
-        parallelism = f"{world} GPUs x one C3b design each (independent evaluations, no collective)"
+        parallelism = f"{world} GPUs x one {args.workload} design each (independent evaluations, no collective)"
     elif world > 1:
-        # strong scaling: C3b split into `world` node strips, one per GPU; halos of p
-        # and the CG scalars travel through NCCL
+        # strong scaling: the workload split into `world` node strips, one per GPU; halos of u
+        # and one allreduce of the CG scalars per iteration through NCCL
         import torch.distributed as dist
         obj = [sso.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         m = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index, nranks=world,
-                      rank=rank, nccl_id=obj[0])
-        parallelism = f"{world} node strips (NCCL halo + allreduce), strong scaling"
+                      rank=rank, nccl_id=obj[0], precond=args.precond)
+        parallelism = (f"{world} node strips (NCCL halo overlapped with the interior SpMV, one allreduce "
+                       f"per CG iteration), strong scaling")
     elif args.virtual_parts > 1:
         m = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index,
-                      n_parts=args.virtual_parts)
+                      n_parts=args.virtual_parts, precond=args.precond)
         parallelism = f"{args.virtual_parts} node strips on 1 GPU (in-process transport)"
     else:
         m = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index, storage=args.storage,
@@ -341,19 +411,15 @@ def run_gpu(args):
 
     # ---- roofline of the dominant kernel (SpMV inside PCG) --------------------
     peak, peak_src = measured_peaks()
-    # algorithmic bytes of the stored format: values + block column ids + node_ptr + x read,
-    # y written; symmetric storage adds the transpose slots (written and read back once)
+    # algorithmic bytes of the stored format (per rank: its owned rows)
     if symmetric == 3:  # values once + the 64-byte node descriptor (block columns, pull list) + p, q
         spmv_bytes = 8 * stored_vals + 64 * n_nodes + 16 * ndof
-    else:               # values + block column ids + node_ptr + p, q (+ transpose slots, storage 2)
+    else:               # values + block column ids + node_ptr + p, q
         spmv_bytes = 8 * stored_vals + 4 * stored_blocks + 8 * (n_nodes + 1) + 16 * ndof
-        if symmetric == 2:
-            spmv_bytes += 2 * 48 * (stored_blocks - n_nodes) + 8 * (n_nodes + 1) + 4 * (stored_blocks - n_nodes)
     spmv_avg_ms = spmv_ms / max(spmv_n, 1)
     achieved = spmv_bytes / (spmv_avg_ms / 1000.0) / 1e9 if spmv_n else None
     roofline = {"bound": "hbm",
                 "kernel": {0: "spmv_dot (CG q = K p, p^T q)",
-                           2: "spmv_sym pass1+pass2 (upper-block K, CG q = K p, p^T q)",
                            3: "spmv_pull_dot (upper-block K, one-pass pull, CG q = K p, p^T q)"}[symmetric],
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(symmetric),
@@ -362,11 +428,32 @@ def run_gpu(args):
                 "share_of_step": (spmv_avg_ms * (cg_iters + 1) * args.steps / ms_total) if spmv_n else None,
                 "sampling": "CUDA event pairs around every 16th SpMV launch of the CG loop (graph event nodes)"}
     asm_ms = (el_ms + as_ms) / max(args.steps, 1)
+    grad_ms = gr_ms / max(args.steps, 1)
     clocks = clk.summary()
+    # assembly and gradient rooflines: HBM on the survey's algorithmic bytes
+    # (CSR values written 8 nnz + dinv 8 DOF + coordinates 24 n + connectivity, t, rank map
+    # 88 E) and on the bytes the stored format writes; fp64 on the exact instruction counts
+    # (ncu, profiles/r01: 12 495 flop per quad assembled, 37 426 per quad gradient) against
+    # the on-box DFMA microbenchmark (profiles/fp64_peak.json) when present
+    fp64_peak, fp64_src = fp64_peak_tflops()
+    asm_bytes_survey = 8 * nnz + 8 * ndof + 24 * n_nodes + 88 * nq
+    asm_bytes_stored = (8 * 38 if symmetric == 3 else 8 * 36) * stored_blocks + 8 * ndof + 24 * n_nodes + 88 * nq
+    grad_bytes = 8 * ndof + 48 * n_nodes + 32 * nq + 192 * nq
+    rooflines = {
+        "assembly": {"ms": asm_ms, "hbm_bytes_survey": asm_bytes_survey, "hbm_bytes_stored": asm_bytes_stored,
+                     "hbm_frac_survey": asm_bytes_survey / (asm_ms / 1e3) / 1e9 / peak if asm_ms else None,
+                     "hbm_frac_stored": asm_bytes_stored / (asm_ms / 1e3) / 1e9 / peak if asm_ms else None,
+                     "flops": FLOP_ASM * nq, "fp64_frac": (FLOP_ASM * nq / (asm_ms / 1e3) / 1e12 / fp64_peak)
+                     if asm_ms else None},
+        "gradient": {"ms": grad_ms, "hbm_bytes": grad_bytes,
+                     "hbm_frac": grad_bytes / (grad_ms / 1e3) / 1e9 / peak if grad_ms else None,
+                     "flops": FLOP_GRAD * nq, "fp64_frac": (FLOP_GRAD * nq / (grad_ms / 1e3) / 1e12 / fp64_peak)
+                     if grad_ms else None},
+        "fp64_peak_tflops": fp64_peak, "fp64_peak_source": fp64_src, "hbm_peak_gbs": peak}
 
     # ---- the same evaluation with the node-block Jacobi preconditioner (reading c19) ----
     alt = None
-    if world == 1 and args.precond == 0 and args.virtual_parts == 1 and not args.no_alt:
+    if world == 1 and args.precond == 0 and args.virtual_parts == 1 and not args.no_alt and args.workload == "C3b":
         mb = sso.Model(P, rtol=RTOL, stream=stream.cuda_stream, device=dev.index, storage=args.storage,
                        precond=1)
 
@@ -391,22 +478,22 @@ def run_gpu(args):
 
     out = None
     if rank == 0:
-        cpu = cpu_baseline_obj(P, cg_iters) if (world == 1 and not args.no_cpu) else None
+        cpu = cpu_baseline_obj(args.workload, cg_iters) if (world == 1 and not args.no_cpu) else None
+        strong = (world > 1 and not replicas) or args.virtual_parts > 1 or (world == 1 and not args.replicas)
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-               # the default series (N = 1, 2, 4, ...: one design per GPU) is weak scaling; the
-               # strip modes split one C3b (strong)
-               "scaling": "strong" if (args.strips or args.virtual_parts > 1) else "weak",
+               # the default series (N = 1, 2, 4, 8) splits one workload into N strips: strong
+               "scaling": "strong" if strong else "weak",
                "vs_baseline": None, "dtype": "f64",
-               "data": "synthetic (workloads.config3b, seeded)",
-               "config": {"workload": "C3b: 408x408 MITC-4 shell quads, 1 003 686 DOF (reading c15)",
-                          "n_nodes": n_nodes, "n_quads": nq, "ndof": ndof, "nnz": nnz,
+               "data": f"synthetic (workloads.shell_config3 {args.workload} recipe, seeded)",
+               "config": {"workload": wname,
+                          "n_nodes_per_rank": n_nodes, "n_quads_per_rank": nq, "ndof_per_rank": ndof, "nnz": nnz,
                           "rtol": RTOL, "cg_iters": cg_iters,
                           "parallelism": parallelism,
-                          "precond": {0: "point Jacobi", 1: "node-block Jacobi"}[args.precond if world == 1 else 0],
-                          "storage": {0: "full node-block CSR", 2: "upper blocks, two-pass SpMV",
-                                      3: "upper blocks (column-major runs), one-pass pull SpMV"}[symmetric],
-                          "l2": "working set > L2 (CSR values alone 432 MB vs 126 MB L2); no flush",
+                          "precond": {0: "point Jacobi", 1: "node-block Jacobi"}[args.precond],
+                          "storage": {0: "full node-block CSR",
+                                      3: "upper blocks (38-double 2x2 sub-block records), one-pass pull SpMV"}[symmetric],
+                          "l2": "working set > L2 (CSR values >= 254 MB vs 126 MB L2); no flush",
                           "pattern_build_s": t_create},
                "roofline": roofline,
                "cpu_baseline": cpu,
@@ -417,9 +504,12 @@ def run_gpu(args):
                "extra": {"assembled_elements_per_s": nq / (asm_ms / 1000.0) if asm_ms else None,
                          "assembly_ms": asm_ms, "element_ms": el_ms / max(args.steps, 1),
                          "assemble_gather_ms": as_ms / max(args.steps, 1),
-                         "grad_ms": gr_ms / max(args.steps, 1),
+                         "grad_ms": grad_ms,
                          "cg_iters_per_s": cg_iters / (ms_step / 1000.0),
                          "spmv_ms_per_step_est": spmv_avg_ms * (cg_iters + 1),
+                         "rooflines": rooflines,
+                         "certification": {k: info.get(k) for k in ("true_rel_res", "lanczos_iters", "lanczos_lmin",
+                                                                      "lanczos_lmax", "err_energy_est", "err2_est")},
                          "block_jacobi": alt}}
         print(json.dumps(out))
     if world > 1:
@@ -523,9 +613,9 @@ def main():
                     help="sso_options.precond for single-GPU C3b: 0 point Jacobi (north star), 1 node-block")
     ap.add_argument("--storage", type=int, default=0,
                     help="sso_options.storage for single-GPU C3b (0 = library default)")
-    ap.add_argument("--workload", default="C3b", choices=["C3b", "C5"])
-    ap.add_argument("--strips", action="store_true",
-                    help="N > 1: split one C3b into N node strips (NCCL) instead of one design per GPU")
+    ap.add_argument("--workload", default="C3b", choices=["C3b", "C4", "C5"])
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: one seeded design per GPU (independent, no collective) instead of N strips")
     ap.add_argument("--batch", type=int, default=64, help="C5 designs per GPU")
     ap.add_argument("--virtual-parts", type=int, default=1,
                     help="run the partitioned (strip) algorithm with P strips on one GPU")
@@ -533,7 +623,8 @@ def main():
     if args.impl == "reference":
         if args.cg_iters is None:
             p = os.path.join(ROOT, "profiles", "cg_iters_c3b.json")
-            args.cg_iters = json.load(open(p))["cg_iters"] if os.path.exists(p) else 10000
+            d = json.load(open(p)) if os.path.exists(p) else {}
+            args.cg_iters = d.get("cg_iters_" + args.workload, d.get("cg_iters", 10000)) if args.workload != "C5" else 0
         run_reference(args)
     elif args.workload == "C5":
         run_batch(args)

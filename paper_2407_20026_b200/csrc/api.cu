@@ -139,6 +139,10 @@ struct Part {
   bool cgf = false;                   // fused x / r / p update (cg_update_fused / _block_fused): one
                                       // part, full or pull storage, B <= the co-resident grid
   double* p2 = nullptr;               // cgf: the second p buffer (ping-pong)
+  // partitioned handles: single-reduction CG (cg_sr.cu) vectors u = M^-1 r and s = K p
+  double *u_sr = nullptr, *s_sr = nullptr;
+  // interior / boundary split of the owned rows: rows [bnd_lo, bnd_hi) need no halo value
+  int32_t bnd_lo = 0, bnd_hi = 0;
   // Lanczos certification (lanczos.cu): CG coefficient history [B][lz_cap][2], the
   // tridiagonal scratch of the same size, the M scale per design (device bits, host value)
   double *lz_hist = nullptr, *lz_T = nullptr;
@@ -194,6 +198,14 @@ struct sso_ctx {
   ncclComm_t comm = nullptr;
   std::vector<std::unique_ptr<Part>> parts;
   CgState** d_sts = nullptr;   // device array of the parts' CgState pointers
+  // in-process halo fill (one launch for all parts): entries (dst part, dst node, src part,
+  // src node) and, per vector kind, the device array of the parts' base pointers
+  int4* d_halo_ent = nullptr;
+  int n_halo_ent = 0;
+  double** d_vbase[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool split = false;          // overlap the halo exchange with the interior rows' SpMV
+  cudaStream_t side_stream = nullptr;  // halo exchange stream during capture (split)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double* d_dt_all = nullptr;  // virtual parts: global dC/dt assembly buffer
   double* h_C = nullptr;       // pinned scalar
 
@@ -381,13 +393,14 @@ struct Entry {
 // ---------------------------------------------------------------------------
 // Transports: halo exchange of a per-part vector and allreduce of CgState::red.
 // ---------------------------------------------------------------------------
-enum VecId { V_P = 0, V_X = 1, V_GU = 2, V_TMP = 3 };
+enum VecId { V_P = 0, V_X = 1, V_GU = 2, V_TMP = 3, V_U = 4 };
 
 double* vec_of(Part& P, int v) {
   switch (v) {
     case V_P: return P.p;
     case V_X: return P.xs;
     case V_GU: return P.gu;
+    case V_U: return P.u_sr;
     default: return P.tmp;
   }
 }
@@ -409,28 +422,13 @@ int exchange(sso_ctx* h, int v, cudaStream_t s = nullptr) {
   if (!h->distributed()) return SSO_OK;
   if (!s) s = h->stream;
   long long g0 = g_launches;
-  for (auto& pp : h->parts) {
-    Part& P = *pp;
+  if (h->nranks > 1) {
+    Part& P = h->P0();
     launch_pack(s, (int)P.n_send, P.send_idx, vec_of(P, v), P.sendbuf);
   }
   if (h->nranks == 1) {
-    // local transport: copy every neighbour's packed values into my halo
-    for (auto& pp : h->parts) {
-      Part& P = *pp;
-      double* dst = vec_of(P, v);
-      for (const NeighborPlan& nb : P.lm.nbrs) {
-        if (nb.recv_count == 0) continue;
-        Part& Q = *h->parts[nb.part];
-        size_t k = 0;
-        while (k < Q.lm.nbrs.size() && Q.lm.nbrs[k].part != P.lm.part) ++k;
-        if (k == Q.lm.nbrs.size() || (int64_t)Q.lm.nbrs[k].send_local.size() != nb.recv_count) {
-          h->err = "halo plan mismatch between parts";
-          return SSO_E_STATE;
-        }
-        CK(h, cudaMemcpyAsync(dst + 6 * ((int64_t)P.n_own + nb.recv_offset), Q.sendbuf + 6 * Q.send_off[k],
-                              (size_t)6 * nb.recv_count * sizeof(double), cudaMemcpyDeviceToDevice, s));
-      }
-    }
+    // local transport: one gather kernel fills every part's halo from its neighbours' owned rows
+    launch_halo_gather(s, h->n_halo_ent, h->d_halo_ent, h->d_vbase[v]);
   } else {
     Part& P = h->P0();
     double* dst = vec_of(P, v);
@@ -547,33 +545,45 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev, int it) {
       launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st, P.bs);
     return SSO_OK;
   }
+  // Partitioned: single-reduction CG (cg_sr.cu).  halo of u -> w = K u (+ local delta) ->
+  // one allreduce of (delta, gamma, r^T r, |f|^2) -> x / r / u / p / s update.  With the split,
+  // the halo travels on the side stream while the rows that need no halo value run.
+  if (h->split) {
+    CK(h, cudaEventRecord(h->ev_fork, s));
+    CK(h, cudaStreamWaitEvent(h->side_stream, h->ev_fork, 0));
+    if ((rc = exchange(h, V_U, h->side_stream))) return rc;
+    CK(h, cudaEventRecord(h->ev_join, h->side_stream));
+    if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
+    for (auto& pp : h->parts) {
+      Part& P = *pp;
+      launch_spmv_pull(s, &P.pull_tmap, P.bnd_hi, (int)(P.bs.nnz / PULL_BLOCK), P.pdesc, P.node_col, P.lpull,
+                       P.vals, P.u_sr, P.q, P.partial, P.st, P.bs, P.bnd_lo, 0);
+    }
+    CK(h, cudaStreamWaitEvent(s, h->ev_join, 0));
+    for (auto& pp : h->parts) {
+      Part& P = *pp;
+      launch_spmv_pull(s, &P.pull_tmap, P.bnd_lo, (int)(P.bs.nnz / PULL_BLOCK), P.pdesc, P.node_col, P.lpull,
+                       P.vals, P.u_sr, P.q, P.partial, P.st, P.bs, 0, 1);
+      launch_spmv_pull(s, &P.pull_tmap, P.n_own, (int)(P.bs.nnz / PULL_BLOCK), P.pdesc, P.node_col, P.lpull,
+                       P.vals, P.u_sr, P.q, P.partial, P.st, P.bs, P.bnd_hi, 1);
+    }
+    if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
+  } else {
+    if ((rc = exchange(h, V_U, s))) return rc;
+    bool first = true;
+    for (auto& pp : h->parts) {
+      Part& P = *pp;
+      if (ev && first) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
+      spmv_apply(s, P, P.u_sr, P.q, P.st);
+      if (ev && first) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
+      first = false;
+    }
+  }
+  if ((rc = allreduce(h, 4, s))) return rc;
   for (auto& pp : h->parts) {
     Part& P = *pp;
-    if (P.binv)
-      launch_cg_pupdate_z(s, (int)P.ndof_own, P.zb, P.p, P.st, P.bs);
-    else
-      launch_cg_pupdate(s, (int)P.ndof_own, P.dinv, P.r, P.p, P.st, P.bs);
+    launch_cgsr_update(s, P.n_own, P.dinv, P.binv, P.xs, P.r, P.u_sr, P.q, P.p, P.s_sr, P.partial, P.st);
   }
-  if ((rc = exchange(h, V_P, s))) return rc;
-  bool first = true;
-  for (auto& pp : h->parts) {
-    Part& P = *pp;
-    if (ev && first) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
-    spmv_apply(s, P, P.p, P.q, P.st);
-    if (ev && first) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
-    first = false;
-  }
-  if ((rc = allreduce(h, 1, s))) return rc;
-  for (auto& pp : h->parts) {
-    Part& P = *pp;
-    launch_cg_scalar(s, P.st, PH_ALPHA);
-    if (P.binv)
-      launch_cg_update_block(s, P.n_own, P.binv, P.xs, P.r, P.p, P.q, P.zb, P.partial, P.st, P.bs);
-    else
-      launch_cg_update(s, (int)P.ndof_own, P.dinv, P.xs, P.r, P.p, P.q, P.partial, P.st, P.bs);
-  }
-  if ((rc = allreduce(h, 2, s))) return rc;
-  for (auto& pp : h->parts) launch_cg_scalar(s, pp->st, PH_BETA);
   return SSO_OK;
 }
 
@@ -630,7 +640,7 @@ void free_part(Part& P) {
                   P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
                   P.lptr, P.lpull, P.pdesc, P.binv, P.zb, P.p2, P.dE,
                   P.ub, P.fb, P.lam, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask,
-                  P.rho, P.E0, P.G0, P.lz_hist, P.lz_T, P.mscale_d};
+                  P.rho, P.E0, P.G0, P.lz_hist, P.lz_T, P.mscale_d, P.u_sr, P.s_sr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -647,6 +657,12 @@ void free_all(sso_ctx* h) {
   for (auto& pp : h->parts) free_part(*pp);
   h->parts.clear();
   if (h->d_sts) cudaFree(h->d_sts);
+  if (h->d_halo_ent) cudaFree(h->d_halo_ent);
+  for (auto b : h->d_vbase)
+    if (b) cudaFree(b);
+  if (h->side_stream) cudaStreamDestroy(h->side_stream);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->d_dt_all) cudaFree(h->d_dt_all);
   if (h->h_C) cudaFreeHost(h->h_C);
   if (h->h_st) cudaFreeHost(h->h_st);
@@ -883,6 +899,31 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   }
   AL(q, B * P.ndof);
   AL(tmp, B * P.ndof);
+  if (L.n_parts > 1 || h->nranks > 1) {  // partitioned: single-reduction CG vectors (cg_sr.cu)
+    AL(u_sr, B * P.ndof);
+    AL(s_sr, B * P.ndof);
+    CK(h, cudaMemset(P.u_sr, 0, B * P.ndof * sizeof(double)));
+    // rows that read no halo value form the interior range [bnd_lo, bnd_hi): the widest run
+    // between owned nodes with a halo neighbour (strips of a grid: every row but the first
+    // and last node rows of the strip)
+    std::vector<int32_t> bnd;
+    for (int32_t n = 0; n < P.n_own; ++n)
+      for (int64_t k = P.pat.node_ptr[n]; k < P.pat.node_ptr[n + 1]; ++k)
+        if (P.pat.node_col[k] >= P.n_own) {
+          bnd.push_back(n);
+          break;
+        }
+    int32_t prev = -1, best = -1;
+    bnd.push_back(P.n_own);
+    for (int32_t b : bnd) {
+      if (b - prev - 1 > best) {
+        best = b - prev - 1;
+        P.bnd_lo = prev + 1;
+        P.bnd_hi = b;
+      }
+      prev = b;
+    }
+  }
   AL(gu, B * P.ndof);
   AL(gf, B * P.ndof);
   AL(partial, B * P.bs.partial);
@@ -1172,6 +1213,49 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
     h->user_nodes = mesh->n_nodes;
     h->user_quads = mesh->n_quads;
   }
+  if (h->parts.size() > 1) {  // in-process halo fill: one gather launch for all parts
+    std::vector<int4> ent;
+    for (size_t pi = 0; pi < h->parts.size(); ++pi) {
+      const Part& P = *h->parts[pi];
+      for (const NeighborPlan& nb : P.lm.nbrs) {
+        if (nb.recv_count == 0) continue;
+        const Part& Q = *h->parts[nb.part];
+        size_t k = 0;
+        while (k < Q.lm.nbrs.size() && Q.lm.nbrs[k].part != P.lm.part) ++k;
+        if (k == Q.lm.nbrs.size() || (int64_t)Q.lm.nbrs[k].send_local.size() != nb.recv_count) {
+          h->err = "halo plan mismatch between parts";
+          return bail(SSO_E_STATE);
+        }
+        for (int64_t i = 0; i < nb.recv_count; ++i)
+          ent.push_back(make_int4((int)pi, P.n_own + (int)(nb.recv_offset + i), nb.part,
+                                  Q.lm.nbrs[k].send_local[i]));
+      }
+    }
+    h->n_halo_ent = (int)ent.size();
+    int r = upload(h, &h->d_halo_ent, ent.data(), (int64_t)ent.size());
+    if (r) return bail(r);
+    for (int v = 0; v < 5; ++v) {
+      std::vector<double*> base;
+      for (auto& pp : h->parts) base.push_back(vec_of(*pp, v));
+      if ((r = upload(h, &h->d_vbase[v], base.data(), (int64_t)base.size()))) return bail(r);
+    }
+  }
+  if (h->distributed()) {
+    // overlap the halo exchange with the interior rows: NCCL ranks with pull storage (the SpMV
+    // takes row ranges); in-process parts only on request (SSO_SPLIT=1, for tests)
+    const char* env = getenv("SSO_SPLIT");
+    bool all_pull = true;
+    for (auto& pp : h->parts) all_pull &= pp->pull;
+    h->split = all_pull && (env ? env[0] == '1' : o.nranks > 1);
+    if (h->split) {
+      if (cudaStreamCreateWithFlags(&h->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        h->err = "stream / event create failed";
+        return bail(SSO_E_CUDA);
+      }
+    }
+  }
   {
     std::vector<CgState*> sts;
     for (auto& pp : h->parts) sts.push_back(pp->st);
@@ -1311,6 +1395,10 @@ static int replace_step(sso_ctx* h, int mode) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     launch_cg_check(h->stream, P.st, mode, P.B);
+    if (h->distributed()) {  // single-reduction CG: restart from the true residual (beta = 0 next)
+      launch_cgsr_replace(h->stream, P.n_own, P.fbc, P.tmp, P.dinv, P.binv, P.r, P.u_sr, P.partial, P.st);
+      continue;
+    }
     // fused form: a chunk (even length) ends with the current p in P.p, the previous in
     // P.p2; a replaced r re-forms p from the previous one (the classic form forms p in
     // the next iteration's p update)
@@ -1321,11 +1409,6 @@ static int replace_step(sso_ctx* h, int mode) {
       launch_cg_replace(h->stream, (int)P.ndof_own, P.fbc, P.tmp, P.dinv, P.r, P.p, P.partial, P.st, mode, P.bs);
       if (P.cgf) launch_cg_pfix(h->stream, (int)P.ndof_own, P.dinv, P.r, P.p2, P.p, P.st, P.bs);
     }
-  }
-  if (h->distributed()) {
-    if ((rc = allreduce(h, 2))) return rc;
-    for (auto& pp : h->parts)
-      launch_cg_scalar(h->stream, pp->st, mode == REPL_FINAL ? PH_REPLACED + 1 : PH_REPLACED);
   }
   h->launches += g_launches - g0;
   return SSO_OK;
@@ -1390,7 +1473,9 @@ static int solve_chunks(sso_ctx* h) {
         }
       }
       if (all_done || launched == k + 1) break;
-      if (h->reliable >= 2 && want_repl && (rc = replace_step(h, REPL_PERIODIC))) return rc;
+      // periodic replacements are a single-part refinement; the partitioned single-reduction CG
+      // restarts from the true residual at the end only
+      if (h->reliable >= 2 && want_repl && !h->distributed() && (rc = replace_step(h, REPL_PERIODIC))) return rc;
     }
     // converged by the recurrence: check the true residual, restart if it drifted
     if (h->reliable == 0) break;
@@ -1449,6 +1534,8 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
     h->h_st[bd].max_iter = h->max_iter;
     h->h_st[bd].dist = dist ? 1 : 0;
     h->h_st[bd].defer_alpha = (!dist && h->P0().cgf) ? 1 : 0;  // the fused update forms alpha
+    h->h_st[bd].tol2_rel = h->rtol * h->rtol;
+    if (dist) h->h_st[bd].ff = -1.0;  // single-reduction CG: |f_bc|^2 arrives with the first allreduce
   }
   for (auto& pp : h->parts) {
     for (int bd = 0; bd < h->batch; ++bd) {  // this part's Lanczos history
@@ -1469,18 +1556,15 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
   for (auto& pp : h->parts) {
     Part& P = *pp;
     Scope sc(h, F_UPDATE);
-    if (P.binv)
+    if (dist)  // single-reduction CG (cg_sr.cu): local gamma, r^T r, |f|^2 travel with the first allreduce
+      launch_cgsr_init(h->stream, P.n_own, P.f, P.fixed_mask, P.dinv, P.binv, P.fbc, P.xs, P.r, P.u_sr, P.p,
+                       P.s_sr, P.partial, P.st, warm, P.tmp);
+    else if (P.binv)
       launch_cg_init_block(h->stream, P.n_own, lift ? P.feff : P.f, P.fixed_mask, P.binv, P.fbc, P.xs, P.r, P.p,
                            P.zb, P.partial, P.st, warm, P.tmp, P.bs);
     else
       launch_cg_init(h->stream, (int)P.ndof_own, lift ? P.feff : P.f, P.fixed_mask, P.dinv, P.fbc, P.xs, P.r,
                      P.p, P.partial, P.st, warm, P.tmp, P.bs);
-  }
-  if (dist) {
-    if ((rc = allreduce(h, 3))) return rc;
-    long long g0 = g_launches;
-    for (auto& pp : h->parts) launch_cg_scalar(h->stream, pp->st, PH_INIT);
-    h->launches += g_launches - g0;
   }
   rc = solve_chunks(h);
   if (rc) return rc;

@@ -364,7 +364,8 @@ struct PullChunkSmem {
 
 template <bool DOT, int C, int NB, int MINB, int W>
 __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
-    const __grid_constant__ CUtensorMap tmap, int n_nodes, int rows_per_design, const int32_t* __restrict__ pdesc,
+    const __grid_constant__ CUtensorMap tmap, int n_nodes, int node0, int red_add, int rows_per_design,
+    const int32_t* __restrict__ pdesc,
     const int32_t* __restrict__ ucol, const int2* __restrict__ lpull, const double* __restrict__ vals,
     const double* __restrict__ p, double* __restrict__ q, double* __restrict__ partial, CgState* st,
     BatchStrides bs) {
@@ -391,7 +392,9 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
   }
   if (DOT && st->done) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n_chunks = (n_nodes + C - 1) / C;
+  // rows [node0, n_nodes): the whole owned range, or one piece of it (partitioned handles
+  // overlap the halo exchange with the rows that need no halo values)
+  const int n_chunks = (n_nodes - node0 + C - 1) / C;
   const int cnt = (int)blockIdx.x < n_chunks ? (n_chunks - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   double* sbase = reinterpret_cast<double*>(smem_raw);
   double* red_base = sbase + (size_t)NB * S::BUF;
@@ -411,7 +414,7 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
     const uint64_t pol = evict_first_policy();
     // descriptors of chunk k are loaded one chunk ahead (off the empty-barrier critical path)
     auto load_desc = [&](int k, int4& a, int4& b2, int4& c, int4& d) {
-      const int first = ((int)blockIdx.x + k * (int)gridDim.x) * C;
+      const int first = node0 + ((int)blockIdx.x + k * (int)gridDim.x) * C;
       a = b2 = c = d = make_int4(0, 0, 0, 0);
       if (k < cnt && lane < min(C, n_nodes - first)) {
         const int4* src = reinterpret_cast<const int4*>(pdesc + PULL_DESC * ((int64_t)first + lane));
@@ -430,7 +433,7 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
       if (k >= NB) mbar_wait(&empty_bar[b], (unsigned)(((k / NB) - 1) & 1));
       double* buf = sbase + (size_t)b * S::BUF;
       int32_t* D = reinterpret_cast<int32_t*>(buf + S::PULL + S::OWN);
-      const int first = ((int)blockIdx.x + k * (int)gridDim.x) * C;
+      const int first = node0 + ((int)blockIdx.x + k * (int)gridDim.x) * C;
       const int nc = min(C, n_nodes - first);
       if (lane < nc) {
         int4* dst = reinterpret_cast<int4*>(D + PULL_DESC * lane);
@@ -488,7 +491,7 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
       const double* buf = sbase + (size_t)b * S::BUF;
       const double* own = buf + S::PULL;
       const int32_t* D = reinterpret_cast<const int32_t*>(buf + S::PULL + S::OWN);
-      const int first = ((int)blockIdx.x + k * (int)gridDim.x) * C;
+      const int first = node0 + ((int)blockIdx.x + k * (int)gridDim.x) * C;
       const int nc = min(C, n_nodes - first);
       mbar_wait(&desc_bar[b], (unsigned)((k / NB) & 1));
       if (chunk_fits[b]) {
@@ -637,7 +640,7 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
       }
     } else if (grid_sum<1>(pq, partial, &st->ticket[0], sm) && threadIdx.x == 0) {
       if (st->dist) {
-        st->red[0] = pq[0];
+        st->red[0] = (red_add ? st->red[0] : 0.0) + pq[0];  // pieces add in launch order
         return;
       }
       st->pq = pq[0];
@@ -1328,9 +1331,9 @@ struct PullVariant {
   int minb;
   int threads;
   int chunk;  // nodes per CTA chunk
-  void (*dot)(const CUtensorMap, int, int, const int32_t*, const int32_t*, const int2*, const double*,
+  void (*dot)(const CUtensorMap, int, int, int, int, const int32_t*, const int32_t*, const int2*, const double*,
               const double*, double*, double*, CgState*, BatchStrides);
-  void (*plain)(const CUtensorMap, int, int, const int32_t*, const int32_t*, const int2*, const double*,
+  void (*plain)(const CUtensorMap, int, int, int, int, const int32_t*, const int32_t*, const int2*, const double*,
                 const double*, double*, double*, CgState*, BatchStrides);
 };
 #define PULL_CTA_VARIANT(C, NB, M, W)                                                                 \
@@ -1406,21 +1409,22 @@ int make_pull_tmap(const double* vals, int64_t rows, CUtensorMap* out) {
 
 void launch_spmv_pull(cudaStream_t s, const CUtensorMap* tmap, int n_nodes, int rows_per_design,
                       const int32_t* pdesc, const int32_t* ucol, const int32_t* lpull, const double* vals,
-                      const double* x, double* y, double* partial, CgState* st, const BatchStrides& bs) {
-  if (n_nodes <= 0) return;
+                      const double* x, double* y, double* partial, CgState* st, const BatchStrides& bs, int node0,
+                      int red_add) {
+  if (n_nodes <= node0) return;
   int smem;
   const PullVariant& V = pull_variant(bs.B, &smem);
   const int ctas = std::max(1, V.minb * (cg_grid() / 4) / bs.B);  // persistent: minb CTAs per SM in total
   const int chunk = V.chunk;
-  const int units = (n_nodes + chunk - 1) / chunk;
+  const int units = (n_nodes - node0 + chunk - 1) / chunk;
   const int grid = std::max(1, std::min(ctas, units));
   const int2* lp = reinterpret_cast<const int2*>(lpull);
   if (st)
-    V.dot<<<dim3(grid, bs.B), V.threads, smem, s>>>(*tmap, n_nodes, rows_per_design, pdesc, ucol, lp, vals,
-                                                         x, y, partial, st, bs);
+    V.dot<<<dim3(grid, bs.B), V.threads, smem, s>>>(*tmap, n_nodes, node0, red_add, rows_per_design, pdesc, ucol, lp,
+                                                         vals, x, y, partial, st, bs);
   else
-    V.plain<<<dim3(grid, bs.B), V.threads, smem, s>>>(*tmap, n_nodes, rows_per_design, pdesc, ucol, lp,
-                                                           vals, x, y, nullptr, nullptr, bs);
+    V.plain<<<dim3(grid, bs.B), V.threads, smem, s>>>(*tmap, n_nodes, node0, red_add, rows_per_design, pdesc, ucol,
+                                                           lp, vals, x, y, nullptr, nullptr, bs);
   SSO_POST_LAUNCH(st ? "spmv_pull_dot_kernel" : "spmv_pull_kernel");
 }
 

@@ -92,6 +92,10 @@ struct CgState {
   double* lz;
   int lz_cap, lz_n, lz_frozen;
   double lz_min, lz_max;
+  // single-reduction CG of partitioned handles (cg_sr.cu): rtol^2 (tol2 becomes rtol^2 |f_bc|^2
+  // once |f_bc|^2 is known, ff < 0 until then) and a restart flag (beta = 0 next)
+  double tol2_rel;
+  int sr_restart;
 };
 
 #ifdef __CUDACC__
@@ -204,10 +208,12 @@ int cg_block_fused_grid();
 // the row-owner warp streams its upper run and the upper blocks (n, m) of its lower
 // neighbours (pull list lpull = [(n, upper block index)] per node, via lptr) and
 // forms y = K x in one pass.  With st != nullptr also p^T q and alpha (CG).
+// Rows [node0, n_nodes) (default: all owned rows); on partitioned handles (st->dist) the
+// p^T q piece is written to st->red[0] (red_add = 0) or added to it (red_add = 1).
 void launch_spmv_pull(cudaStream_t s, const CUtensorMap* tmap, int n_nodes, int rows_per_design,
                       const int32_t* pdesc, const int32_t* ucol, const int32_t* lpull, const double* vals,
                       const double* x, double* y, double* partial, CgState* st,
-                      const BatchStrides& bs = BatchStrides());
+                      const BatchStrides& bs = BatchStrides(), int node0 = 0, int red_add = 0);
 // Storage 3 stores each upper 6x6 block as a record of PULL_BLOCK doubles: the nine 2x2
 // sub-blocks (A, B) = K[2A..2A+1][2B..2B+1], 4 doubles each (column-major inside), sub-block
 // 3B + A in slot PULL_SUB_POS nibble, and one 16-byte zero pad word (an odd 19-word record
@@ -254,6 +260,22 @@ void launch_cg_pupdate_z(cudaStream_t s, int ndof, const double* z, double* p, C
 void launch_cg_replace_block(cudaStream_t s, int n_nodes, const double* fbc, const double* Kx, const double* binv,
                              double* r, double* z, double* partial, CgState* st, int mode,
                              const BatchStrides& bs = BatchStrides());
+// Single-reduction Jacobi-PCG of partitioned handles (cg_sr.cu; Chronopoulos & Gear):
+// per iteration halo(u) -> w = K u (SpMV, delta = u^T w into red[0]) -> ONE allreduce of
+// red[0..3] -> update (alpha, beta from gamma = r^T u, delta; p = u + beta p, s = w + beta s,
+// x += alpha p, r -= alpha s, u = M^-1 r; local gamma, r^T r into red[1], red[2]).  binv !=
+// nullptr: node-block M.  init: f_bc, r = f_bc - K x0, u = M^-1 r, p = s = 0, red[1..3].
+void launch_cgsr_init(cudaStream_t s, int n_own, const double* f, const uint8_t* fixed_mask, const double* dinv,
+                      const double* binv, double* fbc, double* x, double* r, double* u, double* p, double* sv,
+                      double* partial, CgState* st, int warm, const double* Kx0);
+void launch_cgsr_update(cudaStream_t s, int n_own, const double* dinv, const double* binv, double* x, double* r,
+                        double* u, const double* w, double* p, double* sv, double* partial, CgState* st);
+void launch_cgsr_replace(cudaStream_t s, int n_own, const double* fbc, const double* Kx, const double* dinv,
+                         const double* binv, double* r, double* u, double* partial, CgState* st);
+// In-process halo fill of all parts in one launch: entry k = (dst part, dst node, src part,
+// src node) copies the 6 values of a node between the parts' vectors base[part].
+void launch_halo_gather(cudaStream_t s, int n_ent, const int4* ent, double* const* base);
+
 // Lanczos certification (lanczos.cu): extreme Ritz values of M^-1 K from the recorded CG
 // coefficients of every design (st->lz_min / lz_max; Tbuf scratch [B][cap][2]); the
 // end-of-solve sums red[0..3] = |r|^2, r^T M^-1 r, f_bc^T x, x^T x of the true residual

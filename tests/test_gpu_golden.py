@@ -1,0 +1,51 @@
+"""Full-solution parity at 242 406 DOF (config C3, BASELINE.json configs[2]) against the
+oracle's stored result (tests/golden/c3_oracle.npz, written by tools/make_golden_c3.py,
+which calls only oracle/: DOK assembly, textbook Jacobi-PCG to rtol 1e-13, complex-step
+adjoint gradient).  The default product path runs: upper-block storage with the pull SpMV
+(its ring of CTA chunks wraps the 40 401 nodes several times), the fused CG update,
+graph-chunked iterations, the fused assembly and the gradient kernels.
+
+Bars: |u - u_ref| / |u_ref| <= 1e-9, |C - C_ref| <= 1e-10 |C_ref|,
+gradients 1e-7 per component (floor 1e-3 of the sample's max).  The same design in 4
+in-process strips (partitioned path) is held to the same bars.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import workloads as W
+from _tol import assert_components
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "c3_oracle.npz")
+
+
+@pytest.fixture(scope="module")
+def gold():
+    if not os.path.exists(GOLD):
+        pytest.fail("tests/golden/c3_oracle.npz missing: run tools/make_golden_c3.py")
+    return dict(np.load(GOLD))
+
+
+@pytest.mark.parametrize("kw", [{}, {"n_parts": 4}, {"precond": 1}])
+def test_c3_against_oracle(gold, kw):
+    import paper_2407_20026_b200 as sso
+    P = W.config3()
+    m = sso.Model(P, rtol=1e-12, device=0, **kw)
+    m.assemble()
+    u, info = m.solve(P["f"])
+    assert info["status"] == 0
+    uref = gold["u"]
+    err = np.linalg.norm(u - uref) / np.linalg.norm(uref)
+    print(f"C3 {kw}: iters {info['iters']}, |u - u_ref|/|u_ref| = {err:.3e}, "
+          f"estimate {info['err2_est']:.3e}")
+    assert err <= 1e-9
+    C, dX, dT = m.grad()
+    Cref = float(gold["C"])
+    assert abs(C - Cref) <= 1e-10 * abs(Cref)
+    nodes, elems = gold["grad_nodes"], gold["grad_elems"]
+    assert_components(dX[:, nodes].T, gold["grad_X"], 1e-7, "dC/dX sample")
+    assert_components(dT[elems], gold["grad_t"], 1e-7, "dC/dt sample")
+    m.close()

@@ -3,9 +3,11 @@
 P contiguous node strips held by one handle on one GPU (in-process transport:
 device-to-device halo copies and a fixed-order allreduce of the CG scalars)
 run exactly the distributed algorithm the NCCL transport runs across GPUs:
-halo exchange of p every CG iteration, allreduce of p^T q and (r^T z, r^T r),
-halo of u before the gradient, owned-slice outputs.  Checked against the
-single-strip handle and the oracle:
+the single-reduction CG of csrc/cg_sr.cu (halo exchange of u = M^-1 r and ONE
+allreduce of (u^T K u, r^T u, r^T r) per iteration), optionally with the interior
+rows' SpMV overlapping the halo exchange (SSO_SPLIT=1: row ranges of the pull
+SpMV, side stream), halo of u before the gradient, owned-slice outputs.  Checked
+against the single-strip handle and the oracle:
 
   * strip-local assembled values concatenate to the global CSR bit-exactly;
   * u within 1e-9 of the oracle (Cholesky), C within 1e-10, gradients 1e-7;
@@ -99,17 +101,30 @@ def test_partitioned_matches_single_and_oracle(sso, name, make, nparts, ranges, 
     assert np.allclose(mp.spmv(x), m1.spmv(x), rtol=0, atol=1e-12 * np.abs(m1.spmv(x)).max())
 
 
-def test_partitioned_c3_family_iterations(sso):
-    """A 60x60 C3-recipe shell (clamped edges) in 4 strips: same solution, same iteration count."""
+@pytest.mark.parametrize("split", ["0", "1"])
+@pytest.mark.parametrize("precond", [0, 1])
+def test_partitioned_c3_family_iterations(sso, split, precond, monkeypatch):
+    """A 60x60 C3-recipe shell (clamped edges) in 4 strips: same solution and iteration count
+    (within 2) as one strip, with and without the interior / boundary split of the SpMV
+    (which also takes the row-range pieces of the pull kernel and the side-stream halo), and
+    the certification fields consistent with the single strip's."""
+    monkeypatch.setenv("SSO_SPLIT", split)
     P = W.shell_config3(60, cfg=3)
-    m1 = sso.Model(P, rtol=1e-10)
+    m1 = sso.Model(P, rtol=1e-10, precond=precond)
     m1.assemble()
-    m4 = sso.Model(P, rtol=1e-10, n_parts=4)
+    m4 = sso.Model(P, rtol=1e-10, n_parts=4, precond=precond)
     m4.assemble()
     u1, i1 = m1.solve(P["f"])
     u4, i4 = m4.solve(P["f"])
-    assert abs(i1["iters"] - i4["iters"]) <= 2
-    assert np.linalg.norm(u4 - u1) <= 1e-8 * np.linalg.norm(u1)
+    assert i4["status"] == 0 and abs(i1["iters"] - i4["iters"]) <= 2
+    d = np.linalg.norm(u4 - u1) / np.linalg.norm(u1)
+    assert d <= 1e-8 and d <= 1.01 * (i1["err2_est"] + i4["err2_est"]) + 1e-14
+    assert i4["lanczos_lmax"] == pytest.approx(i1["lanczos_lmax"], rel=1e-6)
+    assert i4["lanczos_lmin"] == pytest.approx(i1["lanczos_lmin"], rel=1e-3)
+    C1, dX1, dT1 = m1.grad()
+    C4, dX4, dT4 = m4.grad()
+    assert C4 == pytest.approx(C1, rel=1e-9)
+    assert_components(dX4, dX1, 1e-7, "dC/dX 4 strips vs 1")
 
 
 def test_batched_designs_match_single(sso):
