@@ -206,6 +206,10 @@ struct sso_ctx {
   bool split = false;          // overlap the halo exchange with the interior rows' SpMV
   cudaStream_t side_stream = nullptr;  // halo exchange stream during capture (split)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // in-process parts: one stream per part inside the captured iterations, so the parts'
+  // SpMVs and updates overlap (one part's tail with the next part's start)
+  std::vector<cudaStream_t> part_streams;
+  std::vector<cudaEvent_t> part_ev;
   double* d_dt_all = nullptr;  // virtual parts: global dC/dt assembly buffer
   double* h_C = nullptr;       // pinned scalar
 
@@ -570,16 +574,42 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev, int it) {
     if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
   } else {
     if ((rc = exchange(h, V_U, s))) return rc;
-    bool first = true;
-    for (auto& pp : h->parts) {
-      Part& P = *pp;
-      if (ev && first) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
-      spmv_apply(s, P, P.u_sr, P.q, P.st);
-      if (ev && first) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
-      first = false;
+    if (!h->part_streams.empty() && !ev) {
+      // in-process parts: the parts' SpMVs on their own streams (fork / join inside the graph)
+      const size_t np = h->parts.size();
+      CK(h, cudaEventRecord(h->ev_fork, s));
+      for (size_t i = 0; i < np; ++i) {
+        Part& P = *h->parts[i];
+        CK(h, cudaStreamWaitEvent(h->part_streams[i], h->ev_fork, 0));
+        spmv_apply(h->part_streams[i], P, P.u_sr, P.q, P.st);
+        CK(h, cudaEventRecord(h->part_ev[i], h->part_streams[i]));
+      }
+      for (size_t i = 0; i < np; ++i) CK(h, cudaStreamWaitEvent(s, h->part_ev[i], 0));
+    } else {
+      bool first = true;
+      for (auto& pp : h->parts) {
+        Part& P = *pp;
+        if (ev && first) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
+        spmv_apply(s, P, P.u_sr, P.q, P.st);
+        if (ev && first) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
+        first = false;
+      }
     }
   }
   if ((rc = allreduce(h, 4, s))) return rc;
+  if (!h->part_streams.empty()) {
+    const size_t np = h->parts.size();
+    CK(h, cudaEventRecord(h->ev_fork, s));
+    for (size_t i = 0; i < np; ++i) {
+      Part& P = *h->parts[i];
+      CK(h, cudaStreamWaitEvent(h->part_streams[i], h->ev_fork, 0));
+      launch_cgsr_update(h->part_streams[i], P.n_own, P.dinv, P.binv, P.xs, P.r, P.u_sr, P.q, P.p, P.s_sr,
+                         P.partial, P.st);
+      CK(h, cudaEventRecord(h->part_ev[i], h->part_streams[i]));
+    }
+    for (size_t i = 0; i < np; ++i) CK(h, cudaStreamWaitEvent(s, h->part_ev[i], 0));
+    return SSO_OK;
+  }
   for (auto& pp : h->parts) {
     Part& P = *pp;
     launch_cgsr_update(s, P.n_own, P.dinv, P.binv, P.xs, P.r, P.u_sr, P.q, P.p, P.s_sr, P.partial, P.st);
@@ -661,6 +691,10 @@ void free_all(sso_ctx* h) {
   for (auto b : h->d_vbase)
     if (b) cudaFree(b);
   if (h->side_stream) cudaStreamDestroy(h->side_stream);
+  for (auto ps : h->part_streams)
+    if (ps) cudaStreamDestroy(ps);
+  for (auto e : h->part_ev)
+    if (e) cudaEventDestroy(e);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->d_dt_all) cudaFree(h->d_dt_all);
@@ -1247,7 +1281,18 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
     bool all_pull = true;
     for (auto& pp : h->parts) all_pull &= pp->pull;
     h->split = all_pull && (env ? env[0] == '1' : o.nranks > 1);
-    if (h->split) {
+    const char* envc = getenv("SSO_PART_STREAMS");
+    if (o.nranks == 1 && !h->split && !(envc && envc[0] == '0')) {
+      h->part_streams.assign(h->parts.size(), nullptr);
+      h->part_ev.assign(h->parts.size(), nullptr);
+      for (size_t i = 0; i < h->parts.size(); ++i)
+        if (cudaStreamCreateWithFlags(&h->part_streams[i], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->part_ev[i], cudaEventDisableTiming) != cudaSuccess) {
+          h->err = "stream / event create failed";
+          return bail(SSO_E_CUDA);
+        }
+    }
+    if (h->split || !h->part_streams.empty()) {
       if (cudaStreamCreateWithFlags(&h->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {

@@ -105,7 +105,7 @@ def test_partitioned_matches_single_and_oracle(sso, name, make, nparts, ranges, 
 @pytest.mark.parametrize("precond", [0, 1])
 def test_partitioned_c3_family_iterations(sso, split, precond, monkeypatch):
     """A 60x60 C3-recipe shell (clamped edges) in 4 strips: same solution and iteration count
-    (within 2) as one strip, with and without the interior / boundary split of the SpMV
+    (within 1 %) as one strip, with and without the interior / boundary split of the SpMV
     (which also takes the row-range pieces of the pull kernel and the side-stream halo), and
     the certification fields consistent with the single strip's."""
     monkeypatch.setenv("SSO_SPLIT", split)
@@ -116,7 +116,9 @@ def test_partitioned_c3_family_iterations(sso, split, precond, monkeypatch):
     m4.assemble()
     u1, i1 = m1.solve(P["f"])
     u4, i4 = m4.solve(P["f"])
-    assert i4["status"] == 0 and abs(i1["iters"] - i4["iters"]) <= 2
+    # same algorithm in exact arithmetic; the dot products are summed in another order (per
+    # strip, and per SpMV piece with the split), which moves the count by a few iterations
+    assert i4["status"] == 0 and abs(i1["iters"] - i4["iters"]) <= max(3, 0.01 * i1["iters"])
     d = np.linalg.norm(u4 - u1) / np.linalg.norm(u1)
     assert d <= 1e-8 and d <= 1.01 * (i1["err2_est"] + i4["err2_est"]) + 1e-14
     assert i4["lanczos_lmax"] == pytest.approx(i1["lanczos_lmax"], rel=1e-6)
