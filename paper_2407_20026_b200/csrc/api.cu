@@ -143,6 +143,7 @@ struct Part {
   SweepPlan sweep;
   bool use_sweep = false;
   int32_t* sdesc = nullptr;
+  int32_t* sxrun = nullptr;
   double* sw_carry = nullptr;
   unsigned* sw_flags = nullptr;
   // partitioned handles: single-reduction CG (cg_sr.cu) vectors u = M^-1 r and s = K p
@@ -420,7 +421,7 @@ double* vec_of(Part& P, int v) {
 // (partitioned handles).
 void spmv_apply(cudaStream_t s, Part& P, const double* x, double* y, CgState* st) {
   if (P.use_sweep)
-    launch_spmv_sweep(s, P.sweep, P.n_own, P.sdesc, P.vals, x, y, st ? P.partial : nullptr, st, P.sw_carry,
+    launch_spmv_sweep(s, P.sweep, P.n_own, P.sdesc, P.node_ptr, P.sxrun, P.vals, x, y, st ? P.partial : nullptr, st, P.sw_carry,
                       P.sw_flags, P.bs);
   else if (P.pull)
     launch_spmv_pull(s, &P.pull_tmap, P.n_own, (int)(P.bs.nnz / PULL_BLOCK), P.pdesc, P.node_col, P.lpull, P.vals, x, y,
@@ -679,7 +680,7 @@ void free_part(Part& P) {
                   P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
                   P.lptr, P.lpull, P.pdesc, P.binv, P.zb, P.p2, P.dE,
                   P.ub, P.fb, P.lam, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask,
-                  P.rho, P.E0, P.G0, P.lz_hist, P.lz_T, P.mscale_d, P.u_sr, P.s_sr, P.sdesc, P.sw_carry, P.sw_flags};
+                  P.rho, P.E0, P.G0, P.lz_hist, P.lz_T, P.mscale_d, P.u_sr, P.s_sr, P.sdesc, P.sxrun, P.sw_carry, P.sw_flags};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -906,11 +907,14 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
         sweep_config_ok(P.sweep, B)) {
       P.use_sweep = true;
       UP(sdesc, P.sweep.desc.data(), (int64_t)P.sweep.desc.size());
-      AL(sw_carry, (int64_t)B * P.sweep.G * P.sweep.bw * 24);
+      UP(sxrun, P.sweep.xrun.data(), (int64_t)P.sweep.xrun.size());
+      AL(sw_carry, (int64_t)B * P.n_own * 24);  // K^T x staging: [B][n_own][4 slots][6]
       AL(sw_flags, (int64_t)B * P.sweep.G);
       CK(h, cudaMemset(P.sw_flags, 0, (size_t)B * P.sweep.G * sizeof(unsigned)));
       P.sweep.desc.clear();
       P.sweep.desc.shrink_to_fit();
+      P.sweep.xrun.clear();
+      P.sweep.xrun.shrink_to_fit();
     }
   } else {
     UP(node_ptr, P.pat.node_ptr.data(), P.n_nodes + 1);

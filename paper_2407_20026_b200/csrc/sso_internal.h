@@ -243,6 +243,7 @@ __host__ __device__ constexpr int rec_off(int a, int b) {
 constexpr int SWEEP_DESC = 16;
 struct SweepPlan {
   std::vector<int32_t> desc;
+  std::vector<int32_t> xrun;  // per chunk of 8 nodes: 4 runs (first node, rows) of the x rows it reads
   int bw = 0, R = 0, G = 0, L = 0, smem = 0;
 };
 // false when the mesh does not qualify (a node with > 5 upper or > 4 lower neighbours, or a
@@ -250,7 +251,8 @@ struct SweepPlan {
 bool build_sweep_plan(const UpperPattern& U, int32_t n_own, int sms, int B, SweepPlan& plan);
 // nonzero when every range of every design can be co-resident (cooperative launch)
 int sweep_config_ok(const SweepPlan& plan, int B);
-void launch_spmv_sweep(cudaStream_t s, const SweepPlan& plan, int n_own, const int32_t* sdesc, const double* vals,
+void launch_spmv_sweep(cudaStream_t s, const SweepPlan& plan, int n_own, const int32_t* sdesc, const int64_t* uptr,
+                       const int32_t* xrun, const double* vals,
                        const double* x, double* y, double* partial, CgState* st, double* carry, unsigned* flags,
                        const BatchStrides& bs, int red_add = 0);
 // 16-int per-node descriptors of the pull SpMV (see pcg.cu)
