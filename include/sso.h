@@ -324,12 +324,6 @@ int sso_export_dinv(sso_handle h, double* dinv);
  * sub-blocks) with the one-pass pull SpMV.  stored_values counts the 36 values per block (not the record pads). */
 int sso_storage_info(sso_handle h, int64_t* stored_values, int64_t* stored_blocks, int32_t* symmetric);
 
-/* SpMV kernel of part 0: *kernel = 0 full-storage (spmv_tma), 1 pull (upper-block records,
- * pulled blocks gathered from L2), 2 sweep (the same records read once; K^T x contributions
- * in a shared-memory ring; meshes with <= 5 upper / <= 4 lower neighbours per node and a
- * node-ordering bandwidth that fits the ring).  bandwidth = max m - n over stored blocks and
- * ranges = CTAs per design of the sweep (0 otherwise).  Any pointer may be NULL. */
-int sso_spmv_info(sso_handle h, int32_t* kernel, int32_t* bandwidth, int32_t* ranges);
 
 /* Partition of this handle: number of strips held, first owned global node, owned
  * node count and owned quad count (the extents of the caller's f / u / gradients). */

@@ -111,7 +111,6 @@ _sig = {
     "sso_launch_count": (C.c_int64, [_H]),
     "sso_part_info": (C.c_int, [_H, _ip, _ip, _ip, _ip]),
     "sso_storage_info": (C.c_int, [_H, _lp, _lp, _ip]),
-    "sso_spmv_info": (C.c_int, [_H, _ip, _ip, _ip]),
     "sso_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "sso_local_pattern": (C.c_int, [C.POINTER(sso_mesh), _ip, C.c_int32, C.c_int32, _lp, C.c_void_p, C.c_void_p]),
     "sso_halo_plan": (C.c_int, [C.POINTER(sso_mesh), _ip, C.c_int32, C.c_int32, _ip, C.c_void_p, _ip,
@@ -300,12 +299,6 @@ class Model:
         v, b, s = C.c_int64(), C.c_int64(), C.c_int32()
         self._check(_lib.sso_storage_info(self.h, C.byref(v), C.byref(b), C.byref(s)))
         return v.value, b.value, s.value  # 0 full, 2 two-pass symmetric, 3 pull symmetric
-
-    def spmv_info(self):
-        """(kernel, bandwidth, ranges): kernel 0 full storage, 1 pull, 2 sweep."""
-        k, b, r = C.c_int32(), C.c_int32(), C.c_int32()
-        self._check(_lib.sso_spmv_info(self.h, C.byref(k), C.byref(b), C.byref(r)))
-        return k.value, b.value, r.value
 
     def set_design(self, x=None, y=None, z=None, t=None):
         dev = self._mode(x, y, z, t)

@@ -139,13 +139,6 @@ struct Part {
   bool cgf = false;                   // fused x / r / p update (cg_update_fused / _block_fused): one
                                       // part, full or pull storage, B <= the co-resident grid
   double* p2 = nullptr;               // cgf: the second p buffer (ping-pong)
-  // sweep SpMV (spmv_sweep.cu): plan, descriptors, carry buffer and per-range counters
-  SweepPlan sweep;
-  bool use_sweep = false;
-  int32_t* sdesc = nullptr;
-  int32_t* sxrun = nullptr;
-  double* sw_carry = nullptr;
-  unsigned* sw_flags = nullptr;
   // partitioned handles: single-reduction CG (cg_sr.cu) vectors u = M^-1 r and s = K p
   double *u_sr = nullptr, *s_sr = nullptr;
   // interior / boundary split of the owned rows: rows [bnd_lo, bnd_hi) need no halo value
@@ -420,10 +413,7 @@ double* vec_of(Part& P, int v) {
 // p^T q (and alpha, unless the fused update forms it).  x must have its halo filled
 // (partitioned handles).
 void spmv_apply(cudaStream_t s, Part& P, const double* x, double* y, CgState* st) {
-  if (P.use_sweep)
-    launch_spmv_sweep(s, P.sweep, P.n_own, P.sdesc, P.node_ptr, P.sxrun, P.vals, x, y, st ? P.partial : nullptr, st, P.sw_carry,
-                      P.sw_flags, P.bs);
-  else if (P.pull)
+  if (P.pull)
     launch_spmv_pull(s, &P.pull_tmap, P.n_own, (int)(P.bs.nnz / PULL_BLOCK), P.pdesc, P.node_col, P.lpull, P.vals, x, y,
                      st ? P.partial : nullptr, st, P.bs);
   else if (st)
@@ -680,7 +670,7 @@ void free_part(Part& P) {
                   P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
                   P.lptr, P.lpull, P.pdesc, P.binv, P.zb, P.p2, P.dE,
                   P.ub, P.fb, P.lam, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask,
-                  P.rho, P.E0, P.G0, P.lz_hist, P.lz_T, P.mscale_d, P.u_sr, P.s_sr, P.sdesc, P.sxrun, P.sw_carry, P.sw_flags};
+                  P.rho, P.E0, P.G0, P.lz_hist, P.lz_T, P.mscale_d, P.u_sr, P.s_sr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -901,21 +891,6 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
     std::vector<int32_t> desc;
     build_pull_desc(P.up, desc);
     UP(pdesc, desc.data(), (int64_t)desc.size());
-    // the sweep SpMV when the mesh qualifies (SSO_SWEEP=0 keeps the pull kernel: A/B switch)
-    const char* envs = getenv("SSO_SWEEP");
-    if (!(envs && envs[0] == '0') && build_sweep_plan(P.up, P.n_own, cg_grid() / 4, B, P.sweep) &&
-        sweep_config_ok(P.sweep, B)) {
-      P.use_sweep = true;
-      UP(sdesc, P.sweep.desc.data(), (int64_t)P.sweep.desc.size());
-      UP(sxrun, P.sweep.xrun.data(), (int64_t)P.sweep.xrun.size());
-      AL(sw_carry, (int64_t)B * P.n_own * 24);  // K^T x staging: [B][n_own][4 slots][6]
-      AL(sw_flags, (int64_t)B * P.sweep.G);
-      CK(h, cudaMemset(P.sw_flags, 0, (size_t)B * P.sweep.G * sizeof(unsigned)));
-      P.sweep.desc.clear();
-      P.sweep.desc.shrink_to_fit();
-      P.sweep.xrun.clear();
-      P.sweep.xrun.shrink_to_fit();
-    }
   } else {
     UP(node_ptr, P.pat.node_ptr.data(), P.n_nodes + 1);
     UP(node_col, P.pat.node_col.data(), P.n_blocks);
@@ -2271,15 +2246,6 @@ int sso_storage_info(sso_handle h, int64_t* stored_values, int64_t* stored_block
   return SSO_OK;
 }
 
-int sso_spmv_info(sso_handle h, int32_t* kernel, int32_t* bandwidth, int32_t* ranges) {
-  ENTER(h);
-  if (!h) return SSO_E_INVALID;
-  const Part& P = h->P0();
-  if (kernel) *kernel = P.use_sweep ? 2 : (P.pull ? 1 : 0);
-  if (bandwidth) *bandwidth = P.use_sweep ? P.sweep.bw : 0;
-  if (ranges) *ranges = P.use_sweep ? P.sweep.G : 0;
-  return SSO_OK;
-}
 
 int sso_part_info(sso_handle h, int32_t* n_parts_here, int32_t* own_node_begin, int32_t* own_nodes,
                   int32_t* own_quads) {

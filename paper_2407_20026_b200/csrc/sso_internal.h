@@ -236,25 +236,6 @@ __host__ __device__ constexpr int pull_sub_off(int s) {
 __host__ __device__ constexpr int rec_off(int a, int b) {
   return pull_sub_off(3 * (b >> 1) + (a >> 1)) + 2 * (b & 1) + (a & 1);
 }
-// Sweep SpMV (spmv_sweep.cu): every stored upper block read once, K^T x_n contributions kept
-// in a shared-memory ring; per-node 16-int descriptors (first upper block, udeg | ldeg << 8,
-// upper columns, the node's slot in each upper neighbour's lower list, lower sources), the
-// mesh bandwidth bw, ring size R, G ranges of L nodes per design, dynamic shared memory.
-constexpr int SWEEP_DESC = 16;
-struct SweepPlan {
-  std::vector<int32_t> desc;
-  std::vector<int32_t> xrun;  // per chunk of 8 nodes: 4 runs (first node, rows) of the x rows it reads
-  int bw = 0, R = 0, G = 0, L = 0, smem = 0;
-};
-// false when the mesh does not qualify (a node with > 5 upper or > 4 lower neighbours, or a
-// bandwidth whose ring does not fit in shared memory)
-bool build_sweep_plan(const UpperPattern& U, int32_t n_own, int sms, int B, SweepPlan& plan);
-// nonzero when every range of every design can be co-resident (cooperative launch)
-int sweep_config_ok(const SweepPlan& plan, int B);
-void launch_spmv_sweep(cudaStream_t s, const SweepPlan& plan, int n_own, const int32_t* sdesc, const int64_t* uptr,
-                       const int32_t* xrun, const double* vals,
-                       const double* x, double* y, double* partial, CgState* st, double* carry, unsigned* flags,
-                       const BatchStrides& bs, int red_add = 0);
 // 16-int per-node descriptors of the pull SpMV (see pcg.cu)
 void build_pull_desc(const UpperPattern& U, std::vector<int32_t>& desc);
 // TMA map of the [rows][36] fp64 view of the values (gather4 of pulled blocks); 0 on success
@@ -413,21 +394,6 @@ inline cudaError_t launch_cooperative(void (*kern)(K...), dim3 grid, dim3 block,
   static const bool coop = !(getenv("SSO_COOP") && getenv("SSO_COOP")[0] == '0');  // A/B switch
   cfg.attrs = at;
   cfg.numAttrs = coop ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
-}
-template <typename... K, typename... A>
-inline cudaError_t launch_cooperative_smem(void (*kern)(K...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                                           A&&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
 }
 #define SSO_POST_LAUNCH_RC(name, rc)                           \

@@ -1,4 +1,4 @@
-// mbarrier / bulk-copy (TMA) helpers shared by the SpMV kernels (pcg.cu, spmv_sweep.cu):
+// mbarrier / bulk-copy (TMA) helpers of the SpMV kernels (pcg.cu):
 // inline PTX for sm_100a (mbarrier.try_wait parity loops, cp.async.bulk global -> shared with
 // an L2 cache hint and complete_tx accounting, an L2 evict-first policy).
 #pragma once
@@ -37,15 +37,6 @@ static __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsi
           "r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
-}
-static __device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-static __device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 static __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t pol;

@@ -520,54 +520,3 @@ def test_single_element(sso, sup, storage):
     gX, gT = OG.adjoint_gradient(P, uref, 1.0)
     assert_components(dX, gX, TOL_G, "dC/dX")
     assert_components(dT, gT, TOL_G, "dC/dt")
-
-
-@pytest.mark.parametrize("make", [W.config2, lambda: W.shell_config3(40, cfg=3), lambda: W.shell_config3(60, cfg=4, supports="c4"),
-                                  lambda: W.tiny_shell(3, 2), lambda: W.tiny_shell(1)])
-def test_sweep_spmv_against_pull_and_oracle(sso, make, monkeypatch):
-    """The sweep SpMV (csrc/spmv_sweep.cu: every upper-block record read once, K^T x in a
-    shared-memory ring, ranges handing their carry to the next) equals the pull kernel on the
-    same records to rounding, and the solve through it matches the oracle."""
-    P = make()
-    ms = sso.Model(P, rtol=1e-12)
-    monkeypatch.setenv("SSO_SWEEP", "0")
-    mp = sso.Model(P, rtol=1e-12)
-    monkeypatch.delenv("SSO_SWEEP")
-    assert ms.spmv_info()[0] == 2 and mp.spmv_info()[0] == 1
-    ms.assemble()
-    mp.assemble()
-    for seed in range(3):
-        x = np.random.default_rng(seed).standard_normal(ms.ndof)
-        ys, yp = ms.spmv(x), mp.spmv(x)
-        assert np.abs(ys - yp).max() <= 1e-13 * np.abs(yp).max()
-    assert np.array_equal(ms.spmv(x), ms.spmv(x))   # deterministic
-    us, i_s = ms.solve(P["f"])
-    assert i_s["status"] == 0
-    uref, _, _ = OG.evaluate(P)
-    assert np.linalg.norm(us - uref) <= TOL_U * np.linalg.norm(uref)
-    Cs, dXs, _ = ms.grad()
-    assert abs(Cs - OG.compliance(P["f"], uref)) <= TOL_C * abs(OG.compliance(P["f"], uref))
-
-
-def test_sweep_spmv_batched_and_strips(sso):
-    """Batches (one range set per design) and in-process strips (halo columns dropped from the
-    ring) take the sweep kernel too and agree with single-design / single-strip runs."""
-    designs = [W.config5_design(b, n=16) for b in range(3)]
-    mb = sso.Model(designs[0], rtol=1e-12, batch=3)
-    assert mb.spmv_info()[0] == 2
-    mb.set_design(z=np.stack([d["z"] for d in designs]), t=np.stack([d["t"] for d in designs]))
-    mb.assemble()
-    U, infos = mb.solve(np.stack([d["f"] for d in designs]))
-    for b, d in enumerate(designs):
-        m1 = sso.Model(d, rtol=1e-12)
-        m1.assemble()
-        u1, _ = m1.solve(d["f"])
-        assert np.linalg.norm(U[b] - u1) <= 1e-9 * np.linalg.norm(u1)
-    P = W.shell_config3(48, cfg=3)
-    m4 = sso.Model(P, rtol=1e-12, n_parts=4)
-    assert m4.spmv_info()[0] == 2
-    m1 = sso.Model(P, rtol=1e-12)
-    m4.assemble()
-    m1.assemble()
-    x = np.random.default_rng(9).standard_normal(m1.ndof)
-    assert np.abs(m4.spmv(x) - m1.spmv(x)).max() <= 1e-13 * np.abs(m1.spmv(x)).max()
