@@ -4,24 +4,27 @@
 // c1) with the CG of reading c10: x0 = 0, M = diag(K_bc), stop when
 // |r|_2 <= rtol |f_bc|_2, breakdown p^T K p <= 0 -> NOT_SPD.
 //
-// One iteration = 3 kernels, all HBM-bound, no host synchronisation:
-//   spmv_dot  q = K p and p^T q; the last CTA forms alpha = r^T z / p^T q
-//   update    x += alpha p, r -= alpha q, z = dinv r; partial r^T z, r^T r;
-//             the last CTA forms beta, tests convergence, sets `done`
-//   pupdate   p = dinv r + beta p
-// Every kernel returns immediately once `done` is set, so a fixed chunk of
-// iterations can be captured once in a CUDA graph and replayed; the host only
-// polls `done` between chunks.  Reductions are atomic-free: per-CTA partials
-// in fixed order, reduced by the last CTA to finish (ticket counter) in fixed
-// order -> bit-reproducible for a fixed grid.
+// Single-part handles (the default path), one iteration = 2 kernels, no host sync:
+//   spmv_pull_cta_kernel   q = K p over the upper-block records (storage 3) and the
+//                          per-CTA p^T q partials (left for the update: defer_alpha)
+//   cg_update_fused_kernel every CTA sums the p^T q partials in one fixed order (alpha),
+//                          x += alpha p, r -= alpha q, z = dinv r, r^T z, r^T r -> one
+//                          all-CTA all-reduce (cg_fused.cuh; cooperative launch) -> beta,
+//                          convergence test, p_next = z + beta p into the other p buffer
+// (spmv_tma_kernel replaces the pull kernel with full storage; node-block Jacobi has its
+// own fused update in block_jacobi.cu; partitioned handles run the single-reduction CG of
+// cg_sr.cu).  The classic 3-kernel form (spmv_dot, cg_update, cg_pupdate) remains for
+// SSO_CG_FUSED=0 and batches larger than the co-resident grid.  Every kernel returns
+// immediately once `done` is set, so a fixed chunk of iterations is captured once in a CUDA
+// graph and replayed; the host only polls `done` between chunks.  Reductions are
+// atomic-free and in fixed order (per-CTA partials; last-CTA ticket reductions or the
+// all-CTA all-reduce) -> bit-reproducible for a fixed grid.
 //
-// SpMV layout: the scalar CSR values of node n's six rows are contiguous at
-// 36 node_ptr[n]; row 6n+a, column 6m+b with m = node_col[node_ptr[n]+k] sits at
-// 36 node_ptr[n] + a (6 deg) + 6k + b.  One warp per node: lane rem walks the
-// row positions, gathers p[6m+b] ONCE and applies it to all six rows (6
-// coalesced value streams); a 9-shuffle transposed butterfly reduces the six
-// row sums.  Column indices are read per 6x6 block (4 B / 36 values) instead
-// of per value (4 B / value): 8.1 B per non-zero instead of 12.
+// Full-storage layout (storage 1): the scalar CSR values of node n's six rows are contiguous
+// at 36 node_ptr[n]; row 6n+a, column 6m+b with m = node_col[node_ptr[n]+k] sits at
+// 36 node_ptr[n] + a (6 deg) + 6k + b; a warp streams each node's run through a shared
+// memory ring and applies one x gather to all six rows.  Upper-block layout (storage 3,
+// default): see the pull kernel below and DESIGN.md §5.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
