@@ -581,7 +581,11 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev, int it) {
       for (size_t i = 0; i < np; ++i) {
         Part& P = *h->parts[i];
         CK(h, cudaStreamWaitEvent(h->part_streams[i], h->ev_fork, 0));
-        spmv_apply(h->part_streams[i], P, P.u_sr, P.q, P.st);
+        if (P.pull)  // each part on 1/np of the persistent grid: the parts run side by side
+          launch_spmv_pull(h->part_streams[i], &P.pull_tmap, P.n_own, (int)(P.bs.nnz / PULL_BLOCK), P.pdesc,
+                           P.node_col, P.lpull, P.vals, P.u_sr, P.q, P.partial, P.st, P.bs, 0, 0, (int)np);
+        else
+          spmv_apply(h->part_streams[i], P, P.u_sr, P.q, P.st);
         CK(h, cudaEventRecord(h->part_ev[i], h->part_streams[i]));
       }
       for (size_t i = 0; i < np; ++i) CK(h, cudaStreamWaitEvent(s, h->part_ev[i], 0));
@@ -604,7 +608,7 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev, int it) {
       Part& P = *h->parts[i];
       CK(h, cudaStreamWaitEvent(h->part_streams[i], h->ev_fork, 0));
       launch_cgsr_update(h->part_streams[i], P.n_own, P.dinv, P.binv, P.xs, P.r, P.u_sr, P.q, P.p, P.s_sr,
-                         P.partial, P.st);
+                         P.partial, P.st, (int)np);
       CK(h, cudaEventRecord(h->part_ev[i], h->part_streams[i]));
     }
     for (size_t i = 0; i < np; ++i) CK(h, cudaStreamWaitEvent(s, h->part_ev[i], 0));

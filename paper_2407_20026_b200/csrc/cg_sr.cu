@@ -220,9 +220,9 @@ void launch_cgsr_init(cudaStream_t s, int n_own, const double* f, const uint8_t*
 }
 
 void launch_cgsr_update(cudaStream_t s, int n_own, const double* dinv, const double* binv, double* x, double* r,
-                        double* u, const double* w, double* p, double* sv, double* partial, CgState* st) {
-  cgsr_update_kernel<<<vgrid(n_own), 256, 0, s>>>(n_own, binv ? nullptr : dinv, binv, x, r, u, w, p, sv, partial,
-                                                  st);
+                        double* u, const double* w, double* p, double* sv, double* partial, CgState* st, int share) {
+  const int g = std::max(1, vgrid(n_own) / std::max(share, 1));
+  cgsr_update_kernel<<<g, 256, 0, s>>>(n_own, binv ? nullptr : dinv, binv, x, r, u, w, p, sv, partial, st);
   SSO_POST_LAUNCH("cgsr_update_kernel");
 }
 

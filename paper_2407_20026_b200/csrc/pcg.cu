@@ -1377,11 +1377,12 @@ int make_pull_tmap(const double* vals, int64_t rows, CUtensorMap* out) {
 void launch_spmv_pull(cudaStream_t s, const CUtensorMap* tmap, int n_nodes, int rows_per_design,
                       const int32_t* pdesc, const int32_t* ucol, const int32_t* lpull, const double* vals,
                       const double* x, double* y, double* partial, CgState* st, const BatchStrides& bs, int node0,
-                      int red_add) {
+                      int red_add, int share) {
   if (n_nodes <= node0) return;
   int smem;
   const PullVariant& V = pull_variant(bs.B, &smem);
-  const int ctas = std::max(1, V.minb * (cg_grid() / 4) / bs.B);  // persistent: minb CTAs per SM in total
+  // persistent: minb CTAs per SM in total, divided among `share` concurrently running launches
+  const int ctas = std::max(1, V.minb * (cg_grid() / 4) / (bs.B * std::max(share, 1)));
   const int chunk = V.chunk;
   const int units = (n_nodes - node0 + chunk - 1) / chunk;
   const int grid = std::max(1, std::min(ctas, units));

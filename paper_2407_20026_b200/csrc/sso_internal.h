@@ -209,11 +209,13 @@ int cg_block_fused_grid();
 // neighbours (pull list lpull = [(n, upper block index)] per node, via lptr) and
 // forms y = K x in one pass.  With st != nullptr also p^T q and alpha (CG).
 // Rows [node0, n_nodes) (default: all owned rows); on partitioned handles (st->dist) the
-// p^T q piece is written to st->red[0] (red_add = 0) or added to it (red_add = 1).
+// p^T q piece is written to st->red[0] (red_add = 0) or added to it (red_add = 1).  share > 1:
+// the launch runs concurrently with share - 1 others (in-process parts on their own streams)
+// and takes 1/share of the persistent grid, so the parts run side by side on disjoint SMs.
 void launch_spmv_pull(cudaStream_t s, const CUtensorMap* tmap, int n_nodes, int rows_per_design,
                       const int32_t* pdesc, const int32_t* ucol, const int32_t* lpull, const double* vals,
                       const double* x, double* y, double* partial, CgState* st,
-                      const BatchStrides& bs = BatchStrides(), int node0 = 0, int red_add = 0);
+                      const BatchStrides& bs = BatchStrides(), int node0 = 0, int red_add = 0, int share = 1);
 // Storage 3 stores each upper 6x6 block as a record of PULL_BLOCK doubles: the nine 2x2
 // sub-blocks (A, B) = K[2A..2A+1][2B..2B+1], 4 doubles each (column-major inside), sub-block
 // 3B + A in slot PULL_SUB_POS nibble, and one 16-byte zero pad word (an odd 19-word record
@@ -269,7 +271,8 @@ void launch_cgsr_init(cudaStream_t s, int n_own, const double* f, const uint8_t*
                       const double* binv, double* fbc, double* x, double* r, double* u, double* p, double* sv,
                       double* partial, CgState* st, int warm, const double* Kx0);
 void launch_cgsr_update(cudaStream_t s, int n_own, const double* dinv, const double* binv, double* x, double* r,
-                        double* u, const double* w, double* p, double* sv, double* partial, CgState* st);
+                        double* u, const double* w, double* p, double* sv, double* partial, CgState* st,
+                        int share = 1);
 void launch_cgsr_replace(cudaStream_t s, int n_own, const double* fbc, const double* Kx, const double* dinv,
                          const double* binv, double* r, double* u, double* partial, CgState* st);
 // In-process halo fill of all parts in one launch: entry k = (dst part, dst node, src part,
