@@ -1,5 +1,8 @@
 """Write tests/golden/c3_oracle.npz: the CPU fp64 oracle's result on config C3 (200 x 200
-MITC-4 quads, 242 406 DOF; BASELINE.json configs[2]).
+MITC-4 quads, 242 406 DOF; BASELINE.json configs[2]).  With `c4` it
+writes tests/golden/c4r120_oracle.npz instead: the C4 recipe (edge y = 0 clamped, two
+pinned corners; BASELINE.json configs[3]) at n = 120 (87 846 DOF), whose conditioning is
+the C4 one (one clamped edge instead of four).
 
 Calls only oracle/ (and the seeded input generator workloads/): DOK assembly, supports by
 elimination, the oracle's textbook Jacobi-PCG to rtol 1e-13 (SURVEY §8(c) C5 "CG for
@@ -8,6 +11,7 @@ seeded sample of nodes and elements.  Stored: u (all 242 406 entries), C, the sa
 gradient components, and the oracle's iteration count / true residual as metadata.
 
     python tools/make_golden_c3.py        # ~5-10 min of CPU
+    python tools/make_golden_c3.py c4     # the C4-recipe file
 """
 import os
 import sys
@@ -21,12 +25,11 @@ sys.path.insert(0, ROOT)
 import workloads as W  # noqa: E402
 from oracle import assembly as A, grad as G, solve as S  # noqa: E402
 
-OUT = os.path.join(ROOT, "tests", "golden", "c3_oracle.npz")
-
-
 def main():
+    c4 = len(sys.argv) > 1 and sys.argv[1] == "c4"
+    OUT = os.path.join(ROOT, "tests", "golden", "c4r120_oracle.npz" if c4 else "c3_oracle.npz")
     t0 = time.time()
-    P = W.config3()
+    P = W.shell_config3(120, cfg=4, supports="c4") if c4 else W.config3()
     nn, nq = len(P["x"]), len(P["quad_conn"])
     nd = 6 * nn
     dok = A.assemble_dok(P)
