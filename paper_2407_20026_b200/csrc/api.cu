@@ -558,6 +558,8 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev, int it) {
     if ((rc = exchange(h, V_U, h->side_stream))) return rc;
     CK(h, cudaEventRecord(h->ev_join, h->side_stream));
     if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
+    // the u^T w pieces add up in launch order; the first piece that runs writes (empty pieces
+    // launch nothing)
     for (auto& pp : h->parts) {
       Part& P = *pp;
       launch_spmv_pull(s, &P.pull_tmap, P.bnd_hi, (int)(P.bs.nnz / PULL_BLOCK), P.pdesc, P.node_col, P.lpull,
@@ -566,10 +568,11 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev, int it) {
     CK(h, cudaStreamWaitEvent(s, h->ev_join, 0));
     for (auto& pp : h->parts) {
       Part& P = *pp;
+      const bool mid = P.bnd_hi > P.bnd_lo, lo = P.bnd_lo > 0;
       launch_spmv_pull(s, &P.pull_tmap, P.bnd_lo, (int)(P.bs.nnz / PULL_BLOCK), P.pdesc, P.node_col, P.lpull,
-                       P.vals, P.u_sr, P.q, P.partial, P.st, P.bs, 0, 1);
+                       P.vals, P.u_sr, P.q, P.partial, P.st, P.bs, 0, mid ? 1 : 0);
       launch_spmv_pull(s, &P.pull_tmap, P.n_own, (int)(P.bs.nnz / PULL_BLOCK), P.pdesc, P.node_col, P.lpull,
-                       P.vals, P.u_sr, P.q, P.partial, P.st, P.bs, P.bnd_hi, 1);
+                       P.vals, P.u_sr, P.q, P.partial, P.st, P.bs, P.bnd_hi, (mid || lo) ? 1 : 0);
     }
     if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
   } else {
