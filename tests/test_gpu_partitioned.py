@@ -157,3 +157,20 @@ def test_batched_designs_match_single(sso):
         assert np.array_equal(dXg[b], dX1g) and np.array_equal(dTg[b], dT1g)
     uref, _, _ = OG.evaluate(designs[2])
     assert np.linalg.norm(U[2] - uref) <= 1e-9 * np.linalg.norm(uref)
+
+
+@pytest.mark.parametrize("nparts", [5, 11])
+def test_split_thin_strips(sso, nparts, monkeypatch):
+    """Strips of one or two node rows have no interior rows: every SpMV piece of the
+    interior/boundary split is a boundary piece (or empty), and the u^T K u pieces must still
+    start from zero each iteration."""
+    monkeypatch.setenv("SSO_SPLIT", "1")
+    P = W.shell_config3(10, cfg=3)
+    m1 = sso.Model(P, rtol=1e-12)
+    m1.assemble()
+    mp = sso.Model(P, rtol=1e-12, n_parts=nparts)
+    mp.assemble()
+    u1, i1 = m1.solve(P["f"])
+    up, ip = mp.solve(P["f"])
+    assert ip["status"] == 0 and abs(ip["iters"] - i1["iters"]) <= max(3, 0.01 * i1["iters"])
+    assert np.linalg.norm(up - u1) <= 1e-9 * np.linalg.norm(u1)
