@@ -28,6 +28,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "nccl.h"
 #include "sso_internal.h"
 
@@ -393,6 +395,14 @@ struct Entry {
   }
 };
 #define ENTER(h) Entry entry_guard_(h)
+
+// NVTX range per ABI call and per solve phase (SURVEY.md §5 "Tracing"): free without a tool
+// attached (NVTX v3 is header-only; the ranges show in nsys / ncu timelines).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define TRACE(name) NvtxRange nvtx_range_(name)
 
 // ---------------------------------------------------------------------------
 // Transports: halo exchange of a per-part vector and allreduce of CgState::red.
@@ -1147,6 +1157,7 @@ int sso_nccl_unique_id(void* out) {
 
 int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_materials* mat,
                const sso_supports* sup, const sso_options* opt, sso_handle* out) {
+  TRACE("sso_create");
   if (!out) { g_create_err = "null out"; return SSO_E_INVALID; }
   *out = nullptr;
   std::string err;
@@ -1356,6 +1367,7 @@ int sso_set_stream(sso_handle h, void* cuda_stream, sso_mem mem) {
 
 int sso_set_design(sso_handle h, const double* x, const double* y, const double* z, const double* t) {
   ENTER(h);
+  TRACE("sso_set_design");
   if (!h) return SSO_E_INVALID;
   int rc;
   if (x && (rc = design_in(h, x, h->g_nodes, &Part::x, false))) return rc;
@@ -1401,6 +1413,7 @@ static int assemble_pass(sso_ctx* h, bool unconstrained) {
 
 int sso_assemble(sso_handle h) {
   ENTER(h);
+  TRACE("sso_assemble");
   if (!h) return SSO_E_INVALID;
   int rc = reset_flags(h);
   if (rc) return rc;
@@ -1543,6 +1556,7 @@ static int solve_chunks(sso_ctx* h) {
 
 int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
   ENTER(h);
+  TRACE("sso_solve");
   const bool add_load = h && h->area_load && !h->skip_load;
   if (!h || (!f && !add_load) || !u) {
     if (h) h->err = "null argument";
@@ -1618,7 +1632,10 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
       launch_cg_init(h->stream, (int)P.ndof_own, lift ? P.feff : P.f, P.fixed_mask, P.dinv, P.fbc, P.xs, P.r,
                      P.p, P.partial, P.st, warm, P.tmp, P.bs);
   }
-  rc = solve_chunks(h);
+  {
+    TRACE("cg_loop");
+    rc = solve_chunks(h);
+  }
   if (rc) return rc;
   CK(h, cudaEventRecord(h->ev_b, h->stream));
   // true residual |f_bc - K x| / |f_bc|: local sums of squares into red[0], allreduced
@@ -1632,6 +1649,7 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
   }
   if ((rc = allreduce(h, 4))) return rc;
   {  // extreme Ritz values of M^-1 K from part 0's coefficient history (the same in every part)
+    TRACE("certification");
     Part& P = h->P0();
     long long g1 = g_launches;
     launch_lanczos_ritz(h->stream, P.st, P.lz_T, P.lz_cap, P.B);
@@ -1768,6 +1786,7 @@ static int grad_prescribed(sso_ctx* h, sso_objective obj, double* C, double* dC_
 
 int sso_grad(sso_handle h, sso_objective obj, double* C, double* dC_dxyz, double* dC_dt) {
   ENTER(h);
+  TRACE("sso_grad");
   if (!h) return SSO_E_INVALID;
   if (obj != SSO_OBJ_COMPLIANCE && obj != SSO_OBJ_STRAIN_ENERGY) FAIL(h, SSO_E_INVALID, "unknown objective");
   if (!h->solved) FAIL(h, SSO_E_STATE, "sso_grad before a successful sso_solve");
@@ -1778,6 +1797,7 @@ int sso_grad(sso_handle h, sso_objective obj, double* C, double* dC_dxyz, double
 int sso_grad_at(sso_handle h, sso_objective obj, const double* f, const double* u, double* C,
                 double* dC_dxyz, double* dC_dt) {
   ENTER(h);
+  TRACE("sso_grad_at");
   if (!h || !f || !u) return SSO_E_INVALID;
   if (obj != SSO_OBJ_COMPLIANCE && obj != SSO_OBJ_STRAIN_ENERGY) FAIL(h, SSO_E_INVALID, "unknown objective");
   if (h->prescribed) FAIL(h, SSO_E_INVALID, "sso_grad_at is not defined with prescribed displacements (use sso_grad)");
@@ -1790,6 +1810,7 @@ int sso_grad_at(sso_handle h, sso_objective obj, const double* f, const double* 
 // Gradient kernels at state U with scale s into P.dxyz (owned nodes), P.dt, P.dE.
 int sso_adjoint_solve(sso_handle h, const double* dg_du, double* lambda, sso_solve_info* info) {
   ENTER(h);
+  TRACE("sso_adjoint_solve");
   if (!h || !dg_du || !lambda) return SSO_E_INVALID;
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_adjoint_solve is defined for single-strip handles");
   if (!h->assembled) FAIL(h, SSO_E_STATE, "sso_adjoint_solve before sso_assemble");
@@ -1840,6 +1861,7 @@ static int adjoint_grad_dev(sso_ctx* h, double u_load_s) {
 
 int sso_grad_adjoint(sso_handle h, const double* lambda, double* dg_dxyz, double* dg_dt, double* dg_dE) {
   ENTER(h);
+  TRACE("sso_grad_adjoint");
   if (!h || !lambda) return SSO_E_INVALID;
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_grad_adjoint is defined for single-strip handles");
   if (!h->solved) FAIL(h, SSO_E_STATE, "sso_grad_adjoint before a successful sso_solve");
@@ -1910,6 +1932,7 @@ static int grad_prescribed(sso_ctx* h, sso_objective obj, double* C, double* dC_
 
 int sso_grad_E(sso_handle h, sso_objective obj, double* dC_dE) {
   ENTER(h);
+  TRACE("sso_grad_E");
   if (!h || !dC_dE) return SSO_E_INVALID;
   if (obj != SSO_OBJ_COMPLIANCE && obj != SSO_OBJ_STRAIN_ENERGY) FAIL(h, SSO_E_INVALID, "unknown objective");
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_grad_E is defined for single-strip handles");
@@ -1920,6 +1943,7 @@ int sso_grad_E(sso_handle h, sso_objective obj, double* dC_dE) {
 
 int sso_set_prescribed(sso_handle h, const double* b) {
   ENTER(h);
+  TRACE("sso_set_prescribed");
   if (!h) return SSO_E_INVALID;
   if (!b) {
     if (h->prescribed) h->assembled = false;
@@ -1957,6 +1981,7 @@ int sso_set_prescribed(sso_handle h, const double* b) {
 
 int sso_set_area_load(sso_handle h, const double* q, const double* w, const double* dir) {
   ENTER(h);
+  TRACE("sso_set_area_load");
   if (!h) return SSO_E_INVALID;
   if (!q && !w) {
     h->area_load = false;
@@ -1998,6 +2023,7 @@ int sso_set_area_load(sso_handle h, const double* q, const double* w, const doub
 
 int sso_set_density(sso_handle h, const double* rho, double penal, const double* E0, const double* G0) {
   ENTER(h);
+  TRACE("sso_set_density");
   if (!h || !rho || !E0) return SSO_E_INVALID;
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_set_density is defined for single-strip handles");
   if (!(penal >= 1.0) || !std::isfinite(penal)) FAIL(h, SSO_E_INVALID, "sso_set_density: penalty P must be >= 1");
@@ -2037,6 +2063,7 @@ int sso_set_density(sso_handle h, const double* rho, double penal, const double*
 
 int sso_grad_density(sso_handle h, sso_objective obj, double* dC_drho) {
   ENTER(h);
+  TRACE("sso_grad_density");
   if (!h || !dC_drho) return SSO_E_INVALID;
   if (!h->simp) FAIL(h, SSO_E_STATE, "sso_grad_density without sso_set_density");
   h->simp_chain = true;
@@ -2047,6 +2074,7 @@ int sso_grad_density(sso_handle h, sso_objective obj, double* dC_drho) {
 
 int sso_set_material(sso_handle h, const double* E) {
   ENTER(h);
+  TRACE("sso_set_material");
   if (!h || !E) return SSO_E_INVALID;
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_set_material is defined for single-strip handles");
   h->simp = false;
@@ -2168,6 +2196,7 @@ extern "C" {
 int sso_hat_filter(sso_handle h, int32_t on_elements, double radius, int32_t ncomp, const double* in,
                    double* out) {
   ENTER(h);
+  TRACE("sso_hat_filter");
   if (!h || !in || !out) return SSO_E_INVALID;
   if (h->distributed()) FAIL(h, SSO_E_INVALID, "sso_hat_filter is defined for single-strip handles");
   if (!(radius > 0.0) || !std::isfinite(radius)) FAIL(h, SSO_E_INVALID, "radius must be positive and finite");
@@ -2207,6 +2236,7 @@ int sso_hat_filter(sso_handle h, int32_t on_elements, double radius, int32_t nco
 
 int sso_spmv(sso_handle h, const double* xin, double* yout) {
   ENTER(h);
+  TRACE("sso_spmv");
   if (!h || !xin || !yout) return SSO_E_INVALID;
   if (!h->assembled) FAIL(h, SSO_E_STATE, "sso_spmv before sso_assemble");
   int rc;
