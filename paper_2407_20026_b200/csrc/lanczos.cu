@@ -11,8 +11,8 @@
 //   lanczos_ritz_kernel     one CTA per (design, extreme): Gershgorin interval, then
 //                           multisection with 128 shifts per round on the Sturm count of
 //                           T - s I, evaluated by the three-term recurrence of the leading
-//                           principal minors (two FMAs per step, exact power-of-two
-//                           rescaling; no division on the dependency chain).  lambda_max on
+//                           principal minors (one FMA per step on the dependency chain, exact
+//                           power-of-two rescaling, no division) over shared-memory tiles of T.  lambda_max on
 //                           a linear grid, lambda_min on a geometric grid (T is SPD: its
 //                           smallest eigenvalue can sit many decades below the largest);
 //                           rounds stop at 1e-10 relative width.
@@ -31,7 +31,7 @@ namespace sso {
 
 namespace {
 
-constexpr int RITZ_THREADS = 128;
+constexpr int RITZ_THREADS = 128;  // the recurrence is issue-bound: few warps, more rounds
 
 __global__ void __launch_bounds__(256) lanczos_tridiag_kernel(const CgState* st, double2* T, int cap) {
   const int bd = blockIdx.y;
@@ -48,18 +48,29 @@ __global__ void __launch_bounds__(256) lanczos_tridiag_kernel(const CgState* st,
   }
 }
 
-// Number of eigenvalues of T below s: sign changes of the leading principal minors
-// p_0 = 1, p_1 = d_0 - s, p_{k+1} = (d_k - s) p_k - e_{k-1}^2 p_{k-1} (negative LDL^T pivots).
-__device__ __forceinline__ int sturm_count(const double2* __restrict__ T, int n, double s) {
-  double pp = 1.0, p = T[0].x - s;
-  int cnt = p < 0.0;
-  for (int k = 1; k < n; ++k) {
-    const double2 t = T[k];
-    const double e2 = T[k - 1].y;
+// Sturm count state of one shift: the number of eigenvalues of T below s = sign changes of the
+// leading principal minors p_0 = 1, p_1 = d_0 - s, p_{k+1} = (d_k - s) p_k - e_{k-1}^2 p_{k-1}
+// (negative LDL^T pivots).  Advanced over a shared-memory tile of T (every thread of the CTA
+// walks the same entries: broadcast reads), four steps between exact power-of-two rescalings
+// (the pair's magnitude changes by far less than 2^500 in four steps): the dependency chain is
+// one FMA per step.
+struct Sturm {
+  double pp, p, e2;
+  int cnt;
+  __device__ void start(double2 t0, double s) {
+    pp = 1.0;
+    p = t0.x - s;
+    cnt = p < 0.0;
+    e2 = t0.y;
+  }
+  __device__ __forceinline__ void step(double2 t, double s) {
     const double pn = fma(t.x - s, p, -e2 * pp);
     cnt += ((pn < 0.0) != (p < 0.0)) || pn == 0.0;
     pp = p;
     p = pn;
+    e2 = t.y;
+  }
+  __device__ __forceinline__ void rescale() {
     const double m = fmax(fabs(p), fabs(pp));
     if (m > 0x1p+500) {
       p *= 0x1p-500;
@@ -69,7 +80,40 @@ __device__ __forceinline__ int sturm_count(const double2* __restrict__ T, int n,
       pp *= 0x1p+500;
     }
   }
-  return cnt;
+  // entries [k0, k1) of the tile (k0 >= 1 globally handled by the caller)
+  __device__ void run(const double2* tile, int k0, int k1, double s) {
+    int k = k0;
+    for (; k + 3 < k1; k += 4) {
+      const double2 t0 = tile[k], t1 = tile[k + 1], t2 = tile[k + 2], t3 = tile[k + 3];
+      step(t0, s);
+      step(t1, s);
+      step(t2, s);
+      step(t3, s);
+      rescale();
+    }
+    for (; k < k1; ++k) step(tile[k], s);
+    rescale();
+  }
+};
+
+constexpr int RITZ_TILE = 2048;  // double2 entries of T per shared-memory tile (32 KB)
+
+// count(s) for this thread's shift over all n entries of T, tile by tile (all threads call it)
+__device__ int sturm_count_tiled(const double2* __restrict__ T, int n, double s, double2* tile) {
+  Sturm S;
+  for (int base = 0; base < n; base += RITZ_TILE) {
+    const int len = min(RITZ_TILE, n - base);
+    __syncthreads();
+    for (int i = threadIdx.x; i < len; i += blockDim.x) tile[i] = T[base + i];
+    __syncthreads();
+    if (base == 0) {
+      S.start(tile[0], s);
+      S.run(tile, 1, len, s);
+    } else {
+      S.run(tile, 0, len, s);
+    }
+  }
+  return S.cnt;
 }
 
 __global__ void __launch_bounds__(RITZ_THREADS) lanczos_ritz_kernel(CgState* st, const double2* T, int cap) {
@@ -79,6 +123,7 @@ __global__ void __launch_bounds__(RITZ_THREADS) lanczos_ritz_kernel(CgState* st,
   const int n = S->lz_n;
   __shared__ double s_lo[RITZ_THREADS], s_hi[RITZ_THREADS];
   __shared__ int s_cnt[RITZ_THREADS];
+  __shared__ double2 tile[RITZ_TILE];
   __shared__ double s_a, s_b;
   if (n <= 0) {
     if (threadIdx.x == 0) {
@@ -118,7 +163,7 @@ __global__ void __launch_bounds__(RITZ_THREADS) lanczos_ritz_kernel(CgState* st,
     const double f = (double)(threadIdx.x + 1) / (RITZ_THREADS + 1);
     const double s = which == 1 ? a + (b - a) * f : a * exp2(log2(b / a) * f);
     s_lo[threadIdx.x] = s;
-    s_cnt[threadIdx.x] = sturm_count(T, n, s);
+    s_cnt[threadIdx.x] = sturm_count_tiled(T, n, s, tile);
     __syncthreads();
     if (threadIdx.x == 0) {
       if (which == 1) {  // first shift with all n eigenvalues below it
