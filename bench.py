@@ -417,10 +417,6 @@ def run_gpu(args):
     else:               # values + block column ids + node_ptr + p, q
         spmv_bytes = 8 * stored_vals + 4 * stored_blocks + 8 * (n_nodes + 1) + 16 * ndof
     spmv_avg_ms = spmv_ms / max(spmv_n, 1)
-    if args.virtual_parts > 1:
-        # the sampled launch is part 0's SpMV: its share of the stored values (strips of equal
-        # node counts; the halo rows are not processed)
-        spmv_bytes = spmv_bytes / args.virtual_parts
     achieved = spmv_bytes / (spmv_avg_ms / 1000.0) / 1e9 if spmv_n else None
     roofline = {"bound": "hbm",
                 "kernel": {0: "spmv_dot (CG q = K p, p^T q)",
@@ -431,7 +427,7 @@ def run_gpu(args):
                 "launches": spmv_n, "peak_source": peak_src,
                 "share_of_step": (spmv_avg_ms * (cg_iters + 1) * args.steps / ms_total) if spmv_n else None,
                 "sampling": ("CUDA event pairs around every 16th SpMV launch of the CG loop (graph event nodes)"
-                             + ("; part 0 of the strips, bytes = stored values / parts" if args.virtual_parts > 1 else ""))}
+                             + ("; one launch covers every strip" if args.virtual_parts > 1 else ""))}
     asm_ms = (el_ms + as_ms) / max(args.steps, 1)
     grad_ms = gr_ms / max(args.steps, 1)
     clocks = clk.summary()

@@ -212,6 +212,11 @@ struct sso_ctx {
   // SpMVs and updates overlap (one part's tail with the next part's start)
   std::vector<cudaStream_t> part_streams;
   std::vector<cudaEvent_t> part_ev;
+  // in-process parts in ONE launch per step (grid.y = part): device arrays of per-part
+  // operands for the pull SpMV (u -> q) and the single-reduction update
+  PullPart* d_pull_parts = nullptr;
+  SrPart* d_sr_parts = nullptr;
+  int max_own = 0;
   double* d_dt_all = nullptr;  // virtual parts: global dC/dt assembly buffer
   double* h_C = nullptr;       // pinned scalar
 
@@ -587,7 +592,11 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev, int it) {
     if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
   } else {
     if ((rc = exchange(h, V_U, s))) return rc;
-    if (!h->part_streams.empty() && !ev) {
+    if (h->d_pull_parts) {  // every part's SpMV in one launch
+      if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
+      launch_spmv_pull_multi(s, h->d_pull_parts, (int)h->parts.size(), h->max_own);
+      if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
+    } else if (!h->part_streams.empty() && !ev) {
       // in-process parts: the parts' SpMVs on their own streams (fork / join inside the graph)
       const size_t np = h->parts.size();
       CK(h, cudaEventRecord(h->ev_fork, s));
@@ -614,6 +623,10 @@ int cg_iteration(sso_ctx* h, cudaStream_t s, const cudaEvent_t* ev, int it) {
     }
   }
   if ((rc = allreduce(h, 4, s))) return rc;
+  if (h->d_sr_parts) {
+    launch_cgsr_update_multi(s, h->d_sr_parts, (int)h->parts.size(), h->max_own);
+    return SSO_OK;
+  }
   if (!h->part_streams.empty()) {
     const size_t np = h->parts.size();
     CK(h, cudaEventRecord(h->ev_fork, s));
@@ -705,6 +718,8 @@ void free_all(sso_ctx* h) {
   h->parts.clear();
   if (h->d_sts) cudaFree(h->d_sts);
   if (h->d_halo_ent) cudaFree(h->d_halo_ent);
+  if (h->d_pull_parts) cudaFree(h->d_pull_parts);
+  if (h->d_sr_parts) cudaFree(h->d_sr_parts);
   for (auto b : h->d_vbase)
     if (b) cudaFree(b);
   if (h->side_stream) cudaStreamDestroy(h->side_stream);
@@ -1309,6 +1324,38 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
           h->err = "stream / event create failed";
           return bail(SSO_E_CUDA);
         }
+    }
+    // in-process parts with pull storage: one launch per step for all parts (SSO_MULTI=0: per-part
+    // launches on per-part streams, for A/B)
+    const char* envm = getenv("SSO_MULTI");
+    if (o.nranks == 1 && !h->split && all_pull && !(envm && envm[0] == '0')) {
+      std::vector<PullPart> pp(h->parts.size());
+      std::vector<SrPart> sp(h->parts.size());
+      for (size_t i = 0; i < h->parts.size(); ++i) {
+        Part& P = *h->parts[i];
+        std::memset(&pp[i], 0, sizeof(PullPart));
+        pp[i].tmap = P.pull_tmap;
+        pp[i].pdesc = P.pdesc;
+        pp[i].ucol = P.node_col;
+        pp[i].lpull = reinterpret_cast<const int2*>(P.lpull);
+        pp[i].vals = P.vals;
+        pp[i].x = P.u_sr;
+        pp[i].y = P.q;
+        pp[i].partial = P.partial;
+        pp[i].st = P.st;
+        pp[i].n_nodes = P.n_own;
+        sp[i] = SrPart{P.binv ? nullptr : P.dinv, P.binv, P.xs, P.r, P.u_sr, P.q, P.p, P.s_sr, P.partial, P.st,
+                       P.n_own, 0};
+        h->max_own = std::max(h->max_own, P.n_own);
+      }
+      int r = upload(h, &h->d_pull_parts, pp.data(), (int64_t)pp.size());
+      if (r || (r = upload(h, &h->d_sr_parts, sp.data(), (int64_t)sp.size()))) return bail(r);
+      for (auto ps : h->part_streams)
+        if (ps) cudaStreamDestroy(ps);
+      for (auto e : h->part_ev)
+        if (e) cudaEventDestroy(e);
+      h->part_streams.clear();
+      h->part_ev.clear();
     }
     if (h->split || !h->part_streams.empty()) {
       if (cudaStreamCreateWithFlags(&h->side_stream, cudaStreamNonBlocking) != cudaSuccess ||

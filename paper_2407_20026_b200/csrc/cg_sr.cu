@@ -86,8 +86,23 @@ __global__ void __launch_bounds__(256) cgsr_update_kernel(int n_own, const doubl
                                                           const double* __restrict__ binv, double* __restrict__ x,
                                                           double* __restrict__ r, double* __restrict__ u,
                                                           const double* __restrict__ w, double* __restrict__ p,
-                                                          double* __restrict__ sv, double* partial, CgState* st) {
+                                                          double* __restrict__ sv, double* partial, CgState* st,
+                                                          const SrPart* __restrict__ mp) {
   __shared__ double sm[64];
+  if (mp) {  // part blockIdx.y of a multi-part launch
+    const SrPart& A = mp[blockIdx.y];
+    n_own = A.n_own;
+    dinv = A.dinv;
+    binv = A.binv;
+    x = A.x;
+    r = A.r;
+    u = A.u;
+    w = A.w;
+    p = A.p;
+    sv = A.sv;
+    partial = A.partial;
+    st = A.st;
+  }
   if (st->done) return;
   // allreduced: delta (this iteration's SpMV), gamma and r^T r (the previous update), |f|^2
   const double delta = st->red[0], gamma = st->red[1], rr = st->red[2];
@@ -222,8 +237,16 @@ void launch_cgsr_init(cudaStream_t s, int n_own, const double* f, const uint8_t*
 void launch_cgsr_update(cudaStream_t s, int n_own, const double* dinv, const double* binv, double* x, double* r,
                         double* u, const double* w, double* p, double* sv, double* partial, CgState* st, int share) {
   const int g = std::max(1, vgrid(n_own) / std::max(share, 1));
-  cgsr_update_kernel<<<g, 256, 0, s>>>(n_own, binv ? nullptr : dinv, binv, x, r, u, w, p, sv, partial, st);
+  cgsr_update_kernel<<<g, 256, 0, s>>>(n_own, binv ? nullptr : dinv, binv, x, r, u, w, p, sv, partial, st, nullptr);
   SSO_POST_LAUNCH("cgsr_update_kernel");
+}
+
+void launch_cgsr_update_multi(cudaStream_t s, const SrPart* mp, int n_parts, int max_own) {
+  if (n_parts <= 0) return;
+  const int g = std::max(1, vgrid(max_own) / n_parts);
+  cgsr_update_kernel<<<dim3(g, n_parts), 256, 0, s>>>(max_own, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                                      nullptr, nullptr, nullptr, nullptr, mp);
+  SSO_POST_LAUNCH("cgsr_update_kernel (parts)");
 }
 
 void launch_cgsr_replace(cudaStream_t s, int n_own, const double* fbc, const double* Kx, const double* dinv,

@@ -31,6 +31,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "cg_common.cuh"
 #include "tma.cuh"
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
     const int32_t* __restrict__ pdesc,
     const int32_t* __restrict__ ucol, const int2* __restrict__ lpull, const double* __restrict__ vals,
     const double* __restrict__ p, double* __restrict__ q, double* __restrict__ partial, CgState* st,
-    BatchStrides bs) {
+    BatchStrides bs, const PullPart* __restrict__ mp) {
   using S = PullChunkSmem<C, W>;
   constexpr int NPW = S::NPW;
   constexpr unsigned FULL = 0xffffffffu;
@@ -346,8 +347,24 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
   __shared__ __align__(8) uint64_t empty_bar[NB];  // consumers done with the buffer
   __shared__ int chunk_fits[NB];
   __shared__ double sm[32];
-  const int row0 = blockIdx.y * rows_per_design;
-  {  // design of a batch (blockIdx.y)
+  int row0 = blockIdx.y * rows_per_design;
+  const CUtensorMap* tm = &tmap;
+  if (mp) {  // part blockIdx.y of a multi-part launch: its own operands and tensor map
+    const PullPart& A = mp[blockIdx.y];
+    tm = &A.tmap;
+    row0 = 0;
+    n_nodes = A.n_nodes;
+    pdesc = A.pdesc;
+    ucol = A.ucol;
+    lpull = A.lpull;
+    vals = A.vals;
+    p = A.x;
+    q = A.y;
+    if (DOT) {
+      partial = A.partial;
+      st = A.st;
+    }
+  } else {  // design of a batch (blockIdx.y)
     const int bd = blockIdx.y;
     vals += bd * bs.nnz;
     p += bd * bs.dof;
@@ -438,7 +455,7 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
         int r[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) r[i] = row0 + (i < ldeg ? Dl[2 * i] : d0.x);
-        tma_gather4(buf + S::PSLOT * lane, &tmap, r[0], r[1], r[2], r[3], &full_bar[b], pol);
+        tma_gather4(buf + S::PSLOT * lane, tm, r[0], r[1], r[2], r[3], &full_bar[b], pol);
       }
     }
   } else {
@@ -1299,9 +1316,9 @@ struct PullVariant {
   int threads;
   int chunk;  // nodes per CTA chunk
   void (*dot)(const CUtensorMap, int, int, int, int, const int32_t*, const int32_t*, const int2*, const double*,
-              const double*, double*, double*, CgState*, BatchStrides);
+              const double*, double*, double*, CgState*, BatchStrides, const PullPart*);
   void (*plain)(const CUtensorMap, int, int, int, int, const int32_t*, const int32_t*, const int2*, const double*,
-                const double*, double*, double*, CgState*, BatchStrides);
+                const double*, double*, double*, CgState*, BatchStrides, const PullPart*);
 };
 #define PULL_CTA_VARIANT(C, NB, M, W)                                                                 \
   {                                                                                                   \
@@ -1389,11 +1406,26 @@ void launch_spmv_pull(cudaStream_t s, const CUtensorMap* tmap, int n_nodes, int 
   const int2* lp = reinterpret_cast<const int2*>(lpull);
   if (st)
     V.dot<<<dim3(grid, bs.B), V.threads, smem, s>>>(*tmap, n_nodes, node0, red_add, rows_per_design, pdesc, ucol, lp,
-                                                         vals, x, y, partial, st, bs);
+                                                         vals, x, y, partial, st, bs, nullptr);
   else
     V.plain<<<dim3(grid, bs.B), V.threads, smem, s>>>(*tmap, n_nodes, node0, red_add, rows_per_design, pdesc, ucol,
-                                                           lp, vals, x, y, nullptr, nullptr, bs);
+                                                           lp, vals, x, y, nullptr, nullptr, bs, nullptr);
   SSO_POST_LAUNCH(st ? "spmv_pull_dot_kernel" : "spmv_pull_kernel");
+}
+
+void launch_spmv_pull_multi(cudaStream_t s, const PullPart* mp, int n_parts, int max_nodes) {
+  if (n_parts <= 0 || max_nodes <= 0) return;
+  int smem;
+  const PullVariant& V = pull_variant(1, &smem);  // the single-design variant: parts are large
+  const int ctas = std::max(1, V.minb * (cg_grid() / 4) / n_parts);  // the parts side by side
+  const int units = (max_nodes + V.chunk - 1) / V.chunk;
+  const int grid = std::max(1, std::min(ctas, units));
+  // the per-launch tensor map parameter is unused (each part brings its own)
+  CUtensorMap dummy;
+  std::memset(&dummy, 0, sizeof dummy);
+  V.dot<<<dim3(grid, n_parts), V.threads, smem, s>>>(dummy, max_nodes, 0, 0, 0, nullptr, nullptr, nullptr, nullptr,
+                                                          nullptr, nullptr, nullptr, nullptr, BatchStrides(), mp);
+  SSO_POST_LAUNCH("spmv_pull_dot_kernel (parts)");
 }
 
 void launch_spmv(cudaStream_t s, int n_nodes, const int64_t* node_ptr, const int32_t* node_col,

@@ -208,6 +208,23 @@ int cg_block_fused_grid();
 // the row-owner warp streams its upper run and the upper blocks (n, m) of its lower
 // neighbours (pull list lpull = [(n, upper block index)] per node, via lptr) and
 // forms y = K x in one pass.  With st != nullptr also p^T q and alpha (CG).
+// In-process parts in ONE launch (grid.y = part): each part's SpMV operands, its own tensor map
+// (global memory, 64-byte aligned) and owned row count.
+struct alignas(64) PullPart {
+  CUtensorMap tmap;
+  const int32_t* pdesc;
+  const int32_t* ucol;
+  const int2* lpull;
+  const double* vals;
+  const double* x;
+  double* y;
+  double* partial;
+  CgState* st;
+  int n_nodes;
+  int pad_[3];
+};
+// y = K x with p^T q pieces into st->red[0] for every part of `mp` (device array of n_parts).
+void launch_spmv_pull_multi(cudaStream_t s, const PullPart* mp, int n_parts, int max_nodes);
 // Rows [node0, n_nodes) (default: all owned rows); on partitioned handles (st->dist) the
 // p^T q piece is written to st->red[0] (red_add = 0) or added to it (red_add = 1).  share > 1:
 // the launch runs concurrently with share - 1 others (in-process parts on their own streams)
@@ -273,6 +290,18 @@ void launch_cgsr_init(cudaStream_t s, int n_own, const double* f, const uint8_t*
 void launch_cgsr_update(cudaStream_t s, int n_own, const double* dinv, const double* binv, double* x, double* r,
                         double* u, const double* w, double* p, double* sv, double* partial, CgState* st,
                         int share = 1);
+// The single-reduction update of every in-process part in one launch (grid.y = part).
+struct SrPart {
+  const double* dinv;
+  const double* binv;
+  double *x, *r, *u;
+  const double* w;
+  double *p, *sv, *partial;
+  CgState* st;
+  int n_own;
+  int pad_;
+};
+void launch_cgsr_update_multi(cudaStream_t s, const SrPart* mp, int n_parts, int max_own);
 void launch_cgsr_replace(cudaStream_t s, int n_own, const double* fbc, const double* Kx, const double* dinv,
                          const double* binv, double* r, double* u, double* partial, CgState* st);
 // In-process halo fill of all parts in one launch: entry k = (dst part, dst node, src part,
