@@ -395,7 +395,11 @@ __global__ void __launch_bounds__(32 * (W + 1), MINB) spmv_pull_cta_kernel(
   double pq[1] = {0.0};
   if (warp == W) {
     // ---------------- producer ----------------
-    const uint64_t pol = evict_first_policy();
+    // evict-first: a record is pulled again (by its column node) by a chunk of the same window
+    // soon after; parts launched together stretch that distance, so they keep records
+    // evict-normal (C4 in 8 strips: 516 -> 505 us per iteration; a single C3b part loses its
+    // L2-resident CG vectors with evict-normal: 68.9 -> 76.1 us)
+    const uint64_t pol = mp ? evict_normal_policy() : evict_first_policy();
     // descriptors of chunk k are loaded one chunk ahead (off the empty-barrier critical path)
     auto load_desc = [&](int k, int4& a, int4& b2, int4& c, int4& d) {
       const int first = node0 + ((int)blockIdx.x + k * (int)gridDim.x) * C;
