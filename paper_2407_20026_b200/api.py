@@ -239,7 +239,13 @@ class Model:
         self._mem = MEM_HOST
         self._stream = stream
         self._dev_opt = device
-        self._device_idx = None
+        self._device_idx = device if device >= 0 else None
+        if self._device_idx is None:  # the device sso_create made current (-1: the caller's current)
+            try:
+                import torch
+                self._device_idx = torch.cuda.current_device()
+            except Exception:
+                self._device_idx = None
 
     # -- plumbing ----------------------------------------------------------
     def _check(self, rc):
