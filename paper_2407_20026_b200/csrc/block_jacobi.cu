@@ -155,12 +155,6 @@ __global__ void __launch_bounds__(256) cg_init_block_kernel(int n_nodes, const d
     }
   }
   if (grid_sum<3>(v, partial, &st->ticket[2], sm) && threadIdx.x == 0) {
-    if (st->dist) {
-      st->red[0] = v[0];
-      st->red[1] = v[1];
-      st->red[2] = v[2];
-      return;
-    }
     st->ff = v[0];
     st->rz = v[1];
     st->rr = v[2];
@@ -218,11 +212,6 @@ __global__ void __launch_bounds__(256) cg_update_block_kernel(int n_nodes, const
     }
   }
   if (grid_sum<2>(v, partial, &st->ticket[1], sm) && threadIdx.x == 0) {
-    if (st->dist) {
-      st->red[0] = v[0];
-      st->red[1] = v[1];
-      return;
-    }
     const double rz_new = v[0];
     st->beta = rz_new / st->rz;
     st->rz_prev = st->rz;
@@ -410,16 +399,12 @@ __global__ void __launch_bounds__(256) cg_replace_block_kernel(int n_nodes, cons
     }
   }
   if (grid_sum<2>(v, partial, &st->ticket[1], sm) && threadIdx.x == 0) {
-    st->red[0] = v[0];
-    st->red[1] = v[1];
-    if (!st->dist) {
-      st->rz = v[0];
-      st->rr = v[1];
-      st->rr_ref = v[1];
-      st->beta = (mode == REPL_FINAL || st->act == 2) ? 0.0 : v[0] / st->rz_prev;
-      st->act = 0;
-      st->pfix = 1;
-    }
+    st->rz = v[0];
+    st->rr = v[1];
+    st->rr_ref = v[1];
+    st->beta = (mode == REPL_FINAL || st->act == 2) ? 0.0 : v[0] / st->rz_prev;
+    st->act = 0;
+    st->pfix = 1;
   }
 }
 

@@ -685,11 +685,6 @@ __global__ void __launch_bounds__(256) cg_update_kernel(int ndof, const double* 
     v[1] += ri.x * ri.x + ri.y * ri.y;
   }
   if (grid_sum<2>(v, partial, &st->ticket[1], sm) && threadIdx.x == 0) {
-    if (st->dist) {
-      st->red[0] = v[0];
-      st->red[1] = v[1];
-      return;
-    }
     const double rz_new = v[0];
     st->beta = rz_new / st->rz;
     st->rz_prev = st->rz;
@@ -896,12 +891,6 @@ __global__ void __launch_bounds__(256) cg_init_kernel(int ndof, const double* __
     v[2] += ri * ri;
   }
   if (grid_sum<3>(v, partial, &st->ticket[2], sm) && threadIdx.x == 0) {
-    if (st->dist) {
-      st->red[0] = v[0];
-      st->red[1] = v[1];
-      st->red[2] = v[2];
-      return;
-    }
     st->ff = v[0];
     st->rz = v[1];
     st->rr = v[2];
@@ -942,61 +931,6 @@ __global__ void __launch_bounds__(256) residual_kernel(int ndof, const double* _
     v[0] += d * d;
   }
   if (grid_sum<1>(v, partial, &st->ticket[3], sm) && threadIdx.x == 0) st->red[0] = v[0];
-}
-
-// Scalar step of the partitioned CG after the cross-part allreduce of red[].
-__global__ void cg_scalar_kernel(CgState* st, int phase) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  if (phase == PH_INIT) {
-    const double ff = st->red[0], rz = st->red[1], rr = st->red[2];
-    st->ff = ff;
-    st->rz = rz;
-    st->rr = rr;
-    st->iter = 0;
-    st->status = SSO_OK;
-    st->done = (rr <= st->tol2 * ff || ff == 0.0) ? 1 : 0;
-    st->tol2 = st->tol2 * ff;
-    st->alpha = st->beta = 0.0;
-    st->rr_ref = rr;
-    return;
-  }
-  if (phase == PH_REPLACED || phase == PH_REPLACED + 1) {  // after the allreduce of the replaced r
-    if (st->act) {
-      st->rz = st->red[0];
-      st->rr = st->red[1];
-      st->rr_ref = st->red[1];
-      // restart (final): p = z; periodic: beta from the replaced r^T z
-      st->beta = (phase == PH_REPLACED + 1 || st->act == 2) ? 0.0 : st->red[0] / st->rz_prev;
-      st->act = 0;
-    }
-    return;
-  }
-  if (st->done) return;
-  if (phase == PH_ALPHA) {
-    const double pq = st->red[0];
-    st->pq = pq;
-    if (!(pq > 0.0)) {
-      st->status = SSO_E_NOT_SPD;
-      st->done = 1;
-    } else {
-      st->alpha = st->rz / pq;
-    }
-  } else {
-    const double rz_new = st->red[0];
-    st->beta = rz_new / st->rz;
-    st->rz_prev = st->rz;
-    st->rz = rz_new;
-    st->rr = st->red[1];
-    st->iter += 1;
-    lz_record(st, st->alpha, st->beta);
-    if (st->rr <= st->tol2) {
-      st->done = 1;
-      st->status = SSO_OK;
-    } else if (st->iter >= st->max_iter) {
-      st->done = 1;
-      st->status = SSO_E_NOT_CONVERGED;
-    }
-  }
 }
 
 // |f_bc - K x|^2 (local part) into red[0]; design from blockIdx.y.
@@ -1083,17 +1017,13 @@ __global__ void __launch_bounds__(256) cg_replace_kernel(int ndof, const double*
     v[1] += ri * ri;
   }
   if (grid_sum<2>(v, partial, &st->ticket[1], sm) && threadIdx.x == 0) {
-    st->red[0] = v[0];
-    st->red[1] = v[1];
-    if (!st->dist) {
-      st->rz = v[0];
-      st->rr = v[1];
-      st->rr_ref = v[1];
-      // the next p update forms p = z + beta p: restart (final) -> beta = 0
-      st->beta = (mode == REPL_FINAL || st->act == 2) ? 0.0 : v[0] / st->rz_prev;
-      st->act = 0;
-      st->pfix = 1;
-    }
+    st->rz = v[0];
+    st->rr = v[1];
+    st->rr_ref = v[1];
+    // the next p update forms p = z + beta p: restart (final) -> beta = 0
+    st->beta = (mode == REPL_FINAL || st->act == 2) ? 0.0 : v[0] / st->rz_prev;
+    st->act = 0;
+    st->pfix = 1;
   }
 }
 
@@ -1185,10 +1115,6 @@ void launch_lincomb(cudaStream_t s, int64_t n, double a, const double* x, double
   SSO_POST_LAUNCH("lincomb_kernel");
 }
 
-void launch_cg_scalar(cudaStream_t s, CgState* st, int phase) {
-  cg_scalar_kernel<<<1, 32, 0, s>>>(st, phase);
-  SSO_POST_LAUNCH("cg_scalar_kernel");
-}
 
 void launch_pack(cudaStream_t s, int count, const int32_t* idx, const double* vec, double* buf) {
   if (count <= 0) return;

@@ -71,8 +71,8 @@ struct CgState {
   int done;         // 1 = converged or failed: all later kernels return immediately
   int status;       // sso_status
   unsigned int ticket[4];  // last-block-done counters (one per reduction site)
-  int dist;         // 1 = partitioned: kernels write local sums to red[], a scalar
-                    //     kernel forms alpha / beta after the cross-part allreduce
+  int dist;         // 1 = partitioned: the SpMV writes its local p^T q piece to red[0] (the
+                    //     single-reduction CG of cg_sr.cu allreduces red[] across parts)
   int act;         // residual replacement selected for this design (see cg_check)
   double red[4];    // local (then global) reduction values
   double rr_ref;    // r^T r at the last residual replacement
@@ -325,7 +325,6 @@ void launch_zero_fixed(cudaStream_t s, int ndof, const uint8_t* fixed_mask, doub
     const BatchStrides& bs = BatchStrides());
 
 // Partitioned-solve helpers
-enum ScalarPhase { PH_INIT = 0, PH_ALPHA = 1, PH_BETA = 2, PH_REPLACED = 3 };
 // Reliable updates (residual replacement): REPL_PERIODIC replaces r by f - K x for
 // active designs whose r^T r fell below REPL_FACTOR * rr_ref; REPL_FINAL restarts
 // (r = f - K x, p = z) converged designs whose TRUE residual exceeds 2 rtol.  Both
@@ -343,7 +342,6 @@ void launch_cg_check(cudaStream_t s, CgState* st, int mode, int B);
 void launch_cg_replace(cudaStream_t s, int ndof, const double* fbc, const double* Kx,
                        const double* dinv, double* r, double* p, double* partial, CgState* st, int mode,
                        const BatchStrides& bs = BatchStrides());
-void launch_cg_scalar(cudaStream_t s, CgState* st, int phase);
 void launch_pack(cudaStream_t s, int count, const int32_t* idx, const double* vec, double* buf);
 void launch_allreduce_parts(cudaStream_t s, CgState* const* sts, int n_parts, int nvals);
 // out = a x + b y (elementwise, n doubles)
