@@ -1002,9 +1002,9 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   AL(dt, (int64_t)B * std::max<int32_t>(P.n_quads, 1));
   AL(dt_own, std::max<int32_t>(P.n_own_quads, 1));
   AL(dE, (int64_t)B * std::max<int64_t>(ne, 1));
-  // Lanczos history: the first CG segment of up to 2^18 iterations per design (2^22 / B for
+  // Lanczos history: the first CG segment of up to 2^18 iterations per design (2^20 / B, at least 4096, for
   // batches); longer solves keep the leading 2^18 coefficients (still interlacing Ritz values)
-  P.lz_cap = (int)std::min<int64_t>(h->max_iter, B == 1 ? (1 << 18) : std::max(1024, (1 << 22) / B));
+  P.lz_cap = (int)std::min<int64_t>(h->max_iter, B == 1 ? (1 << 18) : std::max(4096, (1 << 20) / B));
   AL(lz_hist, 2 * (int64_t)B * P.lz_cap);
   AL(lz_T, 2 * (int64_t)B * P.lz_cap);
   AL(mscale_d, B);
