@@ -140,7 +140,7 @@ _WP = None
 def _worker_init(workload):
     global _WP
     import workloads as W
-    _WP = {"C3b": W.config3b, "C4": W.config4}[workload]()
+    _WP = {"C3b": W.config3b, "C4": W.config4, "C5": lambda: W.config5_design(0)}[workload]()
 
 
 def _worker_elems(elems):
@@ -189,7 +189,8 @@ def oracle_sample(workload, n_quads, cores, n_elem_per_core=250, n_grad_per_core
     import workloads as W
     rng = np.random.default_rng(0)
     n_elem, n_grad = n_elem_per_core * cores, n_grad_per_core * cores
-    elems = rng.choice(n_quads, max(n_elem, n_grad), replace=False)
+    k = max(n_elem, n_grad)
+    elems = rng.choice(n_quads, k, replace=k > n_quads)  # C5 has 2 500 quads: many host cores revisit some
     ctx = mp.get_context("fork")
     with ctx.Pool(cores, initializer=_worker_init, initargs=(workload,)) as pool:
         pool.map(_worker_elems, [elems[:1]] * cores)  # workers built their inputs
@@ -199,7 +200,7 @@ def oracle_sample(workload, n_quads, cores, n_elem_per_core=250, n_grad_per_core
         t0 = time.perf_counter()
         pool.map(_worker_grads, np.array_split(elems[:n_grad], cores))
         t_grad = (time.perf_counter() - t0) / n_grad
-    Q = W.shell_config3(pcg_grid, cfg=3)
+    Q = W.config5_design(0) if workload == "C5" else W.shell_config3(pcg_grid, cfg=3)
     nd = 6 * len(Q["x"])
     rp, ci, v = OA.csr_from_dok(OA.assemble_dok(Q), nd)
     fixed = OA.fixed_dofs(Q)
@@ -242,9 +243,57 @@ def cpu_baseline_obj(workload, cg_iters, cores=None):
             "per_unit_s": {"element": te, "grad_element": tg, "cg_iter_per_nnz": ti}}
 
 
+C5_N = 50
+
+
+def cpu_baseline_c5(cg_iters, cores=None, n_elem_per_core=250, n_grad_per_core=40, pcg_iters=200):
+    """Oracle baseline for C5 in designs/s: the C5 designs are independent, so each host core
+    evaluates its own design — per-design time on one core (pool element rates x cores, the
+    PCG sample is single-threaded already) and `cores` designs in flight."""
+    cores = cores or host_cores()
+    nq = C5_N * C5_N
+    t0 = time.perf_counter()
+    te, tg, ti = oracle_sample("C5", nq, cores, n_elem_per_core, n_grad_per_core, pcg_iters=pcg_iters)
+    wall = time.perf_counter() - t0
+    t_design = nq * (te + tg) * cores + cg_iters * grid_nnz(C5_N) * ti
+    return {"value": cores / t_design, "unit": "designs/s", "cores": cores, "kind": "oracle",
+            "sample": (f"oracle as it stands on C5 design 0 (extrapolated, not a full run): "
+                       f"{n_elem_per_core * cores} elements (K_e + DOK) and {n_grad_per_core * cores} element "
+                       f"gradients over a {cores}-process pool, {pcg_iters} PCG iterations (scipy CSR, 1 "
+                       f"thread) on the design itself; {wall:.1f} s wall; scaled to {nq} elements, "
+                       f"{grid_nnz(C5_N)} nnz, {cg_iters} CG iterations = {t_design:.1f} s per design on one "
+                       f"core, {cores} designs in flight"),
+            "extrapolated": True,
+            "per_unit_s": {"element": te, "grad_element": tg, "cg_iter_per_nnz": ti}}
+
+
+C5_METRIC = "C5 batched shell design evaluations (solve + adjoint gradient) per second"
+C5_ITERS = 3400  # median CG iterations of the 64 seeded C5 designs at rtol 1e-10 (profiles/r02/bench_c5.json)
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
+        return
+    if args.workload == "C5":
+        times, vals = [], []
+        for k in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            cb = cpu_baseline_c5(C5_ITERS, n_elem_per_core=40, n_grad_per_core=6, pcg_iters=60)
+            if k >= args.warmup:
+                times.append(time.perf_counter() - t0)
+                vals.append(cb["value"])
+        value = float(np.median(vals))
+        cb["value"] = value
+        print(json.dumps({"impl": "reference", "metric": C5_METRIC, "value": value, "unit": "designs/s",
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                          "config": {"workload": f"C5: {args.batch} designs/GPU x 50x50 MITC-4 quads (15 606 DOF each)",
+                                     "rtol": RTOL, "cg_iters": C5_ITERS},
+                          "cpu_baseline": cb,
+                          "e2e": {"value": value, "unit": "designs/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}))
         return
     n, wname = WORKLOADS[args.workload if args.workload in WORKLOADS else "C3b"]
     cg_iters = args.cg_iters
@@ -565,6 +614,8 @@ def run_batch(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    m.profile_enable(True)
+    m.profile_reset()
     l0 = m.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
@@ -574,7 +625,10 @@ def run_batch(args):
             infos = step()
         ev1.record(stream)
         barrier()
+    launches = m.launch_count() - l0
     ms = ev0.elapsed_time(ev1)
+    spmv_ms, spmv_n = m.profile_read("spmv")
+    m.profile_enable(False)
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -582,8 +636,54 @@ def run_batch(args):
         ms = float(t.item())
     its = [i["iters"] for i in infos]
     value = world * B * args.steps / (ms / 1000.0)
+
+    # e2e: host (pinned) design arrays and loads in, u / C / gradients out, every step
+    Zh, Th, Fh = Z.cpu().pin_memory(), T.cpu().pin_memory(), F.cpu().pin_memory()
+    Uh = torch.zeros_like(Fh).pin_memory()
+    Ch = torch.zeros(B, dtype=torch.float64).pin_memory()
+    dXh = torch.zeros(B * 3 * m.n_nodes, dtype=torch.float64).pin_memory()
+    dTh = torch.zeros(B * m.n_quads, dtype=torch.float64).pin_memory()
+
+    def step_host():
+        m.set_design(z=Zh.numpy(), t=Th.numpy())
+        m.assemble()
+        m.solve(Fh.numpy(), Uh.numpy())
+        m.grad(sso.OBJ_COMPLIANCE, out=(Ch.numpy(), dXh.numpy(), dTh.numpy()))
+
+    step_host()
+    e2e_steps = max(1, min(args.steps, 5))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        step_host()
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    # roofline of the batched SpMV (one launch covers all B designs)
+    peak, peak_src = measured_peaks()
+    ndof = m.ndof
+    stored_vals, stored_blocks, symmetric = m.storage_info()
+    # values and p, q per design; the shared pattern (node descriptors / block columns) once
+    per_design = 8 * stored_vals + 16 * ndof
+    shared = 64 * m.n_nodes if symmetric == 3 else 4 * stored_blocks + 8 * (m.n_nodes + 1)
+    spmv_bytes = B * per_design + shared
+    spmv_avg_ms = spmv_ms / max(spmv_n, 1)
+    achieved = spmv_bytes / (spmv_avg_ms / 1000.0) / 1e9 if spmv_n else None
+    roofline = {"bound": "hbm", "kernel": "batched SpMV of the CG loop (all designs in one launch)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None, "traffic": None,
+                "algorithmic_bytes_per_launch": spmv_bytes, "avg_launch_ms": spmv_avg_ms,
+                "launches": spmv_n, "peak_source": peak_src,
+                "share_of_step": (spmv_avg_ms * (max(its) + 1) * args.steps / ms) if spmv_n else None,
+                "sampling": "CUDA event pairs around every 16th SpMV launch of the CG loop (graph event nodes)"}
     if rank == 0:
-        print(json.dumps({"metric": "C5 batched shell design evaluations (solve + adjoint gradient) per second",
+        cpu = cpu_baseline_c5(int(np.median(its))) if (world == 1 and not args.no_cpu) else None
+        print(json.dumps({"metric": C5_METRIC,
                           "value": value, "unit": "designs/s", "n_gpus": world, "steps": args.steps,
                           "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -591,8 +691,15 @@ def run_batch(args):
                           "config": {"workload": f"C5: {B} designs/GPU x 50x50 MITC-4 quads (15 606 DOF each)",
                                      "rtol": RTOL, "cg_iters_max": max(its), "cg_iters_min": min(its),
                                      "precond": {0: "point Jacobi", 1: "node-block Jacobi"}[args.precond],
-                                     "parallelism": f"{world} GPU(s) x {B} designs, no collective"},
-                          "gpu_launches": m.launch_count() - l0, "clocks": clk.summary()}))
+                                     "parallelism": f"{world} GPU(s) x {B} designs, no collective",
+                                     "storage": {0: "full node-block CSR", 3: "upper blocks (38-double records), "
+                                                 "one-pass pull SpMV"}[symmetric],
+                                     "l2": f"working set {spmv_bytes / 1e6:.0f} MB per SpMV vs 126 MB L2; no flush"},
+                          "roofline": roofline, "cpu_baseline": cpu,
+                          "e2e": {"value": world * B * e2e_steps / e2e_s, "unit": "designs/s",
+                                  "h2d_bytes_per_step": 8 * (Z.numel() + T.numel() + F.numel()),
+                                  "d2h_bytes_per_step": 8 * (U.numel() + B + dX.numel() + dT.numel())},
+                          "gpu_launches": launches, "clocks": clk.summary()}))
     if world > 1:
         import torch.distributed as dist
         dist.barrier()

@@ -28,6 +28,6 @@ byts = 8 * sv + 4 * sb + 8 * (m.n_nodes + 1) + 16 * ndof if kind != 3 else 8 * s
 avg = ms / max(cnt, 1)
 print(json.dumps({"precond": os.environ.get("PRECOND", "0"), "variant": os.environ.get("SSO_SPMV_VARIANT", "0"), "rel": os.environ.get("REL", "1"), "storage": os.environ.get("STORAGE", "0"),
                   "sup": sup, "n": n, "parts": os.environ.get("PARTS", "1"), "coop": os.environ.get("SSO_COOP", "1"), "iters": info["iters"],
-                  "solve_ms": min(ts), "us_per_iter": 1000 * min(ts) / info["iters"],
-                  "spmv_us": 1000 * avg, "spmv_GBs": byts / (avg / 1000) / 1e9,
+                  "solve_ms": min(ts), "us_per_iter": 1000 * min(ts) / (info["iters"] or int(os.environ.get("MAXIT", "1"))),
+                  "spmv_us": 1000 * avg, "spmv_GBs": byts / (avg / 1000) / 1e9 if avg else 0,
                   "true_rel_res": info["true_rel_res"]}))
