@@ -132,6 +132,8 @@ struct Part {
   std::vector<char> g_derived;          // G = E / (2 (1 + nu)) when G was not given
   // partition maps
   int32_t* block_rank = nullptr;      // quads [n_quads][16] (fused assembly; upper ranks when sym)
+  int32_t* inc_rec = nullptr;         // fused assembly: [n_own][inc_pad][8] incidence records
+  int inc_pad = 0;                    // max incident quads per node, rounded up to 4
   bool sym = false;                   // upper-block (symmetric) storage = pull (kept as one name)
   bool pull = false;                  // upper blocks with the one-pass pull SpMV (storage 3, 2x2 sub-block records)
   int32_t* lpull = nullptr;           // pull: (source node, upper block) per incoming block
@@ -699,7 +701,7 @@ void free_part(Part& P) {
                   P.gf, P.partial, P.st, P.flags, P.tickets, P.scal, P.slot_partial, P.dxyz, P.dt,
                   P.dt_own, P.own_quad_local, P.own_quad_gid, P.send_idx, P.sendbuf, P.block_rank,
                   P.lptr, P.lpull, P.pdesc, P.binv, P.zb, P.p2, P.dE,
-                  P.ub, P.fb, P.lam, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask,
+                  P.ub, P.fb, P.inc_rec, P.lam, P.ld_q, P.ld_w, P.ld_a, P.pb, P.kb, P.feff, P.free_mask,
                   P.rho, P.E0, P.G0, P.lz_hist, P.lz_T, P.mscale_d, P.u_sr, P.s_sr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -931,7 +933,37 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   }
   UP(inc_ptr, P.pat.inc_ptr.data(), P.n_nodes + 1);
   UP(inc_slot, P.pat.inc_slot.data(), P.n_slots);
-  if (P.fused) UP(block_rank, (P.sym ? P.up.urank : P.pat.block_rank).data(), 16 * (int64_t)P.n_quads);
+  if (P.fused) {
+    const std::vector<int32_t>& rk = P.sym ? P.up.urank : P.pat.block_rank;
+    UP(block_rank, rk.data(), 16 * (int64_t)P.n_quads);
+    // per (owned node, incident slot) record {quad, local index, its 4 nodes, its 4 block ranks
+    // (int8, -1 = not stored), 0}; quad -1 pads: the fused kernel's load chain node ->
+    // incidence -> element -> coordinates becomes record -> coordinates
+    P.inc_pad = std::max(4, (P.max_inc + 3) / 4 * 4);
+    std::vector<int32_t> rec((size_t)8 * P.n_own * P.inc_pad, 0);
+    for (int32_t n = 0; n < P.n_own; ++n) {
+      const int64_t i0 = P.pat.inc_ptr[n], ni = P.pat.inc_ptr[n + 1] - i0;
+      for (int kk = 0; kk < P.inc_pad; ++kk) {
+        int32_t* o = rec.data() + 8 * ((int64_t)n * P.inc_pad + kk);
+        if (kk >= ni) {
+          o[0] = -1;
+          continue;
+        }
+        const int32_t slot = P.pat.inc_slot[i0 + kk];  // 4 q + il (quad meshes)
+        const int64_t q = slot >> 2;
+        const int il = slot & 3;
+        o[0] = (int32_t)q;
+        o[1] = il;
+        uint32_t r4 = 0;
+        for (int c = 0; c < 4; ++c) {
+          o[2 + c] = L.quad_conn[4 * q + c];
+          r4 |= (uint32_t)(uint8_t)(int8_t)rk[16 * q + 4 * il + c] << (8 * c);
+        }
+        o[6] = (int32_t)r4;
+      }
+    }
+    UP(inc_rec, rec.data(), (int64_t)rec.size());
+  }
   UP(own_quad_local, L.own_quad_local.data(), P.n_own_quads);
   UP(own_quad_gid, own_gid.data(), P.n_own_quads);
   UP(send_idx, send.data(), P.n_send);
@@ -1434,8 +1466,8 @@ static int assemble_pass(sso_ctx* h, bool unconstrained) {
     const uint8_t* mask = unconstrained ? P.free_mask : P.fixed_mask;
     if (P.fused) {
       Scope sc(h, F_ASSEMBLE);
-      launch_quad_assemble_fused(h->stream, P.n_own, P.max_inc, P.node_ptr, P.node_col, P.inc_ptr, P.inc_slot,
-                                 P.block_rank, P.x, P.y, P.z, P.quad_conn, P.t, P.E + P.n_beams,
+      launch_quad_assemble_fused(h->stream, P.n_own, P.inc_pad, P.node_ptr, P.node_col, P.inc_rec,
+                                 P.x, P.y, P.z, P.t, P.E + P.n_beams,
                                  P.nu + P.n_beams, h->drill_alpha, mask, P.vals, P.dinv, P.flags,
                                  P.bs, P.pull ? 1 : 0);
       continue;

@@ -14,7 +14,11 @@
 // order of the staged path), then supports and dinv are applied and the run is
 // written once, coalesced.  HBM traffic is the CSR values written once plus the
 // (L2-resident) coordinates: the staged path's 2 x 36 x 16 x 8 B per quad of
-// element-matrix staging disappears.
+// element-matrix staging disappears.  Latency: each (node, incident quad) reads one
+// 32-byte incidence record {quad, local index, its 4 nodes, its 4 block ranks} built on the
+// host, so the load chain is record -> coordinates (was node -> incidence -> quad ->
+// connectivity -> coordinates, + block rank), and the column blocks' fixed masks are staged
+// in shared memory at the start (C3b: 0.419 -> 0.374 ms).
 #include <climits>
 
 #include "shell_math.cuh"
@@ -48,15 +52,15 @@ __device__ __forceinline__ void node_tying(int k, bool xi_dir, const double* G, 
 }
 
 __global__ void __launch_bounds__(128, 4) quad_assemble_fused_kernel(
-    int n_own, int max_inc, const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ node_col,
-    const int64_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc_slot,
-    const int32_t* __restrict__ block_rank, const double* __restrict__ gx, const double* __restrict__ gy,
-    const double* __restrict__ gz, const int32_t* __restrict__ conn, const double* __restrict__ gt,
+    int n_own, int inc_pad, const int64_t* __restrict__ node_ptr, const int32_t* __restrict__ node_col,
+    const int32_t* __restrict__ inc_rec, const double* __restrict__ gx, const double* __restrict__ gy,
+    const double* __restrict__ gz, const double* __restrict__ gt,
     const double* __restrict__ gE, const double* __restrict__ gnu, double drill_alpha,
     const uint8_t* __restrict__ fixed_mask, double* __restrict__ vals, double* __restrict__ dinv,
     DevFlags* flags, BatchStrides bs, int cm) {
   __shared__ double geo[NPC * 4 * GS];
   __shared__ double buf[NPC * 36 * MAXDEG];
+  __shared__ uint16_t ccol[NPC][MAXDEG];  // per column block: fixed mask of its node | self << 8
   {  // design of a batch (blockIdx.y)
     const int bd = blockIdx.y;
     gx += bd * bs.node;
@@ -74,35 +78,40 @@ __global__ void __launch_bounds__(128, 4) quad_assemble_fused_kernel(
   const int t16 = tid & 15;
   const int64_t n = (int64_t)blockIdx.x * NPC + ns;
   const bool node_ok = n < n_own;
-  int64_t b0 = 0, i0 = 0;
-  int deg = 0, ninc = 0;
+  int64_t b0 = 0;
+  int deg = 0;
   if (node_ok) {
     b0 = node_ptr[n];
     deg = (int)(node_ptr[n + 1] - b0);
-    i0 = inc_ptr[n];
-    ninc = (int)(inc_ptr[n + 1] - i0);
   }
   const int rowlen = 6 * deg;
   double* nbuf = buf + ns * 36 * MAXDEG;
   for (int v = t16; v < 36 * deg; v += 16) nbuf[v] = 0.0;
+  if (t16 < deg) {  // off the write phase's critical path (read after the group loop's barrier)
+    const int m = node_col[b0 + t16];
+    ccol[ns][t16] = (uint16_t)(fixed_mask[m] | (m == n ? 256 : 0));
+  }
 
-  for (int grp = 0; grp * 4 < max_inc; ++grp) {
+  for (int grp = 0; grp * 4 < inc_pad; ++grp) {
     const int kk = grp * 4 + k;
-    const bool has = node_ok && kk < ninc;
-    int64_t q = 0;
-    int il = 0;
-    if (has) {
-      const int32_t slot = inc_slot[i0 + kk];
-      q = slot >> 2;
-      il = slot & 3;
+    // incidence record {quad, local index, its 4 nodes, 4 int8 block ranks}: one load level
+    int4 r0 = make_int4(-1, 0, 0, 0), r1 = make_int4(0, 0, 0, 0);
+    if (node_ok) {
+      const int4* rp = reinterpret_cast<const int4*>(inc_rec + 8 * (n * inc_pad + kk));
+      r0 = __ldg(rp);
+      r1 = __ldg(rp + 1);
     }
+    const bool has = r0.x >= 0;
+    const int64_t q = has ? r0.x : 0;
+    const int il = r0.y;
+    const int cn[4] = {r0.z, r0.w, r1.x, r1.y};
     double* G = geo + (ns * 4 + k) * GS;
     // ---- phase 1: geometry of (node, element) once ------------------------
     if (has && j == 0) {
       double X[4][3];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const int m = __ldg(conn + 4 * q + c);
+        const int m = cn[c];
         X[c][0] = __ldg(gx + m);
         X[c][1] = __ldg(gy + m);
         X[c][2] = __ldg(gz + m);
@@ -227,7 +236,7 @@ __global__ void __launch_bounds__(128, 4) quad_assemble_fused_kernel(
 #pragma unroll
       for (int b = 0; b < 6; ++b) K[a][b] = 0.0;
     // symmetric storage keeps only blocks (n, m >= n): rank < 0 marks a skipped block
-    const int rank = has ? block_rank[16 * q + 4 * il + j] : -1;
+    const int rank = has ? (int)(int8_t)((r1.z >> (8 * j)) & 255) : -1;
     const bool blk = has && rank >= 0;
     if (blk) {
       const int bi = il, bj = j;
@@ -329,11 +338,11 @@ __global__ void __launch_bounds__(128, 4) quad_assemble_fused_kernel(
       const int kb = rem / 6;
       const int b = rem - 6 * kb;
       const int dst = cm ? PULL_BLOCK * kb + rec_off(a, b) : v;
-      const int m = node_col[b0 + kb];
+      const int cc = ccol[ns][kb];
       double s = nbuf[a * rowlen + rem];
-      const bool diag = (m == n) && (a == b);
+      const bool diag = (cc >> 8) && (a == b);
       const bool rfix = (mrow >> a) & 1;
-      const bool cfix = (fixed_mask[m] >> b) & 1;
+      const bool cfix = (cc >> b) & 1;
       if (rfix || cfix) {
         if (diag) {
           if (s == 0.0) s = 1.0;
@@ -354,17 +363,16 @@ __global__ void __launch_bounds__(128, 4) quad_assemble_fused_kernel(
 
 int fused_max_degree() { return MAXDEG; }
 
-void launch_quad_assemble_fused(cudaStream_t s, int n_own, int max_inc, const int64_t* node_ptr,
-                                const int32_t* node_col, const int64_t* inc_ptr, const int32_t* inc_slot,
-                                const int32_t* block_rank, const double* x, const double* y,
-                                const double* z, const int32_t* conn, const double* t, const double* E,
+void launch_quad_assemble_fused(cudaStream_t s, int n_own, int inc_pad, const int64_t* node_ptr,
+                                const int32_t* node_col, const int32_t* inc_rec, const double* x,
+                                const double* y, const double* z, const double* t, const double* E,
                                 const double* nu, double drill_alpha, const uint8_t* fixed_mask,
                                 double* vals, double* dinv, DevFlags* flags, const BatchStrides& bs,
                                 int cm) {
   if (n_own <= 0) return;
   const dim3 grid((n_own + NPC - 1) / NPC, bs.B);
-  quad_assemble_fused_kernel<<<grid, 128, 0, s>>>(n_own, max_inc, node_ptr, node_col, inc_ptr, inc_slot,
-                                                  block_rank, x, y, z, conn, t, E, nu, drill_alpha,
+  quad_assemble_fused_kernel<<<grid, 128, 0, s>>>(n_own, inc_pad, node_ptr, node_col, inc_rec, x, y, z, t, E,
+                                                  nu, drill_alpha,
                                                   fixed_mask, vals, dinv, flags, bs, cm);
   SSO_POST_LAUNCH("quad_assemble_fused_kernel");
 }

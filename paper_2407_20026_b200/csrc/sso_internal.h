@@ -161,10 +161,9 @@ void launch_assemble(cudaStream_t s, int n_nodes, const int64_t* node_ptr,
 
 // Fused element stiffness + assembly for quad-only meshes (no staging).
 int fused_max_degree();
-void launch_quad_assemble_fused(cudaStream_t s, int n_own, int max_inc, const int64_t* node_ptr,
-                                const int32_t* node_col, const int64_t* inc_ptr, const int32_t* inc_slot,
-                                const int32_t* block_rank, const double* x, const double* y,
-                                const double* z, const int32_t* conn, const double* t, const double* E,
+void launch_quad_assemble_fused(cudaStream_t s, int n_own, int inc_pad, const int64_t* node_ptr,
+                                const int32_t* node_col, const int32_t* inc_rec, const double* x,
+                                const double* y, const double* z, const double* t, const double* E,
                                 const double* nu, double drill_alpha, const uint8_t* fixed_mask,
                                 double* vals, double* dinv, DevFlags* flags,
                                 const BatchStrides& bs = BatchStrides(), int cm = 0);
