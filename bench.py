@@ -226,6 +226,34 @@ WORKLOADS = {"C3b": (408, "C3b: 408x408 MITC-4 shell quads, 1 003 686 DOF (readi
              "C4": (1000, "C4: 1000x1000 MITC-4 shell quads, 6 012 006 DOF, edge y=0 clamped + 2 pinned corners")}
 
 
+SMALL = {"C1": ("config1", "C1: grid-shell, 40 frame elements (25 nodes, 150 DOF), corners pinned"),
+         "C2": ("config2", "C2: 20x20 MITC-4 shallow shell (441 nodes, 2 646 DOF), boundary pinned")}
+
+
+def small_metric(workload):
+    return f"{workload} solve+adjoint grad evals/sec (latency configuration)"
+
+
+def oracle_full_eval(workload):
+    """One complete evaluation by the oracle as it stands (not a sample): DOK assembly, supports,
+    dense Cholesky solve, compliance and the complex-step adjoint gradient.  Returns seconds."""
+    import workloads as W
+    from oracle import grad as OG
+    P = getattr(W, SMALL[workload][0])()
+    t0 = time.perf_counter()
+    u, _, _ = OG.evaluate(P, solver="cholesky")
+    OG.compliance(P["f"], u)
+    OG.adjoint_gradient(P, u)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline_full(workload):
+    dt = oracle_full_eval(workload)
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": 1, "kind": "oracle", "extrapolated": False,
+            "sample": (f"one complete {workload} evaluation by the oracle as it stands (DOK assembly, dense "
+                       f"Cholesky, complex-step adjoint gradient), single process: {dt:.2f} s")}
+
+
 def cpu_baseline_obj(workload, cg_iters, cores=None):
     n = WORKLOADS[workload][0]
     cores = cores or host_cores()
@@ -274,6 +302,22 @@ C5_ITERS = 3400  # median CG iterations of the 64 seeded C5 designs at rtol 1e-1
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
+        return
+    if args.workload in SMALL:
+        times = []
+        for k in range(args.warmup + args.steps):
+            dt = oracle_full_eval(args.workload)
+            if k >= args.warmup:
+                times.append(dt)
+        value = args.steps / sum(times)
+        print(json.dumps({"impl": "reference", "metric": small_metric(args.workload), "value": value, "unit": UNIT,
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
+                          "higher_is_better": True, "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic", "config": {"workload": SMALL[args.workload][1]},
+                          "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                           "extrapolated": False,
+                                           "sample": f"{args.steps} complete {args.workload} evaluations by the oracle"},
+                          "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
     if args.workload == "C5":
         times, vals = [], []
@@ -346,10 +390,14 @@ def run_gpu(args):
 
     # N > 1: the workload split into N node strips over NCCL (strong scaling, the default);
     # --replicas: every GPU evaluates its own seeded design of the workload (weak scaling).
-    replicas = world > 1 and args.replicas
-    n_grid, wname = WORKLOADS[args.workload]
-    cfg, sup = (4, "c4") if args.workload == "C4" else (3, "clamped_edges")
-    P = W.shell_config3(n_grid, cfg=cfg, supports=sup, design=rank if replicas else 0)
+    replicas = world > 1 and (args.replicas or args.workload in SMALL)  # C1, C2: replicas only
+    if args.workload in SMALL:  # latency configs (replicas only across GPUs)
+        wname = SMALL[args.workload][1]
+        P = getattr(W, SMALL[args.workload][0])()
+    else:
+        n_grid, wname = WORKLOADS[args.workload]
+        cfg, sup = (4, "c4") if args.workload == "C4" else (3, "clamped_edges")
+        P = W.shell_config3(n_grid, cfg=cfg, supports=sup, design=rank if replicas else 0)
     t0 = time.perf_counter()
     stream = torch.cuda.current_stream()
     if replicas:
@@ -528,9 +576,11 @@ def run_gpu(args):
 
     out = None
     if rank == 0:
-        cpu = cpu_baseline_obj(args.workload, cg_iters) if (world == 1 and not args.no_cpu) else None
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            cpu = cpu_baseline_full(args.workload) if args.workload in SMALL else cpu_baseline_obj(args.workload, cg_iters)
         strong = (world > 1 and not replicas) or args.virtual_parts > 1 or (world == 1 and not args.replicas)
-        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        out = {"metric": small_metric(args.workload) if args.workload in SMALL else METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
                # the default series (N = 1, 2, 4, 8) splits one workload into N strips: strong
                "scaling": "strong" if strong else "weak",
@@ -543,7 +593,9 @@ def run_gpu(args):
                           "precond": {0: "point Jacobi", 1: "node-block Jacobi"}[args.precond],
                           "storage": {0: "full node-block CSR",
                                       3: "upper blocks (38-double 2x2 sub-block records), one-pass pull SpMV"}[symmetric],
-                          "l2": "working set > L2 (CSR values >= 254 MB vs 126 MB L2); no flush",
+                          "l2": ("working set > L2 (CSR values >= 254 MB vs 126 MB L2); no flush"
+                                 if args.workload not in SMALL else
+                                 "working set < L2 (a latency configuration; no flush)"),
                           "pattern_build_s": t_create},
                "roofline": roofline,
                "cpu_baseline": cpu,
@@ -721,7 +773,7 @@ def main():
                     help="sso_options.precond for single-GPU C3b: 0 point Jacobi (north star), 1 node-block")
     ap.add_argument("--storage", type=int, default=0,
                     help="sso_options.storage for single-GPU C3b (0 = library default)")
-    ap.add_argument("--workload", default="C3b", choices=["C3b", "C4", "C5"])
+    ap.add_argument("--workload", default="C3b", choices=["C1", "C2", "C3b", "C4", "C5"])
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: one seeded design per GPU (independent, no collective) instead of N strips")
     ap.add_argument("--batch", type=int, default=64, help="C5 designs per GPU")
@@ -732,7 +784,8 @@ def main():
         if args.cg_iters is None:
             p = os.path.join(ROOT, "profiles", "cg_iters_c3b.json")
             d = json.load(open(p)) if os.path.exists(p) else {}
-            args.cg_iters = d.get("cg_iters_" + args.workload, d.get("cg_iters", 10000)) if args.workload != "C5" else 0
+            args.cg_iters = (d.get("cg_iters_" + args.workload, d.get("cg_iters", 10000))
+                             if args.workload in WORKLOADS else 0)
         run_reference(args)
     elif args.workload == "C5":
         run_batch(args)
