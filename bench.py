@@ -453,13 +453,14 @@ def run_gpu(args):
     m.profile_reset()
     l0 = m.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    iters = []
+    iters, solve_ms = [], []
     with ClockSampler(dev.index) as clk:
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
             info = step()
             iters.append(info["iters"])
+            solve_ms.append(info["ms"])
         ev1.record(stream)
         barrier()
     launches = m.launch_count() - l0
@@ -525,6 +526,15 @@ def run_gpu(args):
                 "share_of_step": (spmv_avg_ms * (cg_iters + 1) * args.steps / ms_total) if spmv_n else None,
                 "sampling": ("CUDA event pairs around every 16th SpMV launch of the CG loop (graph event nodes)"
                              + ("; one launch covers every strip" if args.virtual_parts > 1 else ""))}
+    if args.workload in SMALL:
+        # latency configuration: the CG loop runs in the persistent cluster kernel (cg_small.cu),
+        # no per-iteration SpMV launch to sample; the figure that bounds it is the time per
+        # iteration (3 cluster barriers + the row products), not bandwidth
+        us_it = 1000.0 * float(np.median(solve_ms)) / max(cg_iters, 1)
+        roofline = {"bound": "latency", "kernel": "cg_cluster_kernel (persistent cluster PCG, csrc/cg_small.cu)",
+                    "achieved": us_it, "unit": "us/iteration", "peak": None, "frac": None, "traffic": None,
+                    "note": "solve time (incl. init, true-residual check, Lanczos) / CG iterations, median of the "
+                            "timed steps"}
     asm_ms = (el_ms + as_ms) / max(args.steps, 1)
     grad_ms = gr_ms / max(args.steps, 1)
     clocks = clk.summary()

@@ -8,7 +8,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsso.so")
 SOURCES = ["api.cu", "elements.cu", "assemble.cu", "assemble_fused.cu", "pcg.cu", "grad.cu",
-           "filter.cu", "loads.cu", "block_jacobi.cu", "lanczos.cu", "cg_sr.cu", "pattern.cpp"]
+           "filter.cu", "loads.cu", "block_jacobi.cu", "lanczos.cu", "cg_sr.cu", "cg_small.cu", "pattern.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -143,6 +143,8 @@ struct Part {
   bool cgf = false;                   // fused x / r / p update (cg_update_fused / _block_fused): one
                                       // part, full or pull storage, B <= the co-resident grid
   double* p2 = nullptr;               // cgf: the second p buffer (ping-pong)
+  bool small = false;                 // cgf + small model: chunks of iterations in one persistent
+                                      // kernel (cg_small.cu)
   // partitioned handles: single-reduction CG (cg_sr.cu) vectors u = M^-1 r and s = K p
   double *u_sr = nullptr, *s_sr = nullptr;
   // interior / boundary split of the owned rows: rows [bnd_lo, bnd_hi) need no halo value
@@ -666,9 +668,14 @@ int build_chunk_graph(sso_ctx* h, int prof_slot, cudaGraphExec_t* out) {
   long long g0 = g_launches, l0 = h->launches;
   CK(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
   int rc = SSO_OK;
-  for (int i = 0; i < K && rc == SSO_OK; ++i) {
-    const bool rec = prof_slot >= 0 && (i % PROF_EVERY) == 0;
-    rc = cg_iteration(h, h->cap_stream, rec ? &h->chunk_ev[prof_slot][2 * i] : nullptr, i);
+  if (!h->distributed() && h->P0().small) {  // the whole chunk in one persistent kernel
+    Part& P = h->P0();
+    launch_cg_small(h->cap_stream, P.n_own, K, P.pdesc, P.vals, P.dinv, P.xs, P.r, P.p, P.p2, P.st, P.bs);
+  } else {
+    for (int i = 0; i < K && rc == SSO_OK; ++i) {
+      const bool rec = prof_slot >= 0 && (i % PROF_EVERY) == 0;
+      rc = cg_iteration(h, h->cap_stream, rec ? &h->chunk_ev[prof_slot][2 * i] : nullptr, i);
+    }
   }
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
@@ -994,6 +1001,11 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   if (P.cgf) {
     AL(p2, B * P.ndof);
     CK(h, cudaMemset(P.p2, 0, B * P.ndof * sizeof(double)));
+    const char* env = getenv("SSO_SMALL");
+    P.small = h->precond == 0 && P.pull && P.n_own == P.n_nodes && cg_small_fits(P.n_own) &&
+              !(env && env[0] == '0');
+    for (int32_t n = 0; P.small && n < P.n_nodes; ++n)  // every node within the pull descriptor
+      P.small = P.up.uptr[n + 1] - P.up.uptr[n] <= 5 && P.up.lptr[n + 1] - P.up.lptr[n] <= 4;
   }
   AL(q, B * P.ndof);
   AL(tmp, B * P.ndof);
@@ -1609,7 +1621,8 @@ static int solve_chunks(sso_ctx* h) {
         long long ran = it_max - iters_before;
         if (not_spd && ran < h->check_every) ran += 1;
         iters_before = it_max;
-        for (long long i = 0; i < std::min<long long>(ran, h->check_every); i += PROF_EVERY) {
+        // (the persistent small-model kernel has no per-iteration SpMV to sample)
+        for (long long i = 0; !P.small && i < std::min<long long>(ran, h->check_every); i += PROF_EVERY) {
           float ms = 0.f;
           CK(h, cudaEventElapsedTime(&ms, h->chunk_ev[slot][2 * i], h->chunk_ev[slot][2 * i + 1]));
           h->tm.total_ms[F_SPMV] += ms;

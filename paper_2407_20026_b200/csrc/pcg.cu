@@ -1183,16 +1183,6 @@ static const SpmvVariant kSpmvVariants[] = {
     SPMV_VARIANT(4, 10, 2), SPMV_VARIANT(3, 10, 3), SPMV_VARIANT(2, 9, 4), SPMV_VARIANT(3, 9, 3),
     SPMV_VARIANT(2, 10, 4)};
 
-// true the first time it is called for the current device with this mask (kernel attributes
-// are per device: a process may hold handles on several GPUs)
-static bool first_on_device(uint64_t& mask) {
-  int d = 0;
-  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) d = 0;
-  const uint64_t bit = 1ull << d;
-  if (mask & bit) return false;
-  mask |= bit;
-  return true;
-}
 
 static const SpmvVariant& spmv_variant() {
   static int v = -1;

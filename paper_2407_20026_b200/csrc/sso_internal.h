@@ -203,6 +203,25 @@ void launch_cg_update_block_fused(cudaStream_t s, int n_nodes, const double* bin
 void launch_cg_pfix_z(cudaStream_t s, int ndof, const double* z, const double* pin, double* pout,
                       const CgState* st, const BatchStrides& bs);
 int cg_block_fused_grid();
+// Cluster-resident PCG for small models (cg_small.cu): `iters` iterations of the fused
+// point-Jacobi recurrence, one thread-block cluster (<= 16 CTAs) per design, over the
+// storage-3 records; p_prev gets the previous p (the fused path's ping-pong convention).
+// cg_small_fits: the model fits one cluster (<= 1 152 nodes; the caller also requires every
+// node to fit the pull descriptor: <= 5 upper and <= 4 pulled blocks).
+bool cg_small_fits(int n_nodes);
+void launch_cg_small(cudaStream_t s, int n_nodes, int iters, const int32_t* pdesc, const double* vals,
+                     const double* dinv, double* x, double* r, double* p, double* p_prev, CgState* st,
+                     const BatchStrides& bs);
+// true the first time it is called for the current device with this mask (kernel attributes
+// are per device: a process may hold handles on several GPUs)
+inline bool first_on_device(uint64_t& mask) {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) d = 0;
+  const uint64_t bit = 1ull << d;
+  if (mask & bit) return false;
+  mask |= bit;
+  return true;
+}
 // Symmetric pull SpMV (storage 3): upper node blocks stored column-major per run;
 // the row-owner warp streams its upper run and the upper blocks (n, m) of its lower
 // neighbours (pull list lpull = [(n, upper block index)] per node, via lptr) and
