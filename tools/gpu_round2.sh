@@ -7,7 +7,9 @@ nvcc -O3 -gencode arch=compute_100a,code=sm_100a tools/dfma_peak.cu -o /tmp/dfma
 timeout 900 python -m pytest tests -m gpu -q -s -rf > $O/gpu_tests.log 2>&1; echo "tests rc=$?"; tail -2 $O/gpu_tests.log
 timeout 600 python bench.py > $O/bench_c3b.json 2> $O/bench_c3b.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err; echo "ref rc=$?"
-timeout 600 python bench.py --workload C5 --steps 3 --warmup 3 --no-cpu > $O/bench_c5.json 2> $O/bench_c5.err; echo "c5 rc=$?"
+timeout 600 python bench.py --workload C5 --steps 3 --warmup 3 > $O/bench_c5.json 2> $O/bench_c5.err; echo "c5 rc=$?"
+timeout 300 python bench.py --workload C1 --steps 1000 --warmup 5 > $O/bench_c1.json 2> $O/bench_c1.err; echo "c1 rc=$?"
+timeout 300 python bench.py --workload C2 --steps 300 --warmup 5 > $O/bench_c2.json 2> $O/bench_c2.err; echo "c2 rc=$?"
 timeout 900 python bench.py --workload C4 --steps 1 --warmup 3 --no-cpu > $O/bench_c4.json 2> $O/bench_c4.err; echo "c4 rc=$?"
 timeout 900 python bench.py --workload C4 --steps 1 --warmup 3 --no-cpu --virtual-parts 8 > $O/bench_c4_vp8.json 2> $O/bench_c4_vp8.err; echo "c4 vp8 rc=$?"
 timeout 300 compute-sanitizer --tool memcheck --leak-check full python tools/sanitize_target.py > $O/san_memcheck.log 2>&1; echo "memcheck rc=$?"
