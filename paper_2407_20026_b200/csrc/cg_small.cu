@@ -296,7 +296,37 @@ size_t cl_smem(int npt) { return (size_t)6 * npt * (sizeof(double) * (1 + CL_VAL
 
 }  // namespace
 
-bool cg_small_fits(int n_nodes) { return n_nodes > 0 && cl_npt(n_nodes) <= CL_MAX_NPT; }
+static void cl_attributes() {
+  static uint64_t attr_mask = 0;
+  if (first_on_device(attr_mask)) {
+    cudaFuncSetAttribute(cg_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(cg_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem(CL_MAX_NPT));
+  }
+}
+
+bool cg_small_fits(int n_nodes) {
+  if (n_nodes <= 0 || cl_npt(n_nodes) > CL_MAX_NPT) return false;
+  // the device must be able to place the cluster (its CTAs on SMs of one GPC)
+  cl_attributes();
+  const int npt = cl_npt(n_nodes), cs = (n_nodes + npt - 1) / npt;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(CL_THREADS);
+  cfg.dynamicSmemBytes = cl_smem(npt);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, cg_cluster_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return nclusters >= 1;
+}
 
 void launch_cg_small(cudaStream_t s, int n_nodes, int iters, const int32_t* pdesc, const double* vals,
                      const double* dinv, double* x, double* r, double* p, double* p_prev, CgState* st,
@@ -304,11 +334,7 @@ void launch_cg_small(cudaStream_t s, int n_nodes, int iters, const int32_t* pdes
   const int npt = cl_npt(n_nodes);
   const int cs = (n_nodes + npt - 1) / npt;
   const size_t smem = cl_smem(npt);
-  static uint64_t attr_mask = 0;
-  if (first_on_device(attr_mask)) {
-    cudaFuncSetAttribute(cg_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(cg_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cl_smem(CL_MAX_NPT));
-  }
+  cl_attributes();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs * bs.B);
   cfg.blockDim = dim3(CL_THREADS);
