@@ -148,8 +148,10 @@ __global__ void __launch_bounds__(CL_THREADS) cg_cluster_kernel(
   if (st->done) return;  // the same for every CTA of the cluster
   const int rows = 6 * npt;              // row capacity of a CTA
   double* p_s = dsm;                     // this CTA's p rows [rows]
-  double* red = dsm + rows;              // [0] p^T q, [2], [3] r^T z, r^T r partials of this CTA
-  double* kv = red + 4;                  // [54][rows] staged values
+  // [c][0] p^T q, [c][2], [c][3] r^T z, r^T r partials of cluster CTA c: every CTA pushes its
+  // partials into every CTA's table (remote stores, no load latency), then sums its own table
+  double* red = dsm + rows;
+  double* kv = red + 4 * CL_MAX_CS;      // [54][rows] staged values
   const double2** km = reinterpret_cast<const double2**>(kv + CL_VALS * rows);  // [9][rows] p_m rows
   const bool writer = cr == 0 && threadIdx.x == 0;
   const int node0 = cr * npt;
@@ -195,10 +197,10 @@ __global__ void __launch_bounds__(CL_THREADS) cg_cluster_kernel(
       }
     }
     cl_block_sum2(a0, a1, sm);
-    if (threadIdx.x == 0) red[0] = a0;
+    if (threadIdx.x < CS) cl.map_shared_rank(red, (int)threadIdx.x)[4 * cr] = a0;
     csync(cl, CS);
     double pqv = 0.0;
-    for (int c = 0; c < CS; ++c) pqv += c == cr ? red[0] : *cl.map_shared_rank(red, c);  // rank order
+    for (int c = 0; c < CS; ++c) pqv += red[4 * c];  // rank order: the same total in every CTA
     if (!(pqv > 0.0)) {
       if (writer) {
         st->pq = pqv;
@@ -223,14 +225,12 @@ __global__ void __launch_bounds__(CL_THREADS) cg_cluster_kernel(
       }
     }
     cl_block_sum2(b0, b1, sm);
-    if (threadIdx.x == 0) {
-      red[2] = b0;
-      red[3] = b1;
-    }
+    if (threadIdx.x < CS)
+      *reinterpret_cast<double2*>(cl.map_shared_rank(red, (int)threadIdx.x) + 4 * cr + 2) = make_double2(b0, b1);
     csync(cl, CS);
     double rz_new = 0.0, rr = 0.0;
     for (int c = 0; c < CS; ++c) {  // rank order: the same totals in every CTA
-      const double2 w = *reinterpret_cast<const double2*>((c == cr ? red : cl.map_shared_rank(red, c)) + 2);
+      const double2 w = *reinterpret_cast<const double2*>(red + 4 * c + 2);
       rz_new += w.x;
       rr += w.y;
     }
@@ -292,7 +292,9 @@ int cl_npt(int n_nodes) {  // nodes per CTA: one CTA when the model fits it, els
   return std::max(16, (n_nodes + CL_MAX_CS - 1) / CL_MAX_CS);
 }
 
-size_t cl_smem(int npt) { return (size_t)6 * npt * (sizeof(double) * (1 + CL_VALS) + sizeof(void*) * 9) + 32; }
+size_t cl_smem(int npt) {
+  return (size_t)6 * npt * (sizeof(double) * (1 + CL_VALS) + sizeof(void*) * 9) + sizeof(double) * 4 * CL_MAX_CS;
+}
 
 }  // namespace
 
