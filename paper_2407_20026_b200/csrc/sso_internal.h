@@ -203,14 +203,15 @@ void launch_cg_update_block_fused(cudaStream_t s, int n_nodes, const double* bin
 void launch_cg_pfix_z(cudaStream_t s, int ndof, const double* z, const double* pin, double* pout,
                       const CgState* st, const BatchStrides& bs);
 int cg_block_fused_grid();
-// Cluster-resident PCG for small models (cg_small.cu): `iters` iterations of the fused
-// point-Jacobi recurrence, one thread-block cluster (<= 16 CTAs) per design, over the
-// storage-3 records; p_prev gets the previous p (the fused path's ping-pong convention).
+// Cluster-resident PCG for small models (cg_small.cu): `iters` iterations of the
+// single-reduction point-Jacobi recurrence, one thread-block cluster (<= 16 CTAs) per design,
+// over the storage-3 records; s_vec (the fused path's second p buffer) keeps s = K p between
+// chunks.
 // cg_small_fits: the model fits one cluster (<= 1 152 nodes; the caller also requires every
 // node to fit the pull descriptor: <= 5 upper and <= 4 pulled blocks).
 bool cg_small_fits(int n_nodes);
 void launch_cg_small(cudaStream_t s, int n_nodes, int iters, const int32_t* pdesc, const double* vals,
-                     const double* dinv, double* x, double* r, double* p, double* p_prev, CgState* st,
+                     const double* dinv, double* x, double* r, double* p, double* s_vec, CgState* st,
                      const BatchStrides& bs);
 // true the first time it is called for the current device with this mask (kernel attributes
 // are per device: a process may hold handles on several GPUs)
