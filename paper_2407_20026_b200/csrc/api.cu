@@ -670,7 +670,10 @@ int build_chunk_graph(sso_ctx* h, int prof_slot, cudaGraphExec_t* out) {
   int rc = SSO_OK;
   if (!h->distributed() && h->P0().small) {  // the whole chunk in one persistent kernel
     Part& P = h->P0();
-    launch_cg_small(h->cap_stream, P.n_own, K, P.pdesc, P.vals, P.dinv, P.xs, P.r, P.p, P.p2, P.st, P.bs);
+    // 4 chunks' worth of iterations per launch (the kernel stops at convergence) unless periodic
+    // residual replacements need the chunk boundaries: fewer launches and state polls
+    const int iters = h->reliable >= 2 ? K : 4 * K;
+    launch_cg_small(h->cap_stream, P.n_own, iters, P.pdesc, P.vals, P.dinv, P.xs, P.r, P.p, P.p2, P.st, P.bs);
   } else {
     for (int i = 0; i < K && rc == SSO_OK; ++i) {
       const bool rec = prof_slot >= 0 && (i % PROF_EVERY) == 0;
