@@ -61,3 +61,15 @@ def test_gpu_arm_line():
     assert d["clocks"]["samples"] >= 1
     cert = d["extra"]["certification"]
     assert cert["true_rel_res"] < 1e-9 and cert["lanczos_lmin"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workload", ["C1", "C2"])
+def test_gpu_latency_lines(workload):
+    lines = _run(["--workload", workload, "--steps", "20", "--warmup", "3"], timeout=600)
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert BASE_KEYS <= set(d) and d["metric"].startswith(workload) and d["value"] > 0
+    assert d["roofline"]["bound"] == "latency" and d["roofline"]["achieved"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["extrapolated"] is False
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
