@@ -248,26 +248,43 @@ __global__ void __launch_bounds__(128) quad_element_kernel(
   }
 }
 
-// Local 12x12 frame stiffness entry (reading C1), local DOF (u, v, w, th_x, th_y, th_z).
-__device__ __forceinline__ double beam_kloc(int r, int c, double EA, double GJ, double EIy,
-                                            double EIz, double L) {
+// The distinct entries of the local 12x12 frame stiffness (reading C1), each formed once per
+// element with the expressions (and so the rounding) of the entry table below.
+struct BeamK {
+  double ea, gj, z12, y12, z4, z2, y4, y2, z6, y6;
+  __device__ BeamK(double EA, double GJ, double EIy, double EIz, double L) {
+    const double L2 = L * L, L3 = L2 * L;
+    ea = EA / L;
+    gj = GJ / L;
+    z12 = 12.0 * EIz / L3;
+    y12 = 12.0 * EIy / L3;
+    z4 = 4.0 * EIz / L;
+    z2 = 2.0 * EIz / L;
+    y4 = 4.0 * EIy / L;
+    y2 = 2.0 * EIy / L;
+    z6 = 6.0 * EIz / L2;
+    y6 = 6.0 * EIy / L2;
+  }
+};
+
+// Local 12x12 frame stiffness entry, local DOF (u, v, w, th_x, th_y, th_z).
+__device__ __forceinline__ double beam_kloc(int r, int c, const BeamK& k) {
   if (r > c) { int tmp = r; r = c; c = tmp; }
-  const double L2 = L * L, L3 = L2 * L;
   const int ra = r % 6, ca = c % 6;
   const bool same = (r / 6) == (c / 6);
   switch (ra * 6 + ca) {
-    case 0 * 6 + 0: return same ? EA / L : -EA / L;
-    case 3 * 6 + 3: return same ? GJ / L : -GJ / L;
-    case 1 * 6 + 1: return same ? 12.0 * EIz / L3 : -12.0 * EIz / L3;
-    case 2 * 6 + 2: return same ? 12.0 * EIy / L3 : -12.0 * EIy / L3;
-    case 5 * 6 + 5: return same ? 4.0 * EIz / L : 2.0 * EIz / L;
-    case 4 * 6 + 4: return same ? 4.0 * EIy / L : 2.0 * EIy / L;
+    case 0 * 6 + 0: return same ? k.ea : -k.ea;
+    case 3 * 6 + 3: return same ? k.gj : -k.gj;
+    case 1 * 6 + 1: return same ? k.z12 : -k.z12;
+    case 2 * 6 + 2: return same ? k.y12 : -k.y12;
+    case 5 * 6 + 5: return same ? k.z4 : k.z2;
+    case 4 * 6 + 4: return same ? k.y4 : k.y2;
     // v - th_z couplings: k(1,5) = k(1,11) = 6EIz/L^2 ; k(5,7) = k(7,11) = -6EIz/L^2
-    case 1 * 6 + 5: return (r == 1) ? 6.0 * EIz / L2 : -6.0 * EIz / L2;   // (1,5),(1,11) | (7,11)
-    case 5 * 6 + 1: return -6.0 * EIz / L2;                               // (5,7)
+    case 1 * 6 + 5: return (r == 1) ? k.z6 : -k.z6;   // (1,5),(1,11) | (7,11)
+    case 5 * 6 + 1: return -k.z6;                     // (5,7)
     // w - th_y couplings: k(2,4) = k(2,10) = -6EIy/L^2 ; k(4,8) = k(8,10) = +6EIy/L^2
-    case 2 * 6 + 4: return (r == 2) ? -6.0 * EIy / L2 : 6.0 * EIy / L2;   // (2,4),(2,10) | (8,10)
-    case 4 * 6 + 2: return 6.0 * EIy / L2;                                // (4,8)
+    case 2 * 6 + 4: return (r == 2) ? -k.y6 : k.y6;   // (2,4),(2,10) | (8,10)
+    case 4 * 6 + 2: return k.y6;                      // (4,8)
     default: return 0.0;
   }
 }
@@ -321,10 +338,11 @@ __global__ void __launch_bounds__(128) beam_element_kernel(
       const double E = __ldg(gE + e);
       const double EA = E * __ldg(gA + e), GJ = __ldg(gG + e) * __ldg(gJ + e);
       const double EIy = E * __ldg(gIy + e), EIz = E * __ldg(gIz + e);
+      const BeamK kk(EA, GJ, EIy, EIz, L);
 #pragma unroll
       for (int a2 = 0; a2 < 6; ++a2)
 #pragma unroll
-        for (int b2 = 0; b2 < 6; ++b2) K[a2][b2] = beam_kloc(6 * bi + a2, 6 * bj + b2, EA, GJ, EIy, EIz, L);
+        for (int b2 = 0; b2 < 6; ++b2) K[a2][b2] = beam_kloc(6 * bi + a2, 6 * bj + b2, kk);
       const double R[3][3] = {{ex[0], ex[1], ex[2]}, {ey[0], ey[1], ey[2]}, {ez[0], ez[1], ez[2]}};
       transform_block(K, R, 0.0, 0.0);
     }
