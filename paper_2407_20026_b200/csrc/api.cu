@@ -1704,8 +1704,10 @@ int sso_solve(sso_handle h, const double* f, double* u, sso_solve_info* info) {
       h->h_st[bd].lz_cap = pp->lz_cap;
     }
     CK(h, cudaMemcpyAsync(pp->st, h->h_st, pp->B * sizeof(CgState), cudaMemcpyHostToDevice, h->stream));
-    // the pinned staging struct is reused: make the upload complete first
-    if ((rc = sync(h))) return rc;
+    // the pinned staging struct is reused by the next part: make the upload complete first (the
+    // last part's upload is ordered before the solve's own host reads of the state, and the
+    // next solve rewrites the struct only after this one has synchronised)
+    if (pp != h->parts.back() && (rc = sync(h))) return rc;
   }
   const bool lift = h->prescribed && !h->skip_load;
   if (lift) {  // K_ff u_f = f_f - K_fc b (reading c18)
