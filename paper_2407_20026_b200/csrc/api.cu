@@ -1580,6 +1580,25 @@ static int solve_chunks(sso_ctx* h) {
   Part& P = h->P0();
   int rc;
   const bool prof = h->tm.on;
+  if (!h->distributed() && P.small && h->reliable < 2) {
+    // small models: the cluster kernel runs to convergence (or max_iter) in ONE launch and the
+    // final true-residual check follows in stream order -- one host synchronisation per pass
+    // instead of chunk polling
+    for (int pass = 0; pass <= MAX_RESTARTS; ++pass) {
+      long long g0 = g_launches;
+      launch_cg_small(h->stream, P.n_own, (int)std::min<long long>(h->max_iter, INT_MAX), P.pdesc, P.vals, P.dinv,
+                      P.xs, P.r, P.p, P.p2, P.st, P.bs);
+      h->launches += g_launches - g0;
+      if (h->reliable == 0) break;
+      if ((rc = replace_step(h, REPL_FINAL))) return rc;
+      CK(h, cudaMemcpyAsync(h->h_chunk, P.st, P.B * sizeof(CgState), cudaMemcpyDeviceToHost, h->stream));
+      if ((rc = sync(h))) return rc;
+      bool restarted = false;
+      for (int bd = 0; bd < P.B; ++bd) restarted |= h->h_chunk[bd].done == 0;
+      if (!restarted) break;
+    }
+    return SSO_OK;
+  }
   if (!prof && !h->chunk_exec) {
     if ((rc = build_chunk_graph(h, -1, &h->chunk_exec))) return rc;
   }
