@@ -486,45 +486,51 @@ int allreduce(sso_ctx* h, int nvals, cudaStream_t s = nullptr) {
 }
 
 int check_flags(sso_ctx* h) {
-  for (auto& pp : h->parts)
-   for (int bd = 0; bd < pp->B; ++bd) {
+  for (auto& pp : h->parts) {
     Part& P = *pp;
-    CK(h, cudaMemcpyAsync(h->h_flags, P.flags + bd, sizeof(DevFlags), cudaMemcpyDeviceToHost, h->stream));
+    // every design's flags in one copy and one synchronisation
+    CK(h, cudaMemcpyAsync(h->h_flags, P.flags, P.B * sizeof(DevFlags), cudaMemcpyDeviceToHost, h->stream));
     int rc = sync(h);
     if (rc) return rc;
-    const std::string dsg = P.B > 1 ? " in design " + std::to_string(bd) : std::string();
-    if (h->h_flags->degenerate_elem != INT_MAX) {
-      const int e = h->h_flags->degenerate_elem;
-      const bool beam = e < P.n_beams;
-      const int g = beam ? P.lm.beam_gid[e] : P.lm.quad_gid[e - P.n_beams];
-      char buf[256];
-      snprintf(buf, sizeof buf, "degenerate element %d (%s %d): zero length / zero normal / det J <= 0",
-               beam ? g : h->g_beams + g, beam ? "beam" : "quad", g);
-      h->err = buf + dsg;
-      return SSO_E_DEGENERATE;
-    }
-    if (h->h_flags->singular_dof != INT_MAX) {
-      const int d = h->h_flags->singular_dof;
-      const int gnode = P.lm.node_gid[d / 6];
-      char buf[256];
-      snprintf(buf, sizeof buf, "singular: free DOF %d (node %d, component %d) has diagonal <= 0",
-               6 * gnode + d % 6, gnode, d % 6);
-      h->err = buf + dsg;
-      return SSO_E_SINGULAR;
+    for (int bd = 0; bd < P.B; ++bd) {
+      const DevFlags& F = h->h_flags[bd];
+      const std::string dsg = P.B > 1 ? " in design " + std::to_string(bd) : std::string();
+      if (F.degenerate_elem != INT_MAX) {
+        const int e = F.degenerate_elem;
+        const bool beam = e < P.n_beams;
+        const int g = beam ? P.lm.beam_gid[e] : P.lm.quad_gid[e - P.n_beams];
+        char buf[256];
+        snprintf(buf, sizeof buf, "degenerate element %d (%s %d): zero length / zero normal / det J <= 0",
+                 beam ? g : h->g_beams + g, beam ? "beam" : "quad", g);
+        h->err = buf + dsg;
+        return SSO_E_DEGENERATE;
+      }
+      if (F.singular_dof != INT_MAX) {
+        const int d = F.singular_dof;
+        const int gnode = P.lm.node_gid[d / 6];
+        char buf[256];
+        snprintf(buf, sizeof buf, "singular: free DOF %d (node %d, component %d) has diagonal <= 0",
+                 6 * gnode + d % 6, gnode, d % 6);
+        h->err = buf + dsg;
+        return SSO_E_SINGULAR;
+      }
     }
   }
   return SSO_OK;
 }
 
+__global__ void reset_flags_kernel(DevFlags* flags, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flags[i] = DevFlags{INT_MAX, INT_MAX};
+}
+
+// the device error flags back to "none", stream-ordered (no host round trip)
 int reset_flags(sso_ctx* h) {
-  h->h_flags->degenerate_elem = INT_MAX;
-  h->h_flags->singular_dof = INT_MAX;
   for (auto& pp : h->parts) {
-    for (int bd = 0; bd < pp->B; ++bd)
-      CK(h, cudaMemcpyAsync(pp->flags + bd, h->h_flags, sizeof(DevFlags), cudaMemcpyHostToDevice, h->stream));
-    CK(h, cudaStreamSynchronize(h->stream));  // h_flags is reused for every design
+    reset_flags_kernel<<<(pp->B + 127) / 128, 128, 0, h->stream>>>(pp->flags, pp->B);
+    SSO_POST_LAUNCH("reset_flags_kernel");
   }
-  return sync(h);
+  return SSO_OK;
 }
 
 // Capture K = check_every CG iterations of the single-part solver into a graph.
@@ -1430,7 +1436,7 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
       cudaMallocHost(&h->h_chunk, 2 * h->batch * sizeof(CgState)) != cudaSuccess ||
       cudaMallocHost(&h->h_scal, 8 * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&h->h_C, sizeof(double)) != cudaSuccess ||
-      cudaMallocHost(&h->h_flags, sizeof(DevFlags)) != cudaSuccess) { h->err = "cudaMallocHost failed"; return bail(SSO_E_OOM); }
+      cudaMallocHost(&h->h_flags, h->batch * sizeof(DevFlags)) != cudaSuccess) { h->err = "cudaMallocHost failed"; return bail(SSO_E_OOM); }
   cudaEventCreate(&h->ev_a);
   cudaEventCreate(&h->ev_b);
   cudaEventCreateWithFlags(&h->ev_done[0], cudaEventDisableTiming);
