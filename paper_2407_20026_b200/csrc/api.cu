@@ -228,6 +228,8 @@ struct sso_ctx {
   CgState* h_chunk = nullptr;  // [2]
   DevFlags* h_flags = nullptr;
   double* h_scal = nullptr;
+  unsigned long long* h_mscale = nullptr;  // [parts][batch] pinned: the assembly's m_min bits
+  bool mscale_pending = false;             // h_mscale written by the stream, not yet read
 
   bool assembled = false, solved = false;
   cudaGraphExec_t chunk_exec = nullptr;
@@ -753,6 +755,7 @@ void free_all(sso_ctx* h) {
   if (h->h_chunk) cudaFreeHost(h->h_chunk);
   if (h->h_scal) cudaFreeHost(h->h_scal);
   if (h->h_flags) cudaFreeHost(h->h_flags);
+  if (h->h_mscale) cudaFreeHost(h->h_mscale);
   if (h->chunk_exec) cudaGraphExecDestroy(h->chunk_exec);
   for (int k = 0; k < 2; ++k) {
     if (h->prof_exec[k]) cudaGraphExecDestroy(h->prof_exec[k]);
@@ -1129,12 +1132,12 @@ int design_in(sso_ctx* h, const double* src, int64_t n_global, double* Part::*ds
 
 // Per-design scale of the preconditioner for the 2-norm error estimate (lanczos.cu
 // mscale_kernel): min over parts / ranks, kept on the host after every assembly.
+// The kernels and the copy into the pinned h_mscale are stream-ordered; the host reads the
+// values when a solve's certification needs them (mscale_read, after that solve's synchronisation).
 int mscale_update(sso_ctx* h) {
   const int B = h->batch;
-  std::vector<double> m((size_t)B, 0.0);
-  bool first = true;
-  for (auto& pp : h->parts) {
-    Part& P = *pp;
+  for (size_t ip = 0; ip < h->parts.size(); ++ip) {
+    Part& P = *h->parts[ip];
     CK(h, cudaMemsetAsync(P.mscale_d, 0xff, B * sizeof(unsigned long long), h->stream));
     {
       long long g0 = g_launches;
@@ -1143,21 +1146,29 @@ int mscale_update(sso_ctx* h) {
     }
     if (h->nranks > 1)  // positive doubles order like their bit patterns: min of the bits
       CKN(h, nccl().AllReduce(P.mscale_d, P.mscale_d, B, ncclUint64, ncclMin, h->comm, h->stream));
-    std::vector<unsigned long long> bits((size_t)B);
-    CK(h, cudaMemcpyAsync(bits.data(), P.mscale_d, B * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                          h->stream));
-    int rc = sync(h);
-    if (rc) return rc;
-    for (int bd = 0; bd < B; ++bd) {
-      double v;
-      std::memcpy(&v, &bits[bd], sizeof v);
-      if (bits[bd] == ~0ull) v = 0.0;
-      m[bd] = first ? v : std::min(m[bd], v);
-    }
-    first = false;
+    CK(h, cudaMemcpyAsync(h->h_mscale + ip * B, P.mscale_d, B * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, h->stream));
   }
-  for (auto& pp : h->parts) pp->mscale_h = m;
+  h->mscale_pending = true;
   return SSO_OK;
+}
+
+// m_min per design (min over the parts) from h_mscale; call after a stream synchronisation
+// that follows mscale_update's copy
+void mscale_read(sso_ctx* h) {
+  if (!h->mscale_pending) return;
+  const int B = h->batch;
+  std::vector<double> m((size_t)B, 0.0);
+  for (size_t ip = 0; ip < h->parts.size(); ++ip)
+    for (int bd = 0; bd < B; ++bd) {
+      const unsigned long long b = h->h_mscale[ip * B + bd];
+      double v;
+      std::memcpy(&v, &b, sizeof v);
+      if (b == ~0ull) v = 0.0;
+      m[bd] = ip == 0 ? v : std::min(m[bd], v);
+    }
+  for (auto& pp : h->parts) pp->mscale_h = m;
+  h->mscale_pending = false;
 }
 
 // Error estimates of a finished solve (include/sso.h sso_solve_info): with lambda_min the
@@ -1171,6 +1182,7 @@ void fill_cert(sso_ctx* h, int bd, const CgState& S, sso_solve_info& info) {
   info.lanczos_lmax = S.lz_max;
   info.lanczos_iters = S.lz_n;
   const double lmin = S.lz_min, rz = S.red[1], fx = S.red[2], xx = S.red[3];
+  mscale_read(h);
   const double mmin = h->P0().mscale_h[bd];
   info.err_energy_est = (lmin > 0.0 && fx > 0.0 && rz >= 0.0) ? std::sqrt(rz / (lmin * fx)) : nanv;
   info.err2_est = (lmin > 0.0 && mmin > 0.0 && xx > 0.0 && rz >= 0.0)
@@ -1436,7 +1448,11 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
       cudaMallocHost(&h->h_chunk, 2 * h->batch * sizeof(CgState)) != cudaSuccess ||
       cudaMallocHost(&h->h_scal, 8 * sizeof(double)) != cudaSuccess ||
       cudaMallocHost(&h->h_C, sizeof(double)) != cudaSuccess ||
-      cudaMallocHost(&h->h_flags, h->batch * sizeof(DevFlags)) != cudaSuccess) { h->err = "cudaMallocHost failed"; return bail(SSO_E_OOM); }
+      cudaMallocHost(&h->h_flags, h->batch * sizeof(DevFlags)) != cudaSuccess ||
+      cudaMallocHost(&h->h_mscale, h->parts.size() * h->batch * sizeof(unsigned long long)) != cudaSuccess) {
+    h->err = "cudaMallocHost failed";
+    return bail(SSO_E_OOM);
+  }
   cudaEventCreate(&h->ev_a);
   cudaEventCreate(&h->ev_b);
   cudaEventCreateWithFlags(&h->ev_done[0], cudaEventDisableTiming);
@@ -1537,9 +1553,11 @@ int sso_assemble(sso_handle h) {
     }
     CKL(h);
   }
+  // m_min (certification) is enqueued before the flag check: its copy completes under the
+  // check's synchronisation
+  if ((rc = mscale_update(h))) return rc;
   rc = check_flags(h);
   if (rc) return rc;
-  if ((rc = mscale_update(h))) return rc;
   h->assembled = true;
   h->solved = false;
   return SSO_OK;
