@@ -73,3 +73,15 @@ def test_gpu_latency_lines(workload):
     assert d["roofline"]["bound"] == "latency" and d["roofline"]["achieved"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["extrapolated"] is False
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+
+
+@pytest.mark.gpu
+def test_gpu_c5_line():
+    lines = _run(["--workload", "C5", "--steps", "1", "--warmup", "3"], timeout=900)
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert BASE_KEYS <= set(d) and d["unit"] == "designs/s" and d["scaling"] == "weak" and d["value"] > 0
+    assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1.2
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["gpu_launches"] > 0
+    assert d["config"]["cg_iters_max"] >= d["config"]["cg_iters_min"] > 0
