@@ -98,3 +98,18 @@ def test_beyond_one_cluster_uses_the_fused_path(sso):
     u0, info0, C0, dX0 = _solve(sso, P, False, rtol=1e-10)
     assert info["status"] == 0 and info["iters"] == info0["iters"]
     assert np.array_equal(u, u0)  # the same kernels ran
+
+
+def test_cluster_pcg_deterministic(sso):
+    """Fixed-order reductions: repeated solves (and a second handle) give bit-identical u."""
+    P = W.config2()
+    u1, i1, C1, dX1 = _solve(sso, P, True, rtol=1e-10)
+    u2, i2, C2, dX2 = _solve(sso, P, True, rtol=1e-10)
+    m = _model(sso, P, True, rtol=1e-10)
+    m.assemble()
+    u3, i3 = m.solve(P["f"])
+    u4, i4 = m.solve(P["f"])
+    m.close()
+    assert np.array_equal(u1, u2) and np.array_equal(u1, u3) and np.array_equal(u3, u4)
+    assert i1["iters"] == i2["iters"] == i3["iters"] == i4["iters"]
+    assert C1 == C2 and np.array_equal(dX1, dX2)
