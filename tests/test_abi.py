@@ -81,3 +81,13 @@ def test_no_gpu_reports_cuda_error():
         pytest.skip("GPU present")
     import paper_2407_20026_b200.api as A
     _expect(W.tiny_shell(2, 0), A.SSO_E_CUDA)
+
+
+def test_nccl_resolves_at_run_time():
+    """The strips' NCCL transport is resolved with dlopen (no link-time dependency): the
+    library finds libnccl.so.2 in this environment and forms a unique id (bootstrap only, no
+    GPU needed) -- what bench.py --gpus N broadcasts before creating the rank handles."""
+    import torch  # noqa: F401  (the process's libnccl.so.2, as under torchrun)
+    import paper_2407_20026_b200 as sso
+    uid = sso.nccl_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == 128 and any(uid)
