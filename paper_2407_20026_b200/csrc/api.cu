@@ -254,7 +254,11 @@ struct sso_ctx {
   long long launches = 0;
   std::string err;
 
-  bool distributed() const { return parts.size() > 1 || nranks > 1; }
+  // NCCL transport: every multi-rank handle; a 1-rank handle with a unique id when
+  // SSO_NCCL_SELF=1 (tests: the whole NCCL path -- comm, captured allreduces, the split --
+  // on one GPU with no peer to wait for)
+  bool use_nccl = false;
+  bool distributed() const { return parts.size() > 1 || use_nccl; }
   Part& P0() { return *parts[0]; }
 };
 
@@ -447,11 +451,11 @@ int exchange(sso_ctx* h, int v, cudaStream_t s = nullptr) {
   if (!h->distributed()) return SSO_OK;
   if (!s) s = h->stream;
   long long g0 = g_launches;
-  if (h->nranks > 1) {
+  if (h->use_nccl) {
     Part& P = h->P0();
     launch_pack(s, (int)P.n_send, P.send_idx, vec_of(P, v), P.sendbuf);
   }
-  if (h->nranks == 1) {
+  if (!h->use_nccl) {
     // local transport: one gather kernel fills every part's halo from its neighbours' owned rows
     launch_halo_gather(s, h->n_halo_ent, h->d_halo_ent, h->d_vbase[v]);
   } else {
@@ -477,7 +481,7 @@ int allreduce(sso_ctx* h, int nvals, cudaStream_t s = nullptr) {
   if (!h->distributed()) return SSO_OK;
   if (!s) s = h->stream;
   long long g0 = g_launches;
-  if (h->nranks == 1) {
+  if (!h->use_nccl) {
     launch_allreduce_parts(s, h->d_sts, (int)h->parts.size(), nvals);
   } else {
     double* red = h->P0().st->red;
@@ -1007,7 +1011,7 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   {
     const char* env = getenv("SSO_CG_FUSED");
     const int fg = h->precond == 1 ? cg_block_fused_grid() : cg_fused_grid();
-    P.cgf = B <= fg && L.n_parts == 1 && h->nranks == 1 && h->check_every % 2 == 0 &&
+    P.cgf = B <= fg && L.n_parts == 1 && !h->use_nccl && h->check_every % 2 == 0 &&
             !(env && env[0] == '0');
   }
   if (P.cgf) {
@@ -1021,7 +1025,7 @@ int setup_part(sso_ctx* h, Part& P, const sso_mesh* mesh, const sso_sections* se
   }
   AL(q, B * P.ndof);
   AL(tmp, B * P.ndof);
-  if (L.n_parts > 1 || h->nranks > 1) {  // partitioned: single-reduction CG vectors (cg_sr.cu)
+  if (L.n_parts > 1 || h->use_nccl) {  // partitioned: single-reduction CG vectors (cg_sr.cu)
     AL(u_sr, B * P.ndof);
     AL(s_sr, B * P.ndof);
     CK(h, cudaMemset(P.u_sr, 0, B * P.ndof * sizeof(double)));
@@ -1144,7 +1148,7 @@ int mscale_update(sso_ctx* h) {
       launch_mscale(h->stream, P.n_own, P.dinv, P.binv, P.mscale_d, P.bs);
       h->launches += g_launches - g0;
     }
-    if (h->nranks > 1)  // positive doubles order like their bit patterns: min of the bits
+    if (h->use_nccl)  // positive doubles order like their bit patterns: min of the bits
       CKN(h, nccl().AllReduce(P.mscale_d, P.mscale_d, B, ncclUint64, ncclMin, h->comm, h->stream));
     CK(h, cudaMemcpyAsync(h->h_mscale + ip * B, P.mscale_d, B * sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, h->stream));
@@ -1299,6 +1303,11 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
   h->mem = o.mem;
   h->nranks = o.nranks;
   h->rank = o.rank;
+  {
+    const char* e = getenv("SSO_NCCL_SELF");
+    h->use_nccl = o.nranks > 1 ||
+                  (o.nranks == 1 && o.n_parts == 1 && o.batch == 1 && o.nccl_unique_id && e && e[0] == '1');
+  }
   h->batch = o.batch;
   h->reliable = o.reliable;
   h->assembly = o.assembly;
@@ -1378,9 +1387,9 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
     const char* env = getenv("SSO_SPLIT");
     bool all_pull = true;
     for (auto& pp : h->parts) all_pull &= pp->pull;
-    h->split = all_pull && (env ? env[0] == '1' : o.nranks > 1);
+    h->split = all_pull && (env ? env[0] == '1' : h->use_nccl);
     const char* envc = getenv("SSO_PART_STREAMS");
-    if (o.nranks == 1 && !h->split && !(envc && envc[0] == '0')) {
+    if (!h->use_nccl && !h->split && !(envc && envc[0] == '0')) {
       h->part_streams.assign(h->parts.size(), nullptr);
       h->part_ev.assign(h->parts.size(), nullptr);
       for (size_t i = 0; i < h->parts.size(); ++i)
@@ -1393,7 +1402,7 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
     // in-process parts with pull storage: one launch per step for all parts (SSO_MULTI=0: per-part
     // launches on per-part streams, for A/B)
     const char* envm = getenv("SSO_MULTI");
-    if (o.nranks == 1 && !h->split && all_pull && !(envm && envm[0] == '0')) {
+    if (!h->use_nccl && !h->split && all_pull && !(envm && envm[0] == '0')) {
       std::vector<PullPart> pp(h->parts.size());
       std::vector<SrPart> sp(h->parts.size());
       for (size_t i = 0; i < h->parts.size(); ++i) {
@@ -1436,9 +1445,11 @@ int sso_create(const sso_mesh* mesh, const sso_sections* sec, const sso_material
     for (auto& pp : h->parts) sts.push_back(pp->st);
     int r = upload(h, &h->d_sts, sts.data(), (int64_t)sts.size());
     if (r) return bail(r);
-    if (h->parts.size() > 1 && (r = dalloc(h, &h->d_dt_all, std::max<int32_t>(mesh->n_quads, 1)))) return bail(r);
+    if ((h->parts.size() > 1 || (h->use_nccl && o.nranks == 1)) &&
+        (r = dalloc(h, &h->d_dt_all, std::max<int32_t>(mesh->n_quads, 1))))
+      return bail(r);
   }
-  if (o.nranks > 1) {
+  if (h->use_nccl) {
     if (!nccl().ok) { h->err = nccl().err; return bail(SSO_E_NCCL); }
     ncclUniqueId id;
     std::memcpy(&id, o.nccl_unique_id, sizeof(id));

@@ -174,3 +174,31 @@ def test_split_thin_strips(sso, nparts, monkeypatch):
     up, ip = mp.solve(P["f"])
     assert ip["status"] == 0 and abs(ip["iters"] - i1["iters"]) <= max(3, 0.01 * i1["iters"])
     assert np.linalg.norm(up - u1) <= 1e-9 * np.linalg.norm(u1)
+
+
+@pytest.mark.parametrize("precond", [0, 1])
+@pytest.mark.parametrize("make", [W.config2, lambda: W.shell_config3(40, cfg=3)])
+def test_nccl_transport_single_rank(sso, make, precond, monkeypatch):
+    """The NCCL transport of the strips on ONE rank (SSO_NCCL_SELF=1: a 1-rank communicator, no
+    peer to wait for): comm init from a unique id, the halo group (empty) and the allreduces of
+    the single-reduction CG inside the captured graphs, the interior / boundary split on the
+    side stream -- the code a multi-GPU run executes, here against the local single-part solve."""
+    P = make()
+    monkeypatch.setenv("SSO_NCCL_SELF", "1")
+    m = sso.Model(P, rtol=1e-12, nranks=1, rank=0, nccl_id=sso.nccl_unique_id(), precond=precond)
+    m.assemble()
+    u, info = m.solve(P["f"])
+    C, dX, dT = m.grad()
+    m.close()
+    monkeypatch.delenv("SSO_NCCL_SELF")
+    m0 = sso.Model(P, rtol=1e-12, precond=precond)
+    m0.assemble()
+    u0, info0 = m0.solve(P["f"])
+    C0, dX0, dT0 = m0.grad()
+    m0.close()
+    assert info["status"] == 0 and info["true_rel_res"] < 1e-11
+    assert np.linalg.norm(u - u0) <= 1e-10 * np.linalg.norm(u0)
+    assert C == pytest.approx(C0, rel=1e-10)
+    assert np.max(np.abs(dX - dX0)) <= 1e-8 * np.max(np.abs(dX0))
+    assert np.max(np.abs(dT - dT0)) <= 1e-8 * np.max(np.abs(dT0))
+    assert abs(info["iters"] - info0["iters"]) <= max(3, info0["iters"] // 50)
